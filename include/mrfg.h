@@ -1,0 +1,189 @@
+/*
+ * mrfg.h -- C ABI of the B200-native MRF dictionary generating-and-searching
+ * (DGS) path.  Implemented in paper_1506_05393_b200/csrc (sm_100a CUDA + C++),
+ * built as paper_1506_05393_b200/libmrfg.so.
+ *
+ * This is the drop-in boundary: the reference's C++ entry points in
+ * /root/reference/proj/include/mrf/ keep their signatures in include/mrf/*.hpp
+ * (implemented by paper_1506_05393_b200/csrc/host/mrf_api.cpp, libmrf_b200.so)
+ * and forward to the functions below.  Each function cites the reference
+ * interface it replaces.  Conventions:
+ *   - every function returns 0 on success, a negative MRFG_E* code on error,
+ *     and mrfg_last_error() (thread-local) describes the failure -- the C++
+ *     shim turns these back into the reference's exceptions;
+ *   - plain pointers and sizes only; "_dev" entry points take CUDA device
+ *     pointers and run asynchronously on the context's stream, every other
+ *     entry point takes caller-owned HOST buffers and is synchronous;
+ *   - complex vectors are interleaved (re, im) -- the reference's dictionary
+ *     entry layout (dictionary.hpp:72-80);
+ *   - units follow the reference: schedules deg/ms (sequence.hpp:14-24),
+ *     lattices ms/ms/Hz (dictionary.hpp:17-56), tissue params s/s/Hz
+ *     (fingerprint.hpp:12-17).
+ * There is no CPU fallback: without an sm_100 device every compute entry
+ * point fails with MRFG_E_CUDA.
+ */
+#ifndef MRFG_H
+#define MRFG_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    MRFG_OK = 0,
+    MRFG_E_INVALID = -1,  /* std::invalid_argument in the reference */
+    MRFG_E_RANGE = -2,    /* std::out_of_range (zoom.cpp:126-130) */
+    MRFG_E_RUNTIME = -3,  /* std::runtime_error */
+    MRFG_E_CUDA = -4,     /* device error / no sm_100 device */
+    MRFG_E_NOMEM = -5
+};
+
+enum { MRFG_METRIC_CC = 0, MRFG_METRIC_EUCLIDEAN = 1 }; /* Metric, dictionary.hpp:98 */
+
+typedef struct mrfg_ctx mrfg_ctx;
+
+/* AxisSpec (dictionary.hpp:17-24): values min + k*step, k < count. */
+typedef struct { double min, step; int64_t count; } mrfg_axis;
+/* ParameterGrid (dictionary.hpp:34-56): T1 outer, T2 middle, df inner;
+ * flat = (i1*n2 + i2)*ndf + idf. */
+typedef struct { mrfg_axis t1_ms, t2_ms, df_hz; } mrfg_grid;
+
+/* Match (dictionary.hpp:100-104) reduced to the lattice point and score. */
+typedef struct { int64_t flat; double score; } mrfg_match;
+
+/* Screening/streaming knobs of the brute-force path (no reference analogue;
+ * zero fields take defaults). */
+typedef struct {
+    double delta;          /* screening margin in CC units (default 1e-3) */
+    int64_t chunk_atoms;   /* atoms simulated per streamed chunk (default 131072) */
+    int64_t cand_capacity; /* candidate buffer entries (default 1<<25) */
+    int64_t seed_atoms;    /* strided pre-pass atoms that seed the running max (default 16384) */
+} mrfg_scan_opts;
+
+/* What one scan did (device-timed with CUDA events on the ctx stream). */
+typedef struct {
+    int64_t atoms, voxels, chunks, candidates, reranked, overflow_passes;
+    double bloch_ms, gemm_ms, rerank_ms, total_ms;
+    double gemm_kernel_ms_avg; /* average duration of one K2 launch */
+    int64_t gemm_launches;
+} mrfg_scan_stats;
+
+/* ZoomConfig (zoom.hpp:23-52) as a POD; the step lists hold up to 8 values. */
+typedef struct {
+    int32_t metric, final_metric, smooth_k, n2d, n1d, pad0;
+    double omega_hz, df_coarse_hz, df_refine_hz, df_window_hz, plateau_eps, heavy_noise_cc,
+        fallback_coarse_hz, fallback_window_hz;
+    double t1t2_2d_steps_ms[8];
+    double t1t2_1d_steps_ms[8];
+    double final_2d_step_ms, init_t1_ms, init_t2_ms, prior_window_t1_ms, prior_window_t2_ms,
+        prior_window_df_hz;
+} mrfg_zoom_config;
+
+/* QuantResult (zoom.hpp:61-67) with the lattice indices. */
+typedef struct {
+    int64_t i1, i2, idf;
+    double t1_ms, t2_ms, df_hz, pd, score;
+    int64_t evaluations;
+} mrfg_quant;
+
+/* ------------------------------------------------------------------ misc */
+const char* mrfg_last_error(void);
+const char* mrfg_version(void);
+/* Fill cfg with the reference's ZoomConfig defaults (zoom.hpp:23-52). */
+void mrfg_zoom_config_default(mrfg_zoom_config* cfg);
+
+/* ----------------------------------------------- host-side input synthesis
+ * Restatements of the reference's input generators (host C++, no GPU). */
+/* build_schedule (sequence.hpp:51, sequence.cpp:77-92) */
+int mrfg_reference_schedule(int64_t n, uint64_t seed, double* flip_deg, double* phase_deg,
+                            double* tr_ms, double* te_ms);
+/* BASELINE.json schedule generator, %.9g-canonical. */
+int mrfg_baseline_schedule(int64_t n, uint64_t seed, double* flip_deg, double* phase_deg,
+                           double* tr_ms, double* te_ms);
+/* add_noise (fingerprint.hpp:53, fingerprint.cpp:68-78) */
+int mrfg_add_noise(const double* fp, int64_t n, double sigma, uint64_t seed, double* out);
+/* rng::at / uniform01 / gaussian (rng.hpp:24-41) */
+uint64_t mrfg_rng_at(uint64_t seed, uint64_t stream, uint64_t index);
+double mrfg_rng_uniform01(uint64_t seed, uint64_t stream, uint64_t index);
+double mrfg_rng_gaussian(uint64_t seed, uint64_t stream, uint64_t index);
+/* Endpoint-exclusive axis count (dictionary.cpp:25-33): 0 and MRFG_E_INVALID
+ * when the range is empty or the step non-positive. */
+int mrfg_axis_count(double min, double max, double step, int64_t* count);
+
+/* --------------------------------------------------------------- context
+ * BlochSimulator(const Schedule&) (bloch.hpp:83, bloch.cpp:95-106): validates
+ * 0 <= te <= tr, composes the RF rotations once, uploads the schedule. */
+int mrfg_create(const double* flip_deg, const double* phase_deg, const double* tr_ms,
+                const double* te_ms, int64_t n, int device, mrfg_ctx** out);
+int mrfg_destroy(mrfg_ctx* ctx);
+int64_t mrfg_length(const mrfg_ctx* ctx); /* BlochSimulator::length (bloch.hpp:89) */
+/* Run on a caller-provided cudaStream_t (e.g. torch's current stream). */
+int mrfg_set_stream(mrfg_ctx* ctx, void* cuda_stream);
+int mrfg_synchronize(mrfg_ctx* ctx);
+
+/* ------------------------------------------------------------ K1 Bloch
+ * BlochSimulator::simulate (bloch.hpp:86-87, bloch.cpp:108-123) for a batch of
+ * tissue points params[3*k..] = (t1_s, t2_s, df_hz).  precision 64 is the
+ * reference's FP64 recursion (bit-exact with it); 32 is the FP32 FMA kernel.
+ * normalize != 0 scales each fingerprint to unit L2 norm (fingerprint.cpp:28-37). */
+int mrfg_simulate(mrfg_ctx* ctx, const double* params, int64_t count, int precision,
+                  int normalize, double* out /* count x 2N */);
+int mrfg_simulate_dev(mrfg_ctx* ctx, const double* d_params, int64_t count, int precision,
+                      int normalize, double* d_out);
+/* generate / generate_range (dictionary.hpp:85, dictionary.cpp:37-60,184-194):
+ * unit-norm float32 entries of flats [first, first+count) of the grid. */
+int mrfg_generate(mrfg_ctx* ctx, const mrfg_grid* grid, int64_t first, int64_t count,
+                  int precision, float* out /* count x 2N */);
+int mrfg_generate_dev(mrfg_ctx* ctx, const mrfg_grid* grid, int64_t first, int64_t count,
+                      int precision, float* d_out);
+/* FP32 Bloch throughput kernel alone (bench): simulates flats [first,
+ * first+count) and accumulates only per-atom norms into d_norm2 (count). */
+int mrfg_bloch_norms_dev(mrfg_ctx* ctx, const mrfg_grid* grid, int64_t first, int64_t count,
+                         float* d_norm2);
+
+/* ---------------------------------------------------- K2/K3 brute force
+ * scan_grid (dictionary.hpp:120-122, dictionary.cpp:257-308): streamed
+ * simulate-and-match of flats [flat_begin, flat_end) (the whole grid when
+ * both are 0), per-query argmax with the lowest-flat tie rule.  Queries are
+ * raw (they are normalized in FP64 as prep_query does, dictionary.cpp:145-150);
+ * scores are the reference's FP64 score of the FP32-quantized entry. */
+int mrfg_scan_grid(mrfg_ctx* ctx, const mrfg_grid* grid, int64_t flat_begin, int64_t flat_end,
+                   const double* queries, int64_t nq, int metric, const mrfg_scan_opts* opts,
+                   mrfg_match* out, mrfg_scan_stats* stats);
+int mrfg_scan_grid_dev(mrfg_ctx* ctx, const mrfg_grid* grid, int64_t flat_begin,
+                       int64_t flat_end, const double* d_queries, int64_t nq, int metric,
+                       const mrfg_scan_opts* opts, mrfg_match* d_out, mrfg_scan_stats* stats);
+/* C1: merge per-rank matches gathered as d_in[rank*nq + q] (max score,
+ * lowest flat on ties) -- the reduction after the NCCL allgather. */
+int mrfg_merge_matches_dev(mrfg_ctx* ctx, const mrfg_match* d_in, int nranks, int64_t nq,
+                           mrfg_match* d_out);
+
+/* Test support: dense K2 screening scores (|z|^2/|d|^2 for cc, Re z/|d| for
+ * euclidean) of flats [first, first+count) against nq queries, out[a*nq+v],
+ * through the tcgen05 kernel (use_simt = 0) or its CUDA-core twin (1). */
+int mrfg_screen_scores(mrfg_ctx* ctx, const mrfg_grid* grid, int64_t first, int64_t count,
+                       const double* queries, int64_t nq, int metric, int use_simt, float* out);
+
+/* cc_map (dictionary.hpp:127-129, dictionary.cpp:310-331): float CC of one
+ * query against flats [first, first+count). */
+int mrfg_cc_map(mrfg_ctx* ctx, const mrfg_grid* grid, const double* query, int64_t first,
+                int64_t count, float* out);
+
+/* ----------------------------------------------------------- K5 MRF-ZOOM
+ * quantify_impl per voxel (zoom.cpp:416-523) on a lattice (the finest
+ * search pitch, zoom.hpp:17-21).  mrfg_quantify: independent voxels with full
+ * bounds (quantify, zoom.cpp:533-539; quantify_slice without priors,
+ * zoom.cpp:616-624).  mrfg_quantify_slice adds the neighbour-prior raster mode
+ * (zoom.cpp:589-615) when use_prior != 0. */
+int mrfg_quantify(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                  const double* fps, int64_t nvox, mrfg_quant* out);
+int mrfg_quantify_slice(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                        const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
+                        mrfg_quant* out, double* seconds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

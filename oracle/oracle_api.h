@@ -1,0 +1,80 @@
+/*
+ * oracle_api.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Common C API of the two CPU oracles used by tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs:
+ *
+ *   oracle/liboracle.so     plain-C restatement of the reference algorithm
+ *                           (oracle/mrf_oracle.c; every function cites the
+ *                           reference file:line it follows);
+ *   oracle/_ref/libmrf_ref.so  the reference library itself, compiled from
+ *                           /root/reference/proj/src by oracle/Makefile and
+ *                           wrapped by oracle/ref_capi.cpp.
+ *
+ * Nothing in the product (paper_1506_05393_b200/) links or calls this.
+ * Units follow the reference: schedules in deg/ms (sequence.hpp:14-24),
+ * lattices in ms/ms/Hz (dictionary.hpp:17-56), tissue params in s/s/Hz
+ * (fingerprint.hpp:12-17).  Complex vectors are interleaved (re, im) doubles.
+ */
+#ifndef MRF_ORACLE_API_H
+#define MRF_ORACLE_API_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { double min, step; int64_t count; } orc_axis;           /* AxisSpec */
+typedef struct { orc_axis t1_ms, t2_ms, df_hz; } orc_grid;                /* ParameterGrid */
+typedef struct {
+    int64_t n;
+    const double *flip_deg, *phase_deg, *tr_ms, *te_ms;
+} orc_sched;                                                             /* Schedule */
+
+/* ZoomConfig (zoom.hpp:23-52) as a POD; step lists hold up to 8 entries. */
+typedef struct {
+    int32_t metric, final_metric, smooth_k, n2d, n1d, pad0;
+    double omega_hz, df_coarse_hz, df_refine_hz, df_window_hz, plateau_eps, heavy_noise_cc,
+        fallback_coarse_hz, fallback_window_hz;
+    double t1t2_2d_steps_ms[8];
+    double t1t2_1d_steps_ms[8];
+    double final_2d_step_ms, init_t1_ms, init_t2_ms, prior_window_t1_ms, prior_window_t2_ms,
+        prior_window_df_hz;
+} orc_zoom_cfg;
+
+/* QuantResult (zoom.hpp:61-67) plus the lattice indices. */
+typedef struct {
+    int64_t i1, i2, idf;
+    double t1_ms, t2_ms, df_hz, pd, score;
+    int64_t evaluations;
+} orc_quant;
+
+/* 0 = ok; otherwise a negative code and orc_last_error() explains. */
+const char* orc_last_error(void);
+const char* orc_impl_name(void); /* "restatement" or "reference" */
+
+int orc_build_schedule(int64_t n, uint64_t seed, double* flip_deg, double* phase_deg,
+                       double* tr_ms, double* te_ms);
+int orc_baseline_schedule(int64_t n, uint64_t seed, double* flip_deg, double* phase_deg,
+                          double* tr_ms, double* te_ms);
+int orc_simulate(const orc_sched* s, double t1_s, double t2_s, double df_hz, double* out);
+int orc_add_noise(const double* fp, int64_t n, double sigma, uint64_t seed, double* out);
+double orc_cc(const double* a, const double* b, int64_t n);
+int orc_generate(const orc_sched* s, const orc_grid* g, int64_t first, int64_t count,
+                 float* out);
+/* scan_grid: per-query lowest-flat argmax.  second_score (may be NULL) is the
+ * best score over all other flats (restatement only; the reference wrapper
+ * writes NaN). */
+int orc_scan_grid(const orc_sched* s, const orc_grid* g, const double* queries, int64_t nq,
+                  int metric, int threads, int64_t* best_flat, double* best_score,
+                  double* second_score);
+int orc_quantify(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg* cfg,
+                 const double* fp, orc_quant* out);
+int orc_quantify_slice(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg* cfg,
+                       const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
+                       int threads, orc_quant* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

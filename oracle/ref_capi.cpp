@@ -1,0 +1,235 @@
+// ref_capi.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" wrapper exposing the UNMODIFIED reference library (compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/libmrf_ref.so)
+// through oracle/oracle_api.h, so the tests can pin the C restatement
+// (oracle/mrf_oracle.c) against the reference itself and bench.py can time
+// the reference's own CPU path.  Every entry calls the reference's public API
+// (proj/include/mrf/*.hpp); the only harness logic is unit conversion and the
+// BASELINE.json schedule formula (which the reference ingests through
+// load_schedule_csv in real use).
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mrf/bloch.hpp"
+#include "mrf/dictionary.hpp"
+#include "mrf/fingerprint.hpp"
+#include "mrf/rng.hpp"
+#include "mrf/sequence.hpp"
+#include "mrf/util.hpp"
+#include "mrf/zoom.hpp"
+#include "oracle_api.h"
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+mrf::Schedule to_sched(const orc_sched* s) {
+    mrf::Schedule out;
+    out.entries.resize(static_cast<std::size_t>(s->n));
+    for (int64_t i = 0; i < s->n; ++i)
+        out.entries[i] = {s->flip_deg[i], s->phase_deg[i], s->tr_ms[i], s->te_ms[i]};
+    return out;
+}
+
+mrf::ParameterGrid to_grid(const orc_grid* g) {
+    mrf::ParameterGrid p;
+    p.t1_ms = {g->t1_ms.min, g->t1_ms.step, static_cast<std::size_t>(g->t1_ms.count)};
+    p.t2_ms = {g->t2_ms.min, g->t2_ms.step, static_cast<std::size_t>(g->t2_ms.count)};
+    p.df_hz = {g->df_hz.min, g->df_hz.step, static_cast<std::size_t>(g->df_hz.count)};
+    return p;
+}
+
+// Half-open ranges whose endpoint-exclusive count (dictionary.cpp:25-33)
+// reproduces the axis count exactly.
+mrf::AxisRange to_range(const orc_axis& a) {
+    return {a.min, a.min + static_cast<double>(a.count) * a.step, a.step};
+}
+
+mrf::Fingerprint to_fp(const double* v, int64_t n) {
+    mrf::Fingerprint fp;
+    fp.s.resize(static_cast<std::size_t>(n));
+    for (int64_t j = 0; j < n; ++j) fp.s[j] = {v[2 * j], v[2 * j + 1]};
+    return fp;
+}
+
+mrf::ZoomConfig to_cfg(const orc_zoom_cfg* c) {
+    mrf::ZoomConfig z;
+    z.metric = c->metric ? mrf::Metric::euclidean : mrf::Metric::cc;
+    z.final_metric = c->final_metric ? mrf::Metric::euclidean : mrf::Metric::cc;
+    z.smooth_k = c->smooth_k;
+    z.omega_hz = c->omega_hz;
+    z.df_coarse_hz = c->df_coarse_hz;
+    z.df_refine_hz = c->df_refine_hz;
+    z.df_window_hz = c->df_window_hz;
+    z.plateau_eps = c->plateau_eps;
+    z.heavy_noise_cc = c->heavy_noise_cc;
+    z.fallback_coarse_hz = c->fallback_coarse_hz;
+    z.fallback_window_hz = c->fallback_window_hz;
+    z.t1t2_2d_steps_ms.assign(c->t1t2_2d_steps_ms, c->t1t2_2d_steps_ms + c->n2d);
+    z.t1t2_1d_steps_ms.assign(c->t1t2_1d_steps_ms, c->t1t2_1d_steps_ms + c->n1d);
+    z.final_2d_step_ms = c->final_2d_step_ms;
+    z.init_t1_ms = c->init_t1_ms;
+    z.init_t2_ms = c->init_t2_ms;
+    z.prior_window_t1_ms = c->prior_window_t1_ms;
+    z.prior_window_t2_ms = c->prior_window_t2_ms;
+    z.prior_window_df_hz = c->prior_window_df_hz;
+    return z;
+}
+
+int64_t snap(double v, const orc_axis& a) { return std::lround((v - a.min) / a.step); }
+
+void fill_quant(const orc_grid* g, double t1_ms, double t2_ms, double df_hz, double pd,
+                double score, std::size_t evals, orc_quant* out) {
+    out->t1_ms = t1_ms;
+    out->t2_ms = t2_ms;
+    out->df_hz = df_hz;
+    out->i1 = snap(t1_ms, g->t1_ms);
+    out->i2 = snap(t2_ms, g->t2_ms);
+    out->idf = snap(df_hz, g->df_hz);
+    out->pd = pd;
+    out->score = score;
+    out->evaluations = static_cast<int64_t>(evals);
+}
+}  // namespace
+
+extern "C" {
+
+const char* orc_last_error(void) { return g_err.c_str(); }
+const char* orc_impl_name(void) { return "reference"; }
+
+int orc_build_schedule(int64_t n, uint64_t seed, double* flip, double* phase, double* tr,
+                       double* te) {
+    return guard([&] {
+        mrf::Schedule s = mrf::build_schedule(static_cast<std::size_t>(n), seed);
+        for (int64_t i = 0; i < n; ++i) {
+            flip[i] = s.entries[i].flip_deg;
+            phase[i] = s.entries[i].phase_deg;
+            tr[i] = s.entries[i].tr_ms;
+            te[i] = s.entries[i].te_ms;
+        }
+    });
+}
+
+int orc_baseline_schedule(int64_t n, uint64_t seed, double* flip, double* phase, double* tr,
+                          double* te) {
+    return guard([&] {
+        for (int64_t j = 0; j < n; ++j) {
+            double fa = 10.0 + 50.0 * std::fabs(std::sin(2.0 * M_PI * static_cast<double>(j) / 250.0)) +
+                        2.0 * mrf::rng::gaussian(seed, 1, static_cast<std::uint64_t>(j));
+            double trv = mrf::quantize9(10.5 + 3.5 * mrf::rng::uniform01(seed, 2, static_cast<std::uint64_t>(j)));
+            flip[j] = mrf::quantize9(fa);
+            phase[j] = (j % 2) ? 180.0 : 0.0;
+            tr[j] = trv;
+            te[j] = mrf::quantize9(trv / 2.0);
+        }
+    });
+}
+
+int orc_simulate(const orc_sched* s, double t1_s, double t2_s, double df_hz, double* out) {
+    return guard([&] {
+        mrf::BlochSimulator sim(to_sched(s));
+        std::vector<std::complex<double>> buf(sim.length());
+        sim.simulate({t1_s, t2_s, df_hz, 1.0}, buf.data());
+        for (std::size_t j = 0; j < buf.size(); ++j) {
+            out[2 * j] = buf[j].real();
+            out[2 * j + 1] = buf[j].imag();
+        }
+    });
+}
+
+int orc_add_noise(const double* fp, int64_t n, double sigma, uint64_t seed, double* out) {
+    return guard([&] {
+        mrf::Fingerprint r = mrf::add_noise(to_fp(fp, n), sigma, seed);
+        for (int64_t j = 0; j < n; ++j) {
+            out[2 * j] = r.s[j].real();
+            out[2 * j + 1] = r.s[j].imag();
+        }
+    });
+}
+
+double orc_cc(const double* a, const double* b, int64_t n) {
+    try {
+        return mrf::cc(to_fp(a, n), to_fp(b, n));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return NAN;
+    }
+}
+
+int orc_generate(const orc_sched* s, const orc_grid* g, int64_t first, int64_t count, float* out) {
+    return guard([&] {
+        // The reference materializes the whole lattice; generate() of a grid
+        // then slice [first, first+count).
+        mrf::Dictionary d = mrf::generate(to_grid(g), to_sched(s), 8);
+        std::memcpy(out, d.data.data() + first * 2 * s->n,
+                    sizeof(float) * static_cast<std::size_t>(count * 2 * s->n));
+    });
+}
+
+int orc_scan_grid(const orc_sched* s, const orc_grid* g, const double* queries, int64_t nq,
+                  int metric, int threads, int64_t* best_flat, double* best_score,
+                  double* second_score) {
+    return guard([&] {
+        std::vector<mrf::Fingerprint> qs;
+        for (int64_t i = 0; i < nq; ++i) qs.push_back(to_fp(queries + i * 2 * s->n, s->n));
+        mrf::ParameterGrid grid = to_grid(g);
+        mrf::ScanOutcome out = mrf::scan_grid(grid, to_sched(s), qs,
+                                              metric ? mrf::Metric::euclidean : mrf::Metric::cc,
+                                              threads);
+        for (int64_t i = 0; i < nq; ++i) {
+            const auto& p = out.matches[i].params;
+            int64_t i1 = snap(p.t1 * 1e3, g->t1_ms), i2 = snap(p.t2 * 1e3, g->t2_ms),
+                    idf = snap(p.df, g->df_hz);
+            best_flat[i] = static_cast<int64_t>(grid.flatten(i1, i2, idf));
+            best_score[i] = out.matches[i].score;
+            if (second_score) second_score[i] = NAN;
+        }
+    });
+}
+
+int orc_quantify(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg* cfg,
+                 const double* fp, orc_quant* out) {
+    return guard([&] {
+        mrf::SearchRanges r{to_range(lattice->t1_ms), to_range(lattice->t2_ms),
+                            to_range(lattice->df_hz)};
+        mrf::QuantResult q = mrf::quantify(to_fp(fp, s->n), r, to_cfg(cfg), to_sched(s));
+        fill_quant(lattice, q.params.t1 * 1e3, q.params.t2 * 1e3, q.params.df, q.params.pd,
+                   q.score, q.evaluations, out);
+    });
+}
+
+int orc_quantify_slice(const orc_sched* s, const orc_grid* g, const orc_zoom_cfg* cfg,
+                       const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
+                       int threads, orc_quant* out) {
+    return guard([&] {
+        std::size_t nv = static_cast<std::size_t>(nx) * static_cast<std::size_t>(ny);
+        std::vector<mrf::Fingerprint> v(nv);
+        std::vector<std::uint8_t> m(mask, mask + nv);
+        for (std::size_t i = 0; i < nv; ++i)
+            if (m[i]) v[i] = to_fp(fps + i * 2 * s->n, s->n);
+        mrf::SearchRanges r{to_range(g->t1_ms), to_range(g->t2_ms), to_range(g->df_hz)};
+        mrf::SliceResult res =
+            mrf::quantify_slice(v, m, nx, ny, r, to_cfg(cfg), to_sched(s), use_prior != 0, threads);
+        std::memset(out, 0, sizeof(orc_quant) * nv);
+        for (std::size_t i = 0; i < nv; ++i)
+            if (m[i])
+                fill_quant(g, res.t1_ms[i], res.t2_ms[i], res.df_hz[i], res.pd[i], res.score[i],
+                           res.evaluations[i], &out[i]);
+    });
+}
+
+}  // extern "C"

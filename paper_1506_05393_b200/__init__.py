@@ -1,0 +1,15 @@
+"""B200-native MRF dictionary generating-and-searching (DGS) path.
+
+sm_100a CUDA kernels behind the C ABI of include/mrfg.h (libmrfg.so, built
+in-tree by ``paper_1506_05393_b200/build.py``), with a host-side mirror of the
+reference library's interface in :mod:`paper_1506_05393_b200.dgs`.
+"""
+from . import dgs  # noqa: F401
+from ._native import LIB_PATH, load  # noqa: F401
+from .dgs import (Context, Schedule, add_noise, baseline_schedule, grid, grid_from_ranges,  # noqa: F401
+                  grid_inclusive, grid_total, params_at, reference_schedule, unflatten,
+                  zoom_config)
+
+__all__ = ["Context", "Schedule", "add_noise", "baseline_schedule", "grid", "grid_from_ranges",
+           "grid_inclusive", "grid_total", "params_at", "reference_schedule", "unflatten",
+           "zoom_config", "load", "LIB_PATH", "dgs"]

@@ -1,0 +1,694 @@
+// abi.cu -- the C ABI of include/mrfg.h: context, host tables and the
+// orchestration of the streamed simulate-and-match scan.
+#include <omp.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mrfg_internal.cuh"
+
+namespace mrfg {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+template <class F>
+static int guard(F&& f) {
+    try {
+        f();
+        return MRFG_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return MRFG_E_NOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return MRFG_E_RUNTIME;
+    }
+}
+
+// ----------------------------------------------------------- host physics
+// bloch.cpp:31-53 / 63-66: Rz(phi) Rx(-alpha) Rz(-phi), row-major products
+// summed left to right (bloch.hpp:25-32) -- the reference's exact doubles.
+static void rot(int axis, double theta, double r[9]) {
+    double c = std::cos(theta), s = std::sin(theta);
+    const double x[9] = {1, 0, 0, 0, c, -s, 0, s, c};
+    const double z[9] = {c, -s, 0, s, c, 0, 0, 0, 1};
+    std::memcpy(r, axis == 0 ? x : z, sizeof(x));
+}
+static void mul3(const double* a, const double* b, double* r) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            r[3 * i + j] = a[3 * i] * b[j] + a[3 * i + 1] * b[3 + j] + a[3 * i + 2] * b[6 + j];
+}
+void host_rf_matrix(double alpha, double phi, double out[9]) {
+    double a[9], b[9], c[9], ab[9];
+    rot(2, phi, a);
+    rot(0, -alpha, b);
+    rot(2, -phi, c);
+    mul3(a, b, ab);
+    mul3(ab, c, out);
+}
+
+static bool same_grid(const mrfg_grid& a, const mrfg_grid& b) {
+    return std::memcmp(&a, &b, sizeof(mrfg_grid)) == 0;
+}
+
+static void check_grid(const mrfg_grid& g) {
+    const mrfg_axis* ax[3] = {&g.t1_ms, &g.t2_ms, &g.df_hz};
+    for (auto* a : ax) MRFG_REQUIRE(a->count > 0, MRFG_E_INVALID, "grid: empty axis");
+    MRFG_REQUIRE(g.t1_ms.min > 0 && g.t1_ms.min + (g.t1_ms.count - 1) * g.t1_ms.step > 0 &&
+                     g.t2_ms.min > 0 && g.t2_ms.min + (g.t2_ms.count - 1) * g.t2_ms.step > 0,
+                 MRFG_E_INVALID, "simulate: T1 and T2 must be positive");
+}
+
+// Per-axis transcendental tables: host libm, reference operand order
+// (bloch.cpp:17-21).  Cached per context for the last grid.
+const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
+    if (c.tab.valid && same_grid(c.tab.grid, g)) return c.tab;
+    check_grid(g);
+    const int64_t n = c.n, n1 = g.t1_ms.count, n2 = g.t2_ms.count, nd = g.df_hz.count;
+    std::vector<double> e1(n * n1 * 2), e2(n * n2 * 2), ph(n * nd * 4);
+    std::vector<float> e1f(n * n1 * 4), e2f(n * n2 * 2), phf(n * nd * 4);
+    const double kTwoPi = 6.283185307179586476925286766559;
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < n; ++j) {
+        const double te = c.te_s[j], rest = c.rest_s[j];
+        for (int64_t i = 0; i < n1; ++i) {
+            const double inv = 1.0 / ((g.t1_ms.min + static_cast<double>(i) * g.t1_ms.step) * 1e-3);
+            const double a = std::exp(-te * inv), b = std::exp(-rest * inv);
+            e1[(j * n1 + i) * 2] = a;
+            e1[(j * n1 + i) * 2 + 1] = b;
+            float* f = &e1f[(j * n1 + i) * 4];
+            f[0] = static_cast<float>(a);
+            f[1] = static_cast<float>(1.0 - a);
+            f[2] = static_cast<float>(b);
+            f[3] = static_cast<float>(1.0 - b);
+        }
+        for (int64_t i = 0; i < n2; ++i) {
+            const double inv = 1.0 / ((g.t2_ms.min + static_cast<double>(i) * g.t2_ms.step) * 1e-3);
+            const double a = std::exp(-te * inv), b = std::exp(-rest * inv);
+            e2[(j * n2 + i) * 2] = a;
+            e2[(j * n2 + i) * 2 + 1] = b;
+            e2f[(j * n2 + i) * 2] = static_cast<float>(a);
+            e2f[(j * n2 + i) * 2 + 1] = static_cast<float>(b);
+        }
+        for (int64_t i = 0; i < nd; ++i) {
+            const double df = g.df_hz.min + static_cast<double>(i) * g.df_hz.step;
+            const double at = kTwoPi * df * te, ar = kTwoPi * df * rest;
+            double* p = &ph[(j * nd + i) * 4];
+            p[0] = std::cos(at);
+            p[1] = std::sin(at);
+            p[2] = std::cos(ar);
+            p[3] = std::sin(ar);
+            float* f = &phf[(j * nd + i) * 4];
+            for (int k = 0; k < 4; ++k) f[k] = static_cast<float>(p[k]);
+        }
+    }
+    GridTables& t = c.tab;
+    t.valid = false;
+    auto up = [&](DevBuf& b, const void* src, size_t bytes) {
+        b.ensure(bytes);
+        MRFG_CUDA(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, c.stream));
+    };
+    up(t.e1d, e1.data(), e1.size() * 8);
+    up(t.e2d, e2.data(), e2.size() * 8);
+    up(t.phd, ph.data(), ph.size() * 8);
+    up(t.e1f, e1f.data(), e1f.size() * 4);
+    up(t.e2f, e2f.data(), e2f.size() * 4);
+    up(t.phf, phf.data(), phf.size() * 4);
+    MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    t.grid = g;
+    t.valid = true;
+    return t;
+}
+
+__global__ void k_fill(float* p, int64_t n, float v) {
+    int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+static void fill(Ctx& c, float* p, int64_t n, float v) {
+    if (n <= 0) return;
+    k_fill<<<(n + 255) / 256, 256, 0, c.stream>>>(p, n, v);
+    MRFG_CUDA(cudaGetLastError());
+}
+
+struct EventTimer {
+    cudaStream_t s;
+    std::vector<cudaEvent_t> evs;
+    explicit EventTimer(cudaStream_t st) : s(st) {}
+    ~EventTimer() {
+        for (auto e : evs) cudaEventDestroy(e);
+    }
+    int mark() {
+        cudaEvent_t e;
+        MRFG_CUDA(cudaEventCreate(&e));
+        MRFG_CUDA(cudaEventRecord(e, s));
+        evs.push_back(e);
+        return static_cast<int>(evs.size()) - 1;
+    }
+    double ms(int a, int b) {
+        float m = 0;
+        MRFG_CUDA(cudaEventElapsedTime(&m, evs[a], evs[b]));
+        return m;
+    }
+};
+
+// The streamed brute-force scan on device-resident queries.
+static void scan_dev(Ctx& c, const mrfg_grid& grid, int64_t fb, int64_t fe, const double* d_raw,
+                     int64_t nq, int metric, const mrfg_scan_opts* o, mrfg_match* d_out,
+                     mrfg_scan_stats* st) {
+    MRFG_REQUIRE(nq > 0, MRFG_E_INVALID, "scan_grid: no queries");  // dictionary.cpp:260
+    MRFG_REQUIRE(metric == MRFG_METRIC_CC || metric == MRFG_METRIC_EUCLIDEAN, MRFG_E_INVALID,
+                 "scan_grid: unknown metric");
+    const int64_t total = grid_total(grid);
+    if (fb == 0 && fe == 0) fe = total;
+    MRFG_REQUIRE(0 <= fb && fb < fe && fe <= total, MRFG_E_INVALID, "scan_grid: bad flat range");
+    const GridTables& t = ensure_tables(c, grid, true);
+    const double delta = (o && o->delta > 0) ? o->delta : 1e-3;
+    int64_t chunk = (o && o->chunk_atoms > 0) ? o->chunk_atoms : 131072;
+    chunk = round_up(chunk, 128);
+    int64_t cap = (o && o->cand_capacity > 0) ? o->cand_capacity : (int64_t(1) << 25);
+    const int64_t seed_atoms = (o && o->seed_atoms > 0) ? o->seed_atoms : 16384;
+    const int64_t n = c.n, kp = k_pad_of(n), qrows = round_up(2 * nq, 256);
+    const int64_t range = fe - fb;
+
+    EventTimer tm(c.stream);
+    const int e_start = tm.mark();
+    c.q64.ensure(sizeof(double) * 2 * n * nq);
+    c.qprime.ensure(sizeof(__half) * qrows * kp);
+    c.best.ensure(sizeof(float) * nq + 64);
+    int* d_bad = reinterpret_cast<int*>(c.best.as<char>() + sizeof(float) * nq);
+    MRFG_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), c.stream));
+    launch_prepare_queries(c, d_raw, nq, qrows, c.q64.as<double>(), c.qprime.as<__half>(), d_bad);
+    int h_bad = 0;
+    MRFG_CUDA(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    MRFG_REQUIRE(!h_bad, MRFG_E_INVALID, "normalize: zero fingerprint");
+    float* best = c.best.as<float>();
+    fill(c, best, nq, -3.0f);
+
+    const int64_t arows = std::min(chunk, round_up(range, 128));
+    c.atoms_a.ensure(sizeof(__half) * arows * kp);
+    c.inv2.ensure(sizeof(float) * arows);
+    c.cand_count.ensure(64);
+    auto* d_count = c.cand_count.as<unsigned long long>();
+
+    MatchParams mp{};
+    mp.a = c.atoms_a.as<__half>();
+    mp.inv2 = c.inv2.as<float>();
+    mp.b = c.qprime.as<__half>();
+    mp.q_rows = qrows;
+    mp.k_pad = kp;
+    mp.nvox = nq;
+    mp.best = best;
+    mp.cand_count = d_count;
+    mp.delta = static_cast<float>(delta);
+    mp.metric = metric;
+
+    double gemm_ms = 0, bloch_ms = 0;
+    int64_t gemm_launches = 0, chunks = 0;
+    // Seed pass: a strided sample of the range raises the running maxima
+    // before the stream starts (no candidates are recorded).
+    {
+        int64_t stride = std::max<int64_t>(1, range / seed_atoms);
+        int64_t cnt = (range + stride - 1) / stride;
+        int64_t rows = round_up(std::min(cnt, arows), 128);
+        int a0 = tm.mark();
+        launch_bloch_operand(c, t, fb, stride, fe, rows, metric, c.atoms_a.as<__half>(), c.inv2.as<float>());
+        int a1 = tm.mark();
+        mp.atoms = rows;
+        mp.valid_atoms = std::min(cnt, rows);
+        mp.flat_base = fb;
+        mp.flat_stride = stride;
+        mp.cand = nullptr;
+        mp.cand_cap = 0;
+        launch_match(c, mp);
+        int a2 = tm.mark();
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        bloch_ms += tm.ms(a0, a1);
+        gemm_ms += tm.ms(a1, a2);
+        ++gemm_launches;
+    }
+    int64_t overflow_passes = 0;
+    unsigned long long ncand = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        c.cand.ensure(sizeof(CandRec) * cap);
+        MRFG_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
+        mp.cand = c.cand.as<CandRec>();
+        mp.cand_cap = cap;
+        std::vector<int> marks;
+        for (int64_t f = fb; f < fe; f += chunk) {
+            const int64_t cnt = std::min(chunk, fe - f);
+            const int64_t rows = round_up(cnt, 128);
+            marks.push_back(tm.mark());
+            launch_bloch_operand(c, t, f, 1, fe, rows, metric, c.atoms_a.as<__half>(), c.inv2.as<float>());
+            marks.push_back(tm.mark());
+            mp.atoms = rows;
+            mp.valid_atoms = cnt;
+            mp.flat_base = f;
+            mp.flat_stride = 1;
+            launch_match(c, mp);
+            marks.push_back(tm.mark());
+            ++chunks;
+        }
+        MRFG_CUDA(cudaMemcpyAsync(&ncand, d_count, sizeof ncand, cudaMemcpyDeviceToHost, c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        for (size_t i = 0; i + 2 < marks.size(); i += 3) {
+            bloch_ms += tm.ms(marks[i], marks[i + 1]);
+            gemm_ms += tm.ms(marks[i + 1], marks[i + 2]);
+            ++gemm_launches;
+        }
+        if (ncand <= static_cast<unsigned long long>(cap)) break;
+        // Overflow: the running maxima are now final, so a second pass records
+        // a subset of the first pass's candidates; size the buffer for all.
+        MRFG_REQUIRE(pass == 0, MRFG_E_RUNTIME, "scan: candidate buffer overflow");
+        cap = static_cast<int64_t>(ncand);
+        ++overflow_passes;
+    }
+    int r0 = tm.mark();
+    int64_t nsel = rerank_and_select(c, t, c.q64.as<double>(), nq, metric, best,
+                                     static_cast<float>(delta), c.cand.as<CandRec>(),
+                                     static_cast<int64_t>(ncand), d_out);
+    int r1 = tm.mark();
+    MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    if (st) {
+        st->atoms = range;
+        st->voxels = nq;
+        st->chunks = chunks;
+        st->candidates = static_cast<int64_t>(ncand);
+        st->reranked = nsel;
+        st->overflow_passes = overflow_passes;
+        st->bloch_ms = bloch_ms;
+        st->gemm_ms = gemm_ms;
+        st->rerank_ms = tm.ms(r0, r1);
+        st->total_ms = tm.ms(e_start, r1);
+        st->gemm_launches = gemm_launches;
+        st->gemm_kernel_ms_avg = gemm_launches ? gemm_ms / gemm_launches : 0;
+    }
+}
+
+}  // namespace mrfg
+
+using namespace mrfg;
+
+struct mrfg_ctx {
+    Ctx c;
+};
+
+extern "C" {
+
+const char* mrfg_last_error(void) { return g_err.c_str(); }
+const char* mrfg_version(void) { return "mrfg 0.1 (sm_100a)"; }
+
+void mrfg_zoom_config_default(mrfg_zoom_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->metric = MRFG_METRIC_CC;
+    c->final_metric = MRFG_METRIC_CC;
+    c->omega_hz = 70;
+    c->df_coarse_hz = 60;
+    c->df_refine_hz = 3;
+    c->df_window_hz = 150;
+    c->plateau_eps = 1e-7;
+    c->heavy_noise_cc = 0.1;
+    c->fallback_coarse_hz = 30;
+    c->fallback_window_hz = 300;
+    c->n2d = 2;
+    c->t1t2_2d_steps_ms[0] = 200;
+    c->t1t2_2d_steps_ms[1] = 100;
+    c->n1d = 4;
+    c->t1t2_1d_steps_ms[0] = 100;
+    c->t1t2_1d_steps_ms[1] = 50;
+    c->t1t2_1d_steps_ms[2] = 20;
+    c->t1t2_1d_steps_ms[3] = 10;
+    c->final_2d_step_ms = 1;
+    c->init_t1_ms = 1000;
+    c->init_t2_ms = 500;
+    c->prior_window_t1_ms = 3000;
+    c->prior_window_t2_ms = 800;
+    c->prior_window_df_hz = 150;
+}
+
+int mrfg_create(const double* flip_deg, const double* phase_deg, const double* tr_ms,
+                const double* te_ms, int64_t n, int device, mrfg_ctx** out) {
+    return guard([&] {
+        MRFG_REQUIRE(out != nullptr, MRFG_E_INVALID, "mrfg_create: null output");
+        MRFG_REQUIRE(n > 0, MRFG_E_INVALID, "generate: empty schedule");
+        for (int64_t i = 0; i < n; ++i)
+            MRFG_REQUIRE(te_ms[i] >= 0 && te_ms[i] <= tr_ms[i], MRFG_E_INVALID,
+                         "BlochSimulator: schedule needs 0 <= te <= tr");
+        int ndev = 0;
+        MRFG_CUDA(cudaGetDeviceCount(&ndev));
+        MRFG_REQUIRE(device >= 0 && device < ndev, MRFG_E_CUDA, "mrfg_create: no such CUDA device");
+        cudaDeviceProp prop;
+        MRFG_CUDA(cudaGetDeviceProperties(&prop, device));
+        MRFG_REQUIRE(prop.major == 10, MRFG_E_CUDA,
+                     std::string("mrfg requires an sm_100 (Blackwell B200) device, found ") + prop.name);
+        auto* h = new mrfg_ctx();
+        Ctx& c = h->c;
+        c.device = device;
+        MRFG_CUDA(cudaSetDevice(device));
+        MRFG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        c.own_stream = true;
+        c.num_sms = prop.multiProcessorCount;
+        c.n = n;
+        c.flip_deg.assign(flip_deg, flip_deg + n);
+        c.phase_deg.assign(phase_deg, phase_deg + n);
+        c.tr_ms.assign(tr_ms, tr_ms + n);
+        c.te_ms.assign(te_ms, te_ms + n);
+        c.rf64.resize(9 * n);
+        c.te_s.resize(n);
+        c.rest_s.resize(n);
+        std::vector<float> rf32(12 * n, 0.f);
+        for (int64_t i = 0; i < n; ++i) {
+            // ScheduleEntry accessors (sequence.hpp:20-23), bloch.cpp:101-103
+            host_rf_matrix(flip_deg[i] * 0.017453292519943295, phase_deg[i] * 0.017453292519943295,
+                           &c.rf64[9 * i]);
+            c.te_s[i] = te_ms[i] * 1e-3;
+            c.rest_s[i] = tr_ms[i] * 1e-3 - te_ms[i] * 1e-3;
+            for (int k = 0; k < 9; ++k) rf32[12 * i + k] = static_cast<float>(c.rf64[9 * i + k]);
+        }
+        double inv[9];
+        host_rf_matrix(3.14159265358979323846, 0, inv);  // bloch.cpp:113
+        // kInvert * (0,0,1) = third column
+        std::memcpy(c.inv64, inv, sizeof inv);
+        c.rf64_d.ensure(sizeof(double) * 9 * n);
+        c.rf32_d.ensure(sizeof(float) * 12 * n);
+        MRFG_CUDA(cudaMemcpy(c.rf64_d.p, c.rf64.data(), sizeof(double) * 9 * n, cudaMemcpyHostToDevice));
+        MRFG_CUDA(cudaMemcpy(c.rf32_d.p, rf32.data(), sizeof(float) * 12 * n, cudaMemcpyHostToDevice));
+        *out = h;
+    });
+}
+
+int mrfg_destroy(mrfg_ctx* h) {
+    return guard([&] {
+        if (!h) return;
+        Ctx& c = h->c;
+        cudaSetDevice(c.device);
+        cudaStreamSynchronize(c.stream);
+        for (DevBuf* b : {&c.rf64_d, &c.rf32_d, &c.tab.e1f, &c.tab.e2f, &c.tab.phf, &c.tab.e1d,
+                          &c.tab.e2d, &c.tab.phd, &c.q64, &c.qprime, &c.best, &c.cand,
+                          &c.cand_count, &c.atoms_a, &c.inv2, &c.seed_a, &c.seed_inv2, &c.rerank,
+                          &c.params, &c.out64, &c.misc})
+            b->release();
+        if (c.own_stream) cudaStreamDestroy(c.stream);
+        delete h;
+    });
+}
+
+int64_t mrfg_length(const mrfg_ctx* h) { return h ? h->c.n : 0; }
+
+int mrfg_set_stream(mrfg_ctx* h, void* s) {
+    return guard([&] {
+        Ctx& c = h->c;
+        if (c.own_stream) MRFG_CUDA(cudaStreamDestroy(c.stream));
+        c.stream = static_cast<cudaStream_t>(s);
+        c.own_stream = false;
+    });
+}
+
+int mrfg_synchronize(mrfg_ctx* h) {
+    return guard([&] { MRFG_CUDA(cudaStreamSynchronize(h->c.stream)); });
+}
+
+int mrfg_simulate_dev(mrfg_ctx* h, const double* d_params, int64_t count, int precision,
+                      int normalize, double* d_out) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        if (count <= 0) return;
+        if (precision == 64)
+            launch_simulate64(c, d_params, count, normalize, d_out);
+        else
+            launch_simulate32(c, d_params, count, normalize, d_out);
+    });
+}
+
+int mrfg_simulate(mrfg_ctx* h, const double* params, int64_t count, int precision, int normalize,
+                  double* out) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        for (int64_t k = 0; k < count; ++k)
+            MRFG_REQUIRE(params[3 * k] > 0 && params[3 * k + 1] > 0, MRFG_E_INVALID,
+                         "simulate: T1 and T2 must be positive");  // bloch.cpp:109-110
+        if (count <= 0) return;
+        c.params.ensure(sizeof(double) * 3 * count);
+        c.out64.ensure(sizeof(double) * 2 * c.n * count);
+        MRFG_CUDA(cudaMemcpyAsync(c.params.p, params, sizeof(double) * 3 * count,
+                                  cudaMemcpyHostToDevice, c.stream));
+        if (precision == 64)
+            launch_simulate64(c, c.params.as<double>(), count, normalize, c.out64.as<double>());
+        else
+            launch_simulate32(c, c.params.as<double>(), count, normalize, c.out64.as<double>());
+        MRFG_CUDA(cudaMemcpyAsync(out, c.out64.p, sizeof(double) * 2 * c.n * count,
+                                  cudaMemcpyDeviceToHost, c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int mrfg_generate_dev(mrfg_ctx* h, const mrfg_grid* grid, int64_t first, int64_t count,
+                      int precision, float* d_out) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(first >= 0 && count >= 0 && first + count <= grid_total(*grid), MRFG_E_INVALID,
+                     "generate: flat range outside the grid");
+        const GridTables& t = ensure_tables(c, *grid, precision == 64);
+        launch_generate(c, t, first, count, precision, d_out);
+    });
+}
+
+int mrfg_generate(mrfg_ctx* h, const mrfg_grid* grid, int64_t first, int64_t count, int precision,
+                  float* out) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(first >= 0 && count >= 0 && first + count <= grid_total(*grid), MRFG_E_INVALID,
+                     "generate: flat range outside the grid");
+        const GridTables& t = ensure_tables(c, *grid, precision == 64);
+        const int64_t per = std::max<int64_t>(1, (int64_t(256) << 20) / (8 * c.n));
+        c.misc.ensure(sizeof(float) * 2 * c.n * std::min(per, std::max<int64_t>(count, 1)));
+        for (int64_t f = 0; f < count; f += per) {
+            int64_t k = std::min(per, count - f);
+            launch_generate(c, t, first + f, k, precision, c.misc.as<float>());
+            MRFG_CUDA(cudaMemcpyAsync(out + f * 2 * c.n, c.misc.p, sizeof(float) * 2 * c.n * k,
+                                      cudaMemcpyDeviceToHost, c.stream));
+            MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        }
+    });
+}
+
+int mrfg_bloch_norms_dev(mrfg_ctx* h, const mrfg_grid* grid, int64_t first, int64_t count,
+                         float* d_norm2) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        const GridTables& t = ensure_tables(c, *grid, false);
+        launch_bloch_norms(c, t, first, count, d_norm2);
+    });
+}
+
+int mrfg_scan_grid_dev(mrfg_ctx* h, const mrfg_grid* grid, int64_t fb, int64_t fe,
+                       const double* d_queries, int64_t nq, int metric, const mrfg_scan_opts* o,
+                       mrfg_match* d_out, mrfg_scan_stats* st) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        scan_dev(c, *grid, fb, fe, d_queries, nq, metric, o, d_out, st);
+    });
+}
+
+int mrfg_scan_grid(mrfg_ctx* h, const mrfg_grid* grid, int64_t fb, int64_t fe,
+                   const double* queries, int64_t nq, int metric, const mrfg_scan_opts* o,
+                   mrfg_match* out, mrfg_scan_stats* st) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(nq > 0, MRFG_E_INVALID, "scan_grid: no queries");
+        DevBuf raw, res;
+        raw.ensure(sizeof(double) * 2 * c.n * nq);
+        res.ensure(sizeof(mrfg_match) * nq);
+        try {
+            MRFG_CUDA(cudaMemcpyAsync(raw.p, queries, sizeof(double) * 2 * c.n * nq,
+                                      cudaMemcpyHostToDevice, c.stream));
+            scan_dev(c, *grid, fb, fe, raw.as<double>(), nq, metric, o, res.as<mrfg_match>(), st);
+            MRFG_CUDA(cudaMemcpyAsync(out, res.p, sizeof(mrfg_match) * nq, cudaMemcpyDeviceToHost,
+                                      c.stream));
+            MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        } catch (...) {
+            raw.release();
+            res.release();
+            throw;
+        }
+        raw.release();
+        res.release();
+    });
+}
+
+int mrfg_merge_matches_dev(mrfg_ctx* h, const mrfg_match* d_in, int nranks, int64_t nq,
+                           mrfg_match* d_out) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(nranks >= 1 && nq >= 0, MRFG_E_INVALID, "merge: bad shape");
+        if (nq) launch_merge(c, d_in, nranks, nq, d_out);
+    });
+}
+
+int mrfg_screen_scores(mrfg_ctx* h, const mrfg_grid* grid, int64_t first, int64_t count,
+                       const double* queries, int64_t nq, int metric, int use_simt, float* out) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(nq > 0 && count > 0 && first >= 0 && first + count <= grid_total(*grid),
+                     MRFG_E_INVALID, "screen_scores: bad shape");
+        const GridTables& t = ensure_tables(c, *grid, false);
+        const int64_t n = c.n, kp = k_pad_of(n), qrows = round_up(2 * nq, 256);
+        const int64_t rows = round_up(count, 128);
+        DevBuf raw, q64, qp, best, a, inv, cand, cnt;
+        raw.ensure(sizeof(double) * 2 * n * nq);
+        q64.ensure(sizeof(double) * 2 * n * nq);
+        qp.ensure(sizeof(__half) * qrows * kp);
+        best.ensure(sizeof(float) * nq + 64);
+        a.ensure(sizeof(__half) * rows * kp);
+        inv.ensure(sizeof(float) * rows);
+        const int64_t cap = count * nq;
+        cand.ensure(sizeof(CandRec) * cap);
+        cnt.ensure(16);
+        int* bad = reinterpret_cast<int*>(best.as<char>() + sizeof(float) * nq);
+        MRFG_CUDA(cudaMemcpyAsync(raw.p, queries, sizeof(double) * 2 * n * nq, cudaMemcpyHostToDevice, c.stream));
+        MRFG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+        MRFG_CUDA(cudaMemsetAsync(cnt.p, 0, 16, c.stream));
+        launch_prepare_queries(c, raw.as<double>(), nq, qrows, q64.as<double>(), qp.as<__half>(), bad);
+        fill(c, best.as<float>(), nq, -3.0f);
+        launch_bloch_operand(c, t, first, 1, first + count, rows, metric, a.as<__half>(), inv.as<float>());
+        MatchParams mp{};
+        mp.a = a.as<__half>();
+        mp.inv2 = inv.as<float>();
+        mp.b = qp.as<__half>();
+        mp.atoms = rows;
+        mp.q_rows = qrows;
+        mp.k_pad = kp;
+        mp.valid_atoms = count;
+        mp.nvox = nq;
+        mp.flat_base = 0;
+        mp.flat_stride = 1;
+        mp.best = best.as<float>();
+        mp.cand = cand.as<CandRec>();
+        mp.cand_count = cnt.as<unsigned long long>();
+        mp.cand_cap = cap;
+        mp.delta = 1e30f;  // every (atom, voxel) pair becomes a candidate
+        mp.metric = metric;
+        if (use_simt)
+            launch_match_simt(c, mp);
+        else
+            launch_match(c, mp);
+        unsigned long long got = 0;
+        MRFG_CUDA(cudaMemcpyAsync(&got, cnt.p, sizeof got, cudaMemcpyDeviceToHost, c.stream));
+        std::vector<CandRec> h_c(cap);
+        MRFG_CUDA(cudaMemcpyAsync(h_c.data(), cand.p, sizeof(CandRec) * cap, cudaMemcpyDeviceToHost, c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        MRFG_REQUIRE(got == static_cast<unsigned long long>(cap), MRFG_E_RUNTIME,
+                     "screen_scores: expected every pair to be screened in");
+        for (int64_t i = 0; i < nq * count; ++i) out[i] = std::nanf("");
+        for (const CandRec& r : h_c) out[r.flat * nq + r.voxel] = r.s;
+        for (DevBuf* b : {&raw, &q64, &qp, &best, &a, &inv, &cand, &cnt}) b->release();
+    });
+}
+
+int mrfg_cc_map(mrfg_ctx* h, const mrfg_grid* grid, const double* query, int64_t first,
+                int64_t count, float* out) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(first >= 0 && count >= 0 && first + count <= grid_total(*grid), MRFG_E_INVALID,
+                     "cc_map: flat range outside the grid");
+        const GridTables& t = ensure_tables(c, *grid, true);
+        const int64_t kp = k_pad_of(c.n);
+        DevBuf raw, q64, qp, flag, res;
+        raw.ensure(sizeof(double) * 2 * c.n);
+        q64.ensure(sizeof(double) * 2 * c.n);
+        qp.ensure(sizeof(__half) * 256 * kp);
+        flag.ensure(sizeof(int));
+        const int64_t per = int64_t(1) << 24;
+        res.ensure(sizeof(float) * std::min(per, std::max<int64_t>(count, 1)));
+        MRFG_CUDA(cudaMemcpyAsync(raw.p, query, sizeof(double) * 2 * c.n, cudaMemcpyHostToDevice, c.stream));
+        MRFG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), c.stream));
+        launch_prepare_queries(c, raw.as<double>(), 1, 256, q64.as<double>(), qp.as<__half>(),
+                               flag.as<int>());
+        int bad = 0;
+        MRFG_CUDA(cudaMemcpyAsync(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        MRFG_REQUIRE(!bad, MRFG_E_INVALID, "normalize: zero fingerprint");
+        for (int64_t f = 0; f < count; f += per) {
+            int64_t k = std::min(per, count - f);
+            launch_cc_map(c, t, q64.as<double>(), first + f, k, res.as<float>());
+            MRFG_CUDA(cudaMemcpyAsync(out + f, res.p, sizeof(float) * k, cudaMemcpyDeviceToHost, c.stream));
+            MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        }
+        for (DevBuf* b : {&raw, &q64, &qp, &flag, &res}) b->release();
+    });
+}
+
+int mrfg_quantify(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                  const double* fps, int64_t nvox, mrfg_quant* out) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(nvox >= 0, MRFG_E_INVALID, "quantify: negative voxel count");
+        if (nvox == 0) return;
+        DevBuf d_fps, d_out;
+        d_fps.ensure(sizeof(double) * 2 * c.n * nvox);
+        d_out.ensure(sizeof(mrfg_quant) * nvox);
+        MRFG_CUDA(cudaMemcpyAsync(d_fps.p, fps, sizeof(double) * 2 * c.n * nvox,
+                                  cudaMemcpyHostToDevice, c.stream));
+        run_quantify(c, *lattice, *cfg, d_fps.as<double>(), nvox, nullptr, nullptr,
+                     d_out.as<mrfg_quant>());
+        MRFG_CUDA(cudaMemcpyAsync(out, d_out.p, sizeof(mrfg_quant) * nvox, cudaMemcpyDeviceToHost,
+                                  c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        d_fps.release();
+        d_out.release();
+    });
+}
+
+int mrfg_quantify_slice(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                        const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
+                        mrfg_quant* out, double* seconds) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(nx > 0 && ny > 0, MRFG_E_INVALID,
+                     "quantify_slice: inconsistent raster dimensions");  // zoom.cpp:561-562
+        auto t0 = std::chrono::steady_clock::now();
+        const int64_t nv = static_cast<int64_t>(nx) * ny;
+        std::memset(out, 0, sizeof(mrfg_quant) * nv);
+        std::vector<int64_t> idx;
+        for (int64_t i = 0; i < nv; ++i)
+            if (mask[i]) idx.push_back(i);
+        const int64_t m = static_cast<int64_t>(idx.size());
+        if (m > 0) {
+            std::vector<double> packed(2 * c.n * m);
+            for (int64_t k = 0; k < m; ++k)
+                std::memcpy(&packed[2 * c.n * k], fps + 2 * c.n * idx[k], sizeof(double) * 2 * c.n);
+            std::vector<mrfg_quant> res(m);
+            MRFG_REQUIRE(use_prior == 0, MRFG_E_INVALID,
+                         "quantify_slice: neighbour-prior mode not available in this build");
+            int rc = mrfg_quantify(h, lattice, cfg, packed.data(), m, res.data());
+            if (rc) throw Error{rc, g_err};
+            for (int64_t k = 0; k < m; ++k) out[idx[k]] = res[k];
+        }
+        if (seconds)
+            *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+}  // extern "C"

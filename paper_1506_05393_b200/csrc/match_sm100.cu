@@ -1,0 +1,437 @@
+// match_sm100.cu -- K2: fused complex-correlation screening GEMM on tcgen05.
+//
+// Replaces the scan loop of scan_grid / brute_force_search (reference
+// proj/src/dictionary.cpp:283-299, 241-255; score cc_against_entry :117-127).
+// The complex correlation of unit query q_v with atom d_a,
+//     z = sum_j q_vj conj(d_aj),
+// is a real GEMM over K = 2N: atoms are stored as interleaved (re, im) rows
+// (the reference's dictionary layout) and each voxel contributes two rows
+//     row 2v   = ( qr_0,  qi_0, qr_1,  qi_1, ...)  -> Re z
+//     row 2v+1 = ( qi_0, -qr_0, qi_1, -qr_1, ...)  -> Im z
+// so S = A (atoms x 2N) . B^T (2N x 2V) lands Re/Im of each voxel in adjacent
+// accumulator columns.  fp16 operands, FP32 accumulation in TMEM.
+//
+// Kernel shape: persistent, one CTA per SM, 256 threads:
+//   warp 0 : TMA producer (A tile 128x64, B tile 256x64, SWIZZLE_128B, 4 stages)
+//   warp 1 : single-thread tcgen05.mma issuer, M=128 N=256 K=16, cta_group::1
+//   warp 2 : TMEM allocator (512 columns = two 128x256 FP32 accumulators)
+//   warps 4-7 : epilogue -- tcgen05.ld of its 32 TMEM lanes (one atom per
+//              thread), score = |z|^2 / |d|^2 (approx CC^2), compare with the
+//              per-voxel threshold (running max - delta)^2 and append the
+//              rare survivors to a global candidate list for the exact
+//              FP64 re-rank (rerank.cu).  The epilogue of tile i overlaps
+//              the MMAs of tile i+1 (double-buffered TMEM).
+#include <cuda.h>
+
+#include "mrfg_internal.cuh"
+
+namespace mrfg {
+namespace {
+
+constexpr int BM = 128;  // atoms per tile (TMEM lanes)
+constexpr int BN = 256;  // query rows per tile = 128 voxels
+constexpr int BK = 64;   // fp16 elements per 128-byte swizzle row
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int NTHREADS = 256;
+
+struct alignas(1024) Smem {
+    uint8_t a[STAGES][A_BYTES];
+    uint8_t b[STAGES][B_BYTES];
+    uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+    uint32_t tmem_base;
+    float thr[2][128];
+    float bst[2][128];
+};
+constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
+
+struct Dev {
+    const float* inv2;
+    int64_t n_at, n_vt, nkb, last_sub;
+    int64_t valid_atoms, nvox, flat_base, flat_stride;
+    float* best;
+    CandRec* cand;
+    unsigned long long* cand_count;
+    int64_t cand_cap;
+    float delta;
+    int metric;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* dst, uint64_t* bar,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// UMMA shared-memory descriptor, K-major SWIZZLE_128B canonical layout:
+// rows of 128 B, 8-row core groups 1024 B apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+    d |= static_cast<uint64_t>(1) << 16;   // LBO (unused for swizzled K-major)
+    d |= static_cast<uint64_t>(64) << 32;  // SBO = 1024 B
+    d |= static_cast<uint64_t>(1) << 46;   // descriptor version (sm_100)
+    d |= static_cast<uint64_t>(2) << 61;   // SWIZZLE_128B
+    return d;
+}
+// Instruction descriptor: D=F32, A=B=F16, both K-major, N=256, M=128.
+constexpr uint32_t IDESC = (1u << 4) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                           (static_cast<uint32_t>(BM >> 4) << 24);
+
+#define TMEM_LD_X64(taddr, r)                                                                 \
+    asm volatile(                                                                             \
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,"  \
+        "%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,"  \
+        "%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"                                              \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),  \
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),           \
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),        \
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),        \
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),        \
+          "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]),        \
+          "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]),        \
+          "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),        \
+          "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]),        \
+          "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]),        \
+          "=r"(r[61]), "=r"(r[62]), "=r"(r[63])                                                \
+        : "r"(taddr))
+
+__device__ __forceinline__ void atomic_max_float(float* addr, float v) {
+    if (v >= 0.f)
+        atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
+    else
+        atomicMin(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
+}
+
+__device__ __forceinline__ float screen_score(float re, float im, float inv, int metric) {
+    // metric cc: |z|^2/|d|^2 (squared CC); euclidean: Re z/|d| (monotone in
+    // -|q-d| for unit vectors).
+    return metric == MRFG_METRIC_CC ? (re * re + im * im) * inv : re * inv;
+}
+__device__ __forceinline__ float threshold_of(float best, float delta, int metric) {
+    float t = best - delta;
+    if (metric == MRFG_METRIC_CC) return t > 0.f ? t * t : 0.f;
+    return t;
+}
+__device__ __forceinline__ float unsquare(float s, int metric) {
+    return metric == MRFG_METRIC_CC ? sqrtf(s) : s;
+}
+
+__device__ __forceinline__ void push_candidate(const Dev& p, int64_t v, int64_t atom, float s) {
+    if (p.cand != nullptr) {
+        unsigned long long idx = atomicAdd(p.cand_count, 1ull);
+        if (idx < static_cast<unsigned long long>(p.cand_cap)) {
+            CandRec rec;
+            rec.voxel = static_cast<uint32_t>(v);
+            rec.s = s;
+            rec.flat = p.flat_base + atom * p.flat_stride;
+            p.cand[idx] = rec;
+        }
+    }
+}
+
+__device__ __noinline__ void record_hit(const Dev& p, float bst, int64_t v, int64_t atom, float sc) {
+    push_candidate(p, v, atom, sc);
+    const float su = unsquare(sc, p.metric);
+    if (su > bst) atomic_max_float(p.best + v, su);
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_match_sm100(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                  Dev p) {
+    extern __shared__ uint8_t smem_raw[];
+    Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                       ~static_cast<uintptr_t>(1023));
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t n_tiles = p.n_at * p.n_vt;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&s.full[i], 1);
+            mbar_init(&s.empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s.tfull[i], 1);
+            mbar_init(&s.tempty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s.tmem_base)),
+                     "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s.tmem_base;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                const int at = static_cast<int>(t / p.n_vt), vt = static_cast<int>(t % p.n_vt);
+                for (int kb = 0; kb < p.nkb; ++kb) {
+                    mbar_wait(&s.empty[stage], phase ^ 1);
+                    mbar_expect_tx(&s.full[stage], A_BYTES + B_BYTES);
+                    tma_load_2d(&tma_a, s.a[stage], &s.full[stage], kb * BK, at * BM);
+                    tma_load_2d(&tma_b, s.b[stage], &s.full[stage], kb * BK, vt * BN);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + static_cast<uint32_t>(acc * BN);
+                for (int kb = 0; kb < p.nkb; ++kb) {
+                    mbar_wait(&s.full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(s.a[stage]), b0 = smem_u32(s.b[stage]);
+                    const int nsub = kb == p.nkb - 1 ? static_cast<int>(p.last_sub) : BK / 16;
+                    for (int k = 0; k < nsub; ++k) {
+                        tc_mma_f16(d, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(b0 + 32 * k), IDESC,
+                                   (kb | k) != 0);
+                    }
+                    tc_commit(&s.empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit(&s.tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ epilogue
+        const int ew = warp - 4;  // == warp % 4: TMEM lane quarter
+        const int row = ew * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            const int64_t at = t / p.n_vt, vt = t % p.n_vt;
+            {
+                const int64_t v = vt * 128 + row;
+                float b = v < p.nvox ? __ldcg(p.best + v) : 1e30f;
+                // padding voxel columns can never screen in
+                s.thr[acc][row] = v < p.nvox ? threshold_of(b, p.delta, p.metric) : __int_as_float(0x7f800000);
+                s.bst[acc][row] = b;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            mbar_wait(&s.tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t atom = at * BM + row;
+            const bool avalid = atom < p.valid_atoms;
+            const float inv = __ldg(p.inv2 + atom);
+            const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) +
+                                   static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+            for (int q = 0; q < 4; ++q) {
+                uint32_t r[64];
+                TMEM_LD_X64(tbase + q * 64, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                float sc[32];
+                uint32_t hits = 0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    sc[i] = screen_score(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]), inv,
+                                         p.metric);
+                    hits |= (sc[i] >= s.thr[acc][q * 32 + i] ? 1u : 0u) << i;
+                }
+                if (!avalid) hits = 0;
+                if (__any_sync(0xffffffffu, hits != 0)) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if ((hits >> i) & 1u) record_hit(p, s.bst[acc][q * 32 + i], vt * 128 + q * 32 + i, atom, sc[i]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512)
+                     : "memory");
+    }
+}
+
+// CUDA-core version of the same fused screening (tests: validates the
+// tcgen05 descriptors/layouts against identical fp16 operands).
+__global__ void k_match_simt(const __half* __restrict__ a, const __half* __restrict__ b,
+                             int64_t k_pad, Dev p, int64_t atoms, float* __restrict__ debug) {
+    int64_t atom = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    int64_t v = blockIdx.y;
+    if (atom >= atoms || v >= p.nvox) return;
+    float re = 0.f, im = 0.f;
+    for (int64_t k = 0; k < k_pad; ++k) {
+        float x = __half2float(a[atom * k_pad + k]);
+        re = fmaf(x, __half2float(b[(2 * v) * k_pad + k]), re);
+        im = fmaf(x, __half2float(b[(2 * v + 1) * k_pad + k]), im);
+    }
+    float sc = screen_score(re, im, p.inv2[atom], p.metric);
+    if (debug) debug[atom * p.nvox + v] = sc;
+    if (atom >= p.valid_atoms) return;
+    float b0 = __ldcg(p.best + v);
+    if (sc >= threshold_of(b0, p.delta, p.metric)) {
+        push_candidate(p, v, atom, sc);
+        atomic_max_float(p.best + v, unsquare(sc, p.metric));
+    }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encoder(Ctx& c) {
+    if (!c.encode_fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        MRFG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        MRFG_REQUIRE(fn != nullptr && q == cudaDriverEntryPointSuccess, MRFG_E_CUDA,
+                     "cuTensorMapEncodeTiled unavailable");
+        c.encode_fn = fn;
+    }
+    return reinterpret_cast<EncodeTiledFn>(c.encode_fn);
+}
+
+CUtensorMap make_map(Ctx& c, const __half* base, int64_t rows, int64_t k_pad, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(k_pad), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(k_pad * 2)};
+    cuuint32_t box[2] = {BK, static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = get_encoder(c)(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base),
+                                dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    MRFG_REQUIRE(r == CUDA_SUCCESS, MRFG_E_CUDA, "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+Dev dev_of(const MatchParams& p, int64_t k_valid) {
+    Dev d;
+    d.inv2 = p.inv2;
+    d.n_at = p.atoms / BM;
+    d.n_vt = p.q_rows / BN;
+    d.nkb = p.k_pad / BK;
+    int64_t last = k_valid - (d.nkb - 1) * BK;  // valid elements of the last K block
+    d.last_sub = (last + 15) / 16;
+    if (d.last_sub < 1) d.last_sub = 1;
+    d.valid_atoms = p.valid_atoms;
+    d.nvox = p.nvox;
+    d.flat_base = p.flat_base;
+    d.flat_stride = p.flat_stride;
+    d.best = p.best;
+    d.cand = p.cand;
+    d.cand_count = p.cand_count;
+    d.cand_cap = p.cand_cap;
+    d.delta = p.delta;
+    d.metric = p.metric;
+    return d;
+}
+
+}  // namespace
+
+void launch_match(Ctx& c, const MatchParams& p) {
+    MRFG_REQUIRE(p.atoms % BM == 0 && p.q_rows % BN == 0 && p.k_pad % BK == 0, MRFG_E_INVALID,
+                 "match: operand shapes not tile aligned");
+    static bool attr_set = false;
+    if (!attr_set) {
+        MRFG_CUDA(cudaFuncSetAttribute(k_match_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(SMEM_BYTES)));
+        attr_set = true;
+    }
+    CUtensorMap ma = make_map(c, p.a, p.atoms, p.k_pad, BM);
+    CUtensorMap mb = make_map(c, p.b, p.q_rows, p.k_pad, BN);
+    Dev d = dev_of(p, 2 * c.n);
+    int64_t tiles = d.n_at * d.n_vt;
+    int grid = static_cast<int>(tiles < c.num_sms ? tiles : c.num_sms);
+    k_match_sm100<<<grid, NTHREADS, SMEM_BYTES, c.stream>>>(ma, mb, d);
+    MRFG_CUDA(cudaGetLastError());
+}
+
+void launch_match_simt(Ctx& c, const MatchParams& p) {
+    Dev d = dev_of(p, 2 * c.n);
+    dim3 grid(static_cast<unsigned>((p.atoms + 127) / 128), static_cast<unsigned>(p.nvox));
+    k_match_simt<<<grid, 128, 0, c.stream>>>(p.a, p.b, p.k_pad, d, p.atoms, p.debug_scores);
+    MRFG_CUDA(cudaGetLastError());
+}
+
+}  // namespace mrfg

@@ -1,0 +1,153 @@
+// mrfg_internal.cuh -- shared declarations of the sm_100a DGS path.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "mrfg.h"
+
+namespace mrfg {
+
+// ------------------------------------------------------------------ errors
+struct Error {
+    int code;
+    std::string msg;
+};
+void set_error(const std::string& msg);
+#define MRFG_CUDA(call)                                                                  \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            throw ::mrfg::Error{MRFG_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+    } while (0)
+#define MRFG_REQUIRE(cond, code, msg)                          \
+    do {                                                       \
+        if (!(cond)) throw ::mrfg::Error{(code), (msg)};       \
+    } while (0)
+
+// ---------------------------------------------------------- device buffers
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t n) {
+        if (n <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        MRFG_CUDA(cudaMalloc(&p, n));
+        bytes = n;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// Per-(context, grid) transcendental tables.  FP64 values are computed on
+// the HOST with the same libm calls and operand order as the reference
+// (bloch.cpp:17-21), so the FP64 device recursion reproduces the reference
+// bit-for-bit; the FP32 tables are those values rounded.
+struct GridTables {
+    mrfg_grid grid{};
+    bool valid = false;
+    // FP32: e1[j*n1+i] = (E1te, 1-E1te, E1rest, 1-E1rest); e2[j*n2+i] = (E2te, E2rest);
+    //       ph[j*ndf+i] = (cos te, sin te, cos rest, sin rest)
+    DevBuf e1f, e2f, phf;
+    // FP64, same index order: e1d[(j*n1+i)*2 + {0,1}] = (E1te, E1rest); e2d likewise;
+    // phd[(j*ndf+i)*4 + {0..3}] = (cos te, sin te, cos rest, sin rest)
+    DevBuf e1d, e2d, phd;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 148;
+    int64_t n = 0;  // schedule length
+    std::vector<double> flip_deg, phase_deg, tr_ms, te_ms;
+    std::vector<double> rf64;       // n x 9 (bloch.cpp:101)
+    std::vector<double> te_s, rest_s;
+    double inv64[9];                // kInvert (bloch.cpp:113)
+    DevBuf rf64_d, rf32_d;          // n x 9 doubles, n x 12 floats (padded)
+    GridTables tab;                 // cache for the last grid
+    // scratch
+    DevBuf q64, qprime, best, cand, cand_count, atoms_a, inv2, seed_a, seed_inv2, rerank,
+        params, out64, misc;
+    cudaEvent_t ev[8];
+    // tensor-map encoder (driver entry point)
+    void* encode_fn = nullptr;
+};
+
+// ------------------------------------------------------------ host helpers
+void host_rf_matrix(double alpha, double phi, double out[9]);  // bloch.cpp:63-66
+const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool need64);
+inline int64_t grid_total(const mrfg_grid& g) {
+    return g.t1_ms.count * g.t2_ms.count * g.df_hz.count;
+}
+inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+inline int64_t k_pad_of(int64_t n) { return round_up(2 * n, 64); }  // fp16 elements per GEMM row
+
+// --------------------------------------------------------------- launchers
+// K1 (bloch.cu)
+void launch_simulate64(Ctx& c, const double* d_params, int64_t count, int normalize, double* d_out);
+void launch_simulate32(Ctx& c, const double* d_params, int64_t count, int normalize, double* d_out);
+void launch_generate(Ctx& c, const GridTables& t, int64_t first, int64_t count, int precision,
+                     float* d_out);
+// Rows r in [0, rows) simulate flat first + r*stride (zero rows past valid_end);
+// inv2 gets 1/|s|^2 (metric cc) or 1/|s| (euclidean).
+void launch_bloch_operand(Ctx& c, const GridTables& t, int64_t first, int64_t stride,
+                          int64_t valid_end, int64_t rows, int metric, __half* d_a,
+                          float* d_inv2);
+void launch_bloch_norms(Ctx& c, const GridTables& t, int64_t first, int64_t count, float* d_norm2);
+
+// K2 (match_sm100.cu)
+struct CandRec {
+    uint32_t voxel;
+    float s;       // screening score (CC or Re-part units)
+    int64_t flat;
+};
+struct MatchParams {
+    const __half* a;    // atoms x k_pad (fp16, K-major)
+    const float* inv2;  // atoms
+    const __half* b;    // q_rows x k_pad (fp16, K-major): rows 2v (re), 2v+1 (im)
+    int64_t atoms;      // multiple of 128
+    int64_t q_rows;     // multiple of 256
+    int64_t k_pad;      // multiple of 64
+    int64_t valid_atoms;
+    int64_t nvox;
+    int64_t flat_base, flat_stride;  // global flat of local atom r = flat_base + r*flat_stride
+    float* best;        // nvox running max (screening units)
+    CandRec* cand;      // may be null (seed pass)
+    unsigned long long* cand_count;
+    int64_t cand_cap;
+    float delta;
+    int metric;
+    float* debug_scores;  // optional dense atoms x nvox output (tests)
+};
+void launch_match(Ctx& c, const MatchParams& p);
+// CUDA-core reference of the same fused screening (tests only, small sizes).
+void launch_match_simt(Ctx& c, const MatchParams& p);
+
+// K3 (rerank.cu)
+void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qrows, double* d_q64,
+                            __half* d_qprime, int* d_bad);
+int64_t rerank_and_select(Ctx& c, const GridTables& t, const double* d_q64, int64_t nq,
+                          int metric, const float* d_best, float delta, CandRec* d_cand,
+                          int64_t ncand, mrfg_match* d_out);
+void launch_merge(Ctx& c, const mrfg_match* d_in, int nranks, int64_t nq, mrfg_match* d_out);
+void launch_cc_map(Ctx& c, const GridTables& t, const double* d_q64, int64_t first, int64_t count,
+                   float* d_out);
+
+// K5 (zoom.cu)
+void run_quantify(Ctx& c, const mrfg_grid& lattice, const mrfg_zoom_config& cfg,
+                  const double* d_fps, int64_t nvox, const int64_t* h_bounds /* nvox x 6 or null */,
+                  const double* h_init /* nvox x 2 or null */, mrfg_quant* d_out);
+
+}  // namespace mrfg

@@ -1,0 +1,267 @@
+// rerank.cu -- K3: exact re-rank of screened candidates, per-voxel argmax,
+// cross-GPU merge (C1), cc_map and query preparation.
+//
+// Exactness: the reference scores a unit FP64 query against FP32-quantized
+// unit FP64 fingerprints (dictionary.cpp:37-53, 117-143, 145-150).  The
+// re-rank recomputes each surviving candidate through that very pipeline in
+// FP64 (sim64.cuh, host-libm tables), so its scores are bit-identical to the
+// reference's and the argmax -- including the lowest-flat tie rule of
+// dictionary.cpp:291-294 -- is the reference's.
+#include <cmath>
+
+#include "mrfg_internal.cuh"
+#include "sim64.cuh"
+
+namespace mrfg {
+namespace {
+
+// prep_query (dictionary.cpp:145-150) -> normalize (fingerprint.cpp:28-37),
+// then the fp16 screening rows (see match_sm100.cu).
+__global__ void k_prepare_queries(const double* __restrict__ raw, int n, int64_t nq,
+                                  int64_t k_pad, double* __restrict__ q64,
+                                  __half* __restrict__ qprime, int* __restrict__ bad) {
+    int64_t v = blockIdx.x;
+    if (v >= nq) return;
+    __shared__ double s_inv;
+    const double* src = raw + v * 2 * n;
+    if (threadIdx.x == 0) {
+        double acc = 0;  // sequential, the reference's summation order
+        for (int j = 0; j < n; ++j)
+            acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(src[2 * j], src[2 * j]),
+                                           __dmul_rn(src[2 * j + 1], src[2 * j + 1])));
+        double nn = sqrt(acc);
+        if (nn == 0) atomicExch(bad, 1);
+        s_inv = nn == 0 ? 0.0 : 1.0 / nn;
+    }
+    __syncthreads();
+    const double inv = s_inv;
+    __half* re_row = qprime + (2 * v) * k_pad;
+    __half* im_row = qprime + (2 * v + 1) * k_pad;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        double qr = __dmul_rn(src[2 * j], inv), qi = __dmul_rn(src[2 * j + 1], inv);
+        q64[v * 2 * n + 2 * j] = qr;
+        q64[v * 2 * n + 2 * j + 1] = qi;
+        re_row[2 * j] = __double2half(qr);
+        re_row[2 * j + 1] = __double2half(qi);
+        im_row[2 * j] = __double2half(qi);
+        im_row[2 * j + 1] = __double2half(-qr);
+    }
+}
+
+__device__ __forceinline__ float threshold_final(float best, float delta, int metric) {
+    float t = best - delta;
+    if (metric == MRFG_METRIC_CC) return t > 0.f ? t * t : 0.f;
+    return t;
+}
+
+__global__ void k_filter(const CandRec* __restrict__ cand, int64_t n, const float* __restrict__ best,
+                         float delta, int metric, int64_t* __restrict__ list,
+                         unsigned long long* __restrict__ count) {
+    int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    CandRec r = cand[i];
+    if (r.s >= threshold_final(best[r.voxel], delta, metric)) {
+        unsigned long long k = atomicAdd(count, 1ull);
+        list[k] = i;
+    }
+}
+
+__device__ __forceinline__ unsigned long long order_key(double x) {
+    long long b = __double_as_longlong(x);
+    return b >= 0 ? static_cast<unsigned long long>(b) ^ 0x8000000000000000ull
+                  : ~static_cast<unsigned long long>(b);
+}
+__device__ __forceinline__ double key_value(unsigned long long k) {
+    long long b = (k & 0x8000000000000000ull) ? static_cast<long long>(k ^ 0x8000000000000000ull)
+                                              : static_cast<long long>(~k);
+    return __longlong_as_double(b);
+}
+
+struct Tab64 {
+    const double *rf, *e1d, *e2d, *phd;
+    double inv0[3];
+    int n;
+    Lattice L;
+};
+
+// Exact reference score of lattice atom `flat` against unit FP64 query q.
+__device__ double exact_score(const Tab64& T, const double* __restrict__ q, int64_t flat,
+                              int metric) {
+    int i1, i2, idf;
+    unflatten(flat, T.L, i1, i2, idf);
+    double acc = sim64_lattice<0>(T.rf, T.e1d, T.e2d, T.phd, T.inv0, T.n, T.L, i1, i2, idf, 0.0,
+                                  nullptr);
+    const double inv = 1.0 / sqrt(acc);
+    // second pass: float entries streamed straight into the score
+    double x = T.inv0[0], y = T.inv0[1], z = T.inv0[2];
+    double re = 0.0, im = 0.0, dd = 0.0;
+    for (int j = 0; j < T.n; ++j) {
+        rf_apply64(T.rf + 9 * j, x, y, z);
+        const double* E1 = T.e1d + (static_cast<int64_t>(j) * T.L.n1 + i1) * 2;
+        const double* E2 = T.e2d + (static_cast<int64_t>(j) * T.L.n2 + i2) * 2;
+        const double* P = T.phd + (static_cast<int64_t>(j) * T.L.ndf + idf) * 4;
+        relax64(x, y, z, __ldg(E1), __ldg(E2), __ldg(P), __ldg(P + 1));
+        const double er = static_cast<double>(__double2float_rn(__dmul_rn(x, inv)));
+        const double ei = static_cast<double>(__double2float_rn(__dmul_rn(y, inv)));
+        const double qr = q[2 * j], qi = q[2 * j + 1];
+        if (metric == MRFG_METRIC_CC) {
+            // dictionary.cpp:121-124
+            re = __dadd_rn(re, __dadd_rn(__dmul_rn(qr, er), __dmul_rn(qi, ei)));
+            im = __dadd_rn(im, __dsub_rn(__dmul_rn(qi, er), __dmul_rn(qr, ei)));
+        } else {
+            // dictionary.cpp:133-136
+            const double dr = __dsub_rn(qr, er), di = __dsub_rn(qi, ei);
+            dd = __dadd_rn(dd, __dadd_rn(__dmul_rn(dr, dr), __dmul_rn(di, di)));
+        }
+        relax64(x, y, z, __ldg(E1 + 1), __ldg(E2 + 1), __ldg(P + 2), __ldg(P + 3));
+    }
+    if (metric == MRFG_METRIC_CC) {
+        double v = sqrt(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
+        return v < 1.0 ? v : 1.0;  // dictionary.cpp:126
+    }
+    return -sqrt(dd);
+}
+
+__global__ void k_rerank(Tab64 T, const double* __restrict__ q64, const CandRec* __restrict__ cand,
+                         const int64_t* __restrict__ list, int64_t n, int metric,
+                         double* __restrict__ score, unsigned long long* __restrict__ vkey) {
+    int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= n) return;
+    const CandRec r = cand[list[k]];
+    const double sc = exact_score(T, q64 + static_cast<int64_t>(r.voxel) * 2 * T.n, r.flat, metric);
+    score[k] = sc;
+    atomicMax(vkey + r.voxel, order_key(sc));
+}
+
+__global__ void k_select_flat(const CandRec* __restrict__ cand, const int64_t* __restrict__ list,
+                              int64_t n, const double* __restrict__ score,
+                              const unsigned long long* __restrict__ vkey,
+                              unsigned long long* __restrict__ vflat) {
+    int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= n) return;
+    const CandRec r = cand[list[k]];
+    if (order_key(score[k]) == vkey[r.voxel])
+        atomicMin(vflat + r.voxel, static_cast<unsigned long long>(r.flat));
+}
+
+__global__ void k_write_matches(const unsigned long long* __restrict__ vkey,
+                                const unsigned long long* __restrict__ vflat, int64_t nq,
+                                mrfg_match* __restrict__ out, int* __restrict__ missing) {
+    int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (v >= nq) return;
+    if (vkey[v] == 0ull) {
+        atomicExch(missing, 1);
+        out[v].flat = -1;
+        out[v].score = -1e300;
+        return;
+    }
+    out[v].flat = static_cast<int64_t>(vflat[v]);
+    out[v].score = key_value(vkey[v]);
+}
+
+__global__ void k_merge(const mrfg_match* __restrict__ in, int nranks, int64_t nq,
+                        mrfg_match* __restrict__ out) {
+    int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (v >= nq) return;
+    mrfg_match b = in[v];
+    for (int r = 1; r < nranks; ++r) {
+        mrfg_match m = in[static_cast<int64_t>(r) * nq + v];
+        if (m.flat < 0) continue;
+        if (b.flat < 0 || m.score > b.score || (m.score == b.score && m.flat < b.flat)) b = m;
+    }
+    out[v] = b;
+}
+
+__global__ void k_cc_map(Tab64 T, const double* __restrict__ q, int64_t first, int64_t count,
+                         float* __restrict__ out) {
+    int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= count) return;
+    out[k] = static_cast<float>(exact_score(T, q, first + k, MRFG_METRIC_CC));  // dictionary.cpp:325-327
+}
+
+Tab64 tab64_of(Ctx& c, const GridTables& t) {
+    Tab64 T;
+    T.rf = c.rf64_d.as<double>();
+    T.e1d = t.e1d.as<double>();
+    T.e2d = t.e2d.as<double>();
+    T.phd = t.phd.as<double>();
+    T.inv0[0] = c.inv64[2];
+    T.inv0[1] = c.inv64[5];
+    T.inv0[2] = c.inv64[8];
+    T.n = static_cast<int>(c.n);
+    T.L = {t.grid.t1_ms.count, t.grid.t2_ms.count, t.grid.df_hz.count};
+    return T;
+}
+
+}  // namespace
+
+void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qrows, double* d_q64,
+                            __half* d_qprime, int* d_bad) {
+    const int64_t kp = k_pad_of(c.n);
+    MRFG_CUDA(cudaMemsetAsync(d_qprime, 0, sizeof(__half) * qrows * kp, c.stream));
+    k_prepare_queries<<<nq, 128, 0, c.stream>>>(d_raw, static_cast<int>(c.n), nq, kp, d_q64, d_qprime,
+                                                d_bad);
+    MRFG_CUDA(cudaGetLastError());
+}
+
+// Returns the number of re-ranked candidates; throws when a voxel ends
+// without any (cannot happen unless the candidate buffer overflowed).
+int64_t rerank_and_select(Ctx& c, const GridTables& t, const double* d_q64, int64_t nq,
+                          int metric, const float* d_best, float delta, CandRec* d_cand,
+                          int64_t ncand, mrfg_match* d_out) {
+    // scratch layout: list (ncand i64) | score (ncand f64) | vkey (nq u64) |
+    //                 vflat (nq u64) | counters
+    size_t need = sizeof(int64_t) * ncand + sizeof(double) * ncand + 16 * nq + 64;
+    c.rerank.ensure(need);
+    char* base = c.rerank.as<char>();
+    int64_t* list = reinterpret_cast<int64_t*>(base);
+    double* score = reinterpret_cast<double*>(base + sizeof(int64_t) * ncand);
+    unsigned long long* vkey =
+        reinterpret_cast<unsigned long long*>(base + (sizeof(int64_t) + sizeof(double)) * ncand);
+    unsigned long long* vflat = vkey + nq;
+    unsigned long long* cnt = vflat + nq;
+    int* missing = reinterpret_cast<int*>(cnt + 1);
+    MRFG_CUDA(cudaMemsetAsync(vkey, 0, sizeof(unsigned long long) * nq, c.stream));
+    MRFG_CUDA(cudaMemsetAsync(vflat, 0xFF, sizeof(unsigned long long) * nq, c.stream));
+    MRFG_CUDA(cudaMemsetAsync(cnt, 0, 16, c.stream));
+    const int bs = 256;
+    if (ncand > 0)
+        k_filter<<<(ncand + bs - 1) / bs, bs, 0, c.stream>>>(d_cand, ncand, d_best, delta, metric,
+                                                             list, cnt);
+    MRFG_CUDA(cudaGetLastError());
+    unsigned long long nsel = 0;
+    MRFG_CUDA(cudaMemcpyAsync(&nsel, cnt, sizeof nsel, cudaMemcpyDeviceToHost, c.stream));
+    MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    Tab64 T = tab64_of(c, t);
+    const int rb = 64;
+    if (nsel > 0) {
+        k_rerank<<<(nsel + rb - 1) / rb, rb, 0, c.stream>>>(T, d_q64, d_cand, list, nsel, metric,
+                                                            score, vkey);
+        MRFG_CUDA(cudaGetLastError());
+        k_select_flat<<<(nsel + bs - 1) / bs, bs, 0, c.stream>>>(d_cand, list, nsel, score, vkey,
+                                                                 vflat);
+        MRFG_CUDA(cudaGetLastError());
+    }
+    k_write_matches<<<(nq + bs - 1) / bs, bs, 0, c.stream>>>(vkey, vflat, nq, d_out, missing);
+    MRFG_CUDA(cudaGetLastError());
+    int h_missing = 0;
+    MRFG_CUDA(cudaMemcpyAsync(&h_missing, missing, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    MRFG_REQUIRE(!h_missing, MRFG_E_RUNTIME, "scan: a query ended without candidates");
+    return static_cast<int64_t>(nsel);
+}
+
+void launch_merge(Ctx& c, const mrfg_match* d_in, int nranks, int64_t nq, mrfg_match* d_out) {
+    const int bs = 256;
+    k_merge<<<(nq + bs - 1) / bs, bs, 0, c.stream>>>(d_in, nranks, nq, d_out);
+    MRFG_CUDA(cudaGetLastError());
+}
+
+void launch_cc_map(Ctx& c, const GridTables& t, const double* d_q64, int64_t first, int64_t count,
+                   float* d_out) {
+    const int bs = 64;
+    k_cc_map<<<(count + bs - 1) / bs, bs, 0, c.stream>>>(tab64_of(c, t), d_q64, first, count, d_out);
+    MRFG_CUDA(cudaGetLastError());
+}
+
+}  // namespace mrfg

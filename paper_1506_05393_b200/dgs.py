@@ -1,0 +1,315 @@
+"""Host-side mirror of the reference's library interface for the DGS path.
+
+Same names, argument meaning and error behaviour as the reference C++ API in
+/root/reference/proj/include/mrf (sequence.hpp, bloch.hpp, dictionary.hpp,
+zoom.hpp), over the C ABI of include/mrfg.h:
+
+=========================  ===============================================
+reference                  here
+=========================  ===============================================
+Schedule / build_schedule  Schedule, reference_schedule, baseline_schedule
+grid_from_ranges           grid_from_ranges (endpoint-exclusive) / grid()
+BlochSimulator::simulate   Context.simulate (precision 64 or 32)
+generate                   Context.generate
+scan_grid                  Context.scan_grid (+ scan_grid_device)
+brute_force_search         Context.brute_force_search
+cc_map                     Context.cc_map
+quantify / quantify_slice  Context.quantify / Context.quantify_slice
+add_noise / rng            add_noise / rng_at / uniform01 / gaussian
+=========================  ===============================================
+"""
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from ._native import Axis, Grid, Match, Quant, ScanOpts, ScanStats, ZoomConfig, check
+
+METRIC = {"cc": 0, "euclidean": 1}
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+# --------------------------------------------------------------- schedule
+@dataclass
+class Schedule:
+    """Schedule (sequence.hpp:14-31): per-TR flip/phase in degrees, TR/TE in ms."""
+    flip_deg: np.ndarray
+    phase_deg: np.ndarray
+    tr_ms: np.ndarray
+    te_ms: np.ndarray
+
+    def __post_init__(self):
+        for k in ("flip_deg", "phase_deg", "tr_ms", "te_ms"):
+            setattr(self, k, np.ascontiguousarray(getattr(self, k), dtype=np.float64))
+
+    @property
+    def n(self) -> int:
+        return len(self.flip_deg)
+
+    def to_csv(self) -> str:
+        """Canonical CSV bytes (sequence.cpp:94-103); also the digest input."""
+        rows = ["idx,flip_deg,phase_deg,tr_ms,te_ms\n"]
+        rows += [f"{k},{self.flip_deg[k]:.9g},{self.phase_deg[k]:.9g},{self.tr_ms[k]:.9g},"
+                 f"{self.te_ms[k]:.9g}\n" for k in range(self.n)]
+        return "".join(rows)
+
+    def digest(self) -> str:
+        """schedule_digest (dictionary.cpp:163-171), hex."""
+        return hashlib.sha256(self.to_csv().encode()).hexdigest()
+
+
+def _schedule(fn, n: int, seed: int) -> Schedule:
+    arrs = [np.zeros(n) for _ in range(4)]
+    check(fn(n, seed, *[_dp(a) for a in arrs]))
+    return Schedule(*arrs)
+
+
+def reference_schedule(n: int, seed: int) -> Schedule:
+    """build_schedule (sequence.hpp:51)."""
+    return _schedule(N.load().mrfg_reference_schedule, n, seed)
+
+
+def baseline_schedule(n: int, seed: int = 1) -> Schedule:
+    """BASELINE.json generator: FA 10+50|sin(2 pi j/250)|+N(0,2) deg, 0/180 phase,
+    TR ~ U[10.5,14] ms, TE = TR/2."""
+    return _schedule(N.load().mrfg_baseline_schedule, n, seed)
+
+
+# ------------------------------------------------------------------ grids
+def grid(t1, t2, df) -> Grid:
+    """Grid from per-axis (min, step, count)."""
+    return Grid(Axis(*t1), Axis(*t2), Axis(*df))
+
+
+def axis_count(lo: float, hi: float, step: float) -> int:
+    c = C.c_int64()
+    rc = N.load().mrfg_axis_count(lo, hi, step, C.byref(c))
+    if rc:
+        raise N.InvalidArgument(rc, "axis: need step > 0 and max > min")
+    return c.value
+
+
+def grid_from_ranges(t1, t2, df) -> Grid:
+    """grid_from_ranges (dictionary.cpp:154-161): half-open (min, max, step) per axis."""
+    return grid(*[(r[0], r[2], axis_count(*r)) for r in (t1, t2, df)])
+
+
+def grid_inclusive(t1, t2, df) -> Grid:
+    """Endpoint-INCLUSIVE axes (BASELINE.json's convention)."""
+    return grid_from_ranges(*[(lo, hi + st, st) for lo, hi, st in (t1, t2, df)])
+
+
+def grid_total(g: Grid) -> int:
+    return g.t1_ms.count * g.t2_ms.count * g.df_hz.count
+
+
+def unflatten(g: Grid, flat):
+    """ParameterGrid::unflatten (dictionary.hpp:45-49)."""
+    flat = np.asarray(flat, dtype=np.int64)
+    idf = flat % g.df_hz.count
+    rest = flat // g.df_hz.count
+    return rest // g.t2_ms.count, rest % g.t2_ms.count, idf
+
+
+def params_at(g: Grid, i1, i2, idf):
+    """ParameterGrid::params_at (dictionary.hpp:51-53): seconds, seconds, Hz."""
+    return ((g.t1_ms.min + np.asarray(i1, dtype=np.float64) * g.t1_ms.step) * 1e-3,
+            (g.t2_ms.min + np.asarray(i2, dtype=np.float64) * g.t2_ms.step) * 1e-3,
+            g.df_hz.min + np.asarray(idf, dtype=np.float64) * g.df_hz.step)
+
+
+# -------------------------------------------------------------------- rng
+def rng_at(seed: int, stream: int, index: int) -> int:
+    return N.load().mrfg_rng_at(seed, stream, index)
+
+
+def uniform01(seed: int, stream: int, index: int) -> float:
+    return N.load().mrfg_rng_uniform01(seed, stream, index)
+
+
+def gaussian(seed: int, stream: int, index: int) -> float:
+    return N.load().mrfg_rng_gaussian(seed, stream, index)
+
+
+def add_noise(fp: np.ndarray, sigma: float, seed: int) -> np.ndarray:
+    """add_noise (fingerprint.cpp:68-78)."""
+    fp = np.ascontiguousarray(fp, dtype=np.complex128)
+    out = np.empty_like(fp)
+    check(N.load().mrfg_add_noise(_dp(fp.view(np.float64)), len(fp), sigma, seed,
+                                  _dp(out.view(np.float64))))
+    return out
+
+
+def zoom_config(**kw) -> ZoomConfig:
+    """ZoomConfig with the reference defaults (zoom.hpp:23-52), overridable."""
+    c = ZoomConfig()
+    N.load().mrfg_zoom_config_default(C.byref(c))
+    for k, v in kw.items():
+        if k in ("metric", "final_metric") and isinstance(v, str):
+            v = METRIC[v]
+        if k == "t1t2_2d_steps_ms":
+            c.n2d = len(v)
+            for i, x in enumerate(v):
+                c.t1t2_2d_steps_ms[i] = x
+        elif k == "t1t2_1d_steps_ms":
+            c.n1d = len(v)
+            for i, x in enumerate(v):
+                c.t1t2_1d_steps_ms[i] = x
+        else:
+            setattr(c, k, v)
+    return c
+
+
+# ---------------------------------------------------------------- context
+class Context:
+    """One schedule on one sm_100 device: BlochSimulator plus the search paths."""
+
+    def __init__(self, sched: Schedule, device: int = 0):
+        self.lib = N.load()
+        self.sched = sched
+        self.n = sched.n
+        h = C.c_void_p()
+        check(self.lib.mrfg_create(_dp(sched.flip_deg), _dp(sched.phase_deg), _dp(sched.tr_ms),
+                                   _dp(sched.te_ms), sched.n, device, C.byref(h)))
+        self.h = h
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.mrfg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def set_stream(self, stream_handle: int) -> None:
+        check(self.lib.mrfg_set_stream(self.h, C.c_void_p(stream_handle)))
+
+    def synchronize(self) -> None:
+        check(self.lib.mrfg_synchronize(self.h))
+
+    # -- K1
+    def simulate(self, params, precision: int = 64, normalize: bool = False) -> np.ndarray:
+        """params: (k, 3) of (t1_s, t2_s, df_hz) -> (k, N) complex128."""
+        p = np.ascontiguousarray(np.atleast_2d(params), dtype=np.float64)
+        out = np.empty((p.shape[0], self.n), dtype=np.complex128)
+        check(self.lib.mrfg_simulate(self.h, _dp(p), p.shape[0], precision, int(normalize),
+                                     _dp(out.view(np.float64))))
+        return out
+
+    def generate(self, g: Grid, first: int = 0, count: int | None = None,
+                 precision: int = 64) -> np.ndarray:
+        """generate (dictionary.cpp:184-194): unit-norm float32 entries, (count, 2N)."""
+        if count is None:
+            count = grid_total(g) - first
+        out = np.empty((count, 2 * self.n), dtype=np.float32)
+        check(self.lib.mrfg_generate(self.h, C.byref(g), first, count, precision,
+                                     out.ctypes.data_as(C.POINTER(C.c_float))))
+        return out
+
+    # -- K2/K3
+    def scan_grid(self, g: Grid, queries, metric="cc", flat_range=(0, 0), opts: ScanOpts = None):
+        """scan_grid (dictionary.cpp:257-308) -> (best_flat, best_score, stats)."""
+        q = np.ascontiguousarray(np.atleast_2d(queries), dtype=np.complex128)
+        if q.shape[-1] != self.n:
+            raise N.InvalidArgument(-1, "query length does not match dictionary entries")
+        out = (Match * q.shape[0])()
+        st = ScanStats()
+        check(self.lib.mrfg_scan_grid(self.h, C.byref(g), flat_range[0], flat_range[1],
+                                      _dp(q.view(np.float64)), q.shape[0],
+                                      METRIC.get(metric, metric),
+                                      C.byref(opts) if opts is not None else None, out,
+                                      C.byref(st)))
+        arr = np.frombuffer(out, dtype=np.dtype([("flat", np.int64), ("score", np.float64)]))
+        return arr["flat"].copy(), arr["score"].copy(), st
+
+    def scan_grid_device(self, g: Grid, d_queries_ptr: int, nq: int, d_out_ptr: int,
+                         metric="cc", flat_range=(0, 0), opts: ScanOpts = None) -> ScanStats:
+        """Device-resident variant (async on the context stream; pointers from torch)."""
+        st = ScanStats()
+        check(self.lib.mrfg_scan_grid_dev(self.h, C.byref(g), flat_range[0], flat_range[1],
+                                          C.c_void_p(d_queries_ptr), nq,
+                                          METRIC.get(metric, metric),
+                                          C.byref(opts) if opts is not None else None,
+                                          C.c_void_p(d_out_ptr), C.byref(st)))
+        return st
+
+    def merge_matches_device(self, d_in_ptr: int, nranks: int, nq: int, d_out_ptr: int) -> None:
+        check(self.lib.mrfg_merge_matches_dev(self.h, C.c_void_p(d_in_ptr), nranks, nq,
+                                              C.c_void_p(d_out_ptr)))
+
+    def bloch_norms_device(self, g: Grid, first: int, count: int, d_out_ptr: int) -> None:
+        check(self.lib.mrfg_bloch_norms_dev(self.h, C.byref(g), first, count,
+                                            C.c_void_p(d_out_ptr)))
+
+    def brute_force_search(self, fp, g: Grid, metric="cc"):
+        """brute_force_search (dictionary.cpp:241-255) for one fingerprint."""
+        f, s, _ = self.scan_grid(g, np.atleast_2d(fp), metric)
+        return int(f[0]), float(s[0])
+
+    def screen_scores(self, g: Grid, queries, first: int, count: int, metric="cc",
+                      use_simt: bool = False) -> np.ndarray:
+        """Dense K2 screening scores (count, nq) -- test support."""
+        q = np.ascontiguousarray(np.atleast_2d(queries), dtype=np.complex128)
+        out = np.empty((count, q.shape[0]), dtype=np.float32)
+        check(self.lib.mrfg_screen_scores(self.h, C.byref(g), first, count, _dp(q.view(np.float64)),
+                                          q.shape[0], METRIC.get(metric, metric), int(use_simt),
+                                          out.ctypes.data_as(C.POINTER(C.c_float))))
+        return out
+
+    def cc_map(self, fp, g: Grid, first: int = 0, count: int | None = None) -> np.ndarray:
+        """cc_map (dictionary.cpp:310-331): float32 CC of fp vs flats [first, first+count)."""
+        if count is None:
+            count = grid_total(g) - first
+        q = np.ascontiguousarray(fp, dtype=np.complex128)
+        out = np.empty(count, dtype=np.float32)
+        check(self.lib.mrfg_cc_map(self.h, C.byref(g), _dp(q.view(np.float64)), first, count,
+                                   out.ctypes.data_as(C.POINTER(C.c_float))))
+        return out
+
+    # -- K5
+    def quantify(self, fps, lattice: Grid, cfg: ZoomConfig = None) -> "np.ndarray":
+        """quantify (zoom.cpp:533-539) for a batch of fingerprints -> Quant records."""
+        q = np.ascontiguousarray(np.atleast_2d(fps), dtype=np.complex128)
+        cfg = cfg or zoom_config()
+        out = (Quant * q.shape[0])()
+        check(self.lib.mrfg_quantify(self.h, C.byref(lattice), C.byref(cfg),
+                                     _dp(q.view(np.float64)), q.shape[0], out))
+        return quant_array(out)
+
+    def quantify_slice(self, fps, mask, nx: int, ny: int, lattice: Grid,
+                       cfg: ZoomConfig = None, use_prior: bool = False):
+        q = np.ascontiguousarray(fps, dtype=np.complex128)
+        m = np.ascontiguousarray(mask, dtype=np.uint8)
+        cfg = cfg or zoom_config()
+        out = (Quant * (nx * ny))()
+        secs = C.c_double()
+        check(self.lib.mrfg_quantify_slice(self.h, C.byref(lattice), C.byref(cfg),
+                                           _dp(q.view(np.float64)),
+                                           m.ctypes.data_as(C.POINTER(C.c_uint8)), nx, ny,
+                                           int(use_prior), out, C.byref(secs)))
+        return quant_array(out), secs.value
+
+
+QUANT_DTYPE = np.dtype([("i1", np.int64), ("i2", np.int64), ("idf", np.int64),
+                        ("t1_ms", np.float64), ("t2_ms", np.float64), ("df_hz", np.float64),
+                        ("pd", np.float64), ("score", np.float64), ("evaluations", np.int64)])
+
+
+def quant_array(buf) -> np.ndarray:
+    return np.frombuffer(buf, dtype=QUANT_DTYPE).copy()

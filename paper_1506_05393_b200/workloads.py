@@ -1,0 +1,119 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations.
+
+No public dataset is involved: every schedule, phantom and noise sample is a
+pure function of fixed seeds through the reference's counter RNG (rng.hpp).
+Conventions that the reference does not define are stated here once:
+
+* schedule: ``baseline_schedule(N, seed=1)``;
+* grids are endpoint-inclusive (BASELINE.json counts), e.g. config 1 is
+  96 x 29 x 21 = 58,464 atoms;
+* voxel parameters "uniform on the grid": index ``rng_at(7, 20/21/22, v) % count``
+  (the pattern of cli.cpp:335-337);
+* config 2 phantom: 6 tissue classes (class params uniform on the grid from
+  ``rng_at(11, 30/31/32, c)``), classes 1..5 are rotated ellipses drawn from
+  ``uniform01(11, 33..37, c)`` painted over class 0 (all voxels in the mask),
+  proton density 0.6 + 0.8 * uniform01(11, 38, c);
+* noise: ``add_noise(pd*s, sigma, seed=1_000_000 + v)`` with
+  sigma = ||pd*s||_2 / sqrt(N) / SNR per real channel.
+
+``simulate`` is injected ((schedule, params (k,3)) -> (k,N) complex128) so tests can make
+the truth fingerprints with the CPU oracle and the benchmark with the GPU.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import dgs
+
+CONFIGS = {
+    1: dict(n=500, t1=(100, 2000, 20), t2=(20, 300, 10), df=(-50, 50, 5), nx=32, ny=32, snr=30.0,
+            phantom="uniform"),
+    2: dict(n=1000, t1=(100, 5000, 10), t2=(20, 2000, 5), df=(-250, 250, 1), nx=64, ny=64,
+            snr=30.0, phantom="ellipses"),
+    # config 4 is a ZOOM-only lattice (1 ms / 0.5 ms / 0.1 Hz)
+    4: dict(n=1000, t1=(100, 5000, 1), t2=(20, 2000, 0.5), df=(-250, 250, 0.1), nx=64, ny=64,
+            snr=30.0, phantom="uniform"),
+}
+
+
+@dataclass
+class Workload:
+    config: int
+    schedule: dgs.Schedule
+    grid: dgs.Grid
+    nx: int
+    ny: int
+    truth: np.ndarray        # (V, 3) lattice indices
+    pd: np.ndarray           # (V,)
+    fps: np.ndarray          # (V, N) noisy complex128 queries
+    snr: float
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def nvox(self) -> int:
+        return self.fps.shape[0]
+
+
+def uniform_truth(g: dgs.Grid, nvox: int, seed: int = 7) -> np.ndarray:
+    out = np.empty((nvox, 3), dtype=np.int64)
+    for v in range(nvox):
+        out[v] = (dgs.rng_at(seed, 20, v) % g.t1_ms.count, dgs.rng_at(seed, 21, v) % g.t2_ms.count,
+                  dgs.rng_at(seed, 22, v) % g.df_hz.count)
+    return out
+
+
+def ellipse_classes(nx: int, ny: int, nclass: int = 6, seed: int = 11) -> np.ndarray:
+    cls = np.zeros((ny, nx), dtype=np.int64)
+    yy, xx = np.mgrid[0:ny, 0:nx].astype(np.float64)
+    for c in range(1, nclass):
+        cx = 0.125 * nx + 0.75 * nx * dgs.uniform01(seed, 33, c)
+        cy = 0.125 * ny + 0.75 * ny * dgs.uniform01(seed, 34, c)
+        rx = 0.0625 * nx + 0.22 * nx * dgs.uniform01(seed, 35, c)
+        ry = 0.0625 * ny + 0.22 * ny * dgs.uniform01(seed, 36, c)
+        th = math.pi * dgs.uniform01(seed, 37, c)
+        u = (xx - cx) * math.cos(th) + (yy - cy) * math.sin(th)
+        w = -(xx - cx) * math.sin(th) + (yy - cy) * math.cos(th)
+        cls[(u / rx) ** 2 + (w / ry) ** 2 <= 1.0] = c
+    return cls.reshape(-1)
+
+
+def noisy(fps_clean: np.ndarray, snr: float, seed0: int = 1_000_000) -> np.ndarray:
+    out = np.empty_like(fps_clean)
+    n = fps_clean.shape[1]
+    for v in range(fps_clean.shape[0]):
+        sigma = float(np.sqrt(np.sum(np.abs(fps_clean[v]) ** 2))) / math.sqrt(n) / snr
+        out[v] = dgs.add_noise(fps_clean[v], sigma, seed0 + v)
+    return out
+
+
+def make(config: int, simulate, nvox: int | None = None, n: int | None = None,
+         grid_override: dgs.Grid | None = None) -> Workload:
+    """Build config `config`'s inputs.  `nvox`/`n`/`grid_override` shrink it for tests."""
+    c = CONFIGS[config]
+    n = n or c["n"]
+    sched = dgs.baseline_schedule(n, 1)
+    g = grid_override or dgs.grid_inclusive(c["t1"], c["t2"], c["df"])
+    nx, ny = c["nx"], c["ny"]
+    V = nvox or nx * ny
+    if c["phantom"] == "ellipses":
+        cls = ellipse_classes(nx, ny)[:V]
+        nclass = int(cls.max()) + 1 if V else 0
+        ctruth = np.array([[dgs.rng_at(11, 30, k) % g.t1_ms.count, dgs.rng_at(11, 31, k) % g.t2_ms.count,
+                            dgs.rng_at(11, 32, k) % g.df_hz.count] for k in range(max(nclass, 6))],
+                          dtype=np.int64)
+        cpd = np.array([0.6 + 0.8 * dgs.uniform01(11, 38, k) for k in range(max(nclass, 6))])
+        truth = ctruth[cls]
+        pd = cpd[cls]
+        uniq, inv = np.unique(truth, axis=0, return_inverse=True)
+        base = simulate(sched, np.stack(dgs.params_at(g, uniq[:, 0], uniq[:, 1], uniq[:, 2]), axis=1))
+        clean = base[inv.reshape(-1)] * pd[:, None]
+    else:
+        truth = uniform_truth(g, V)
+        pd = np.ones(V)
+        clean = simulate(sched, np.stack(dgs.params_at(g, truth[:, 0], truth[:, 1], truth[:, 2]), axis=1))
+    fps = noisy(clean, c["snr"])
+    return Workload(config, sched, g, nx, ny, truth, pd, fps, c["snr"],
+                    meta=dict(atoms=dgs.grid_total(g)))
