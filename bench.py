@@ -294,6 +294,10 @@ def run_ours(args, world, rank, local):
         "bloch_fp32_tflops": bloch_rate * BLOCH_FLOP_PER_STEP / 1e12,
         "bloch_frac_of_fp32_peak_nominal": bloch_rate * BLOCH_FLOP_PER_STEP / 1e12 / FP32_PEAK_TFLOPS_NOMINAL,
         "candidates_per_step": cand, "reranked_per_step": rer,
+        "breakdown_ms_per_step": {"bloch": bloch_ms / len(stats), "gemm": gemm_ms / len(stats),
+                                  "rerank": sum(s.rerank_ms for s in stats) / len(stats),
+                                  "scan_total": sum(s.total_ms for s in stats) / len(stats)},
+        "screen_err_max": max(s.screen_err_max for s in stats),
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
                      "frac": gemm_tflops / peak_t, "traffic": None,
                      "kernel": "k_match_sm100 (K2)", "peak_kind": f"{pk_kind} bf16 dense sustained",
@@ -322,7 +326,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--nvox", type=int, default=None)
     ap.add_argument("--atoms", type=int, default=0, help="limit atoms (debug only)")
-    ap.add_argument("--chunk", type=int, default=131072)
+    ap.add_argument("--chunk", type=int, default=524288)
     ap.add_argument("--delta", type=float, default=1e-3)
     ap.add_argument("--ref-voxels", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")

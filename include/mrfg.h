@@ -57,7 +57,7 @@ typedef struct { int64_t flat; double score; } mrfg_match;
  * zero fields take defaults). */
 typedef struct {
     double delta;          /* screening margin in CC units (default 1e-3) */
-    int64_t chunk_atoms;   /* atoms simulated per streamed chunk (default 131072) */
+    int64_t chunk_atoms;   /* atoms simulated per streamed chunk (default 524288) */
     int64_t cand_capacity; /* candidate buffer entries (default 1<<25) */
     int64_t seed_atoms;    /* strided pre-pass atoms that seed the running max (default 16384) */
 } mrfg_scan_opts;
@@ -68,6 +68,7 @@ typedef struct {
     double bloch_ms, gemm_ms, rerank_ms, total_ms;
     double gemm_kernel_ms_avg; /* average duration of one K2 launch */
     int64_t gemm_launches;
+    double screen_err_max;     /* max |screen CC - exact CC| over re-ranked candidates (cc) */
 } mrfg_scan_stats;
 
 /* ZoomConfig (zoom.hpp:23-52) as a POD; the step lists hold up to 8 values. */

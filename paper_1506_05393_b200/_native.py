@@ -37,7 +37,8 @@ class ScanStats(C.Structure):
                 ("candidates", C.c_int64), ("reranked", C.c_int64),
                 ("overflow_passes", C.c_int64), ("bloch_ms", C.c_double),
                 ("gemm_ms", C.c_double), ("rerank_ms", C.c_double), ("total_ms", C.c_double),
-                ("gemm_kernel_ms_avg", C.c_double), ("gemm_launches", C.c_int64)]
+                ("gemm_kernel_ms_avg", C.c_double), ("gemm_launches", C.c_int64),
+                ("screen_err_max", C.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

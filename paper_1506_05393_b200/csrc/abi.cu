@@ -111,6 +111,19 @@ const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
             for (int k = 0; k < 4; ++k) f[k] = static_cast<float>(p[k]);
         }
     }
+    std::vector<StepU> su(n);
+    for (int64_t j = 0; j < n; ++j) {
+        StepU& u = su[j];
+        for (int k = 0; k < 9; ++k) u.r[k] = static_cast<float>(c.rf64[9 * j + k]);
+        u.te = static_cast<float>(c.te_s[j]);
+        u.rest = static_cast<float>(c.rest_s[j]);
+        const double at = kTwoPi * g.df_hz.step * c.te_s[j], ar = kTwoPi * g.df_hz.step * c.rest_s[j];
+        u.wtc = static_cast<float>(std::cos(at));
+        u.wts = static_cast<float>(std::sin(at));
+        u.wrc = static_cast<float>(std::cos(ar));
+        u.wrs = static_cast<float>(std::sin(ar));
+        u.pad = 0.f;
+    }
     GridTables& t = c.tab;
     t.valid = false;
     auto up = [&](DevBuf& b, const void* src, size_t bytes) {
@@ -123,6 +136,7 @@ const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
     up(t.e1f, e1f.data(), e1f.size() * 4);
     up(t.e2f, e2f.data(), e2f.size() * 4);
     up(t.phf, phf.data(), phf.size() * 4);
+    up(t.stepu, su.data(), su.size() * sizeof(StepU));
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
     t.grid = g;
     t.valid = true;
@@ -173,8 +187,10 @@ static void scan_dev(Ctx& c, const mrfg_grid& grid, int64_t fb, int64_t fe, cons
     MRFG_REQUIRE(0 <= fb && fb < fe && fe <= total, MRFG_E_INVALID, "scan_grid: bad flat range");
     const GridTables& t = ensure_tables(c, grid, true);
     const double delta = (o && o->delta > 0) ? o->delta : 1e-3;
-    int64_t chunk = (o && o->chunk_atoms > 0) ? o->chunk_atoms : 131072;
-    chunk = round_up(chunk, 128);
+    int64_t chunk = (o && o->chunk_atoms > 0) ? o->chunk_atoms : 524288;
+    // K1 tiles whole lattice rows (ndf atoms): a chunk is crows rows
+    const int64_t ndf = grid.df_hz.count;
+    const int64_t crows = std::max<int64_t>(1, chunk / ndf);
     int64_t cap = (o && o->cand_capacity > 0) ? o->cand_capacity : (int64_t(1) << 25);
     const int64_t seed_atoms = (o && o->seed_atoms > 0) ? o->seed_atoms : 16384;
     const int64_t n = c.n, kp = k_pad_of(n), qrows = round_up(2 * nq, 256);
@@ -195,7 +211,7 @@ static void scan_dev(Ctx& c, const mrfg_grid& grid, int64_t fb, int64_t fe, cons
     float* best = c.best.as<float>();
     fill(c, best, nq, -3.0f);
 
-    const int64_t arows = std::min(chunk, round_up(range, 128));
+    const int64_t arows = round_up(std::min(crows * ndf, round_up(range, ndf) + ndf), 128);
     c.atoms_a.ensure(sizeof(__half) * arows * kp);
     c.inv2.ensure(sizeof(float) * arows);
     c.cand_count.ensure(64);
@@ -245,15 +261,18 @@ static void scan_dev(Ctx& c, const mrfg_grid& grid, int64_t fb, int64_t fe, cons
         mp.cand = c.cand.as<CandRec>();
         mp.cand_cap = cap;
         std::vector<int> marks;
-        for (int64_t f = fb; f < fe; f += chunk) {
-            const int64_t cnt = std::min(chunk, fe - f);
-            const int64_t rows = round_up(cnt, 128);
+        for (int64_t r0 = fb / ndf; r0 * ndf < fe; r0 += crows) {
+            const int64_t vb = std::max(fb, r0 * ndf), ve = std::min(fe, (r0 + crows) * ndf);
+            const int64_t base = r0 * ndf;
+            const int64_t rows = round_up(ve - base, 128);
             marks.push_back(tm.mark());
-            launch_bloch_operand(c, t, f, 1, fe, rows, metric, c.atoms_a.as<__half>(), c.inv2.as<float>());
+            launch_bloch_rows(c, t, vb, ve, metric, 0, rows, c.atoms_a.as<__half>(), nullptr,
+                              c.inv2.as<float>());
             marks.push_back(tm.mark());
             mp.atoms = rows;
-            mp.valid_atoms = cnt;
-            mp.flat_base = f;
+            mp.valid_begin = vb - base;
+            mp.valid_atoms = ve - base;
+            mp.flat_base = base;
             mp.flat_stride = 1;
             launch_match(c, mp);
             marks.push_back(tm.mark());
@@ -273,10 +292,11 @@ static void scan_dev(Ctx& c, const mrfg_grid& grid, int64_t fb, int64_t fe, cons
         cap = static_cast<int64_t>(ncand);
         ++overflow_passes;
     }
+    double err_max = 0;
     int r0 = tm.mark();
     int64_t nsel = rerank_and_select(c, t, c.q64.as<double>(), nq, metric, best,
                                      static_cast<float>(delta), c.cand.as<CandRec>(),
-                                     static_cast<int64_t>(ncand), d_out);
+                                     static_cast<int64_t>(ncand), d_out, &err_max);
     int r1 = tm.mark();
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
     if (st) {
@@ -292,6 +312,7 @@ static void scan_dev(Ctx& c, const mrfg_grid& grid, int64_t fb, int64_t fe, cons
         st->total_ms = tm.ms(e_start, r1);
         st->gemm_launches = gemm_launches;
         st->gemm_kernel_ms_avg = gemm_launches ? gemm_ms / gemm_launches : 0;
+        st->screen_err_max = err_max;
     }
 }
 

@@ -49,7 +49,7 @@ constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
 struct Dev {
     const float* inv2;
     int64_t n_at, n_vt, nkb, last_sub;
-    int64_t valid_atoms, nvox, flat_base, flat_stride;
+    int64_t valid_atoms, valid_begin, nvox, flat_base, flat_stride;
     float* best;
     CandRec* cand;
     unsigned long long* cand_count;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_wait(&s.tfull[acc], acc_phase);
             tc_fence_after();
             const int64_t atom = at * BM + row;
-            const bool avalid = atom < p.valid_atoms;
+            const bool avalid = atom >= p.valid_begin && atom < p.valid_atoms;
             const float inv = __ldg(p.inv2 + atom);
             const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
@@ -346,7 +346,7 @@ __global__ void k_match_simt(const __half* __restrict__ a, const __half* __restr
     }
     float sc = screen_score(re, im, p.inv2[atom], p.metric);
     if (debug) debug[atom * p.nvox + v] = sc;
-    if (atom >= p.valid_atoms) return;
+    if (atom >= p.valid_atoms || atom < p.valid_begin) return;
     float b0 = __ldcg(p.best + v);
     if (sc >= threshold_of(b0, p.delta, p.metric)) {
         push_candidate(p, v, atom, sc);
@@ -395,6 +395,7 @@ Dev dev_of(const MatchParams& p, int64_t k_valid) {
     d.last_sub = (last + 15) / 16;
     if (d.last_sub < 1) d.last_sub = 1;
     d.valid_atoms = p.valid_atoms;
+    d.valid_begin = p.valid_begin;
     d.nvox = p.nvox;
     d.flat_base = p.flat_base;
     d.flat_stride = p.flat_stride;

@@ -54,8 +54,20 @@ struct DevBuf {
 // the HOST with the same libm calls and operand order as the reference
 // (bloch.cpp:17-21), so the FP64 device recursion reproduces the reference
 // bit-for-bit; the FP32 tables are those values rounded.
+// Per-step data every FP32 producer thread shares (staged in shared memory):
+// RF matrix, te/rest [s], and the off-resonance pitch phasors
+// w = e^{i 2 pi ddf te}, e^{i 2 pi ddf rest} (host FP64 -> FP32).
+struct StepU {
+    float r[9];
+    float te, rest;
+    float wtc, wts, wrc, wrs;
+    float pad;
+};
+static_assert(sizeof(StepU) == 64, "StepU is 4 x 16 B");
+
 struct GridTables {
     mrfg_grid grid{};
+    DevBuf stepu;  // n x StepU
     bool valid = false;
     // FP32: e1[j*n1+i] = (E1te, 1-E1te, E1rest, 1-E1rest); e2[j*n2+i] = (E2te, E2rest);
     //       ph[j*ndf+i] = (cos te, sin te, cos rest, sin rest)
@@ -105,6 +117,11 @@ void launch_generate(Ctx& c, const GridTables& t, int64_t first, int64_t count, 
 void launch_bloch_operand(Ctx& c, const GridTables& t, int64_t first, int64_t stride,
                           int64_t valid_end, int64_t rows, int metric, __half* d_a,
                           float* d_inv2);
+// Row-tiled K1 over flats [vb, ve) (out 0: fp16 operand + inv; 1: raw float
+// entries; 2: |s|^2).  Returns base_flat (operand row = flat - base_flat);
+// for out 0 the buffer rows outside the range, up to `rows`, are zeroed.
+int64_t launch_bloch_rows(Ctx& c, const GridTables& t, int64_t vb, int64_t ve, int metric, int out,
+                          int64_t rows, __half* d_a, float* d_outf, float* d_inv2);
 void launch_bloch_norms(Ctx& c, const GridTables& t, int64_t first, int64_t count, float* d_norm2);
 
 // K2 (match_sm100.cu)
@@ -120,7 +137,8 @@ struct MatchParams {
     int64_t atoms;      // multiple of 128
     int64_t q_rows;     // multiple of 256
     int64_t k_pad;      // multiple of 64
-    int64_t valid_atoms;
+    int64_t valid_atoms;  // local atoms in [valid_begin, valid_atoms) are real
+    int64_t valid_begin;
     int64_t nvox;
     int64_t flat_base, flat_stride;  // global flat of local atom r = flat_base + r*flat_stride
     float* best;        // nvox running max (screening units)
@@ -140,7 +158,7 @@ void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qro
                             __half* d_qprime, int* d_bad);
 int64_t rerank_and_select(Ctx& c, const GridTables& t, const double* d_q64, int64_t nq,
                           int metric, const float* d_best, float delta, CandRec* d_cand,
-                          int64_t ncand, mrfg_match* d_out);
+                          int64_t ncand, mrfg_match* d_out, double* err_max = nullptr);
 void launch_merge(Ctx& c, const mrfg_match* d_in, int nranks, int64_t nq, mrfg_match* d_out);
 void launch_cc_map(Ctx& c, const GridTables& t, const double* d_q64, int64_t first, int64_t count,
                    float* d_out);

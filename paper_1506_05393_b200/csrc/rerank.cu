@@ -8,6 +8,7 @@
 // reference's and the argmax -- including the lowest-flat tie rule of
 // dictionary.cpp:291-294 -- is the reference's.
 #include <cmath>
+#include <cstring>
 
 #include "mrfg_internal.cuh"
 #include "sim64.cuh"
@@ -124,13 +125,18 @@ __device__ double exact_score(const Tab64& T, const double* __restrict__ q, int6
 
 __global__ void k_rerank(Tab64 T, const double* __restrict__ q64, const CandRec* __restrict__ cand,
                          const int64_t* __restrict__ list, int64_t n, int metric,
-                         double* __restrict__ score, unsigned long long* __restrict__ vkey) {
+                         double* __restrict__ score, unsigned long long* __restrict__ vkey,
+                         unsigned int* __restrict__ err_max) {
     int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (k >= n) return;
     const CandRec r = cand[list[k]];
     const double sc = exact_score(T, q64 + static_cast<int64_t>(r.voxel) * 2 * T.n, r.flat, metric);
     score[k] = sc;
     atomicMax(vkey + r.voxel, order_key(sc));
+    if (metric == MRFG_METRIC_CC) {
+        const float e = fabsf(sqrtf(r.s) - static_cast<float>(sc));
+        atomicMax(err_max, __float_as_uint(e));
+    }
 }
 
 __global__ void k_select_flat(const CandRec* __restrict__ cand, const int64_t* __restrict__ list,
@@ -208,7 +214,7 @@ void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qro
 // without any (cannot happen unless the candidate buffer overflowed).
 int64_t rerank_and_select(Ctx& c, const GridTables& t, const double* d_q64, int64_t nq,
                           int metric, const float* d_best, float delta, CandRec* d_cand,
-                          int64_t ncand, mrfg_match* d_out) {
+                          int64_t ncand, mrfg_match* d_out, double* err_max) {
     // scratch layout: list (ncand i64) | score (ncand f64) | vkey (nq u64) |
     //                 vflat (nq u64) | counters
     size_t need = sizeof(int64_t) * ncand + sizeof(double) * ncand + 16 * nq + 64;
@@ -221,6 +227,7 @@ int64_t rerank_and_select(Ctx& c, const GridTables& t, const double* d_q64, int6
     unsigned long long* vflat = vkey + nq;
     unsigned long long* cnt = vflat + nq;
     int* missing = reinterpret_cast<int*>(cnt + 1);
+    unsigned int* d_err = reinterpret_cast<unsigned int*>(missing + 1);
     MRFG_CUDA(cudaMemsetAsync(vkey, 0, sizeof(unsigned long long) * nq, c.stream));
     MRFG_CUDA(cudaMemsetAsync(vflat, 0xFF, sizeof(unsigned long long) * nq, c.stream));
     MRFG_CUDA(cudaMemsetAsync(cnt, 0, 16, c.stream));
@@ -236,7 +243,7 @@ int64_t rerank_and_select(Ctx& c, const GridTables& t, const double* d_q64, int6
     const int rb = 64;
     if (nsel > 0) {
         k_rerank<<<(nsel + rb - 1) / rb, rb, 0, c.stream>>>(T, d_q64, d_cand, list, nsel, metric,
-                                                            score, vkey);
+                                                            score, vkey, d_err);
         MRFG_CUDA(cudaGetLastError());
         k_select_flat<<<(nsel + bs - 1) / bs, bs, 0, c.stream>>>(d_cand, list, nsel, score, vkey,
                                                                  vflat);
@@ -244,10 +251,15 @@ int64_t rerank_and_select(Ctx& c, const GridTables& t, const double* d_q64, int6
     }
     k_write_matches<<<(nq + bs - 1) / bs, bs, 0, c.stream>>>(vkey, vflat, nq, d_out, missing);
     MRFG_CUDA(cudaGetLastError());
-    int h_missing = 0;
-    MRFG_CUDA(cudaMemcpyAsync(&h_missing, missing, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    int h_missing[2] = {0, 0};
+    MRFG_CUDA(cudaMemcpyAsync(h_missing, missing, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
-    MRFG_REQUIRE(!h_missing, MRFG_E_RUNTIME, "scan: a query ended without candidates");
+    if (err_max) {
+        float e;
+        std::memcpy(&e, &h_missing[1], sizeof e);
+        *err_max = e;
+    }
+    MRFG_REQUIRE(!h_missing[0], MRFG_E_RUNTIME, "scan: a query ended without candidates");
     return static_cast<int64_t>(nsel);
 }
 
