@@ -678,6 +678,11 @@ int mrfg_quantify(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config*
         MRFG_CUDA(cudaStreamSynchronize(c.stream));
         d_fps.release();
         d_out.release();
+        for (int64_t k = 0; k < nvox; ++k) {  // AxisSpec::value (dictionary.hpp:22)
+            out[k].t1_ms = lattice->t1_ms.min + static_cast<double>(out[k].i1) * lattice->t1_ms.step;
+            out[k].t2_ms = lattice->t2_ms.min + static_cast<double>(out[k].i2) * lattice->t2_ms.step;
+            out[k].df_hz = lattice->df_hz.min + static_cast<double>(out[k].idf) * lattice->df_hz.step;
+        }
     });
 }
 

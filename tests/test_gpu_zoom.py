@@ -1,0 +1,139 @@
+"""K5 MRF-ZOOM parity on the GPU against the CPU oracle (reference restatement).
+
+The GPU kernel evaluates the reference's FP64 objective bit-exactly and runs
+the reference's decision logic, so lattice answers, scores, proton density
+and the unique-evaluation counts must all match; the BASELINE exemption
+(top-2 gap < 1e-5) is not needed here and not applied.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1506_05393_b200 as P
+from paper_1506_05393_b200 import workloads
+from conftest import to_oracle_grid, to_oracle_sched
+
+pytestmark = pytest.mark.gpu
+
+
+def ocfg(c):
+    """product ZoomConfig -> oracle ZoomCfg (same POD layout)."""
+    o = oracle.ZoomCfg()
+    for name, _ in oracle.ZoomCfg._fields_:
+        v = getattr(c, name)
+        if name.startswith("t1t2"):
+            for i in range(8):
+                getattr(o, name)[i] = v[i]
+        else:
+            setattr(o, name, v)
+    return o
+
+
+def check_same(got, orc, sched, g, cfg, fps):
+    os_, og, oc = to_oracle_sched(sched), to_oracle_grid(g), ocfg(cfg)
+    for v, fp in enumerate(fps):
+        w = orc.quantify(os_, og, oc, fp)
+        assert (got["i1"][v], got["i2"][v], got["idf"][v]) == (w.i1, w.i2, w.idf), v
+        assert got["score"][v] == w.score, v
+        assert got["evaluations"][v] == w.evaluations, v
+        assert got["pd"][v] == pytest.approx(w.pd, rel=1e-12), v
+
+
+def test_zoom_mini_lattice_targets(orc):
+    """test_zoom.cpp:317-345 setup: build_schedule(60, 15), 40x16x25 lattice."""
+    s = P.reference_schedule(60, 15)
+    g = P.grid_from_ranges((600, 1000, 10), (80, 160, 5), (-20, 30, 2))
+    cfg = P.zoom_config(df_coarse_hz=2.0)
+    truth = [(P.dgs.rng_at(92, 0, k) % 40, P.dgs.rng_at(92, 1, k) % 16, P.dgs.rng_at(92, 2, k) % 25)
+             for k in range(5)]
+    fps = np.stack([orc.simulate(to_oracle_sched(s), *[float(x) for x in P.params_at(g, *t)])
+                    for t in truth])
+    with P.Context(s) as c:
+        got = c.quantify(fps, g, cfg)
+        np.testing.assert_array_equal(np.stack([got["i1"], got["i2"], got["idf"]], 1), np.array(truth))
+        check_same(got, orc, s, g, cfg, fps)
+        # final metric euclidean (test_zoom.cpp:339-344)
+        cfge = P.zoom_config(df_coarse_hz=2.0, final_metric="euclidean")
+        got_e = c.quantify(fps, g, cfge)
+        check_same(got_e, orc, s, g, cfge, fps)
+
+
+def test_zoom_exp2_golden_rows(orc):
+    """runs/exp2/zoom.csv: 25 targets on the 2.16M lattice, N=500 seed 1, df_coarse=2."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "exp2.json")))
+    s = P.reference_schedule(500, 1)
+    g = P.grid_from_ranges((500, 2000, 10), (200, 800, 10), (-30, 450, 2))
+    cfg = P.zoom_config(df_coarse_hz=2.0)
+    tg = gold["targets"]
+    fps = np.stack([orc.simulate(to_oracle_sched(s), t[0] * 1e-3, t[1] * 1e-3, float(t[2])) for t in tg])
+    with P.Context(s) as c:
+        got = c.quantify(fps, g, cfg)
+    for k, row in enumerate(gold["zoom"]):
+        t1, t2, df, pd, score, evals = row
+        assert got["t1_ms"][k] == pytest.approx(t1, abs=1e-9)
+        assert got["t2_ms"][k] == pytest.approx(t2, abs=1e-9)
+        assert got["df_hz"][k] == pytest.approx(df, abs=1e-9)
+        assert got["evaluations"][k] == evals
+        assert got["score"][k] == pytest.approx(score, abs=5e-9)
+
+
+def test_zoom_config1_noisy(orc):
+    def sim(sc, params):
+        os_ = to_oracle_sched(sc)
+        return np.stack([orc.simulate(os_, *p) for p in params])
+    wl = workloads.make(1, sim, nvox=48)
+    cfg = P.zoom_config(df_coarse_hz=5.0, omega_hz=82.0)
+    with P.Context(wl.schedule) as c:
+        got = c.quantify(wl.fps, wl.grid, cfg)
+    check_same(got, orc, wl.schedule, wl.grid, cfg, wl.fps)
+
+
+def test_zoom_fine_lattice_config4_like(orc):
+    """Config-4 pitch (1 ms / 0.5 ms / 0.1 Hz) on a reduced lattice."""
+    s = P.baseline_schedule(200, 1)
+    g = P.grid((600, 1, 600), (40, 0.5, 400), (-40, 0.1, 801))
+    cfg = P.zoom_config(df_coarse_hz=10, df_refine_hz=1, df_window_hz=20, omega_hz=82,
+                        t1t2_2d_steps_ms=[100, 10], t1t2_1d_steps_ms=[50, 5, 1], final_2d_step_ms=0.5,
+                        init_t1_ms=900, init_t2_ms=120)
+    rng = np.random.default_rng(3)
+    params = [(0.6 + 0.5 * rng.random(), 0.04 + 0.15 * rng.random(), -35 + 70 * rng.random())
+              for _ in range(6)]
+    os_ = to_oracle_sched(s)
+    fps = np.stack([orc.add_noise(orc.simulate(os_, *p), 0.002, 500 + k) for k, p in enumerate(params)])
+    with P.Context(s) as c:
+        got = c.quantify(fps, g, cfg)
+    check_same(got, orc, s, g, cfg, fps)
+
+
+def test_zoom_slice_noprior_matches_quantify(orc):
+    s = P.reference_schedule(60, 15)
+    g = P.grid_from_ranges((600, 1000, 10), (80, 160, 5), (-20, 30, 2))
+    cfg = P.zoom_config(df_coarse_hz=2.0)
+    nx, ny = 4, 3
+    mask = np.ones(nx * ny, dtype=np.uint8)
+    mask[0] = mask[11] = 0
+    fps = np.zeros((nx * ny, 60), dtype=np.complex128)
+    for v in range(nx * ny):
+        if mask[v]:
+            fps[v] = orc.simulate(to_oracle_sched(s), *[float(x) for x in P.params_at(g, 20 + v % 2, 8 + v % 3, 10)])
+    with P.Context(s) as c:
+        res, secs = c.quantify_slice(fps, mask, nx, ny, g, cfg, use_prior=False)
+    w = orc.quantify_slice(to_oracle_sched(s), to_oracle_grid(g), ocfg(cfg), fps, mask, nx, ny, False)
+    for v in range(nx * ny):
+        if not mask[v]:
+            assert res["evaluations"][v] == 0
+            continue
+        assert (res["i1"][v], res["i2"][v], res["idf"][v]) == (w[v].i1, w[v].i2, w[v].idf)
+        assert res["evaluations"][v] == w[v].evaluations
+
+
+def test_zoom_errors():
+    s = P.reference_schedule(32, 2)
+    g = P.grid((600, 10, 10), (80, 5, 10), (-20, 2, 10))
+    with P.Context(s) as c:
+        with pytest.raises(ValueError):
+            c.quantify(np.zeros((1, 32), dtype=np.complex128), g)
+        with pytest.raises(ValueError):
+            c.quantify(np.ones((1, 32), dtype=np.complex128), g, P.zoom_config(smooth_k=3))
