@@ -94,14 +94,8 @@ __device__ double exact_score(const Tab64& T, const double* __restrict__ q, int6
                                   nullptr);
     const double inv = 1.0 / sqrt(acc);
     // second pass: float entries streamed straight into the score
-    double x = T.inv0[0], y = T.inv0[1], z = T.inv0[2];
     double re = 0.0, im = 0.0, dd = 0.0;
-    for (int j = 0; j < T.n; ++j) {
-        rf_apply64(T.rf + 9 * j, x, y, z);
-        const double* E1 = T.e1d + (static_cast<int64_t>(j) * T.L.n1 + i1) * 2;
-        const double* E2 = T.e2d + (static_cast<int64_t>(j) * T.L.n2 + i2) * 2;
-        const double* P = T.phd + (static_cast<int64_t>(j) * T.L.ndf + idf) * 4;
-        relax64(x, y, z, __ldg(E1), __ldg(E2), __ldg(P), __ldg(P + 1));
+    sim64_walk(T.rf, T.e1d, T.e2d, T.phd, T.inv0, T.n, T.L, i1, i2, idf, [&](int j, double x, double y) {
         const double er = static_cast<double>(__double2float_rn(__dmul_rn(x, inv)));
         const double ei = static_cast<double>(__double2float_rn(__dmul_rn(y, inv)));
         const double qr = q[2 * j], qi = q[2 * j + 1];
@@ -114,8 +108,7 @@ __device__ double exact_score(const Tab64& T, const double* __restrict__ q, int6
             const double dr = __dsub_rn(qr, er), di = __dsub_rn(qi, ei);
             dd = __dadd_rn(dd, __dadd_rn(__dmul_rn(dr, dr), __dmul_rn(di, di)));
         }
-        relax64(x, y, z, __ldg(E1 + 1), __ldg(E2 + 1), __ldg(P + 2), __ldg(P + 3));
-    }
+    });
     if (metric == MRFG_METRIC_CC) {
         double v = sqrt(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
         return v < 1.0 ? v : 1.0;  // dictionary.cpp:126

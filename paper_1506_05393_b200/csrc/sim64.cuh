@@ -47,29 +47,62 @@ __device__ __forceinline__ void unflatten(int64_t flat, const Lattice& L, int& i
     i1 = static_cast<int>(rest / L.n2);
 }
 
-// One FP64 lattice atom, table driven.  mode 0: returns sum |s|^2 only;
-// mode 1: writes float(m * inv) entries (dictionary.cpp:44-51).
+// Per-step transcendental values of one lattice atom (E1, E2, phasor for
+// the te and rest intervals), gathered from the host-libm tables.
+struct StepT {
+    double e1t, e1r, e2t, e2r, ct, st, cr, sr;
+};
+__device__ __forceinline__ StepT load_step(const double* __restrict__ e1d,
+                                           const double* __restrict__ e2d,
+                                           const double* __restrict__ phd, const Lattice& L, int j,
+                                           int i1, int i2, int idf) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(e1d + (static_cast<int64_t>(j) * L.n1 + i1) * 2));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(e2d + (static_cast<int64_t>(j) * L.n2 + i2) * 2));
+    const double2* P = reinterpret_cast<const double2*>(phd + (static_cast<int64_t>(j) * L.ndf + idf) * 4);
+    const double2 p0 = __ldg(P), p1 = __ldg(P + 1);
+    return {a.x, a.y, b.x, b.y, p0.x, p0.y, p1.x, p1.y};
+}
+
+// Walk one lattice atom through the schedule (bloch.cpp:108-123) calling
+// at(j, mx, my) at every echo.  The table gathers run two steps ahead of
+// the recursion (software pipelining) so their latency hides behind the
+// FP64 dependency chain.
+template <class AT>
+__device__ __forceinline__ void sim64_walk(const double* __restrict__ rf,
+                                           const double* __restrict__ e1d,
+                                           const double* __restrict__ e2d,
+                                           const double* __restrict__ phd, const double inv0[3],
+                                           int n, const Lattice& L, int i1, int i2, int idf, AT at) {
+    double x = inv0[0], y = inv0[1], z = inv0[2];
+    StepT c0 = load_step(e1d, e2d, phd, L, 0, i1, i2, idf);
+    StepT c1 = load_step(e1d, e2d, phd, L, n > 1 ? 1 : 0, i1, i2, idf);
+    for (int j = 0; j < n; ++j) {
+        const StepT c2 = load_step(e1d, e2d, phd, L, j + 2 < n ? j + 2 : n - 1, i1, i2, idf);
+        rf_apply64(rf + 9 * j, x, y, z);
+        relax64(x, y, z, c0.e1t, c0.e2t, c0.ct, c0.st);
+        at(j, x, y);
+        relax64(x, y, z, c0.e1r, c0.e2r, c0.cr, c0.sr);
+        c0 = c1;
+        c1 = c2;
+    }
+}
+
+// One FP64 lattice atom.  mode 0: returns sum |s|^2 (fingerprint.cpp:14-18
+// order); mode 1: writes float(m * inv) entries (dictionary.cpp:44-51).
 template <int MODE>
 __device__ double sim64_lattice(const double* __restrict__ rf, const double* __restrict__ e1d,
                                 const double* __restrict__ e2d, const double* __restrict__ phd,
                                 const double inv0[3], int n, const Lattice& L, int i1, int i2,
                                 int idf, double inv, float* __restrict__ out) {
-    double x = inv0[0], y = inv0[1], z = inv0[2];
     double acc = 0.0;
-    for (int j = 0; j < n; ++j) {
-        rf_apply64(rf + 9 * j, x, y, z);
-        const double* E1 = e1d + (static_cast<int64_t>(j) * L.n1 + i1) * 2;
-        const double* E2 = e2d + (static_cast<int64_t>(j) * L.n2 + i2) * 2;
-        const double* P = phd + (static_cast<int64_t>(j) * L.ndf + idf) * 4;
-        relax64(x, y, z, __ldg(E1), __ldg(E2), __ldg(P), __ldg(P + 1));
+    sim64_walk(rf, e1d, e2d, phd, inv0, n, L, i1, i2, idf, [&](int j, double x, double y) {
         if (MODE == 0) {
             acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
         } else {
             out[2 * j] = __double2float_rn(__dmul_rn(x, inv));
             out[2 * j + 1] = __double2float_rn(__dmul_rn(y, inv));
         }
-        relax64(x, y, z, __ldg(E1 + 1), __ldg(E2 + 1), __ldg(P + 2), __ldg(P + 3));
-    }
+    });
     return acc;
 }
 

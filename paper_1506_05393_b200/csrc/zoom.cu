@@ -123,24 +123,19 @@ __device__ void zsim(const Z& z, int i1, int i2, int idf, ZSlot& s) {
     const int n = P.n;
     double acc = sim64_lattice<0>(P.rf, P.e1d, P.e2d, P.phd, P.inv0, n, P.L, i1, i2, idf, 0.0, nullptr);
     const double inv = 1.0 / sqrt(acc);  // fingerprint.cpp:30-32
-    double x = P.inv0[0], y = P.inv0[1], zz = P.inv0[2];
     double re = 0.0, im = 0.0, dd = 0.0;
-    for (int j = 0; j < n; ++j) {
-        rf_apply64(P.rf + 9 * j, x, y, zz);
-        const double* E1 = P.e1d + (static_cast<int64_t>(j) * P.L.n1 + i1) * 2;
-        const double* E2 = P.e2d + (static_cast<int64_t>(j) * P.L.n2 + i2) * 2;
-        const double* Ph = P.phd + (static_cast<int64_t>(j) * P.L.ndf + idf) * 4;
-        relax64(x, y, zz, __ldg(E1), __ldg(E2), __ldg(Ph), __ldg(Ph + 1));
+    const bool euc = P.need_euc;
+    const double* q = z.q;
+    sim64_walk(P.rf, P.e1d, P.e2d, P.phd, P.inv0, n, P.L, i1, i2, idf, [&](int j, double x, double y) {
         const double er = __dmul_rn(x, inv), ei = __dmul_rn(y, inv);
-        const double qr = z.q[2 * j], qi = z.q[2 * j + 1];
+        const double qr = q[2 * j], qi = q[2 * j + 1];
         re = __dadd_rn(re, __dadd_rn(__dmul_rn(qr, er), __dmul_rn(qi, ei)));  // zoom.cpp:79
         im = __dadd_rn(im, __dsub_rn(__dmul_rn(qi, er), __dmul_rn(qr, ei)));  // zoom.cpp:80
-        if (P.need_euc) {
+        if (euc) {
             const double dr = __dsub_rn(qr, er), di = __dsub_rn(qi, ei);  // zoom.cpp:87-89
             dd = __dadd_rn(dd, __dadd_rn(__dmul_rn(dr, dr), __dmul_rn(di, di)));
         }
-        relax64(x, y, zz, __ldg(E1 + 1), __ldg(E2 + 1), __ldg(Ph + 2), __ldg(Ph + 3));
-    }
+    });
     const double v = sqrt(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
     s.cc = v < 1.0 ? v : 1.0;  // zoom.cpp:82-83
     s.euc = -sqrt(dd);          // zoom.cpp:91
