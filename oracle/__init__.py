@@ -133,6 +133,8 @@ class Oracle:
         L.orc_simulate.argtypes = [C.POINTER(Sched), C.c_double, C.c_double, C.c_double, dp]
         L.orc_add_noise.argtypes = [dp, i64, C.c_double, C.c_uint64, dp]
         L.orc_cc.argtypes = [dp, dp, i64]
+        L.orc_cc_unit.restype = C.c_double
+        L.orc_cc_unit.argtypes = [dp, dp, i64]
         L.orc_generate.argtypes = [C.POINTER(Sched), C.POINTER(Grid), i64, i64,
                                    C.POINTER(C.c_float)]
         L.orc_scan_grid.argtypes = [C.POINTER(Sched), C.POINTER(Grid), dp, i64, C.c_int,
@@ -179,6 +181,11 @@ class Oracle:
         a = np.ascontiguousarray(a, dtype=np.complex128)
         b = np.ascontiguousarray(b, dtype=np.complex128)
         return self.lib.orc_cc(self._dp(a.view(np.float64)), self._dp(b.view(np.float64)), len(a))
+
+    def cc_unit(self, a: np.ndarray, b: np.ndarray) -> float:
+        a = np.ascontiguousarray(a, dtype=np.complex128)
+        b = np.ascontiguousarray(b, dtype=np.complex128)
+        return self.lib.orc_cc_unit(self._dp(a.view(np.float64)), self._dp(b.view(np.float64)), len(a))
 
     def generate(self, s: Schedule, g: Grid, first: int, count: int) -> np.ndarray:
         out = np.zeros((count, 2 * s.n), dtype=np.float32)

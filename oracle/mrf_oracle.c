@@ -275,6 +275,24 @@ double orc_cc(const double* a, const double* b, int64_t n) {
     num /= na * nb;
     return num < 1.0 ? num : 1.0;
 }
+double orc_cc_unit(const double* a, const double* b, int64_t n) {
+    double* na = malloc(sizeof(double) * 2 * (size_t)n);
+    double* nb = malloc(sizeof(double) * 2 * (size_t)n);
+    double out = NAN;
+    if (normalize(a, n, na) == 0 && normalize(b, n, nb) == 0) {
+        double re = 0, im = 0;
+        for (int64_t j = 0; j < n; ++j) {
+            re += na[2 * j] * nb[2 * j] + na[2 * j + 1] * nb[2 * j + 1];
+            im += na[2 * j + 1] * nb[2 * j] - na[2 * j] * nb[2 * j + 1];
+        }
+        double num = sqrt(re * re + im * im);
+        out = num < 1.0 ? num : 1.0;
+    }
+    free(na);
+    free(nb);
+    return out;
+}
+
 /* fingerprint.cpp:68-78 */
 int orc_add_noise(const double* fp, int64_t n, double sigma, uint64_t seed, double* out) {
     if (sigma < 0) return fail("add_noise: sigma must be >= 0");

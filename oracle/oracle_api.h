@@ -60,6 +60,9 @@ int orc_baseline_schedule(int64_t n, uint64_t seed, double* flip_deg, double* ph
 int orc_simulate(const orc_sched* s, double t1_s, double t2_s, double df_hz, double* out);
 int orc_add_noise(const double* fp, int64_t n, double sigma, uint64_t seed, double* out);
 double orc_cc(const double* a, const double* b, int64_t n);
+/* cc(normalize(a), normalize(b)): both unit-flagged, no denominator
+ * (fingerprint.cpp:39-55 with unit_norm set by normalize, :28-37). */
+double orc_cc_unit(const double* a, const double* b, int64_t n);
 int orc_generate(const orc_sched* s, const orc_grid* g, int64_t first, int64_t count,
                  float* out);
 /* scan_grid: per-query lowest-flat argmax.  second_score (may be NULL) is the

@@ -170,6 +170,15 @@ double orc_cc(const double* a, const double* b, int64_t n) {
     }
 }
 
+double orc_cc_unit(const double* a, const double* b, int64_t n) {
+    try {
+        return mrf::cc(mrf::normalize(to_fp(a, n)), mrf::normalize(to_fp(b, n)));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return NAN;
+    }
+}
+
 int orc_generate(const orc_sched* s, const orc_grid* g, int64_t first, int64_t count, float* out) {
     return guard([&] {
         // The reference materializes the whole lattice; generate() of a grid

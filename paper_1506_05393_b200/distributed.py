@@ -1,0 +1,76 @@
+"""Multi-GPU data parallelism for the DGS path.
+
+One process per GPU.  Brute force shards the ATOMS: contiguous T1-major slabs
+of the flat lattice, so every rank simulates and matches only its own atoms
+and the reduction order of every score stays intact (K is never split).  The
+per-voxel (flat, score) pairs of all ranks meet in ONE all_gather (NCCL over
+NVLink on GPUs, gloo in the CPU tests) and are reduced with the reference's
+rule: highest score, lowest flat on ties (dictionary.cpp:291-294).  ZOOM
+shards the VOXELS (independent without priors) and gathers the result rows.
+Results are identical for any number of ranks.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+MATCH_DTYPE = np.dtype([("flat", np.int64), ("score", np.float64)])
+
+
+def shard_range(n1: int, slab_atoms: int, world: int, rank: int) -> tuple[int, int]:
+    """Flat range [begin, end) of rank's T1 slab: rows i1 in [n1*r/W, n1*(r+1)/W)."""
+    a = n1 * rank // world
+    b = n1 * (rank + 1) // world
+    return a * slab_atoms, b * slab_atoms
+
+
+def grid_shard(grid, world: int, rank: int) -> tuple[int, int]:
+    return shard_range(grid.t1_ms.count, grid.t2_ms.count * grid.df_hz.count, world, rank)
+
+
+def voxel_shard(nvox: int, world: int, rank: int) -> tuple[int, int]:
+    return nvox * rank // world, nvox * (rank + 1) // world
+
+
+def merge_matches(flats: np.ndarray, scores: np.ndarray):
+    """Host form of the C1 reduction (k_merge in rerank.cu): (ranks, nq) -> (nq,).
+
+    Ranks without atoms report flat -1 and are skipped."""
+    flats = np.asarray(flats)
+    scores = np.asarray(scores)
+    best_f = flats[0].copy()
+    best_s = scores[0].copy()
+    for r in range(1, flats.shape[0]):
+        f, s = flats[r], scores[r]
+        take = (f >= 0) & ((best_f < 0) | (s > best_s) | ((s == best_s) & (f < best_f)))
+        best_f = np.where(take, f, best_f)
+        best_s = np.where(take, s, best_s)
+    return best_f, best_s
+
+
+def scan_grid_distributed(ctx, grid, d_queries, nq: int, group=None, opts=None, metric="cc"):
+    """Brute-force scan of the whole grid across the process group (GPU).
+
+    d_queries: CUDA float64 tensor (nq, 2N) resident on this rank's device.
+    Returns (CUDA uint8 tensor of nq mrfg_match records (flat i64, score f64),
+    identical on every rank; this rank's ScanStats or None)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    fb, fe = grid_shard(grid, world, rank)
+    dev = d_queries.device
+    d_out = torch.empty(nq * 16, dtype=torch.uint8, device=dev)
+    stats = None
+    if fe > fb:
+        stats = ctx.scan_grid_device(grid, d_queries.data_ptr(), nq, d_out.data_ptr(), metric=metric,
+                                     flat_range=(fb, fe), opts=opts)
+    else:  # more ranks than T1 slabs: contribute "no atoms"
+        d_out.view(torch.int64).view(nq, 2)[:, 0] = -1
+    if world == 1:
+        return d_out, stats
+    d_all = torch.empty(world * nq * 16, dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(d_all, d_out, group=group)
+    d_merged = torch.empty(nq * 16, dtype=torch.uint8, device=dev)
+    ctx.merge_matches_device(d_all.data_ptr(), world, nq, d_merged.data_ptr())
+    return d_merged, stats

@@ -1,0 +1,158 @@
+"""Pin the CPU oracle (test infrastructure) before trusting it.
+
+1. The C restatement (oracle/liboracle.so) is bit-identical to the reference
+   library compiled from /root/reference (oracle/_ref) -- skipped where the
+   reference was not built.
+2. The restatement reproduces the reference's RECORDED outputs (committed
+   fixtures under tests/golden/, made by tests/golden/make_golden.py):
+   the build_schedule(500, 1) digest, runs/exp1 CC values at %.9g, runs/exp2
+   MRF-ZOOM answers and evaluation counts, runs/exp3 64x64 slice maps and
+   per-voxel evaluation counts.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def digest(s):
+    csv = "idx,flip_deg,phase_deg,tr_ms,te_ms\n" + "".join(
+        f"{k},{s.flip_deg[k]:.9g},{s.phase_deg[k]:.9g},{s.tr_ms[k]:.9g},{s.te_ms[k]:.9g}\n"
+        for k in range(s.n))
+    return hashlib.sha256(csv.encode()).hexdigest()
+
+
+def test_schedule_digest_golden(orc):
+    # build_schedule(500, 1) digest recorded by the reference
+    assert digest(orc.build_schedule(500, 1)) == \
+        "99b129a4b97065d83595554534b6434b0c5cbe05b7223af5981b79ec6965bc8e"
+
+
+def test_schedule_ranges(orc):
+    s = orc.build_schedule(1000, 3)  # sequence.hpp:33-48 ranges
+    assert s.flip_deg.min() >= 0 and s.flip_deg.max() <= 79 + 1e-6
+    assert set(np.unique(s.phase_deg)) <= {0.0, 90.0, 180.0}
+    assert s.tr_ms.min() >= 14 - 1e-9 and s.tr_ms.max() <= 20 + 1e-6
+    b = orc.baseline_schedule(1000, 1)
+    assert b.tr_ms.min() >= 10.5 and b.tr_ms.max() < 14.0 + 1e-9
+    assert set(np.unique(b.phase_deg)) == {0.0, 180.0}
+    np.testing.assert_allclose(b.te_ms, b.tr_ms / 2, rtol=1e-8)
+
+
+@pytest.mark.parametrize("fn", ["build_schedule", "baseline_schedule"])
+def test_schedules_match_reference(orc, ref, fn):
+    a, b = getattr(orc, fn)(777, 5), getattr(ref, fn)(777, 5)
+    for k in ("flip_deg", "phase_deg", "tr_ms", "te_ms"):
+        assert np.array_equal(getattr(a, k), getattr(b, k))
+
+
+@pytest.mark.parametrize("p", [(1.4, 0.5, 100.0), (0.1, 0.02, -50.0), (5.0, 2.0, 249.0), (0.75, 0.12, 3.3)])
+def test_simulate_bit_exact_vs_reference(orc, ref, p):
+    s = orc.baseline_schedule(1000, 1)
+    assert np.array_equal(orc.simulate(s, *p), ref.simulate(s, *p))
+
+
+def test_noise_and_cc_vs_reference(orc, ref):
+    s = orc.build_schedule(300, 2)
+    fp = orc.simulate(s, 0.9, 0.1, 7.0)
+    assert np.array_equal(orc.add_noise(fp, 0.01, 42), ref.add_noise(fp, 0.01, 42))
+    g = orc.add_noise(fp, 0.05, 43)
+    assert orc.cc(fp, g) == ref.cc(fp, g)
+    assert orc.cc_unit(fp, g) == ref.cc_unit(fp, g)
+
+
+def test_generate_vs_reference(orc, ref):
+    s = orc.build_schedule(60, 3)
+    g = oracle.make_grid((600, 100, 3), (80, 20, 3), (-10, 10, 3))
+    assert np.array_equal(orc.generate(s, g, 0, 27), ref.generate(s, g, 0, 27))
+
+
+def test_scan_grid_vs_reference(orc, ref):
+    s = orc.build_schedule(48, 7)
+    g = oracle.make_grid((600, 100, 5), (80, 20, 5), (-20, 10, 5))
+    rng = np.random.default_rng(0)
+    q = np.stack([orc.add_noise(orc.simulate(s, 0.55 + 0.6 * rng.random(), 0.07 + 0.12 * rng.random(),
+                                             50 * rng.random() - 25), 0.002, 80 + k) for k in range(6)])
+    for metric in (0, 1):
+        a = orc.scan_grid(s, g, q, metric=metric)
+        b = ref.scan_grid(s, g, q, metric=metric, threads=1)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        assert np.all(a[1] >= a[2])  # top-2 bookkeeping
+
+
+def test_quantify_vs_reference(orc, ref):
+    s = orc.build_schedule(60, 15)
+    g = oracle.make_grid((600, 10, 40), (80, 5, 16), (-20, 2, 25))
+    rng = np.random.default_rng(1)
+    for cfg in (oracle.zoom_cfg(df_coarse_hz=2.0), oracle.zoom_cfg(df_coarse_hz=2.0, final_metric=1)):
+        for k in range(4):
+            fp = orc.add_noise(orc.simulate(s, 0.6 + 0.4 * rng.random(), 0.08 + 0.08 * rng.random(),
+                                            -20 + 50 * rng.random()), 0.003, 9 + k)
+            a, b = orc.quantify(s, g, cfg, fp), ref.quantify(s, g, cfg, fp)
+            assert (a.i1, a.i2, a.idf, a.score, a.pd, a.evaluations) == \
+                   (b.i1, b.i2, b.idf, b.score, b.pd, b.evaluations)
+
+
+def test_quantify_slice_prior_vs_reference(orc, ref):
+    s = orc.build_schedule(60, 15)
+    g = oracle.make_grid((600, 10, 40), (80, 5, 16), (-20, 2, 25))
+    cfg = oracle.zoom_cfg(df_coarse_hz=2.0)
+    nx, ny = 4, 3
+    mask = np.ones(nx * ny, dtype=np.uint8)
+    mask[0] = mask[11] = 0
+    fps = np.zeros((nx * ny, 60), dtype=np.complex128)
+    for v in range(nx * ny):
+        if mask[v]:
+            fps[v] = orc.simulate(s, (600 + 10 * (20 + v % 2)) * 1e-3, (80 + 5 * (8 + v % 3)) * 1e-3, 0.0)
+    for prior in (False, True):
+        a = orc.quantify_slice(s, g, cfg, fps, mask, nx, ny, prior)
+        b = ref.quantify_slice(s, g, cfg, fps, mask, nx, ny, prior, threads=1)
+        for v in range(nx * ny):
+            assert (a[v].i1, a[v].i2, a[v].idf, a[v].evaluations) == (b[v].i1, b[v].i2, b[v].idf, b[v].evaluations)
+
+
+def test_golden_exp1_cc_vs_df(orc):
+    """runs/exp1/cc_vs_df.csv: cc(normalize(target), normalize(entry)) at %.9g."""
+    d = np.load(os.path.join(GOLD, "exp1_ccdf.npz"))
+    s = orc.build_schedule(500, 1)
+    target = orc.simulate(s, 1.4, 0.5, 100.0)
+    idx = np.arange(0, len(d["df_hz"]), 7)
+    for i in idx:
+        e = orc.simulate(s, d["t1_ms"][i] * 1e-3, d["t2_ms"][i] * 1e-3, d["df_hz"][i])
+        assert f"{orc.cc_unit(target, e):.9g}" == str(d["cc_text"][i]), i
+
+
+def test_golden_exp2_zoom(orc):
+    gold = json.load(open(os.path.join(GOLD, "exp2.json")))
+    s = orc.build_schedule(500, 1)
+    g = oracle.make_grid((500, 10, 150), (200, 10, 60), (-30, 2, 240))
+    cfg = oracle.zoom_cfg(df_coarse_hz=2.0)
+    for (t1, t2, df), (z1, z2, zdf, pd, score, evals) in zip(gold["targets"], gold["zoom"]):
+        q = orc.quantify(s, g, cfg, orc.simulate(s, t1 * 1e-3, t2 * 1e-3, df))
+        assert (q.t1_ms, q.t2_ms, q.df_hz, q.evaluations) == (z1, z2, zdf, evals)
+        assert float(f"{q.score:.9g}") == score and float(f"{q.pd:.9g}") == pd
+
+
+def test_golden_exp3_slice(orc):
+    """runs/exp3: 64x64 phantom (data/slice64.csv), 1 ms/1 Hz lattice, no prior."""
+    d = np.load(os.path.join(GOLD, "exp3_slice.npz"))
+    s = orc.build_schedule(500, 1)
+    g = oracle.make_grid((800, 1, 2401), (50, 1, 551), (-48, 1, 133))
+    cfg = oracle.zoom_cfg(df_coarse_hz=1.0)
+    mask = d["mask"]
+    fps = np.zeros((4096, 500), dtype=np.complex128)
+    for v in np.nonzero(mask)[0]:
+        fps[v] = orc.simulate(s, d["t1_ms"][v] * 1e-3, d["t2_ms"][v] * 1e-3, d["df_hz"][v]) * d["pd"][v]
+    res = orc.quantify_slice(s, g, cfg, fps, mask, 64, 64, False)
+    got_evals = np.array([r.evaluations for r in res])
+    assert np.array_equal(got_evals, d["evals_noprior"])
+    for v in np.nonzero(mask)[0]:
+        assert float(f"{res[v].t1_ms:.9g}") == pytest.approx(d["t1_map"][v], abs=1e-9)
+        assert float(f"{res[v].t2_ms:.9g}") == pytest.approx(d["t2_map"][v], abs=1e-9)
+        assert float(f"{res[v].df_hz:.9g}") == pytest.approx(d["df_map"][v], abs=1e-9)
