@@ -156,6 +156,18 @@ int mrfg_scan_grid(mrfg_ctx* ctx, const mrfg_grid* grid, int64_t flat_begin, int
 int mrfg_scan_grid_dev(mrfg_ctx* ctx, const mrfg_grid* grid, int64_t flat_begin,
                        int64_t flat_end, const double* d_queries, int64_t nq, int metric,
                        const mrfg_scan_opts* opts, mrfg_match* d_out, mrfg_scan_stats* stats);
+/* K4 -- brute_force_search (dictionary.hpp:108-109, dictionary.cpp:241-255)
+ * over a stored dictionary of natoms unit float32 entries (2N interleaved,
+ * generate()'s layout): same screening GEMM, exact FP64 re-rank against the
+ * stored entries (dictionary.cpp:117-143).  The _dev form takes a device
+ * dictionary and a flat range [flat_begin, flat_end) (both 0: all), so a
+ * dictionary sharded across GPUs needs no copy. */
+int mrfg_scan_dict(mrfg_ctx* ctx, const float* dict, int64_t natoms, const double* queries,
+                   int64_t nq, int metric, const mrfg_scan_opts* opts, mrfg_match* out,
+                   mrfg_scan_stats* stats);
+int mrfg_scan_dict_dev(mrfg_ctx* ctx, const float* d_dict, int64_t natoms, int64_t flat_begin,
+                       int64_t flat_end, const double* d_queries, int64_t nq, int metric,
+                       const mrfg_scan_opts* opts, mrfg_match* d_out, mrfg_scan_stats* stats);
 /* C1: merge per-rank matches gathered as d_in[rank*nq + q] (max score,
  * lowest flat on ties) -- the reduction after the NCCL allgather. */
 int mrfg_merge_matches_dev(mrfg_ctx* ctx, const mrfg_match* d_in, int nranks, int64_t nq,

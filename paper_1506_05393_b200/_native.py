@@ -71,6 +71,7 @@ EXPORTS = [
     "mrfg_rng_gaussian", "mrfg_axis_count", "mrfg_create", "mrfg_destroy", "mrfg_length",
     "mrfg_set_stream", "mrfg_synchronize", "mrfg_simulate", "mrfg_simulate_dev", "mrfg_generate",
     "mrfg_generate_dev", "mrfg_bloch_norms_dev", "mrfg_scan_grid", "mrfg_scan_grid_dev",
+    "mrfg_scan_dict", "mrfg_scan_dict_dev",
     "mrfg_merge_matches_dev", "mrfg_screen_scores", "mrfg_cc_map", "mrfg_quantify", "mrfg_quantify_slice",
 ]
 
@@ -115,6 +116,10 @@ def load() -> C.CDLL:
     L.mrfg_scan_grid.argtypes = [vp, C.POINTER(Grid), i64, i64, dp, i64, C.c_int,
                                  C.POINTER(ScanOpts), C.POINTER(Match), C.POINTER(ScanStats)]
     L.mrfg_scan_grid_dev.argtypes = [vp, C.POINTER(Grid), i64, i64, vp, i64, C.c_int,
+                                     C.POINTER(ScanOpts), vp, C.POINTER(ScanStats)]
+    L.mrfg_scan_dict.argtypes = [vp, C.POINTER(C.c_float), i64, dp, i64, C.c_int,
+                                 C.POINTER(ScanOpts), C.POINTER(Match), C.POINTER(ScanStats)]
+    L.mrfg_scan_dict_dev.argtypes = [vp, vp, i64, i64, i64, vp, i64, C.c_int,
                                      C.POINTER(ScanOpts), vp, C.POINTER(ScanStats)]
     L.mrfg_merge_matches_dev.argtypes = [vp, vp, C.c_int, i64, vp]
     L.mrfg_screen_scores.argtypes = [vp, C.POINTER(Grid), i64, i64, dp, i64, C.c_int, C.c_int,

@@ -175,21 +175,24 @@ struct EventTimer {
     }
 };
 
-// The streamed brute-force scan on device-resident queries.
-static void scan_dev(Ctx& c, const mrfg_grid& grid, int64_t fb, int64_t fe, const double* d_raw,
-                     int64_t nq, int metric, const mrfg_scan_opts* o, mrfg_match* d_out,
-                     mrfg_scan_stats* st) {
+// The streamed brute-force scan on device-resident queries.  Atoms come from
+// the lattice (grid != nullptr: K1 simulates them chunk by chunk) or from a
+// stored float32 dictionary (d_dict: converted to the fp16 operand per chunk).
+static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t dict_atoms,
+                     int64_t fb, int64_t fe, const double* d_raw, int64_t nq, int metric,
+                     const mrfg_scan_opts* o, mrfg_match* d_out, mrfg_scan_stats* st) {
     MRFG_REQUIRE(nq > 0, MRFG_E_INVALID, "scan_grid: no queries");  // dictionary.cpp:260
     MRFG_REQUIRE(metric == MRFG_METRIC_CC || metric == MRFG_METRIC_EUCLIDEAN, MRFG_E_INVALID,
                  "scan_grid: unknown metric");
-    const int64_t total = grid_total(grid);
+    const int64_t total = grid ? grid_total(*grid) : dict_atoms;
     if (fb == 0 && fe == 0) fe = total;
     MRFG_REQUIRE(0 <= fb && fb < fe && fe <= total, MRFG_E_INVALID, "scan_grid: bad flat range");
-    const GridTables& t = ensure_tables(c, grid, true);
+    const GridTables* tp = grid ? &ensure_tables(c, *grid, true) : nullptr;
     const double delta = (o && o->delta > 0) ? o->delta : 1e-3;
     int64_t chunk = (o && o->chunk_atoms > 0) ? o->chunk_atoms : 524288;
-    // K1 tiles whole lattice rows (ndf atoms): a chunk is crows rows
-    const int64_t ndf = grid.df_hz.count;
+    // K1 tiles whole lattice rows (ndf atoms): a chunk is crows rows.  A stored
+    // dictionary is chunked in flat order directly (ndf = 1).
+    const int64_t ndf = grid ? grid->df_hz.count : 1;
     const int64_t crows = std::max<int64_t>(1, chunk / ndf);
     int64_t cap = (o && o->cand_capacity > 0) ? o->cand_capacity : (int64_t(1) << 25);
     const int64_t seed_atoms = (o && o->seed_atoms > 0) ? o->seed_atoms : 16384;
@@ -238,7 +241,12 @@ static void scan_dev(Ctx& c, const mrfg_grid& grid, int64_t fb, int64_t fe, cons
         int64_t cnt = (range + stride - 1) / stride;
         int64_t rows = round_up(std::min(cnt, arows), 128);
         int a0 = tm.mark();
-        launch_bloch_operand(c, t, fb, stride, fe, rows, metric, c.atoms_a.as<__half>(), c.inv2.as<float>());
+        if (tp)
+            launch_bloch_operand(c, *tp, fb, stride, fe, rows, metric, c.atoms_a.as<__half>(),
+                                 c.inv2.as<float>());
+        else
+            launch_dict_operand(c, d_dict, fb, std::min(cnt, rows), rows, stride, metric,
+                                c.atoms_a.as<__half>(), c.inv2.as<float>());
         int a1 = tm.mark();
         mp.atoms = rows;
         mp.valid_atoms = std::min(cnt, rows);
@@ -266,8 +274,12 @@ static void scan_dev(Ctx& c, const mrfg_grid& grid, int64_t fb, int64_t fe, cons
             const int64_t base = r0 * ndf;
             const int64_t rows = round_up(ve - base, 128);
             marks.push_back(tm.mark());
-            launch_bloch_rows(c, t, vb, ve, metric, 0, rows, c.atoms_a.as<__half>(), nullptr,
-                              c.inv2.as<float>());
+            if (tp)
+                launch_bloch_rows(c, *tp, vb, ve, metric, 0, rows, c.atoms_a.as<__half>(), nullptr,
+                                  c.inv2.as<float>());
+            else  // base == vb - (vb - base): rows [vb-base, ve-base) hold the entries
+                launch_dict_operand(c, d_dict, base, ve - base, rows, 1, metric, c.atoms_a.as<__half>(),
+                                    c.inv2.as<float>());
             marks.push_back(tm.mark());
             mp.atoms = rows;
             mp.valid_begin = vb - base;
@@ -294,7 +306,7 @@ static void scan_dev(Ctx& c, const mrfg_grid& grid, int64_t fb, int64_t fe, cons
     }
     double err_max = 0;
     int r0 = tm.mark();
-    int64_t nsel = rerank_and_select(c, t, c.q64.as<double>(), nq, metric, best,
+    int64_t nsel = rerank_and_select(c, tp, d_dict, c.q64.as<double>(), nq, metric, best,
                                      static_cast<float>(delta), c.cand.as<CandRec>(),
                                      static_cast<int64_t>(ncand), d_out, &err_max);
     int r1 = tm.mark();
@@ -523,7 +535,52 @@ int mrfg_scan_grid_dev(mrfg_ctx* h, const mrfg_grid* grid, int64_t fb, int64_t f
     return guard([&] {
         Ctx& c = h->c;
         MRFG_CUDA(cudaSetDevice(c.device));
-        scan_dev(c, *grid, fb, fe, d_queries, nq, metric, o, d_out, st);
+        scan_dev(c, grid, nullptr, 0, fb, fe, d_queries, nq, metric, o, d_out, st);
+    });
+}
+
+int mrfg_scan_dict_dev(mrfg_ctx* h, const float* d_dict, int64_t natoms, int64_t fb, int64_t fe,
+                       const double* d_queries, int64_t nq, int metric, const mrfg_scan_opts* o,
+                       mrfg_match* d_out, mrfg_scan_stats* st) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(natoms > 0, MRFG_E_INVALID, "brute_force_search: empty dictionary");
+        scan_dev(c, nullptr, d_dict, natoms, fb, fe, d_queries, nq, metric, o, d_out, st);
+    });
+}
+
+int mrfg_scan_dict(mrfg_ctx* h, const float* dict, int64_t natoms, const double* queries,
+                   int64_t nq, int metric, const mrfg_scan_opts* o, mrfg_match* out,
+                   mrfg_scan_stats* st) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(nq > 0, MRFG_E_INVALID, "scan_grid: no queries");
+        MRFG_REQUIRE(natoms > 0, MRFG_E_INVALID, "brute_force_search: empty dictionary");
+        DevBuf raw, res, dd;
+        raw.ensure(sizeof(double) * 2 * c.n * nq);
+        res.ensure(sizeof(mrfg_match) * nq);
+        dd.ensure(sizeof(float) * 2 * c.n * natoms);
+        try {
+            MRFG_CUDA(cudaMemcpyAsync(dd.p, dict, sizeof(float) * 2 * c.n * natoms,
+                                      cudaMemcpyHostToDevice, c.stream));
+            MRFG_CUDA(cudaMemcpyAsync(raw.p, queries, sizeof(double) * 2 * c.n * nq,
+                                      cudaMemcpyHostToDevice, c.stream));
+            scan_dev(c, nullptr, dd.as<float>(), natoms, 0, natoms, raw.as<double>(), nq, metric, o,
+                     res.as<mrfg_match>(), st);
+            MRFG_CUDA(cudaMemcpyAsync(out, res.p, sizeof(mrfg_match) * nq, cudaMemcpyDeviceToHost,
+                                      c.stream));
+            MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        } catch (...) {
+            raw.release();
+            res.release();
+            dd.release();
+            throw;
+        }
+        raw.release();
+        res.release();
+        dd.release();
     });
 }
 
@@ -540,7 +597,7 @@ int mrfg_scan_grid(mrfg_ctx* h, const mrfg_grid* grid, int64_t fb, int64_t fe,
         try {
             MRFG_CUDA(cudaMemcpyAsync(raw.p, queries, sizeof(double) * 2 * c.n * nq,
                                       cudaMemcpyHostToDevice, c.stream));
-            scan_dev(c, *grid, fb, fe, raw.as<double>(), nq, metric, o, res.as<mrfg_match>(), st);
+            scan_dev(c, grid, nullptr, 0, fb, fe, raw.as<double>(), nq, metric, o, res.as<mrfg_match>(), st);
             MRFG_CUDA(cudaMemcpyAsync(out, res.p, sizeof(mrfg_match) * nq, cudaMemcpyDeviceToHost,
                                       c.stream));
             MRFG_CUDA(cudaStreamSynchronize(c.stream));

@@ -156,9 +156,15 @@ void launch_match_simt(Ctx& c, const MatchParams& p);
 // K3 (rerank.cu)
 void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qrows, double* d_q64,
                             __half* d_qprime, int* d_bad);
-int64_t rerank_and_select(Ctx& c, const GridTables& t, const double* d_q64, int64_t nq,
-                          int metric, const float* d_best, float delta, CandRec* d_cand,
+// Exact re-rank: lattice atoms re-simulated through the FP64 tables (t), or
+// stored float32 dictionary entries (d_dict != nullptr, flat = row).
+int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, const double* d_q64,
+                          int64_t nq, int metric, const float* d_best, float delta, CandRec* d_cand,
                           int64_t ncand, mrfg_match* d_out, double* err_max = nullptr);
+// Stored float32 rows first + r*stride (r < count) -> fp16 operand (rows, zero
+// padded) + inv.
+void launch_dict_operand(Ctx& c, const float* d_dict, int64_t first, int64_t count, int64_t rows,
+                         int64_t stride, int metric, __half* d_a, float* d_inv2);
 void launch_merge(Ctx& c, const mrfg_match* d_in, int nranks, int64_t nq, mrfg_match* d_out);
 void launch_cc_map(Ctx& c, const GridTables& t, const double* d_q64, int64_t first, int64_t count,
                    float* d_out);

@@ -132,6 +132,67 @@ __global__ void k_rerank(Tab64 T, const double* __restrict__ q64, const CandRec*
     }
 }
 
+// brute_force_search over a stored dictionary: the reference scores the
+// FP64 unit query against the stored float32 entry (dictionary.cpp:117-143).
+__device__ double exact_score_entry(const double* __restrict__ q, const float* __restrict__ e, int n,
+                                    int metric) {
+    double re = 0.0, im = 0.0, dd = 0.0;
+    for (int j = 0; j < n; ++j) {
+        const double er = static_cast<double>(e[2 * j]), ei = static_cast<double>(e[2 * j + 1]);
+        const double qr = q[2 * j], qi = q[2 * j + 1];
+        if (metric == MRFG_METRIC_CC) {
+            re = __dadd_rn(re, __dadd_rn(__dmul_rn(qr, er), __dmul_rn(qi, ei)));
+            im = __dadd_rn(im, __dsub_rn(__dmul_rn(qi, er), __dmul_rn(qr, ei)));
+        } else {
+            const double dr = __dsub_rn(qr, er), di = __dsub_rn(qi, ei);
+            dd = __dadd_rn(dd, __dadd_rn(__dmul_rn(dr, dr), __dmul_rn(di, di)));
+        }
+    }
+    if (metric == MRFG_METRIC_CC) {
+        const double v = sqrt(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
+        return v < 1.0 ? v : 1.0;
+    }
+    return -sqrt(dd);
+}
+
+__global__ void k_rerank_dict(const float* __restrict__ dict, int n, const double* __restrict__ q64,
+                              const CandRec* __restrict__ cand, const int64_t* __restrict__ list,
+                              int64_t cnt, int metric, double* __restrict__ score,
+                              unsigned long long* __restrict__ vkey, unsigned int* __restrict__ err_max) {
+    int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= cnt) return;
+    const CandRec r = cand[list[k]];
+    const double sc = exact_score_entry(q64 + static_cast<int64_t>(r.voxel) * 2 * n, dict + r.flat * 2 * n,
+                                        n, metric);
+    score[k] = sc;
+    atomicMax(vkey + r.voxel, order_key(sc));
+    if (metric == MRFG_METRIC_CC) atomicMax(err_max, __float_as_uint(fabsf(sqrtf(r.s) - static_cast<float>(sc))));
+}
+
+// Stored float32 entries -> fp16 screening operand rows (+ 1/|e|^2 or 1/|e|):
+// one warp per atom, coalesced row reads.
+__global__ void k_dict_operand(const float* __restrict__ dict, int64_t first, int64_t count,
+                               int64_t stride, int n, int64_t k_pad, int inv_mode,
+                               __half* __restrict__ a, float* __restrict__ inv2, int64_t rows) {
+    const int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
+    const int lane = threadIdx.x % 32;
+    if (r >= rows) return;
+    __half* dst = a + r * k_pad;
+    float acc = 0.f;
+    if (r < count) {
+        const float* src = dict + (first + r * stride) * 2 * n;
+        for (int64_t c = lane; c < k_pad; c += 32) {
+            const float v = c < 2 * n ? src[c] : 0.f;
+            acc = fmaf(v, v, acc);
+            dst[c] = __float2half_rn(v);
+        }
+    } else {
+        for (int64_t c = lane; c < k_pad; c += 32) dst[c] = __float2half_rn(0.f);
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) inv2[r] = (r < count && acc > 0.f) ? (inv_mode == 0 ? 1.f / acc : rsqrtf(acc)) : 0.f;
+}
+
 __global__ void k_select_flat(const CandRec* __restrict__ cand, const int64_t* __restrict__ list,
                               int64_t n, const double* __restrict__ score,
                               const unsigned long long* __restrict__ vkey,
@@ -205,8 +266,8 @@ void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qro
 
 // Returns the number of re-ranked candidates; throws when a voxel ends
 // without any (cannot happen unless the candidate buffer overflowed).
-int64_t rerank_and_select(Ctx& c, const GridTables& t, const double* d_q64, int64_t nq,
-                          int metric, const float* d_best, float delta, CandRec* d_cand,
+int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, const double* d_q64,
+                          int64_t nq, int metric, const float* d_best, float delta, CandRec* d_cand,
                           int64_t ncand, mrfg_match* d_out, double* err_max) {
     // scratch layout: list (ncand i64) | score (ncand f64) | vkey (nq u64) |
     //                 vflat (nq u64) | counters
@@ -232,11 +293,15 @@ int64_t rerank_and_select(Ctx& c, const GridTables& t, const double* d_q64, int6
     unsigned long long nsel = 0;
     MRFG_CUDA(cudaMemcpyAsync(&nsel, cnt, sizeof nsel, cudaMemcpyDeviceToHost, c.stream));
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
-    Tab64 T = tab64_of(c, t);
     const int rb = 64;
     if (nsel > 0) {
-        k_rerank<<<(nsel + rb - 1) / rb, rb, 0, c.stream>>>(T, d_q64, d_cand, list, nsel, metric,
-                                                            score, vkey, d_err);
+        if (d_dict) {
+            k_rerank_dict<<<(nsel + rb - 1) / rb, rb, 0, c.stream>>>(
+                d_dict, static_cast<int>(c.n), d_q64, d_cand, list, nsel, metric, score, vkey, d_err);
+        } else {
+            k_rerank<<<(nsel + rb - 1) / rb, rb, 0, c.stream>>>(tab64_of(c, *t), d_q64, d_cand, list,
+                                                                nsel, metric, score, vkey, d_err);
+        }
         MRFG_CUDA(cudaGetLastError());
         k_select_flat<<<(nsel + bs - 1) / bs, bs, 0, c.stream>>>(d_cand, list, nsel, score, vkey,
                                                                  vflat);
@@ -254,6 +319,15 @@ int64_t rerank_and_select(Ctx& c, const GridTables& t, const double* d_q64, int6
     }
     MRFG_REQUIRE(!h_missing[0], MRFG_E_RUNTIME, "scan: a query ended without candidates");
     return static_cast<int64_t>(nsel);
+}
+
+void launch_dict_operand(Ctx& c, const float* d_dict, int64_t first, int64_t count, int64_t rows,
+                         int64_t stride, int metric, __half* d_a, float* d_inv2) {
+    const int bs = 256;
+    k_dict_operand<<<(rows * 32 + bs - 1) / bs, bs, 0, c.stream>>>(
+        d_dict, first, count, stride, static_cast<int>(c.n), k_pad_of(c.n),
+        metric == MRFG_METRIC_CC ? 0 : 1, d_a, d_inv2, rows);
+    MRFG_CUDA(cudaGetLastError());
 }
 
 void launch_merge(Ctx& c, const mrfg_match* d_in, int nranks, int64_t nq, mrfg_match* d_out) {

@@ -257,10 +257,34 @@ class Context:
         check(self.lib.mrfg_bloch_norms_dev(self.h, C.byref(g), first, count,
                                             C.c_void_p(d_out_ptr)))
 
-    def brute_force_search(self, fp, g: Grid, metric="cc"):
-        """brute_force_search (dictionary.cpp:241-255) for one fingerprint."""
-        f, s, _ = self.scan_grid(g, np.atleast_2d(fp), metric)
-        return int(f[0]), float(s[0])
+    def brute_force_search(self, queries, dictionary: np.ndarray, metric="cc",
+                           opts: ScanOpts = None):
+        """brute_force_search (dictionary.cpp:241-255) over a STORED dictionary.
+
+        dictionary: (atoms, 2N) float32 unit entries in flat order (generate()'s
+        layout).  Returns (best_flat, best_score, stats) per query."""
+        q = np.ascontiguousarray(np.atleast_2d(queries), dtype=np.complex128)
+        d = np.ascontiguousarray(dictionary, dtype=np.float32)
+        if q.shape[-1] != self.n or d.shape[-1] != 2 * self.n:
+            raise N.InvalidArgument(-1, "query length does not match dictionary entries")
+        out = (Match * q.shape[0])()
+        st = ScanStats()
+        check(self.lib.mrfg_scan_dict(self.h, d.ctypes.data_as(C.POINTER(C.c_float)), d.shape[0],
+                                      _dp(q.view(np.float64)), q.shape[0], METRIC.get(metric, metric),
+                                      C.byref(opts) if opts is not None else None, out, C.byref(st)))
+        arr = np.frombuffer(out, dtype=np.dtype([("flat", np.int64), ("score", np.float64)]))
+        return arr["flat"].copy(), arr["score"].copy(), st
+
+    def scan_dict_device(self, d_dict_ptr: int, natoms: int, d_queries_ptr: int, nq: int,
+                         d_out_ptr: int, metric="cc", flat_range=(0, 0),
+                         opts: ScanOpts = None) -> ScanStats:
+        st = ScanStats()
+        check(self.lib.mrfg_scan_dict_dev(self.h, C.c_void_p(d_dict_ptr), natoms, flat_range[0],
+                                          flat_range[1], C.c_void_p(d_queries_ptr), nq,
+                                          METRIC.get(metric, metric),
+                                          C.byref(opts) if opts is not None else None,
+                                          C.c_void_p(d_out_ptr), C.byref(st)))
+        return st
 
     def screen_scores(self, g: Grid, queries, first: int, count: int, metric="cc",
                       use_simt: bool = False) -> np.ndarray:

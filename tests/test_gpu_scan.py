@@ -144,3 +144,32 @@ def test_cc_map_bit_identical(orc):
     q = fp / np.linalg.norm(fp)
     want = np.minimum(np.abs(e @ q.conj()), 1.0).astype(np.float32)
     np.testing.assert_allclose(got, want, rtol=1e-6)
+
+
+def test_brute_force_search_stored_dictionary(orc, small, small_ref):
+    """K4: stored float32 dictionary (generate() layout) == lattice scan == reference."""
+    oflat, oscore, osecond = small_ref
+    with P.Context(small.schedule) as c:
+        d = c.generate(small.grid, precision=64)  # bit-identical to the reference's entries
+        flat, score, st = c.brute_force_search(small.fps, d)
+    assert_parity(flat, score, oflat, oscore, osecond)
+    assert st.candidates >= len(flat)
+
+
+def test_brute_force_search_arbitrary_dictionary(orc):
+    """Entries need not come from a lattice: random unit atoms vs a numpy FP64 scan."""
+    rng = np.random.default_rng(5)
+    n, atoms = 64, 3000
+    e = rng.standard_normal((atoms, n)) + 1j * rng.standard_normal((atoms, n))
+    e /= np.linalg.norm(e, axis=1, keepdims=True)
+    d = np.empty((atoms, 2 * n), dtype=np.float32)
+    d[:, 0::2], d[:, 1::2] = e.real, e.imag
+    q = e[[5, 17, 2999]] + 0.05 * (rng.standard_normal((3, n)) + 1j * rng.standard_normal((3, n)))
+    s = P.baseline_schedule(n, 1)
+    with P.Context(s) as c:
+        flat, score, _ = c.brute_force_search(q, d)
+    ed = d[:, 0::2].astype(np.float64) + 1j * d[:, 1::2].astype(np.float64)
+    qn = q / np.linalg.norm(q, axis=1, keepdims=True)
+    cc = np.minimum(np.abs(ed @ qn.conj().T), 1.0)
+    np.testing.assert_array_equal(flat, cc.argmax(axis=0))
+    np.testing.assert_allclose(score, cc.max(axis=0), rtol=1e-12)
