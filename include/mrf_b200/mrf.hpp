@@ -1,0 +1,210 @@
+// mrf_b200/mrf.hpp -- drop-in C++ interface for the DGS path on B200.
+//
+// Declares, in namespace mrf, the entry points and value types of the
+// reference library (/root/reference/proj/include/mrf/{sequence,fingerprint,
+// bloch,dictionary,zoom}.hpp) with the SAME signatures and semantics, so code
+// written against the reference compiles unchanged after replacing its
+// includes with this one header and linking libmrf_b200.so (+ libmrfg.so).
+// Each function cites the reference declaration it replaces.  The compute runs
+// on an sm_100 GPU through the C ABI of include/mrfg.h (device: env
+// MRFG_DEVICE, default 0); errors come back as the reference's exceptions.
+// `workers` arguments are accepted for signature compatibility (the GPU grid
+// replaces the host thread pool; results never depended on them).
+#pragma once
+
+#include <array>
+#include <complex>
+#include <cstdint>
+#include <filesystem>
+#include <functional>
+#include <span>
+#include <string>
+#include <utility>
+#include <vector>
+
+struct mrfg_ctx;
+
+namespace mrf {
+
+// ---------------------------------------------------------- sequence.hpp:14-56
+struct ScheduleEntry {
+    double flip_deg = 0, phase_deg = 0, tr_ms = 0, te_ms = 0;
+    double flip_rad() const { return flip_deg * 0.017453292519943295; }
+    double phase_rad() const { return phase_deg * 0.017453292519943295; }
+    double tr_s() const { return tr_ms * 1e-3; }
+    double te_s() const { return te_ms * 1e-3; }
+};
+struct Schedule {
+    std::vector<ScheduleEntry> entries;
+    std::uint64_t seed = 0;
+    std::size_t size() const { return entries.size(); }
+};
+Schedule build_schedule(std::size_t n, std::uint64_t seed);              // sequence.hpp:51
+std::string to_csv(const Schedule& sched);                              // sequence.hpp:56
+void save_csv(const Schedule& sched, const std::filesystem::path& path);
+Schedule load_schedule_csv(const std::filesystem::path& path);
+
+// ------------------------------------------------------- fingerprint.hpp:12-75
+struct TissueParams {
+    double t1 = 0, t2 = 0, df = 0, pd = 1.0;
+};
+struct Fingerprint {
+    std::vector<std::complex<double>> s;
+    bool unit_norm = false;
+    std::size_t size() const { return s.size(); }
+};
+Fingerprint normalize(const Fingerprint& fp);                           // fingerprint.hpp:34
+double cc(const Fingerprint& a, const Fingerprint& b);                  // fingerprint.hpp:40
+double euclidean(const Fingerprint& a, const Fingerprint& b);           // fingerprint.hpp:43
+Fingerprint add_noise(const Fingerprint& fp, double sigma, std::uint64_t seed);  // :47
+double estimate_pd(const Fingerprint& acquired, const Fingerprint& matched_ideal);  // :71
+
+// ------------------------------------------------------------- bloch.hpp:79-102
+class BlochSimulator {
+  public:
+    explicit BlochSimulator(const Schedule& sched);
+    ~BlochSimulator();
+    BlochSimulator(const BlochSimulator&) = delete;
+    BlochSimulator& operator=(const BlochSimulator&) = delete;
+    void simulate(const TissueParams& p, std::complex<double>* out) const;
+    Fingerprint simulate(const TissueParams& p) const;
+    // Batched form (GPU-native): params.size() fingerprints, row-major.
+    std::vector<std::complex<double>> simulate_batch(const std::vector<TissueParams>& params) const;
+    std::size_t length() const { return n_; }
+    mrfg_ctx* native() const { return ctx_; }
+
+  private:
+    mrfg_ctx* ctx_ = nullptr;
+    std::size_t n_ = 0;
+};
+Fingerprint simulate_fingerprint(const TissueParams& p, const Schedule& sched);  // bloch.hpp:102
+
+// -------------------------------------------------------- dictionary.hpp:16-132
+struct AxisSpec {
+    double min = 0, step = 1;
+    std::size_t count = 0;
+    double value(std::size_t k) const { return min + static_cast<double>(k) * step; }
+};
+struct AxisRange {
+    double min = 0, max = 0, step = 1;
+};
+struct ParameterGrid {
+    AxisSpec t1_ms, t2_ms, df_hz;
+    std::size_t total() const { return t1_ms.count * t2_ms.count * df_hz.count; }
+    std::size_t flatten(std::size_t i1, std::size_t i2, std::size_t idf) const {
+        return (i1 * t2_ms.count + i2) * df_hz.count + idf;
+    }
+    struct Index3 {
+        std::size_t i1, i2, idf;
+    };
+    Index3 unflatten(std::size_t flat) const {
+        const std::size_t idf = flat % df_hz.count, rest = flat / df_hz.count;
+        return {rest / t2_ms.count, rest % t2_ms.count, idf};
+    }
+    TissueParams params_at(std::size_t i1, std::size_t i2, std::size_t idf) const {
+        return {t1_ms.value(i1) * 1e-3, t2_ms.value(i2) * 1e-3, df_hz.value(idf), 1.0};
+    }
+};
+ParameterGrid grid_from_ranges(const AxisRange& t1_ms, const AxisRange& t2_ms,
+                               const AxisRange& df_hz);                 // dictionary.hpp:61
+using Digest = std::array<std::uint8_t, 32>;
+Digest schedule_digest(const Schedule& sched);                          // dictionary.hpp:67
+std::string digest_hex(const Digest& d);
+struct Dictionary {
+    ParameterGrid grid;
+    Digest digest{};
+    std::size_t entry_len = 0;
+    std::vector<float> data;
+    std::span<const float> entry(std::size_t flat) const {
+        return {data.data() + flat * 2 * entry_len, 2 * entry_len};
+    }
+};
+Dictionary generate(const ParameterGrid& grid, const Schedule& sched, int workers = 1);  // :85
+enum class Metric { cc, euclidean };
+struct Match {
+    TissueParams params;
+    double score = 0;
+    std::size_t evaluations = 0;
+};
+Match brute_force_search(const Fingerprint& fp, const Dictionary& dict,
+                         Metric metric = Metric::cc);                   // dictionary.hpp:108
+struct ScanOutcome {
+    std::vector<Match> matches;
+    std::vector<double> scan_seconds;
+    double generate_seconds = 0;
+};
+ScanOutcome scan_grid(const ParameterGrid& grid, const Schedule& sched,
+                      const std::vector<Fingerprint>& queries, Metric metric = Metric::cc,
+                      int workers = 1, std::size_t chunk_entries = 1 << 15);  // :120-122
+void cc_map(const Fingerprint& fp, const ParameterGrid& grid, const Schedule& sched,
+            const std::function<void(std::size_t first_flat, std::span<const float>)>& sink,
+            int workers = 1, std::size_t chunk_entries = 1 << 15);        // :127-129
+
+// -------------------------------------------------------------- zoom.hpp:17-178
+struct SearchRanges {
+    AxisRange t1_ms{100, 5500, 1};
+    AxisRange t2_ms{50, 1200, 1};
+    AxisRange df_hz{-300, 300, 1};
+};
+struct ZoomConfig {
+    Metric metric = Metric::cc;
+    Metric final_metric = Metric::cc;
+    int smooth_k = 0;
+    double omega_hz = 70, df_coarse_hz = 60, df_refine_hz = 3, df_window_hz = 150;
+    double plateau_eps = 1e-7, heavy_noise_cc = 0.1, fallback_coarse_hz = 30,
+           fallback_window_hz = 300;
+    std::vector<double> t1t2_2d_steps_ms{200, 100};
+    std::vector<double> t1t2_1d_steps_ms{100, 50, 20, 10};
+    double final_2d_step_ms = 1;
+    double init_t1_ms = 1000, init_t2_ms = 500;
+    double prior_window_t1_ms = 3000, prior_window_t2_ms = 800, prior_window_df_hz = 150;
+};
+struct StageLog {
+    std::string stage;
+    std::size_t evaluations = 0;
+    double best = 0;
+    double t1_ms = 0, t2_ms = 0, df_hz = 0;
+};
+struct QuantResult {
+    TissueParams params;
+    double score = 0;
+    std::size_t evaluations = 0;
+    double seconds = 0;
+    std::vector<StageLog> trace;  // not recorded by the GPU kernel (empty)
+};
+struct DfSearchParams {
+    long coarse = 60, refine = 3, finest = 1, window_half = 75, omega = 70;
+    double plateau_eps = 1e-7, heavy_cc = 0.1;
+    long fallback_coarse = 30, fallback_window_half = 150;
+    bool allow_fallback = true;
+};
+// Generic host forms over caller objectives (zoom.hpp:127-143).
+long search_df(const std::function<double(long)>& f, long lo, long hi, const DfSearchParams& prm,
+               const std::function<void(const char*, long, double)>& stage = {});
+long zoom_1d(const std::function<double(long)>& f, long lo, long hi, long init,
+             std::span<const long> steps);
+std::pair<long, long> zoom_2d(const std::function<double(long, long)>& f, long lo1, long hi1,
+                              long lo2, long hi2, long init1, long init2,
+                              std::span<const std::pair<long, long>> steps);
+QuantResult quantify(const Fingerprint& fp, const SearchRanges& ranges, const ZoomConfig& cfg,
+                     const Schedule& sched, const Dictionary* df_dict = nullptr,
+                     const Dictionary* full_dict = nullptr);            // zoom.hpp:148-151
+// Batched form (GPU-native): one call, many fingerprints.
+std::vector<QuantResult> quantify_batch(const std::vector<Fingerprint>& fps,
+                                        const SearchRanges& ranges, const ZoomConfig& cfg,
+                                        const Schedule& sched);
+Dictionary make_df_dictionary(const SearchRanges& ranges, const ZoomConfig& cfg,
+                              const Schedule& sched, int workers = 1);  // zoom.hpp:157-158
+struct SliceResult {
+    int nx = 0, ny = 0;
+    std::vector<double> t1_ms, t2_ms, df_hz, pd, score;
+    std::vector<std::size_t> evaluations;
+    std::size_t total_evaluations = 0;
+    double seconds = 0;
+};
+SliceResult quantify_slice(const std::vector<Fingerprint>& fps, const std::vector<std::uint8_t>& mask,
+                           int nx, int ny, const SearchRanges& ranges, const ZoomConfig& cfg,
+                           const Schedule& sched, bool use_prior, int workers = 1,
+                           const Dictionary* df_dict = nullptr);        // zoom.hpp:174-178
+
+}  // namespace mrf

@@ -192,9 +192,20 @@ int mrfg_cc_map(mrfg_ctx* ctx, const mrfg_grid* grid, const double* query, int64
  * (zoom.cpp:589-615) when use_prior != 0. */
 int mrfg_quantify(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
                   const double* fps, int64_t nvox, mrfg_quant* out);
+/* use_prior: 0 = independent voxels (zoom.cpp:616-624); 1 = the reference's
+ * strict raster order, each voxel seeded and windowed by the previous masked
+ * voxel (zoom.cpp:589-615; one voxel in flight, exact); 2 = the row-wavefront
+ * relaxation SPEC.md:449 permits (rows in parallel, a row's first voxel takes
+ * its prior from the first masked voxel of the nearest row above). */
 int mrfg_quantify_slice(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
                         const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
                         mrfg_quant* out, double* seconds);
+/* quantify_impl with explicit per-voxel lattice bounds (lo1,hi1,lo2,hi2,lodf,hidf)
+ * and initial T1/T2 [ms] (zoom.cpp:416-429); either array may be NULL (full
+ * bounds / cfg->init_*). */
+int mrfg_quantify_bounded(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                          const double* fps, int64_t nvox, const int64_t* bounds,
+                          const double* init_ms, mrfg_quant* out);
 
 #ifdef __cplusplus
 }

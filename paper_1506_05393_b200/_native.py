@@ -72,7 +72,7 @@ EXPORTS = [
     "mrfg_set_stream", "mrfg_synchronize", "mrfg_simulate", "mrfg_simulate_dev", "mrfg_generate",
     "mrfg_generate_dev", "mrfg_bloch_norms_dev", "mrfg_scan_grid", "mrfg_scan_grid_dev",
     "mrfg_scan_dict", "mrfg_scan_dict_dev",
-    "mrfg_merge_matches_dev", "mrfg_screen_scores", "mrfg_cc_map", "mrfg_quantify", "mrfg_quantify_slice",
+    "mrfg_merge_matches_dev", "mrfg_screen_scores", "mrfg_cc_map", "mrfg_quantify", "mrfg_quantify_slice", "mrfg_quantify_bounded",
 ]
 
 _lib = None
@@ -127,6 +127,8 @@ def load() -> C.CDLL:
     L.mrfg_cc_map.argtypes = [vp, C.POINTER(Grid), dp, i64, i64, C.POINTER(C.c_float)]
     L.mrfg_quantify.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp, i64,
                                 C.POINTER(Quant)]
+    L.mrfg_quantify_bounded.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp, i64,
+                                        C.POINTER(i64), dp, C.POINTER(Quant)]
     L.mrfg_quantify_slice.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp,
                                       C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int,
                                       C.POINTER(Quant), dp]

@@ -716,23 +716,35 @@ int mrfg_cc_map(mrfg_ctx* h, const mrfg_grid* grid, const double* query, int64_t
     });
 }
 
-int mrfg_quantify(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
-                  const double* fps, int64_t nvox, mrfg_quant* out) {
+int mrfg_quantify_bounded(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                          const double* fps, int64_t nvox, const int64_t* bounds,
+                          const double* init_ms, mrfg_quant* out) {
     return guard([&] {
         Ctx& c = h->c;
         MRFG_CUDA(cudaSetDevice(c.device));
         MRFG_REQUIRE(nvox >= 0, MRFG_E_INVALID, "quantify: negative voxel count");
         if (nvox == 0) return;
+        if (bounds)
+            for (int64_t k = 0; k < nvox; ++k)
+                MRFG_REQUIRE(bounds[6 * k] <= bounds[6 * k + 1] && bounds[6 * k + 2] <= bounds[6 * k + 3] &&
+                                 bounds[6 * k + 4] <= bounds[6 * k + 5],
+                             MRFG_E_INVALID, "zoom_2d: empty range");  // zoom.cpp:176,287
         DevBuf d_fps, d_out;
         d_fps.ensure(sizeof(double) * 2 * c.n * nvox);
         d_out.ensure(sizeof(mrfg_quant) * nvox);
         MRFG_CUDA(cudaMemcpyAsync(d_fps.p, fps, sizeof(double) * 2 * c.n * nvox,
                                   cudaMemcpyHostToDevice, c.stream));
-        run_quantify(c, *lattice, *cfg, d_fps.as<double>(), nvox, nullptr, nullptr,
-                     d_out.as<mrfg_quant>());
-        MRFG_CUDA(cudaMemcpyAsync(out, d_out.p, sizeof(mrfg_quant) * nvox, cudaMemcpyDeviceToHost,
-                                  c.stream));
-        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        try {
+            run_quantify(c, *lattice, *cfg, d_fps.as<double>(), nvox, bounds, init_ms,
+                         d_out.as<mrfg_quant>());
+            MRFG_CUDA(cudaMemcpyAsync(out, d_out.p, sizeof(mrfg_quant) * nvox, cudaMemcpyDeviceToHost,
+                                      c.stream));
+            MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        } catch (...) {
+            d_fps.release();
+            d_out.release();
+            throw;
+        }
         d_fps.release();
         d_out.release();
         for (int64_t k = 0; k < nvox; ++k) {  // AxisSpec::value (dictionary.hpp:22)
@@ -743,6 +755,47 @@ int mrfg_quantify(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config*
     });
 }
 
+int mrfg_quantify(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                  const double* fps, int64_t nvox, mrfg_quant* out) {
+    return mrfg_quantify_bounded(h, lattice, cfg, fps, nvox, nullptr, nullptr, out);
+}
+
+namespace {
+// Prior window around a finished voxel (zoom.cpp:595-610): the prior's
+// parameters round-trip through seconds exactly like QuantResult::params.
+void prior_of(const mrfg_grid& g, const mrfg_zoom_config& cfg, const mrfg_quant& pr, int64_t* b,
+              double* init) {
+    auto snap = [](double v, const mrfg_axis& ax) { return std::lround((v - ax.min) / ax.step); };
+    auto units = [](double s, double fine) {
+        long u = std::lround(s / fine);
+        return u > 0 ? u : 1L;
+    };
+    const double t1 = (g.t1_ms.min + static_cast<double>(pr.i1) * g.t1_ms.step) * 1e-3 * 1e3;
+    const double t2 = (g.t2_ms.min + static_cast<double>(pr.i2) * g.t2_ms.step) * 1e-3 * 1e3;
+    const double df = g.df_hz.min + static_cast<double>(pr.idf) * g.df_hz.step;
+    init[0] = t1;
+    init[1] = t2;
+    const long p1 = snap(t1, g.t1_ms), p2 = snap(t2, g.t2_ms), pdf = snap(df, g.df_hz);
+    const long w1 = units(cfg.prior_window_t1_ms, g.t1_ms.step);
+    const long w2 = units(cfg.prior_window_t2_ms, g.t2_ms.step);
+    const long wdf = units(cfg.prior_window_df_hz, g.df_hz.step);
+    b[0] = std::max<int64_t>(0, p1 - w1);
+    b[1] = std::min<int64_t>(g.t1_ms.count - 1, p1 + w1);
+    b[2] = std::max<int64_t>(0, p2 - w2);
+    b[3] = std::min<int64_t>(g.t2_ms.count - 1, p2 + w2);
+    b[4] = std::max<int64_t>(0, pdf - wdf);
+    b[5] = std::min<int64_t>(g.df_hz.count - 1, pdf + wdf);
+}
+void full_bounds(const mrfg_grid& g, int64_t* b) {
+    b[0] = 0;
+    b[1] = g.t1_ms.count - 1;
+    b[2] = 0;
+    b[3] = g.t2_ms.count - 1;
+    b[4] = 0;
+    b[5] = g.df_hz.count - 1;
+}
+}  // namespace
+
 int mrfg_quantify_slice(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
                         const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
                         mrfg_quant* out, double* seconds) {
@@ -751,23 +804,80 @@ int mrfg_quantify_slice(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_c
         MRFG_CUDA(cudaSetDevice(c.device));
         MRFG_REQUIRE(nx > 0 && ny > 0, MRFG_E_INVALID,
                      "quantify_slice: inconsistent raster dimensions");  // zoom.cpp:561-562
+        MRFG_REQUIRE(use_prior >= 0 && use_prior <= 2, MRFG_E_INVALID, "quantify_slice: bad prior mode");
         auto t0 = std::chrono::steady_clock::now();
-        const int64_t nv = static_cast<int64_t>(nx) * ny;
+        const int64_t nv = static_cast<int64_t>(nx) * ny, n2 = 2 * c.n;
         std::memset(out, 0, sizeof(mrfg_quant) * nv);
-        std::vector<int64_t> idx;
-        for (int64_t i = 0; i < nv; ++i)
-            if (mask[i]) idx.push_back(i);
-        const int64_t m = static_cast<int64_t>(idx.size());
-        if (m > 0) {
-            std::vector<double> packed(2 * c.n * m);
-            for (int64_t k = 0; k < m; ++k)
-                std::memcpy(&packed[2 * c.n * k], fps + 2 * c.n * idx[k], sizeof(double) * 2 * c.n);
-            std::vector<mrfg_quant> res(m);
-            MRFG_REQUIRE(use_prior == 0, MRFG_E_INVALID,
-                         "quantify_slice: neighbour-prior mode not available in this build");
-            int rc = mrfg_quantify(h, lattice, cfg, packed.data(), m, res.data());
+        auto run = [&](const std::vector<int64_t>& vox, const std::vector<int64_t>* b,
+                       const std::vector<double>* init) {
+            std::vector<double> packed(n2 * vox.size());
+            for (size_t k = 0; k < vox.size(); ++k)
+                std::memcpy(&packed[n2 * k], fps + n2 * vox[k], sizeof(double) * n2);
+            std::vector<mrfg_quant> res(vox.size());
+            int rc = mrfg_quantify_bounded(h, lattice, cfg, packed.data(), static_cast<int64_t>(vox.size()),
+                                           b ? b->data() : nullptr, init ? init->data() : nullptr,
+                                           res.data());
             if (rc) throw Error{rc, g_err};
-            for (int64_t k = 0; k < m; ++k) out[idx[k]] = res[k];
+            for (size_t k = 0; k < vox.size(); ++k) out[vox[k]] = res[k];
+        };
+        if (use_prior == 0) {
+            std::vector<int64_t> idx;
+            for (int64_t i = 0; i < nv; ++i)
+                if (mask[i]) idx.push_back(i);
+            if (!idx.empty()) run(idx, nullptr, nullptr);
+        } else if (use_prior == 1) {
+            // strict raster order: one voxel in flight (zoom.cpp:589-615)
+            bool have = false;
+            int64_t prev = -1;
+            for (int64_t i = 0; i < nv; ++i) {
+                if (!mask[i]) continue;
+                std::vector<int64_t> b(6);
+                std::vector<double> init(2);
+                if (have) {
+                    prior_of(*lattice, *cfg, out[prev], b.data(), init.data());
+                } else {
+                    full_bounds(*lattice, b.data());
+                    init = {cfg->init_t1_ms, cfg->init_t2_ms};
+                }
+                run({i}, &b, &init);
+                prev = i;
+                have = true;
+            }
+        } else {
+            // row wavefront: step s runs, for every row y, its (s - rank(y))-th
+            // masked voxel, where rank counts rows that hold masked voxels.
+            std::vector<std::vector<int64_t>> rows;
+            for (int y = 0; y < ny; ++y) {
+                std::vector<int64_t> r;
+                for (int x = 0; x < nx; ++x)
+                    if (mask[static_cast<int64_t>(y) * nx + x]) r.push_back(static_cast<int64_t>(y) * nx + x);
+                if (!r.empty()) rows.push_back(std::move(r));
+            }
+            const int64_t R = static_cast<int64_t>(rows.size());
+            int64_t steps = 0;
+            for (int64_t r = 0; r < R; ++r) steps = std::max<int64_t>(steps, r + static_cast<int64_t>(rows[r].size()));
+            for (int64_t s = 0; s < steps; ++s) {
+                std::vector<int64_t> vox, b;
+                std::vector<double> init;
+                for (int64_t r = 0; r < R; ++r) {
+                    const int64_t k = s - r;
+                    if (k < 0 || k >= static_cast<int64_t>(rows[r].size())) continue;
+                    int64_t bb[6];
+                    double ii[2];
+                    const int64_t prev = k > 0 ? rows[r][k - 1] : (r > 0 ? rows[r - 1][0] : -1);
+                    if (prev >= 0) {
+                        prior_of(*lattice, *cfg, out[prev], bb, ii);
+                    } else {
+                        full_bounds(*lattice, bb);
+                        ii[0] = cfg->init_t1_ms;
+                        ii[1] = cfg->init_t2_ms;
+                    }
+                    vox.push_back(rows[r][k]);
+                    b.insert(b.end(), bb, bb + 6);
+                    init.insert(init.end(), ii, ii + 2);
+                }
+                if (!vox.empty()) run(vox, &b, &init);
+            }
         }
         if (seconds)
             *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

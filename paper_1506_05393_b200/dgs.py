@@ -316,8 +316,24 @@ class Context:
                                      _dp(q.view(np.float64)), q.shape[0], out))
         return quant_array(out)
 
+    def quantify_bounded(self, fps, lattice: Grid, cfg: ZoomConfig = None, bounds=None,
+                         init_ms=None) -> "np.ndarray":
+        """quantify_impl with per-voxel index bounds (V,6) and initial T1/T2 ms (V,2)."""
+        q = np.ascontiguousarray(np.atleast_2d(fps), dtype=np.complex128)
+        cfg = cfg or zoom_config()
+        out = (Quant * q.shape[0])()
+        b = None if bounds is None else np.ascontiguousarray(bounds, dtype=np.int64)
+        i = None if init_ms is None else np.ascontiguousarray(init_ms, dtype=np.float64)
+        check(self.lib.mrfg_quantify_bounded(
+            self.h, C.byref(lattice), C.byref(cfg), _dp(q.view(np.float64)), q.shape[0],
+            None if b is None else b.ctypes.data_as(C.POINTER(C.c_int64)),
+            None if i is None else _dp(i), out))
+        return quant_array(out)
+
     def quantify_slice(self, fps, mask, nx: int, ny: int, lattice: Grid,
-                       cfg: ZoomConfig = None, use_prior: bool = False):
+                       cfg: ZoomConfig = None, use_prior: int = 0):
+        """quantify_slice (zoom.cpp:555-629).  use_prior: 0/False none, 1/True the
+        reference's raster order, 2 the row-wavefront relaxation."""
         q = np.ascontiguousarray(fps, dtype=np.complex128)
         m = np.ascontiguousarray(mask, dtype=np.uint8)
         cfg = cfg or zoom_config()

@@ -137,3 +137,44 @@ def test_zoom_errors():
             c.quantify(np.zeros((1, 32), dtype=np.complex128), g)
         with pytest.raises(ValueError):
             c.quantify(np.ones((1, 32), dtype=np.complex128), g, P.zoom_config(smooth_k=3))
+
+
+def _slice_problem(orc):
+    s = P.reference_schedule(60, 15)
+    g = P.grid_from_ranges((600, 1000, 10), (80, 160, 5), (-20, 30, 2))
+    cfg = P.zoom_config(df_coarse_hz=2.0, prior_window_t1_ms=60, prior_window_t2_ms=30,
+                        prior_window_df_hz=10)
+    nx, ny = 6, 5
+    mask = np.ones(nx * ny, dtype=np.uint8)
+    mask[[0, 7, 29]] = 0
+    fps = np.zeros((nx * ny, 60), dtype=np.complex128)
+    for v in range(nx * ny):
+        if mask[v]:
+            x, y = v % nx, v // nx
+            t = (18 + x // 2, 7 + y // 2, 9 + (x + y) % 3)
+            fps[v] = orc.add_noise(orc.simulate(to_oracle_sched(s), *[float(u) for u in P.params_at(g, *t)]),
+                                   0.001, 70 + v)
+    return s, g, cfg, nx, ny, mask, fps
+
+
+def test_zoom_slice_raster_prior_matches_reference(orc):
+    """use_prior=1: the reference's sequential raster semantics, evals included."""
+    s, g, cfg, nx, ny, mask, fps = _slice_problem(orc)
+    with P.Context(s) as c:
+        res, _ = c.quantify_slice(fps, mask, nx, ny, g, cfg, use_prior=1)
+    w = orc.quantify_slice(to_oracle_sched(s), to_oracle_grid(g), ocfg(cfg), fps, mask, nx, ny, True)
+    for v in range(nx * ny):
+        assert (res["i1"][v], res["i2"][v], res["idf"][v], res["evaluations"][v]) == \
+               (w[v].i1, w[v].i2, w[v].idf, w[v].evaluations), v
+
+
+def test_zoom_slice_wavefront_prior(orc):
+    """use_prior=2 (SPEC.md:449 relaxation): same maps as without priors, fewer evals."""
+    s, g, cfg, nx, ny, mask, fps = _slice_problem(orc)
+    with P.Context(s) as c:
+        a, _ = c.quantify_slice(fps, mask, nx, ny, g, cfg, use_prior=0)
+        b, _ = c.quantify_slice(fps, mask, nx, ny, g, cfg, use_prior=2)
+    m = mask.astype(bool)
+    for k in ("i1", "i2", "idf"):
+        np.testing.assert_array_equal(a[k][m], b[k][m])
+    assert b["evaluations"].sum() < a["evaluations"].sum()
