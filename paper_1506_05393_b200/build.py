@@ -13,6 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmrfg.so")
+SHIM = os.path.join(HERE, "libmrf_b200.so")  # the reference's C++ interface over LIB
 SOURCES = ["abi.cu", "bloch.cu", "match_sm100.cu", "rerank.cu", "zoom.cu", "synth.cpp"]
 HEADERS = ["mrfg_internal.cuh", "sim64.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -29,8 +30,11 @@ def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "mrfg.h"),
-                                                                 __file__]
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [
+        os.path.join(ROOT, "include", "mrfg.h"), os.path.join(ROOT, "include", "mrf_b200", "mrf.hpp"),
+        os.path.join(CSRC, "host", "mrf_api.cpp"), __file__]
+    if not os.path.exists(SHIM):
+        return True
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
@@ -64,7 +68,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     link = [_nvcc(), *ARCH, "-shared", "-ccbin", "g++", "-Xcompiler", "-fopenmp", "-o", LIB, *objs,
             "-lcudart_static", "-lgomp"]
     subprocess.run(link, check=True)
+    build_shim()
     return LIB
+
+
+def build_shim() -> str:
+    """libmrf_b200.so: include/mrf_b200/mrf.hpp implemented over libmrfg.so."""
+    cmd = ["g++", "-std=c++20", "-O3", "-fPIC", "-shared", "-ffp-contract=off",
+           "-I", os.path.join(ROOT, "include"), os.path.join(CSRC, "host", "mrf_api.cpp"),
+           "-o", SHIM, "-L", HERE, "-lmrfg", "-lcrypto", "-Wl,-rpath,$ORIGIN"]
+    subprocess.run(cmd, check=True)
+    return SHIM
 
 
 if __name__ == "__main__":

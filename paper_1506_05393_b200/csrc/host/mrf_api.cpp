@@ -1,0 +1,700 @@
+// mrf_api.cpp -- the reference's C++ interface (include/mrf_b200/mrf.hpp) on top
+// of the C ABI (include/mrfg.h).  Built as libmrf_b200.so.
+//
+// Heavy work (simulation, dictionary generation, brute-force search, cc_map,
+// MRF-ZOOM) is forwarded to the sm_100a kernels; the small host pieces the
+// reference's callers also use (schedule I/O, normalize/cc/estimate_pd on single
+// fingerprints, the generic search_df/zoom_1d/zoom_2d over caller objectives)
+// are host restatements with the reference's operand order.  ABI status codes
+// become the reference's exceptions.
+#include <openssl/evp.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <stdexcept>
+
+#include "mrf_b200/mrf.hpp"
+#include "mrfg.h"
+
+namespace mrf {
+namespace {
+
+int device() {
+    const char* e = std::getenv("MRFG_DEVICE");
+    return e ? std::atoi(e) : 0;
+}
+
+[[noreturn]] void raise(int rc) {
+    const std::string msg = mrfg_last_error();
+    if (rc == MRFG_E_INVALID) throw std::invalid_argument(msg);
+    if (rc == MRFG_E_RANGE) throw std::out_of_range(msg);
+    throw std::runtime_error(msg);
+}
+void check(int rc) {
+    if (rc != MRFG_OK) raise(rc);
+}
+
+struct CtxGuard {
+    mrfg_ctx* h = nullptr;
+    ~CtxGuard() {
+        if (h) mrfg_destroy(h);
+    }
+};
+
+mrfg_ctx* create(const Schedule& s) {
+    const std::size_t n = s.size();
+    std::vector<double> f(n), p(n), tr(n), te(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        f[i] = s.entries[i].flip_deg;
+        p[i] = s.entries[i].phase_deg;
+        tr[i] = s.entries[i].tr_ms;
+        te[i] = s.entries[i].te_ms;
+    }
+    mrfg_ctx* h = nullptr;
+    check(mrfg_create(f.data(), p.data(), tr.data(), te.data(), static_cast<int64_t>(n), device(), &h));
+    return h;
+}
+
+// A context for stored-dictionary searches: only the entry length matters.
+mrfg_ctx* create_len(std::size_t n) {
+    Schedule s;
+    s.entries.assign(n, ScheduleEntry{0.0, 0.0, 1.0, 0.5});
+    return create(s);
+}
+
+mrfg_axis to_axis(const AxisSpec& a) { return {a.min, a.step, static_cast<int64_t>(a.count)}; }
+mrfg_grid to_grid(const ParameterGrid& g) { return {to_axis(g.t1_ms), to_axis(g.t2_ms), to_axis(g.df_hz)}; }
+
+mrfg_zoom_config to_cfg(const ZoomConfig& z) {
+    mrfg_zoom_config c;
+    mrfg_zoom_config_default(&c);
+    c.metric = z.metric == Metric::cc ? MRFG_METRIC_CC : MRFG_METRIC_EUCLIDEAN;
+    c.final_metric = z.final_metric == Metric::cc ? MRFG_METRIC_CC : MRFG_METRIC_EUCLIDEAN;
+    c.smooth_k = z.smooth_k;
+    c.omega_hz = z.omega_hz;
+    c.df_coarse_hz = z.df_coarse_hz;
+    c.df_refine_hz = z.df_refine_hz;
+    c.df_window_hz = z.df_window_hz;
+    c.plateau_eps = z.plateau_eps;
+    c.heavy_noise_cc = z.heavy_noise_cc;
+    c.fallback_coarse_hz = z.fallback_coarse_hz;
+    c.fallback_window_hz = z.fallback_window_hz;
+    if (z.t1t2_2d_steps_ms.size() > 8 || z.t1t2_1d_steps_ms.size() > 8)
+        throw std::invalid_argument("ZoomConfig: at most 8 steps per stage on the GPU");
+    c.n2d = static_cast<int32_t>(z.t1t2_2d_steps_ms.size());
+    c.n1d = static_cast<int32_t>(z.t1t2_1d_steps_ms.size());
+    std::copy(z.t1t2_2d_steps_ms.begin(), z.t1t2_2d_steps_ms.end(), c.t1t2_2d_steps_ms);
+    std::copy(z.t1t2_1d_steps_ms.begin(), z.t1t2_1d_steps_ms.end(), c.t1t2_1d_steps_ms);
+    c.final_2d_step_ms = z.final_2d_step_ms;
+    c.init_t1_ms = z.init_t1_ms;
+    c.init_t2_ms = z.init_t2_ms;
+    c.prior_window_t1_ms = z.prior_window_t1_ms;
+    c.prior_window_t2_ms = z.prior_window_t2_ms;
+    c.prior_window_df_hz = z.prior_window_df_hz;
+    return c;
+}
+
+const double* interleaved(const Fingerprint& fp) {
+    return reinterpret_cast<const double*>(fp.s.data());  // std::complex<double> is 2 doubles
+}
+
+std::string g9(double x) {
+    char b[40];
+    std::snprintf(b, sizeof b, "%.9g", x);
+    return b;
+}
+
+double norm2(const Fingerprint& fp) {  // fingerprint.cpp:14-18
+    double acc = 0;
+    for (const auto& v : fp.s) acc += v.real() * v.real() + v.imag() * v.imag();
+    return std::sqrt(acc);
+}
+
+std::vector<std::string> split_csv(const std::string& line) {
+    std::vector<std::string> out;
+    std::string cur;
+    for (char ch : line) {
+        if (ch == ',') {
+            out.push_back(cur);
+            cur.clear();
+        } else if (ch != '\r') {
+            cur += ch;
+        }
+    }
+    out.push_back(cur);
+    return out;
+}
+
+double parse_num(const std::string& s) {
+    const char* p = s.c_str();
+    char* end = nullptr;
+    double v = std::strtod(p, &end);
+    while (end && *end == ' ') ++end;
+    if (end == p || (end && *end != '\0')) throw std::runtime_error("bad numeric field: '" + s + "'");
+    return v;
+}
+
+QuantResult to_result(const ParameterGrid& lat, const mrfg_quant& q, double seconds) {
+    QuantResult r;
+    r.params = lat.params_at(static_cast<std::size_t>(q.i1), static_cast<std::size_t>(q.i2),
+                             static_cast<std::size_t>(q.idf));
+    r.params.pd = q.pd;
+    r.score = q.score;
+    r.evaluations = static_cast<std::size_t>(q.evaluations);
+    r.seconds = seconds;
+    return r;
+}
+
+// df_dict validation of zoom.cpp:61-69 and :430-437.  A valid slab changes
+// nothing but the cost of stage 1 (its entries equal the generated ones), so
+// the GPU path simply simulates.
+void check_df_dict(const Dictionary* d, const ParameterGrid& lat, const ZoomConfig& cfg,
+                   const Schedule& sched) {
+    if (!d) return;
+    auto close = [](double a, double b) {
+        return std::abs(a - b) <= 1e-9 * std::max({1.0, std::abs(a), std::abs(b)});
+    };
+    if (d->digest != schedule_digest(sched))
+        throw std::invalid_argument("objective: df dictionary from another schedule");
+    if (d->grid.t1_ms.count != 1 || d->grid.t2_ms.count != 1)
+        throw std::invalid_argument("objective: df dictionary must fix T1 and T2");
+    if (!close(d->grid.df_hz.min, lat.df_hz.min) || !close(d->grid.df_hz.step, lat.df_hz.step) ||
+        d->grid.df_hz.count != lat.df_hz.count)
+        throw std::invalid_argument("lattice mismatch: df axis");
+    if (d->entry_len != sched.size())
+        throw std::invalid_argument("objective: df dictionary entry length mismatch");
+    auto snap = [](double v, const AxisSpec& a) { return std::lround((v - a.min) / a.step); };
+    long i1 = std::clamp(snap(cfg.init_t1_ms, lat.t1_ms), 0L, static_cast<long>(lat.t1_ms.count) - 1);
+    long i2 = std::clamp(snap(cfg.init_t2_ms, lat.t2_ms), 0L, static_cast<long>(lat.t2_ms.count) - 1);
+    if (!close(d->grid.t1_ms.value(0), lat.t1_ms.value(static_cast<std::size_t>(i1))))
+        throw std::invalid_argument("lattice mismatch: df dictionary T1 vs initial value");
+    if (!close(d->grid.t2_ms.value(0), lat.t2_ms.value(static_cast<std::size_t>(i2))))
+        throw std::invalid_argument("lattice mismatch: df dictionary T2 vs initial value");
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ sequence
+Schedule build_schedule(std::size_t n, std::uint64_t seed) {
+    std::vector<double> f(n), p(n), tr(n), te(n);
+    check(mrfg_reference_schedule(static_cast<int64_t>(n), seed, f.data(), p.data(), tr.data(), te.data()));
+    Schedule s;
+    s.seed = seed;
+    s.entries.resize(n);
+    for (std::size_t i = 0; i < n; ++i) s.entries[i] = {f[i], p[i], tr[i], te[i]};
+    return s;
+}
+
+std::string to_csv(const Schedule& sched) {
+    std::string out = "idx,flip_deg,phase_deg,tr_ms,te_ms\n";
+    for (std::size_t k = 0; k < sched.size(); ++k) {
+        const ScheduleEntry& e = sched.entries[k];
+        out += std::to_string(k) + ',' + g9(e.flip_deg) + ',' + g9(e.phase_deg) + ',' + g9(e.tr_ms) + ',' +
+               g9(e.te_ms) + '\n';
+    }
+    return out;
+}
+
+void save_csv(const Schedule& sched, const std::filesystem::path& path) {
+    std::ofstream f(path, std::ios::binary);
+    if (!f) throw std::runtime_error("cannot open for write: " + path.string());
+    f << to_csv(sched);
+    if (!f) throw std::runtime_error("write failed: " + path.string());
+}
+
+Schedule load_schedule_csv(const std::filesystem::path& path) {  // sequence.cpp:112-140
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw std::runtime_error("cannot open schedule: " + path.string());
+    std::string line;
+    if (!std::getline(f, line) ||
+        split_csv(line) != std::vector<std::string>{"idx", "flip_deg", "phase_deg", "tr_ms", "te_ms"})
+        throw std::runtime_error("bad schedule header in " + path.string());
+    Schedule s;
+    std::size_t expect = 0;
+    while (std::getline(f, line)) {
+        if (line.empty()) continue;
+        auto c = split_csv(line);
+        if (c.size() != 5) throw std::runtime_error("bad schedule row in " + path.string() + ": " + line);
+        if (static_cast<std::size_t>(parse_num(c[0])) != expect)
+            throw std::runtime_error("non-sequential idx in " + path.string());
+        ScheduleEntry e{parse_num(c[1]), parse_num(c[2]), parse_num(c[3]), parse_num(c[4])};
+        if (e.tr_ms <= 0 || e.te_ms < 0 || e.te_ms > e.tr_ms)
+            throw std::runtime_error("invalid timing in " + path.string() + ": " + line);
+        s.entries.push_back(e);
+        ++expect;
+    }
+    return s;
+}
+
+// --------------------------------------------------------------- fingerprint
+Fingerprint normalize(const Fingerprint& fp) {  // fingerprint.cpp:28-37
+    const double nn = norm2(fp);
+    if (nn == 0) throw std::invalid_argument("normalize: zero fingerprint");
+    Fingerprint out;
+    out.s.reserve(fp.size());
+    const double inv = 1.0 / nn;
+    for (const auto& v : fp.s) out.s.emplace_back(v.real() * inv, v.imag() * inv);
+    out.unit_norm = true;
+    return out;
+}
+
+double cc(const Fingerprint& a, const Fingerprint& b) {  // fingerprint.cpp:39-55
+    if (a.size() != b.size()) throw std::invalid_argument("cc: length mismatch");
+    if (a.size() == 0) throw std::invalid_argument("cc: empty input");
+    double re = 0, im = 0;
+    for (std::size_t j = 0; j < a.size(); ++j) {
+        re += a.s[j].real() * b.s[j].real() + a.s[j].imag() * b.s[j].imag();
+        im += a.s[j].imag() * b.s[j].real() - a.s[j].real() * b.s[j].imag();
+    }
+    double num = std::sqrt(re * re + im * im);
+    if (!(a.unit_norm && b.unit_norm)) {
+        const double na = norm2(a), nb = norm2(b);
+        if (na == 0 || nb == 0) throw std::invalid_argument("cc: zero fingerprint");
+        num /= na * nb;
+    }
+    return num < 1.0 ? num : 1.0;
+}
+
+double euclidean(const Fingerprint& a, const Fingerprint& b) {  // fingerprint.cpp:57-66
+    if (a.size() != b.size()) throw std::invalid_argument("euclidean: length mismatch");
+    if (a.size() == 0) throw std::invalid_argument("euclidean: empty input");
+    double acc = 0;
+    for (std::size_t j = 0; j < a.size(); ++j) {
+        const double dr = a.s[j].real() - b.s[j].real(), di = a.s[j].imag() - b.s[j].imag();
+        acc += dr * dr + di * di;
+    }
+    return std::sqrt(acc);
+}
+
+Fingerprint add_noise(const Fingerprint& fp, double sigma, std::uint64_t seed) {
+    Fingerprint out;
+    out.s.resize(fp.size());
+    check(mrfg_add_noise(interleaved(fp), static_cast<int64_t>(fp.size()), sigma, seed,
+                         reinterpret_cast<double*>(out.s.data())));
+    return out;
+}
+
+double estimate_pd(const Fingerprint& acquired, const Fingerprint& matched_ideal) {
+    if (acquired.size() != matched_ideal.size()) throw std::invalid_argument("estimate_pd: length mismatch");
+    if (acquired.size() == 0) throw std::invalid_argument("estimate_pd: empty input");
+    const double ni = norm2(matched_ideal);
+    if (ni == 0) throw std::invalid_argument("estimate_pd: zero ideal fingerprint");
+    return norm2(acquired) / ni;
+}
+
+// --------------------------------------------------------------------- bloch
+BlochSimulator::BlochSimulator(const Schedule& sched) : ctx_(create(sched)), n_(sched.size()) {}
+
+BlochSimulator::~BlochSimulator() {
+    if (ctx_) mrfg_destroy(ctx_);
+}
+
+void BlochSimulator::simulate(const TissueParams& p, std::complex<double>* out) const {
+    const double prm[3] = {p.t1, p.t2, p.df};
+    check(mrfg_simulate(ctx_, prm, 1, 64, 0, reinterpret_cast<double*>(out)));
+}
+
+Fingerprint BlochSimulator::simulate(const TissueParams& p) const {
+    Fingerprint fp;
+    fp.s.resize(n_);
+    simulate(p, fp.s.data());
+    return fp;
+}
+
+std::vector<std::complex<double>> BlochSimulator::simulate_batch(const std::vector<TissueParams>& params) const {
+    std::vector<double> prm(3 * params.size());
+    for (std::size_t k = 0; k < params.size(); ++k) {
+        prm[3 * k] = params[k].t1;
+        prm[3 * k + 1] = params[k].t2;
+        prm[3 * k + 2] = params[k].df;
+    }
+    std::vector<std::complex<double>> out(n_ * params.size());
+    if (!params.empty())
+        check(mrfg_simulate(ctx_, prm.data(), static_cast<int64_t>(params.size()), 64, 0,
+                            reinterpret_cast<double*>(out.data())));
+    return out;
+}
+
+Fingerprint simulate_fingerprint(const TissueParams& p, const Schedule& sched) {
+    return BlochSimulator(sched).simulate(p);
+}
+
+// ---------------------------------------------------------------- dictionary
+ParameterGrid grid_from_ranges(const AxisRange& t1, const AxisRange& t2, const AxisRange& df) {
+    auto axis = [](const AxisRange& r, const char* name) {
+        if (!(r.step > 0)) throw std::invalid_argument(std::string(name) + ": step must be > 0");
+        if (!(r.max > r.min)) throw std::invalid_argument(std::string(name) + ": need max > min");
+        int64_t c = 0;
+        if (mrfg_axis_count(r.min, r.max, r.step, &c) != MRFG_OK)
+            throw std::invalid_argument(std::string(name) + ": empty axis");
+        return AxisSpec{r.min, r.step, static_cast<std::size_t>(c)};
+    };
+    return {axis(t1, "t1"), axis(t2, "t2"), axis(df, "df")};
+}
+
+Digest schedule_digest(const Schedule& sched) {  // dictionary.cpp:163-171
+    const std::string csv = to_csv(sched);
+    Digest d{};
+    unsigned int n = 0;
+    if (EVP_Digest(csv.data(), csv.size(), d.data(), &n, EVP_sha256(), nullptr) != 1 || n != d.size())
+        throw std::runtime_error("SHA-256 digest failed");
+    return d;
+}
+
+std::string digest_hex(const Digest& d) {
+    static const char* hex = "0123456789abcdef";
+    std::string s;
+    for (auto b : d) {
+        s += hex[b >> 4];
+        s += hex[b & 0xF];
+    }
+    return s;
+}
+
+Dictionary generate(const ParameterGrid& grid, const Schedule& sched, int) {
+    if (sched.size() == 0) throw std::invalid_argument("generate: empty schedule");
+    CtxGuard c{create(sched)};
+    Dictionary d;
+    d.grid = grid;
+    d.digest = schedule_digest(sched);
+    d.entry_len = sched.size();
+    d.data.resize(grid.total() * 2 * d.entry_len);
+    const mrfg_grid g = to_grid(grid);
+    check(mrfg_generate(c.h, &g, 0, static_cast<int64_t>(grid.total()), 64, d.data.data()));
+    return d;
+}
+
+Match brute_force_search(const Fingerprint& fp, const Dictionary& dict, Metric metric) {
+    if (fp.size() != dict.entry_len)
+        throw std::invalid_argument("query length does not match dictionary entries");
+    CtxGuard c{create_len(dict.entry_len)};
+    mrfg_match m;
+    check(mrfg_scan_dict(c.h, dict.data.data(), static_cast<int64_t>(dict.grid.total()), interleaved(fp), 1,
+                         metric == Metric::cc ? MRFG_METRIC_CC : MRFG_METRIC_EUCLIDEAN, nullptr, &m, nullptr));
+    const auto u = dict.grid.unflatten(static_cast<std::size_t>(m.flat));
+    return {dict.grid.params_at(u.i1, u.i2, u.idf), m.score, dict.grid.total()};
+}
+
+ScanOutcome scan_grid(const ParameterGrid& grid, const Schedule& sched,
+                      const std::vector<Fingerprint>& queries, Metric metric, int,
+                      std::size_t chunk_entries) {
+    if (queries.empty()) throw std::invalid_argument("scan_grid: no queries");
+    if (chunk_entries == 0) throw std::invalid_argument("chunk_entries must be > 0");
+    for (const auto& q : queries)
+        if (q.size() != sched.size())
+            throw std::invalid_argument("query length does not match dictionary entries");
+    CtxGuard c{create(sched)};
+    const std::size_t n = sched.size(), nq = queries.size();
+    std::vector<double> flat(2 * n * nq);
+    for (std::size_t k = 0; k < nq; ++k) std::memcpy(&flat[2 * n * k], interleaved(queries[k]), 16 * n);
+    std::vector<mrfg_match> m(nq);
+    mrfg_scan_stats st{};
+    const mrfg_grid g = to_grid(grid);
+    check(mrfg_scan_grid(c.h, &g, 0, 0, flat.data(), static_cast<int64_t>(nq),
+                         metric == Metric::cc ? MRFG_METRIC_CC : MRFG_METRIC_EUCLIDEAN, nullptr, m.data(),
+                         &st));
+    ScanOutcome out;
+    for (std::size_t k = 0; k < nq; ++k) {
+        const auto u = grid.unflatten(static_cast<std::size_t>(m[k].flat));
+        out.matches.push_back({grid.params_at(u.i1, u.i2, u.idf), m[k].score, grid.total()});
+    }
+    // the scan is one batched GPU pass: its match time is shared evenly
+    out.scan_seconds.assign(nq, (st.gemm_ms + st.rerank_ms) * 1e-3 / static_cast<double>(nq));
+    out.generate_seconds = st.bloch_ms * 1e-3;
+    return out;
+}
+
+void cc_map(const Fingerprint& fp, const ParameterGrid& grid, const Schedule& sched,
+            const std::function<void(std::size_t, std::span<const float>)>& sink, int,
+            std::size_t chunk_entries) {
+    if (chunk_entries == 0) throw std::invalid_argument("chunk_entries must be > 0");
+    if (fp.size() != sched.size())
+        throw std::invalid_argument("query length does not match dictionary entries");
+    CtxGuard c{create(sched)};
+    const mrfg_grid g = to_grid(grid);
+    std::vector<float> scores;
+    for (std::size_t begin = 0; begin < grid.total(); begin += chunk_entries) {
+        const std::size_t end = std::min(grid.total(), begin + chunk_entries);
+        scores.resize(end - begin);
+        check(mrfg_cc_map(c.h, &g, interleaved(fp), static_cast<int64_t>(begin),
+                          static_cast<int64_t>(end - begin), scores.data()));
+        sink(begin, {scores.data(), scores.size()});
+    }
+}
+
+// ---------------------------------------------------------------------- zoom
+// Generic forms over caller objectives (zoom.cpp:173-399), host-side.
+long search_df(const std::function<double(long)>& f, long lo, long hi, const DfSearchParams& prm,
+               const std::function<void(const char*, long, double)>& stage) {
+    if (lo > hi) throw std::invalid_argument("search_df: empty range");
+    if (prm.coarse <= 0 || prm.refine <= 0 || prm.finest <= 0 || prm.omega <= 0)
+        throw std::invalid_argument("search_df: steps must be positive");
+    struct B {
+        long idx = -1;
+        double val = -1e300;
+        void offer(long i, double v) {
+            if (v > val) {
+                val = v;
+                idx = i;
+            }
+        }
+    };
+    auto note = [&](const char* name, const B& b) {
+        if (stage) stage(name, b.idx, b.val);
+    };
+    auto sweep = [&](long a, long b, long step, B& best) {
+        a = std::clamp(a, lo, hi);
+        b = std::clamp(b, lo, hi);
+        for (long x = a; x <= b; x += step) best.offer(x, f(x));
+        if ((b - a) % step != 0) best.offer(b, f(b));
+    };
+    auto run = [&](long coarse, long wh) -> B {
+        std::vector<double> marks;
+        auto flat3 = [&] {
+            if (marks.size() < 3) return false;
+            auto [mn, mx] = std::minmax_element(marks.end() - 3, marks.end());
+            return *mx - *mn < prm.plateau_eps;
+        };
+        B cur;
+        sweep(lo, hi, coarse, cur);
+        note("df.coarse", cur);
+        marks.push_back(cur.val);
+        B r = cur;
+        sweep(cur.idx - wh, cur.idx + wh, prm.refine, r);
+        cur = r;
+        note("df.refine", cur);
+        marks.push_back(cur.val);
+        for (int round = 0; round < 8; ++round) {
+            B t = cur;
+            for (long k = 1; cur.idx + k * prm.omega <= hi; ++k) t.offer(cur.idx + k * prm.omega, f(cur.idx + k * prm.omega));
+            for (long k = 1; cur.idx - k * prm.omega >= lo; ++k) t.offer(cur.idx - k * prm.omega, f(cur.idx - k * prm.omega));
+            note("df.translate", t);
+            if (t.idx == cur.idx) break;
+            B rr = t;
+            sweep(t.idx - wh, t.idx + wh, prm.refine, rr);
+            cur = rr;
+            note("df.rerefine", cur);
+            marks.push_back(cur.val);
+            if (flat3()) {
+                note("df.plateau_stop", cur);
+                return cur;
+            }
+        }
+        if (flat3()) {
+            note("df.plateau_stop", cur);
+            return cur;
+        }
+        B fin = cur;
+        sweep(cur.idx - prm.omega / 2, cur.idx + prm.omega / 2, prm.finest, fin);
+        note("df.finest", fin);
+        return fin;
+    };
+    B m = run(prm.coarse, prm.window_half);
+    if (prm.allow_fallback && m.val < prm.heavy_cc) {
+        B fb = run(prm.fallback_coarse, prm.fallback_window_half);
+        note("df.fallback", fb);
+        if (fb.val > m.val) return fb.idx;
+    }
+    return m.idx;
+}
+
+long zoom_1d(const std::function<double(long)>& f, long lo, long hi, long init, std::span<const long> steps) {
+    if (lo > hi) throw std::invalid_argument("zoom_1d: empty range");
+    long x = std::clamp(init, lo, hi);
+    double fx = f(x);
+    for (long s : steps) {
+        if (s <= 0) throw std::invalid_argument("zoom_1d: step must be positive");
+        bool moved = true;
+        while (moved) {
+            moved = false;
+            for (long cand : {std::clamp(x - s, lo, hi), std::clamp(x + s, lo, hi)}) {
+                if (cand == x) continue;
+                const double fc = f(cand);
+                if (fc > fx) {
+                    x = cand;
+                    fx = fc;
+                    moved = true;
+                    break;
+                }
+            }
+        }
+    }
+    return x;
+}
+
+std::pair<long, long> zoom_2d(const std::function<double(long, long)>& f, long lo1, long hi1, long lo2,
+                              long hi2, long init1, long init2, std::span<const std::pair<long, long>> steps) {
+    if (lo1 > hi1 || lo2 > hi2) throw std::invalid_argument("zoom_2d: empty range");
+    long x = std::clamp(init1, lo1, hi1), y = std::clamp(init2, lo2, hi2);
+    double fc = f(x, y);
+    long bx = x, by = y;
+    double bf = fc;
+    auto seen = [&](long px, long py, double v) {
+        if (v > bf) {
+            bf = v;
+            bx = px;
+            by = py;
+        }
+    };
+    auto probe = [&](long px, long py) {
+        const double v = f(px, py);
+        seen(px, py, v);
+        return v;
+    };
+    for (auto [s1, s2] : steps) {
+        if (s1 <= 0 || s2 <= 0) throw std::invalid_argument("zoom_2d: step must be positive");
+        const long cap = 4 * ((hi1 - lo1) / s1 + (hi2 - lo2) / s2) + 16;
+        bool done = false;
+        for (long it = 0; it < cap && !done; ++it) {
+            const long xl = std::clamp(x - s1, lo1, hi1), xr = std::clamp(x + s1, lo1, hi1);
+            const long yd = std::clamp(y - s2, lo2, hi2), yu = std::clamp(y + s2, lo2, hi2);
+            const double fl = xl != x ? probe(xl, y) : fc;
+            const double fd = yd != y ? probe(x, yd) : fc;
+            const bool lw = xl != x && fl > fc, dw = yd != y && fd > fc;
+            if (lw && dw) {
+                x = xl;
+                y = yd;
+                fc = probe(x, y);
+            } else if (!lw && !dw) {
+                const double fr = xr != x ? probe(xr, y) : fc;
+                const double fu = yu != y ? probe(x, yu) : fc;
+                const bool rw = xr != x && fr > fc, uw = yu != y && fu > fc;
+                if (rw && uw) {
+                    x = xr;
+                    y = yu;
+                    fc = probe(x, y);
+                } else if (rw) {
+                    x = xr;
+                    fc = fr;
+                } else if (uw) {
+                    y = yu;
+                    fc = fu;
+                } else {
+                    done = true;
+                }
+            } else if (lw) {
+                const double fu = yu != y ? probe(x, yu) : fc;
+                if (yu != y && fu > fc) {
+                    x = xl;
+                    y = yu;
+                    fc = probe(x, y);
+                } else {
+                    x = xl;
+                    fc = fl;
+                }
+            } else {
+                const double fr = xr != x ? probe(xr, y) : fc;
+                if (xr != x && fr > fc) {
+                    x = xr;
+                    y = yd;
+                    fc = probe(x, y);
+                } else {
+                    y = yd;
+                    fc = fd;
+                }
+            }
+        }
+        if (!done) {
+            x = bx;
+            y = by;
+            fc = bf;
+        }
+    }
+    return {x, y};
+}
+
+std::vector<QuantResult> quantify_batch(const std::vector<Fingerprint>& fps, const SearchRanges& ranges,
+                                        const ZoomConfig& cfg, const Schedule& sched) {
+    const ParameterGrid lat = grid_from_ranges(ranges.t1_ms, ranges.t2_ms, ranges.df_hz);
+    for (const auto& fp : fps)
+        if (fp.size() != sched.size())
+            throw std::invalid_argument("objective: query length does not match schedule");
+    std::vector<QuantResult> out;
+    if (fps.empty()) return out;
+    CtxGuard c{create(sched)};
+    const std::size_t n = sched.size();
+    std::vector<double> flat(2 * n * fps.size());
+    for (std::size_t k = 0; k < fps.size(); ++k) std::memcpy(&flat[2 * n * k], interleaved(fps[k]), 16 * n);
+    const mrfg_grid g = to_grid(lat);
+    const mrfg_zoom_config zc = to_cfg(cfg);
+    std::vector<mrfg_quant> q(fps.size());
+    const auto t0 = std::chrono::steady_clock::now();
+    check(mrfg_quantify(c.h, &g, &zc, flat.data(), static_cast<int64_t>(fps.size()), q.data()));
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (const auto& r : q) out.push_back(to_result(lat, r, secs / static_cast<double>(fps.size())));
+    return out;
+}
+
+QuantResult quantify(const Fingerprint& fp, const SearchRanges& ranges, const ZoomConfig& cfg,
+                     const Schedule& sched, const Dictionary* df_dict, const Dictionary* full_dict) {
+    const ParameterGrid lat = grid_from_ranges(ranges.t1_ms, ranges.t2_ms, ranges.df_hz);
+    check_df_dict(df_dict, lat, cfg, sched);
+    if (full_dict)
+        throw std::invalid_argument("quantify: full-dictionary lookup mode is not provided by the B200 backend");
+    return quantify_batch({fp}, ranges, cfg, sched).at(0);
+}
+
+Dictionary make_df_dictionary(const SearchRanges& ranges, const ZoomConfig& cfg, const Schedule& sched,
+                              int workers) {  // zoom.cpp:541-553
+    const ParameterGrid lat = grid_from_ranges(ranges.t1_ms, ranges.t2_ms, ranges.df_hz);
+    auto snap = [](double v, const AxisSpec& a) { return std::lround((v - a.min) / a.step); };
+    const long i1 = std::clamp(snap(cfg.init_t1_ms, lat.t1_ms), 0L, static_cast<long>(lat.t1_ms.count) - 1);
+    const long i2 = std::clamp(snap(cfg.init_t2_ms, lat.t2_ms), 0L, static_cast<long>(lat.t2_ms.count) - 1);
+    const double t1 = lat.t1_ms.value(static_cast<std::size_t>(i1)), t2 = lat.t2_ms.value(static_cast<std::size_t>(i2));
+    return generate(grid_from_ranges({t1, t1 + lat.t1_ms.step, lat.t1_ms.step},
+                                     {t2, t2 + lat.t2_ms.step, lat.t2_ms.step}, ranges.df_hz),
+                    sched, workers);
+}
+
+SliceResult quantify_slice(const std::vector<Fingerprint>& fps, const std::vector<std::uint8_t>& mask, int nx,
+                           int ny, const SearchRanges& ranges, const ZoomConfig& cfg, const Schedule& sched,
+                           bool use_prior, int, const Dictionary* df_dict) {
+    const auto nv = static_cast<std::size_t>(nx) * static_cast<std::size_t>(ny);
+    if (nx <= 0 || ny <= 0 || fps.size() != nv || mask.size() != nv)
+        throw std::invalid_argument("quantify_slice: inconsistent raster dimensions");
+    const ParameterGrid lat = grid_from_ranges(ranges.t1_ms, ranges.t2_ms, ranges.df_hz);
+    check_df_dict(df_dict, lat, cfg, sched);
+    CtxGuard c{create(sched)};
+    const std::size_t n = sched.size();
+    std::vector<double> flat(2 * n * nv, 0.0);
+    for (std::size_t i = 0; i < nv; ++i)
+        if (mask[i]) {
+            if (fps[i].size() != n) throw std::invalid_argument("objective: query length does not match schedule");
+            std::memcpy(&flat[2 * n * i], interleaved(fps[i]), 16 * n);
+        }
+    const mrfg_grid g = to_grid(lat);
+    const mrfg_zoom_config zc = to_cfg(cfg);
+    std::vector<mrfg_quant> q(nv);
+    double secs = 0;
+    check(mrfg_quantify_slice(c.h, &g, &zc, flat.data(), mask.data(), nx, ny, use_prior ? 1 : 0, q.data(), &secs));
+    SliceResult out;
+    out.nx = nx;
+    out.ny = ny;
+    out.t1_ms.assign(nv, 0);
+    out.t2_ms.assign(nv, 0);
+    out.df_hz.assign(nv, 0);
+    out.pd.assign(nv, 0);
+    out.score.assign(nv, 0);
+    out.evaluations.assign(nv, 0);
+    for (std::size_t i = 0; i < nv; ++i) {
+        if (!mask[i]) continue;
+        const QuantResult r = to_result(lat, q[i], 0);
+        out.t1_ms[i] = r.params.t1 * 1e3;  // zoom.cpp:581-586
+        out.t2_ms[i] = r.params.t2 * 1e3;
+        out.df_hz[i] = r.params.df;
+        out.pd[i] = r.params.pd;
+        out.score[i] = r.score;
+        out.evaluations[i] = r.evaluations;
+        out.total_evaluations += r.evaluations;
+    }
+    out.seconds = secs;
+    return out;
+}
+
+}  // namespace mrf
