@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -215,8 +216,9 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
     fill(c, best, nq, -3.0f);
 
     const int64_t arows = round_up(std::min(crows * ndf, round_up(range, ndf) + ndf), 128);
-    c.atoms_a.ensure(sizeof(__half) * arows * kp);
-    c.inv2.ensure(sizeof(float) * arows);
+    c.atoms_a.ensure(sizeof(__half) * 2 * arows * kp);  // double-buffered operand
+    c.inv2.ensure(sizeof(float) * 2 * arows);
+    c.ensure_aux();
     c.cand_count.ensure(64);
     auto* d_count = c.cand_count.as<unsigned long long>();
 
@@ -268,35 +270,63 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
         MRFG_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
         mp.cand = c.cand.as<CandRec>();
         mp.cand_cap = cap;
-        std::vector<int> marks;
-        for (int64_t r0 = fb / ndf; r0 * ndf < fe; r0 += crows) {
+        // Two operand buffers: with MRFG_OVERLAP=1 the producer (K1 or the
+        // dictionary conversion) fills chunk i+1 on the aux stream while K2
+        // consumes chunk i (the persistent GEMM leaves room for one producer CTA
+        // per SM).  Measured on B200: K2 runs under sw_power_cap, so concurrent
+        // CUDA-core work lowers the SM clock and the GEMM loses what K1 gains
+        // (3.05 s vs 2.99 s per config-2 slice); the default is one stream.
+        static const bool overlap = [] {
+            const char* e = std::getenv("MRFG_OVERLAP");
+            return e && e[0] == '1';
+        }();
+        const cudaStream_t S = c.stream, A = overlap ? c.aux : c.stream;
+        EventTimer ta(A);
+        std::vector<int> pm, gm;
+        MRFG_CUDA(cudaEventRecord(c.ev[0], S));
+        MRFG_CUDA(cudaStreamWaitEvent(A, c.ev[0], 0));
+        int64_t i = 0;
+        for (int64_t r0 = fb / ndf; r0 * ndf < fe; r0 += crows, ++i) {
             const int64_t vb = std::max(fb, r0 * ndf), ve = std::min(fe, (r0 + crows) * ndf);
             const int64_t base = r0 * ndf;
             const int64_t rows = round_up(ve - base, 128);
-            marks.push_back(tm.mark());
+            const int b = static_cast<int>(i & 1);
+            __half* abuf = c.atoms_a.as<__half>() + b * arows * kp;
+            float* ibuf = c.inv2.as<float>() + b * arows;
+            if (i >= 2) MRFG_CUDA(cudaStreamWaitEvent(A, c.ev[2 + b], 0));  // GEMM(i-2) released b
+            pm.push_back(ta.mark());
+            c.stream = A;
             if (tp)
-                launch_bloch_rows(c, *tp, vb, ve, metric, 0, rows, c.atoms_a.as<__half>(), nullptr,
-                                  c.inv2.as<float>());
-            else  // base == vb - (vb - base): rows [vb-base, ve-base) hold the entries
-                launch_dict_operand(c, d_dict, base, ve - base, rows, 1, metric, c.atoms_a.as<__half>(),
-                                    c.inv2.as<float>());
-            marks.push_back(tm.mark());
+                launch_bloch_rows(c, *tp, vb, ve, metric, 0, rows, abuf, nullptr, ibuf);
+            else  // rows [vb-base, ve-base) hold the entries
+                launch_dict_operand(c, d_dict, base, ve - base, rows, 1, metric, abuf, ibuf);
+            c.stream = S;
+            pm.push_back(ta.mark());
+            MRFG_CUDA(cudaEventRecord(c.ev[4 + b], A));
+            MRFG_CUDA(cudaStreamWaitEvent(S, c.ev[4 + b], 0));
+            mp.a = abuf;
+            mp.inv2 = ibuf;
             mp.atoms = rows;
             mp.valid_begin = vb - base;
             mp.valid_atoms = ve - base;
             mp.flat_base = base;
             mp.flat_stride = 1;
+            gm.push_back(tm.mark());
             launch_match(c, mp);
-            marks.push_back(tm.mark());
+            gm.push_back(tm.mark());
+            MRFG_CUDA(cudaEventRecord(c.ev[2 + b], S));
             ++chunks;
         }
-        MRFG_CUDA(cudaMemcpyAsync(&ncand, d_count, sizeof ncand, cudaMemcpyDeviceToHost, c.stream));
-        MRFG_CUDA(cudaStreamSynchronize(c.stream));
-        for (size_t i = 0; i + 2 < marks.size(); i += 3) {
-            bloch_ms += tm.ms(marks[i], marks[i + 1]);
-            gemm_ms += tm.ms(marks[i + 1], marks[i + 2]);
+        MRFG_CUDA(cudaMemcpyAsync(&ncand, d_count, sizeof ncand, cudaMemcpyDeviceToHost, S));
+        MRFG_CUDA(cudaStreamSynchronize(S));
+        MRFG_CUDA(cudaStreamSynchronize(A));
+        for (size_t k = 0; k + 1 < pm.size(); k += 2) bloch_ms += ta.ms(pm[k], pm[k + 1]);
+        for (size_t k = 0; k + 1 < gm.size(); k += 2) {
+            gemm_ms += tm.ms(gm[k], gm[k + 1]);
             ++gemm_launches;
         }
+        mp.a = c.atoms_a.as<__half>();
+        mp.inv2 = c.inv2.as<float>();
         if (ncand <= static_cast<unsigned long long>(cap)) break;
         // Overflow: the running maxima are now final, so a second pass records
         // a subset of the first pass's candidates; size the buffer for all.
@@ -432,6 +462,11 @@ int mrfg_destroy(mrfg_ctx* h) {
                           &c.params, &c.out64, &c.misc})
             b->release();
         if (c.own_stream) cudaStreamDestroy(c.stream);
+        if (c.aux) {
+            cudaStreamSynchronize(c.aux);
+            cudaStreamDestroy(c.aux);
+            for (auto e : c.ev) cudaEventDestroy(e);
+        }
         delete h;
     });
 }

@@ -92,7 +92,14 @@ struct Ctx {
     // scratch
     DevBuf q64, qprime, best, cand, cand_count, atoms_a, inv2, seed_a, seed_inv2, rerank,
         params, out64, misc;
-    cudaEvent_t ev[8];
+    // producer stream + events for the K1/K2 overlap (created on first use)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev[8] = {};
+    void ensure_aux() {
+        if (aux) return;
+        MRFG_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+        for (auto& e : ev) MRFG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     // tensor-map encoder (driver entry point)
     void* encode_fn = nullptr;
 };
