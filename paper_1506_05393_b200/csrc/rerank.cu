@@ -95,7 +95,7 @@ __device__ double exact_score(const Tab64& T, const double* __restrict__ q, int6
     const double inv = 1.0 / sqrt(acc);
     // second pass: float entries streamed straight into the score
     double re = 0.0, im = 0.0, dd = 0.0;
-    sim64_walk(T.rf, T.e1d, T.e2d, T.phd, T.inv0, T.n, T.L, i1, i2, idf, [&](int j, double x, double y) {
+    sim64_walk_pf(T.rf, T.e1d, T.e2d, T.phd, T.inv0, T.n, T.L, i1, i2, idf, [&](int j, double x, double y) {
         const double er = static_cast<double>(__double2float_rn(__dmul_rn(x, inv)));
         const double ei = static_cast<double>(__double2float_rn(__dmul_rn(y, inv)));
         const double qr = q[2 * j], qi = q[2 * j + 1];
@@ -108,7 +108,7 @@ __device__ double exact_score(const Tab64& T, const double* __restrict__ q, int6
             const double dr = __dsub_rn(qr, er), di = __dsub_rn(qi, ei);
             dd = __dadd_rn(dd, __dadd_rn(__dmul_rn(dr, dr), __dmul_rn(di, di)));
         }
-    });
+    }, [&](int jj) -> const void* { return q + 2 * jj; });
     if (metric == MRFG_METRIC_CC) {
         double v = sqrt(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
         return v < 1.0 ? v : 1.0;  // dictionary.cpp:126

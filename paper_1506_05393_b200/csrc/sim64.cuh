@@ -63,20 +63,41 @@ __device__ __forceinline__ StepT load_step(const double* __restrict__ e1d,
     return {a.x, a.y, b.x, b.y, p0.x, p0.y, p1.x, p1.y};
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+constexpr int kPrefetchSteps = 8;
+
 // Walk one lattice atom through the schedule (bloch.cpp:108-123) calling
 // at(j, mx, my) at every echo.  The table gathers run two steps ahead of
-// the recursion (software pipelining) so their latency hides behind the
-// FP64 dependency chain.
-template <class AT>
-__device__ __forceinline__ void sim64_walk(const double* __restrict__ rf,
-                                           const double* __restrict__ e1d,
-                                           const double* __restrict__ e2d,
-                                           const double* __restrict__ phd, const double inv0[3],
-                                           int n, const Lattice& L, int i1, int i2, int idf, AT at) {
+// the recursion in registers and eight steps ahead as L1 prefetches, so their
+// L2 latency hides behind the FP64 dependency chain (measured: the per-step
+// gather latency, not the FP64 pipe, bounded K3/K5).  `extra(j)` returns one
+// more per-step address to prefetch (the query row), or nullptr.
+template <class AT, class PF>
+__device__ __forceinline__ void sim64_walk_pf(const double* __restrict__ rf,
+                                              const double* __restrict__ e1d,
+                                              const double* __restrict__ e2d,
+                                              const double* __restrict__ phd, const double inv0[3],
+                                              int n, const Lattice& L, int i1, int i2, int idf, AT at,
+                                              PF extra) {
     double x = inv0[0], y = inv0[1], z = inv0[2];
+    for (int j = 0; j < kPrefetchSteps && j < n; ++j) {
+        prefetch_l1(e1d + (static_cast<int64_t>(j) * L.n1 + i1) * 2);
+        prefetch_l1(e2d + (static_cast<int64_t>(j) * L.n2 + i2) * 2);
+        prefetch_l1(phd + (static_cast<int64_t>(j) * L.ndf + idf) * 4);
+        if (const void* e = extra(j)) prefetch_l1(e);
+    }
     StepT c0 = load_step(e1d, e2d, phd, L, 0, i1, i2, idf);
     StepT c1 = load_step(e1d, e2d, phd, L, n > 1 ? 1 : 0, i1, i2, idf);
     for (int j = 0; j < n; ++j) {
+        if (j + kPrefetchSteps < n) {
+            const int64_t jp = j + kPrefetchSteps;
+            prefetch_l1(e1d + (jp * L.n1 + i1) * 2);
+            prefetch_l1(e2d + (jp * L.n2 + i2) * 2);
+            prefetch_l1(phd + (jp * L.ndf + idf) * 4);
+            if (const void* e = extra(static_cast<int>(jp))) prefetch_l1(e);
+        }
         const StepT c2 = load_step(e1d, e2d, phd, L, j + 2 < n ? j + 2 : n - 1, i1, i2, idf);
         rf_apply64(rf + 9 * j, x, y, z);
         relax64(x, y, z, c0.e1t, c0.e2t, c0.ct, c0.st);
@@ -85,6 +106,16 @@ __device__ __forceinline__ void sim64_walk(const double* __restrict__ rf,
         c0 = c1;
         c1 = c2;
     }
+}
+
+template <class AT>
+__device__ __forceinline__ void sim64_walk(const double* __restrict__ rf,
+                                           const double* __restrict__ e1d,
+                                           const double* __restrict__ e2d,
+                                           const double* __restrict__ phd, const double inv0[3],
+                                           int n, const Lattice& L, int i1, int i2, int idf, AT at) {
+    sim64_walk_pf(rf, e1d, e2d, phd, inv0, n, L, i1, i2, idf, at,
+                  [](int) -> const void* { return nullptr; });
 }
 
 // One FP64 lattice atom.  mode 0: returns sum |s|^2 (fingerprint.cpp:14-18

@@ -14,7 +14,9 @@
 // Each evaluation is the reference's FP64 pipeline: simulate (sim64.cuh,
 // host-libm tables => bit-identical fingerprint), FP64 normalize, FP64 CC and
 // Euclidean score (zoom.cpp:74-92), clamp at 1.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -46,6 +48,8 @@ struct ZParams {
     long long s2d1[8], s2d2[8], s1d1[8], s1d2[8];
     long long f2d1, f2d2;
     long long init1, init2;  // snapped (not yet clamped) initial indices
+    // speculation widths: 1-D flanks +-1..spec1d steps, 2-D (2*spec2d+1)^2 block
+    long long spec1d, spec2d;
     // data
     const double* fps;  // nvox x 2N raw
     double* q;          // nvox x 2N normalized scratch
@@ -126,7 +130,7 @@ __device__ void zsim(const Z& z, int i1, int i2, int idf, ZSlot& s) {
     double re = 0.0, im = 0.0, dd = 0.0;
     const bool euc = P.need_euc;
     const double* q = z.q;
-    sim64_walk(P.rf, P.e1d, P.e2d, P.phd, P.inv0, n, P.L, i1, i2, idf, [&](int j, double x, double y) {
+    sim64_walk_pf(P.rf, P.e1d, P.e2d, P.phd, P.inv0, n, P.L, i1, i2, idf, [&](int j, double x, double y) {
         const double er = __dmul_rn(x, inv), ei = __dmul_rn(y, inv);
         const double qr = q[2 * j], qi = q[2 * j + 1];
         re = __dadd_rn(re, __dadd_rn(__dmul_rn(qr, er), __dmul_rn(qi, ei)));  // zoom.cpp:79
@@ -135,7 +139,7 @@ __device__ void zsim(const Z& z, int i1, int i2, int idf, ZSlot& s) {
             const double dr = __dsub_rn(qr, er), di = __dsub_rn(qi, ei);  // zoom.cpp:87-89
             dd = __dadd_rn(dd, __dadd_rn(__dmul_rn(dr, dr), __dmul_rn(di, di)));
         }
-    });
+    }, [&](int jj) -> const void* { return q + 2 * jj; });
     const double v = sqrt(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
     s.cc = v < 1.0 ? v : 1.0;  // zoom.cpp:82-83
     s.euc = -sqrt(dd);          // zoom.cpp:91
@@ -311,7 +315,7 @@ __device__ long long zoom_1d(Z& z, int axis, long long i1, long long i2, long lo
     double fx = F(x);
     for (;;) {
         const long long x0 = x;
-        zensure(z, 8, [&](long long k, long long& a, long long& b, long long& c) {
+        zensure(z, 2 * z.p->spec1d, [&](long long k, long long& a, long long& b, long long& c) {
             const long long off = (k / 2 + 1) * s * ((k & 1) ? 1 : -1);
             const long long v = clampll(x0 + off, lo, hi);
             a = axis == 0 ? v : i1;
@@ -359,10 +363,11 @@ __device__ void zoom_2d_step(Z& z, long long idf, int metric, long long& x, long
     bool converged = false;
     for (long long iter = 0; iter < cap && !converged; ++iter) {
         const long long cx = x, cy = y;
-        zensure(z, 8, [&](long long k, long long& a, long long& b, long long& c) {
-            const long long kk = k < 4 ? k : k + 1;  // skip the centre of the 3x3
-            a = clampll(cx + (kk % 3 - 1) * s1, lo1, hi1);
-            b = clampll(cy + (kk / 3 - 1) * s2, lo2, hi2);
+        const long long r = z.p->spec2d, w = 2 * r + 1;  // (2r+1)^2 - 1 neighbours
+        zensure(z, w * w - 1, [&](long long k, long long& a, long long& b, long long& c) {
+            const long long kk = k < (w * w) / 2 ? k : k + 1;  // skip the centre
+            a = clampll(cx + (kk % w - r) * s1, lo1, hi1);
+            b = clampll(cy + (kk / w - r) * s2, lo2, hi2);
             c = idf;
         });
         const long long xl = clampll(x - s1, lo1, hi1);
@@ -623,6 +628,12 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     }
     P.f2d1 = step_units(cfg.final_2d_step_ms, lat.t1_ms.step);
     P.f2d2 = step_units(cfg.final_2d_step_ms, lat.t2_ms.step);
+    {
+        const char* e1 = std::getenv("MRFG_ZOOM_SPEC1D");
+        const char* e2 = std::getenv("MRFG_ZOOM_SPEC2D");
+        P.spec1d = e1 ? std::max(1, std::atoi(e1)) : 16;
+        P.spec2d = e2 ? std::max(1, std::atoi(e2)) : 2;
+    }
     P.init1 = snap_index(cfg.init_t1_ms, lat.t1_ms);
     P.init2 = snap_index(cfg.init_t2_ms, lat.t2_ms);
     P.fps = d_fps;
