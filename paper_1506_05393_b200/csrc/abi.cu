@@ -215,7 +215,7 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
     float* best = c.best.as<float>();
     fill(c, best, nq, -3.0f);
 
-    const int64_t arows = round_up(std::min(crows * ndf, round_up(range, ndf) + ndf), 128);
+    const int64_t arows = round_up(std::min(crows * ndf, round_up(range, ndf) + ndf), 256);  // pair tiles
     c.atoms_a.ensure(sizeof(__half) * 2 * arows * kp);  // double-buffered operand
     c.inv2.ensure(sizeof(float) * 2 * arows);
     c.ensure_aux();
@@ -241,7 +241,7 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
     {
         int64_t stride = std::max<int64_t>(1, range / seed_atoms);
         int64_t cnt = (range + stride - 1) / stride;
-        int64_t rows = round_up(std::min(cnt, arows), 128);
+        int64_t rows = round_up(std::min(cnt, arows), 256);
         int a0 = tm.mark();
         if (tp)
             launch_bloch_operand(c, *tp, fb, stride, fe, rows, metric, c.atoms_a.as<__half>(),
@@ -289,7 +289,7 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
         for (int64_t r0 = fb / ndf; r0 * ndf < fe; r0 += crows, ++i) {
             const int64_t vb = std::max(fb, r0 * ndf), ve = std::min(fe, (r0 + crows) * ndf);
             const int64_t base = r0 * ndf;
-            const int64_t rows = round_up(ve - base, 128);
+            const int64_t rows = round_up(ve - base, 256);
             const int b = static_cast<int>(i & 1);
             __half* abuf = c.atoms_a.as<__half>() + b * arows * kp;
             float* ibuf = c.inv2.as<float>() + b * arows;
@@ -665,7 +665,7 @@ int mrfg_screen_scores(mrfg_ctx* h, const mrfg_grid* grid, int64_t first, int64_
                      MRFG_E_INVALID, "screen_scores: bad shape");
         const GridTables& t = ensure_tables(c, *grid, false);
         const int64_t n = c.n, kp = k_pad_of(n), qrows = round_up(2 * nq, 256);
-        const int64_t rows = round_up(count, 128);
+        const int64_t rows = round_up(count, 256);
         DevBuf raw, q64, qp, best, a, inv, cand, cnt;
         raw.ensure(sizeof(double) * 2 * n * nq);
         q64.ensure(sizeof(double) * 2 * n * nq);

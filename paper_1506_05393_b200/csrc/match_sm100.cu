@@ -23,6 +23,9 @@
 //              the MMAs of tile i+1 (double-buffered TMEM).
 #include <cuda.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "mrfg_internal.cuh"
 
 namespace mrfg {
@@ -331,6 +334,223 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
+// ------------------------------------------------------------------------
+// CTA-pair variant: tcgen05.mma.cta_group::2, M = 256 atoms per pair.
+// Each CTA of the cluster owns 128 atom rows (A) and half of the 256 query
+// rows (B); the leader's single thread issues the pair-wide MMA, the tensor
+// cores of both SMs read both B halves, and each CTA's TMEM receives its
+// 128 atoms x 256 columns.  Per SM the smem/L2 operand traffic per MMA step
+// drops from (128 + 256) to (128 + 128) rows.
+constexpr int STAGES2 = 6;
+constexpr int B2_BYTES = (BN / 2) * BK * 2;
+struct alignas(1024) Smem2 {
+    uint8_t a[STAGES2][A_BYTES];
+    uint8_t b[STAGES2][B2_BYTES];
+    uint64_t full[STAGES2], empty[STAGES2], tfull[2], tempty[2];
+    uint32_t tmem_base;
+    float thr[2][128];
+    float bst[2][128];
+};
+constexpr size_t SMEM2_BYTES = sizeof(Smem2) + 1024;
+constexpr uint32_t IDESC2 = (1u << 4) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                            (static_cast<uint32_t>(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+// Remote arrive with the default (CTA-scope) semantics: the data it guards is
+// either TMA-tracked (transaction bytes) or TMEM (ordered by the tcgen05
+// fences), so no GPU-scope fence is needed -- `.release.cluster` here compiled
+// to MEMBAR.ALL.GPU per pipeline stage and starved the pair's MMA.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, void* dst, uint64_t* bar, int c0,
+                                                 int c1) {
+    // both CTAs load their half; the transaction bytes land on the leader's barrier
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    k_match_sm100_2cta(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                       Dev p) {
+    extern __shared__ uint8_t smem_raw[];
+    Smem2& s = *reinterpret_cast<Smem2*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                         ~static_cast<uintptr_t>(1023));
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int64_t cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+    const int64_t n_at = p.n_at / 2, n_vt = p.n_vt;  // 256-atom pair tiles
+    const int64_t n_tiles = n_at * n_vt;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < STAGES2; ++i) {
+            mbar_init(&s.full[i], 2);  // leader's arrive_expect_tx + the peer's arrive
+            mbar_init(&s.empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s.tfull[i], 1);
+            mbar_init(&s.tempty[i], 8);  // 4 epilogue warps x 2 CTAs
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s.tmem_base)),
+                     "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = s.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = cid; t < n_tiles; t += ncl) {
+                const int at = static_cast<int>(t / n_vt), vt = static_cast<int>(t % n_vt);
+                for (int kb = 0; kb < p.nkb; ++kb) {
+                    mbar_wait(&s.empty[stage], phase ^ 1);
+                    if (leader)
+                        mbar_expect_tx(&s.full[stage], 2 * (A_BYTES + B2_BYTES));
+                    else
+                        mbar_arrive_cluster(map_to_rank(smem_u32(&s.full[stage]), 0));
+                    tma_load_2d_pair(&tma_a, s.a[stage], &s.full[stage], kb * BK,
+                                     at * 256 + static_cast<int>(rank) * 128);
+                    tma_load_2d_pair(&tma_b, s.b[stage], &s.full[stage], kb * BK,
+                                     vt * BN + static_cast<int>(rank) * (BN / 2));
+                    if (++stage == STAGES2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = cid; t < n_tiles; t += ncl) {
+                mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + static_cast<uint32_t>(acc * BN);
+                for (int kb = 0; kb < p.nkb; ++kb) {
+                    mbar_wait(&s.full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(s.a[stage]), b0 = smem_u32(s.b[stage]);
+                    const int nsub = kb == p.nkb - 1 ? static_cast<int>(p.last_sub) : BK / 16;
+                    for (int k = 0; k < nsub; ++k)
+                        tc_mma_f16_pair(d, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(b0 + 32 * k), IDESC2,
+                                        (kb | k) != 0);
+                    tc_commit_pair(&s.empty[stage]);
+                    if (++stage == STAGES2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit_pair(&s.tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        const int ew = warp - 4;
+        const int row = ew * 32 + lane;
+        const uint32_t tempty_leader[2] = {map_to_rank(smem_u32(&s.tempty[0]), 0),
+                                           map_to_rank(smem_u32(&s.tempty[1]), 0)};
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = cid; t < n_tiles; t += ncl) {
+            const int64_t at = t / n_vt, vt = t % n_vt;
+            {
+                const int64_t v = vt * 128 + row;
+                float b = v < p.nvox ? __ldcg(p.best + v) : 1e30f;
+                s.thr[acc][row] = v < p.nvox ? threshold_of(b, p.delta, p.metric) : __int_as_float(0x7f800000);
+                s.bst[acc][row] = b;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            mbar_wait(&s.tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t atom = at * 256 + static_cast<int64_t>(rank) * 128 + row;
+            const bool avalid = atom >= p.valid_begin && atom < p.valid_atoms;
+            const float inv = __ldg(p.inv2 + atom);
+            const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) +
+                                   static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+            for (int q = 0; q < 4; ++q) {
+                uint32_t r[64];
+                TMEM_LD_X64(tbase + q * 64, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                float sc[32];
+                uint32_t hits = 0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    sc[i] = screen_score(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]), inv,
+                                         p.metric);
+                    hits |= (sc[i] >= s.thr[acc][q * 32 + i] ? 1u : 0u) << i;
+                }
+                if (!avalid) hits = 0;
+                if (__any_sync(0xffffffffu, hits != 0)) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if ((hits >> i) & 1u) record_hit(p, s.bst[acc][q * 32 + i], vt * 128 + q * 32 + i, atom, sc[i]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512)
+                     : "memory");
+    }
+}
+
 // CUDA-core version of the same fused screening (tests: validates the
 // tcgen05 descriptors/layouts against identical fp16 operands).
 __global__ void k_match_simt(const __half* __restrict__ a, const __half* __restrict__ b,
@@ -410,6 +630,13 @@ Dev dev_of(const MatchParams& p, int64_t k_valid) {
 
 }  // namespace
 
+// K2 variant: the CTA-pair kernel when the chunk is a multiple of 256 atoms
+// (MRFG_K2_PAIR=0 forces the single-CTA kernel).
+static bool use_pair_kernel() {
+    const char* e = std::getenv("MRFG_K2_PAIR");
+    return !(e && e[0] == '0');
+}
+
 void launch_match(Ctx& c, const MatchParams& p) {
     MRFG_REQUIRE(p.atoms % BM == 0 && p.q_rows % BN == 0 && p.k_pad % BK == 0, MRFG_E_INVALID,
                  "match: operand shapes not tile aligned");
@@ -417,11 +644,22 @@ void launch_match(Ctx& c, const MatchParams& p) {
     if (!attr_set) {
         MRFG_CUDA(cudaFuncSetAttribute(k_match_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(SMEM_BYTES)));
+        MRFG_CUDA(cudaFuncSetAttribute(k_match_sm100_2cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(SMEM2_BYTES)));
         attr_set = true;
+    }
+    Dev d = dev_of(p, 2 * c.n);
+    if (use_pair_kernel() && p.atoms % 256 == 0) {
+        CUtensorMap ma = make_map(c, p.a, p.atoms, p.k_pad, 128);
+        CUtensorMap mb = make_map(c, p.b, p.q_rows, p.k_pad, BN / 2);
+        const int64_t tiles = (p.atoms / 256) * d.n_vt;
+        const int64_t pairs = std::min<int64_t>(tiles, c.num_sms / 2);
+        k_match_sm100_2cta<<<static_cast<int>(2 * pairs), NTHREADS, SMEM2_BYTES, c.stream>>>(ma, mb, d);
+        MRFG_CUDA(cudaGetLastError());
+        return;
     }
     CUtensorMap ma = make_map(c, p.a, p.atoms, p.k_pad, BM);
     CUtensorMap mb = make_map(c, p.b, p.q_rows, p.k_pad, BN);
-    Dev d = dev_of(p, 2 * c.n);
     int64_t tiles = d.n_at * d.n_vt;
     int grid = static_cast<int>(tiles < c.num_sms ? tiles : c.num_sms);
     k_match_sm100<<<grid, NTHREADS, SMEM_BYTES, c.stream>>>(ma, mb, d);

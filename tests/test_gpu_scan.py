@@ -173,3 +173,21 @@ def test_brute_force_search_arbitrary_dictionary(orc):
     cc = np.minimum(np.abs(ed @ qn.conj().T), 1.0)
     np.testing.assert_array_equal(flat, cc.argmax(axis=0))
     np.testing.assert_allclose(score, cc.max(axis=0), rtol=1e-12)
+
+
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_screen_both_k2_variants_match_simt(small, pair, monkeypatch):
+    """cta_group::2 (default) and cta_group::1 kernels vs the CUDA-core twin."""
+    monkeypatch.setenv("MRFG_K2_PAIR", pair)
+    with P.Context(small.schedule) as c:
+        a = c.screen_scores(small.grid, small.fps, 3000, 1500, use_simt=False)
+        b = c.screen_scores(small.grid, small.fps, 3000, 1500, use_simt=True)
+    np.testing.assert_allclose(a, b, rtol=2e-5, atol=2e-6)
+
+
+def test_scan_single_cta_kernel(small, small_ref, monkeypatch):
+    monkeypatch.setenv("MRFG_K2_PAIR", "0")
+    oflat, oscore, osecond = small_ref
+    with P.Context(small.schedule) as c:
+        flat, score, _ = c.scan_grid(small.grid, small.fps)
+    assert_parity(flat, score, oflat, oscore, osecond)
