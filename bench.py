@@ -268,6 +268,28 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     e2e_s = allmax((time.perf_counter() - t0) / e2e_steps, world)
 
+    # ---- MRF-ZOOM on the same slice (K5), voxel-sharded, device-resident
+    zoom = None
+    if not args.no_zoom:
+        from paper_1506_05393_b200 import distributed as Dz
+        zcfg = P.zoom_config(df_coarse_hz=5.0, omega_hz=82.0)
+        vb, ve = Dz.voxel_shard(nq, world, rank)
+        d_zq = torch.empty(max(ve - vb, 1) * P.dgs.QUANT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        ctx.quantify_device(d_q[vb:ve].data_ptr(), ve - vb, g, zcfg, d_zq.data_ptr())  # warm-up
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        z0.record(stream)
+        ctx.quantify_device(d_q[vb:ve].data_ptr(), ve - vb, g, zcfg, d_zq.data_ptr())
+        z1.record(stream)
+        torch.cuda.synchronize()
+        zms = allmax(z0.elapsed_time(z1), world)
+        recs = d_zq[: (ve - vb) * P.dgs.QUANT_DTYPE.itemsize].cpu().numpy().view(P.dgs.QUANT_DTYPE)
+        zoom = {"voxels_per_s": nq / (zms * 1e-3), "slice_ms": zms,
+                "evals_per_voxel_mean": float(recs["evaluations"].mean()),
+                "config": "df_coarse 5 Hz, omega 82 Hz, reference defaults otherwise; voxels sharded"}
+
     # ---- roofline of the dominant kernel (K2) from the in-ABI CUDA events
     pk, pk_kind = peaks()
     gemm_ms = sum(s.gemm_ms for s in stats)
@@ -307,6 +329,7 @@ def run_ours(args, world, rank, local):
                 "d2h_bytes_per_step": nq * 16, "seconds_per_step": e2e_s},
         "gpu_launches": int(sum(2 * s.chunks + 8 for s in stats) + (args.steps if world > 1 else 0)),
         "clocks": clk.summary(),
+        "zoom": zoom,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -331,6 +354,7 @@ def main():
     ap.add_argument("--delta", type=float, default=1e-3)
     ap.add_argument("--ref-voxels", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-zoom", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":

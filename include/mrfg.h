@@ -200,6 +200,11 @@ int mrfg_quantify(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_confi
 int mrfg_quantify_slice(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
                         const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
                         mrfg_quant* out, double* seconds);
+/* mrfg_quantify on device-resident fingerprints (nvox x 2N FP64) and results
+ * (async on the ctx stream; t1_ms/t2_ms/df_hz of d_out are left 0 -- the
+ * lattice indices are filled). */
+int mrfg_quantify_dev(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                      const double* d_fps, int64_t nvox, mrfg_quant* d_out);
 /* quantify_impl with explicit per-voxel lattice bounds (lo1,hi1,lo2,hi2,lodf,hidf)
  * and initial T1/T2 [ms] (zoom.cpp:416-429); either array may be NULL (full
  * bounds / cfg->init_*). */

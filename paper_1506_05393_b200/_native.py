@@ -73,6 +73,7 @@ EXPORTS = [
     "mrfg_generate_dev", "mrfg_bloch_norms_dev", "mrfg_scan_grid", "mrfg_scan_grid_dev",
     "mrfg_scan_dict", "mrfg_scan_dict_dev",
     "mrfg_merge_matches_dev", "mrfg_screen_scores", "mrfg_cc_map", "mrfg_quantify", "mrfg_quantify_slice", "mrfg_quantify_bounded",
+    "mrfg_quantify_dev",
 ]
 
 _lib = None
@@ -127,6 +128,7 @@ def load() -> C.CDLL:
     L.mrfg_cc_map.argtypes = [vp, C.POINTER(Grid), dp, i64, i64, C.POINTER(C.c_float)]
     L.mrfg_quantify.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp, i64,
                                 C.POINTER(Quant)]
+    L.mrfg_quantify_dev.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), vp, i64, vp]
     L.mrfg_quantify_bounded.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp, i64,
                                         C.POINTER(i64), dp, C.POINTER(Quant)]
     L.mrfg_quantify_slice.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp,

@@ -790,6 +790,16 @@ int mrfg_quantify_bounded(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom
     });
 }
 
+int mrfg_quantify_dev(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                      const double* d_fps, int64_t nvox, mrfg_quant* d_out) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(nvox >= 0, MRFG_E_INVALID, "quantify: negative voxel count");
+        if (nvox) run_quantify(c, *lattice, *cfg, d_fps, nvox, nullptr, nullptr, d_out);
+    });
+}
+
 int mrfg_quantify(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
                   const double* fps, int64_t nvox, mrfg_quant* out) {
     return mrfg_quantify_bounded(h, lattice, cfg, fps, nvox, nullptr, nullptr, out);

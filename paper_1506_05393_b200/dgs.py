@@ -316,6 +316,12 @@ class Context:
                                      _dp(q.view(np.float64)), q.shape[0], out))
         return quant_array(out)
 
+    def quantify_device(self, d_fps_ptr: int, nvox: int, lattice: Grid, cfg: ZoomConfig,
+                        d_out_ptr: int) -> None:
+        """quantify on device buffers (nvox x 2N float64 in, nvox Quant records out)."""
+        check(self.lib.mrfg_quantify_dev(self.h, C.byref(lattice), C.byref(cfg),
+                                         C.c_void_p(d_fps_ptr), nvox, C.c_void_p(d_out_ptr)))
+
     def quantify_bounded(self, fps, lattice: Grid, cfg: ZoomConfig = None, bounds=None,
                          init_ms=None) -> "np.ndarray":
         """quantify_impl with per-voxel index bounds (V,6) and initial T1/T2 ms (V,2)."""

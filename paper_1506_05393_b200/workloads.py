@@ -13,6 +13,10 @@ Conventions that the reference does not define are stated here once:
   ``rng_at(11, 30/31/32, c)``), classes 1..5 are rotated ellipses drawn from
   ``uniform01(11, 33..37, c)`` painted over class 0 (all voxels in the mask),
   proton density 0.6 + 0.8 * uniform01(11, 38, c);
+* config 4 phantom: three white fields ``rng::gaussian(13, 40+k, y*64+x)``,
+  periodic Gaussian filter sigma = 3 voxels, each rescaled to [0, 1] and mapped
+  affinely into T1 400-3000 ms, T2 40-300 ms, df -150..150 Hz, snapped to the
+  1 ms / 0.5 ms / 0.1 Hz lattice; ZOOM settings ``CONFIG4_ZOOM``;
 * noise: ``add_noise(pd*s, sigma, seed=1_000_000 + v)`` with
   sigma = ||pd*s||_2 / sqrt(N) / SNR per real channel.
 
@@ -35,7 +39,7 @@ CONFIGS = {
             snr=30.0, phantom="ellipses"),
     # config 4 is a ZOOM-only lattice (1 ms / 0.5 ms / 0.1 Hz)
     4: dict(n=1000, t1=(100, 5000, 1), t2=(20, 2000, 0.5), df=(-250, 250, 0.1), nx=64, ny=64,
-            snr=30.0, phantom="uniform"),
+            snr=30.0, phantom="smooth"),
 }
 
 
@@ -80,6 +84,33 @@ def ellipse_classes(nx: int, ny: int, nclass: int = 6, seed: int = 11) -> np.nda
     return cls.reshape(-1)
 
 
+def smooth_fields(nx: int, ny: int, sigma: float = 3.0, seed: int = 13, nfields: int = 3) -> np.ndarray:
+    """Config 4 phantom: Gaussian-filtered (sigma voxels, periodic) white fields
+    from rng::gaussian(seed, 40+k, y*nx+x), each rescaled to [0, 1]."""
+    r = int(np.ceil(3 * sigma))
+    x = np.arange(-r, r + 1, dtype=np.float64)
+    w = np.exp(-0.5 * (x / sigma) ** 2)
+    w /= w.sum()
+    out = np.empty((nfields, ny * nx))
+    for k in range(nfields):
+        g = np.array([dgs.gaussian(seed, 40 + k, i) for i in range(nx * ny)]).reshape(ny, nx)
+        for axis in (0, 1):
+            g = sum(wi * np.roll(g, s, axis=axis) for wi, s in zip(w, range(-r, r + 1)))
+        g = g.reshape(-1)
+        out[k] = (g - g.min()) / (g.max() - g.min())
+    return out
+
+
+# config 4 tissue ranges the smooth fields are mapped into [ms, ms, Hz]
+CONFIG4_RANGES = ((400.0, 3000.0), (40.0, 300.0), (-150.0, 150.0))
+
+# config 4 ZOOM settings (SURVEY.md 8(d): coarse 100 ms / 50 ms / 10 Hz, x10
+# refinement per level, 3 levels), the same on the GPU and the reference.
+CONFIG4_ZOOM = dict(df_coarse_hz=10.0, df_refine_hz=1.0, df_window_hz=20.0, omega_hz=82.0,
+                    t1t2_2d_steps_ms=[100.0, 10.0], t1t2_1d_steps_ms=[50.0, 5.0, 1.0],
+                    final_2d_step_ms=0.5)
+
+
 def noisy(fps_clean: np.ndarray, snr: float, seed0: int = 1_000_000) -> np.ndarray:
     out = np.empty_like(fps_clean)
     n = fps_clean.shape[1]
@@ -110,6 +141,13 @@ def make(config: int, simulate, nvox: int | None = None, n: int | None = None,
         uniq, inv = np.unique(truth, axis=0, return_inverse=True)
         base = simulate(sched, np.stack(dgs.params_at(g, uniq[:, 0], uniq[:, 1], uniq[:, 2]), axis=1))
         clean = base[inv.reshape(-1)] * pd[:, None]
+    elif c["phantom"] == "smooth":
+        f = smooth_fields(nx, ny)[:, :V]
+        truth = np.empty((V, 3), dtype=np.int64)
+        for k, (ax, (lo, hi)) in enumerate(zip((g.t1_ms, g.t2_ms, g.df_hz), CONFIG4_RANGES)):
+            truth[:, k] = np.clip(np.rint((lo + (hi - lo) * f[k] - ax.min) / ax.step), 0, ax.count - 1)
+        pd = np.ones(V)
+        clean = simulate(sched, np.stack(dgs.params_at(g, truth[:, 0], truth[:, 1], truth[:, 2]), axis=1))
     else:
         truth = uniform_truth(g, V)
         pd = np.ones(V)

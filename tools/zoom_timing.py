@@ -1,6 +1,6 @@
 import time, sys, json
 import numpy as np
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import paper_1506_05393_b200 as P
 from paper_1506_05393_b200 import workloads
 

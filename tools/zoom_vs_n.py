@@ -1,5 +1,5 @@
 import sys, time, json
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import numpy as np
 import paper_1506_05393_b200 as P
 from paper_1506_05393_b200 import workloads
