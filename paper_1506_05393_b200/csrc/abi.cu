@@ -78,37 +78,44 @@ const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
     std::vector<double> e1(n * n1 * 2), e2(n * n2 * 2), ph(n * nd * 4);
     std::vector<float> e1f(n * n1 * 4), e2f(n * n2 * 2), phf(n * nd * 4);
     const double kTwoPi = 6.283185307179586476925286766559;
+    // Layout: parameter-major, [i][j] (one lattice value's n steps contiguous),
+    // so a walker over j streams memory (K3/K4/K5 gather scattered points).
 #pragma omp parallel for schedule(static)
-    for (int64_t j = 0; j < n; ++j) {
-        const double te = c.te_s[j], rest = c.rest_s[j];
-        for (int64_t i = 0; i < n1; ++i) {
-            const double inv = 1.0 / ((g.t1_ms.min + static_cast<double>(i) * g.t1_ms.step) * 1e-3);
-            const double a = std::exp(-te * inv), b = std::exp(-rest * inv);
-            e1[(j * n1 + i) * 2] = a;
-            e1[(j * n1 + i) * 2 + 1] = b;
-            float* f = &e1f[(j * n1 + i) * 4];
+    for (int64_t i = 0; i < n1; ++i) {
+        const double inv = 1.0 / ((g.t1_ms.min + static_cast<double>(i) * g.t1_ms.step) * 1e-3);
+        for (int64_t j = 0; j < n; ++j) {
+            const double a = std::exp(-c.te_s[j] * inv), b = std::exp(-c.rest_s[j] * inv);
+            e1[(i * n + j) * 2] = a;
+            e1[(i * n + j) * 2 + 1] = b;
+            float* f = &e1f[(i * n + j) * 4];
             f[0] = static_cast<float>(a);
             f[1] = static_cast<float>(1.0 - a);
             f[2] = static_cast<float>(b);
             f[3] = static_cast<float>(1.0 - b);
         }
-        for (int64_t i = 0; i < n2; ++i) {
-            const double inv = 1.0 / ((g.t2_ms.min + static_cast<double>(i) * g.t2_ms.step) * 1e-3);
-            const double a = std::exp(-te * inv), b = std::exp(-rest * inv);
-            e2[(j * n2 + i) * 2] = a;
-            e2[(j * n2 + i) * 2 + 1] = b;
-            e2f[(j * n2 + i) * 2] = static_cast<float>(a);
-            e2f[(j * n2 + i) * 2 + 1] = static_cast<float>(b);
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n2; ++i) {
+        const double inv = 1.0 / ((g.t2_ms.min + static_cast<double>(i) * g.t2_ms.step) * 1e-3);
+        for (int64_t j = 0; j < n; ++j) {
+            const double a = std::exp(-c.te_s[j] * inv), b = std::exp(-c.rest_s[j] * inv);
+            e2[(i * n + j) * 2] = a;
+            e2[(i * n + j) * 2 + 1] = b;
+            e2f[(i * n + j) * 2] = static_cast<float>(a);
+            e2f[(i * n + j) * 2 + 1] = static_cast<float>(b);
         }
-        for (int64_t i = 0; i < nd; ++i) {
-            const double df = g.df_hz.min + static_cast<double>(i) * g.df_hz.step;
-            const double at = kTwoPi * df * te, ar = kTwoPi * df * rest;
-            double* p = &ph[(j * nd + i) * 4];
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < nd; ++i) {
+        const double df = g.df_hz.min + static_cast<double>(i) * g.df_hz.step;
+        for (int64_t j = 0; j < n; ++j) {
+            const double at = kTwoPi * df * c.te_s[j], ar = kTwoPi * df * c.rest_s[j];
+            double* p = &ph[(i * n + j) * 4];
             p[0] = std::cos(at);
             p[1] = std::sin(at);
             p[2] = std::cos(ar);
             p[3] = std::sin(ar);
-            float* f = &phf[(j * nd + i) * 4];
+            float* f = &phf[(i * n + j) * 4];
             for (int k = 0; k < 4; ++k) f[k] = static_cast<float>(p[k]);
         }
     }
@@ -437,6 +444,8 @@ int mrfg_create(const double* flip_deg, const double* phase_deg, const double* t
             c.te_s[i] = te_ms[i] * 1e-3;
             c.rest_s[i] = tr_ms[i] * 1e-3 - te_ms[i] * 1e-3;
             for (int k = 0; k < 9; ++k) rf32[12 * i + k] = static_cast<float>(c.rf64[9 * i + k]);
+            rf32[12 * i + 9] = static_cast<float>(c.te_s[i]);  // per-step intervals (s) in the pad
+            rf32[12 * i + 10] = static_cast<float>(c.rest_s[i]);
         }
         double inv[9];
         host_rf_matrix(3.14159265358979323846, 0, inv);  // bloch.cpp:113

@@ -69,11 +69,12 @@ struct GridTables {
     mrfg_grid grid{};
     DevBuf stepu;  // n x StepU
     bool valid = false;
-    // FP32: e1[j*n1+i] = (E1te, 1-E1te, E1rest, 1-E1rest); e2[j*n2+i] = (E2te, E2rest);
-    //       ph[j*ndf+i] = (cos te, sin te, cos rest, sin rest)
+    // Parameter-major (lattice index i, step j):
+    // FP32: e1[i*n+j] = (E1te, 1-E1te, E1rest, 1-E1rest); e2[i*n+j] = (E2te, E2rest);
+    //       ph[i*n+j] = (cos te, sin te, cos rest, sin rest)
     DevBuf e1f, e2f, phf;
-    // FP64, same index order: e1d[(j*n1+i)*2 + {0,1}] = (E1te, E1rest); e2d likewise;
-    // phd[(j*ndf+i)*4 + {0..3}] = (cos te, sin te, cos rest, sin rest)
+    // FP64, same index order: e1d[(i*n+j)*2 + {0,1}] = (E1te, E1rest); e2d likewise;
+    // phd[(i*n+j)*4 + {0..3}] = (cos te, sin te, cos rest, sin rest)
     DevBuf e1d, e2d, phd;
 };
 
@@ -87,7 +88,7 @@ struct Ctx {
     std::vector<double> rf64;       // n x 9 (bloch.cpp:101)
     std::vector<double> te_s, rest_s;
     double inv64[9];                // kInvert (bloch.cpp:113)
-    DevBuf rf64_d, rf32_d;          // n x 9 doubles, n x 12 floats (padded)
+    DevBuf rf64_d, rf32_d;          // n x 9 doubles; n x 12 floats (9 RF, te, rest, pad)
     GridTables tab;                 // cache for the last grid
     // scratch
     DevBuf q64, qprime, best, cand, cand_count, atoms_a, inv2, seed_a, seed_inv2, rerank,

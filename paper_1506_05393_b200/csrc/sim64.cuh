@@ -54,11 +54,12 @@ struct StepT {
 };
 __device__ __forceinline__ StepT load_step(const double* __restrict__ e1d,
                                            const double* __restrict__ e2d,
-                                           const double* __restrict__ phd, const Lattice& L, int j,
-                                           int i1, int i2, int idf) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(e1d + (static_cast<int64_t>(j) * L.n1 + i1) * 2));
-    const double2 b = __ldg(reinterpret_cast<const double2*>(e2d + (static_cast<int64_t>(j) * L.n2 + i2) * 2));
-    const double2* P = reinterpret_cast<const double2*>(phd + (static_cast<int64_t>(j) * L.ndf + idf) * 4);
+                                           const double* __restrict__ phd, const Lattice& L, int n,
+                                           int j, int i1, int i2, int idf) {
+    // parameter-major tables: entry (i, j) at i*n + j
+    const double2 a = __ldg(reinterpret_cast<const double2*>(e1d + (static_cast<int64_t>(i1) * n + j) * 2));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(e2d + (static_cast<int64_t>(i2) * n + j) * 2));
+    const double2* P = reinterpret_cast<const double2*>(phd + (static_cast<int64_t>(idf) * n + j) * 4);
     const double2 p0 = __ldg(P), p1 = __ldg(P + 1);
     return {a.x, a.y, b.x, b.y, p0.x, p0.y, p1.x, p1.y};
 }
@@ -70,7 +71,8 @@ constexpr int kPrefetchSteps = 8;
 
 // Walk one lattice atom through the schedule (bloch.cpp:108-123) calling
 // at(j, mx, my) at every echo.  The table gathers run two steps ahead of
-// the recursion in registers and eight steps ahead as L1 prefetches, so their
+// the recursion in registers and eight steps ahead as L1 prefetches (one per
+// 128-byte line, every fourth step), so their
 // L2 latency hides behind the FP64 dependency chain (measured: the per-step
 // gather latency, not the FP64 pipe, bounded K3/K5).  `extra(j)` returns one
 // more per-step address to prefetch (the query row), or nullptr.
@@ -82,23 +84,28 @@ __device__ __forceinline__ void sim64_walk_pf(const double* __restrict__ rf,
                                               int n, const Lattice& L, int i1, int i2, int idf, AT at,
                                               PF extra) {
     double x = inv0[0], y = inv0[1], z = inv0[2];
+    const double* p1 = e1d + static_cast<int64_t>(i1) * n * 2;
+    const double* p2 = e2d + static_cast<int64_t>(i2) * n * 2;
+    const double* pd = phd + static_cast<int64_t>(idf) * n * 4;
     for (int j = 0; j < kPrefetchSteps && j < n; ++j) {
-        prefetch_l1(e1d + (static_cast<int64_t>(j) * L.n1 + i1) * 2);
-        prefetch_l1(e2d + (static_cast<int64_t>(j) * L.n2 + i2) * 2);
-        prefetch_l1(phd + (static_cast<int64_t>(j) * L.ndf + idf) * 4);
+        prefetch_l1(p1 + j * 2);
+        prefetch_l1(p2 + j * 2);
+        prefetch_l1(pd + j * 4);
         if (const void* e = extra(j)) prefetch_l1(e);
     }
-    StepT c0 = load_step(e1d, e2d, phd, L, 0, i1, i2, idf);
-    StepT c1 = load_step(e1d, e2d, phd, L, n > 1 ? 1 : 0, i1, i2, idf);
+    StepT c0 = load_step(e1d, e2d, phd, L, n, 0, i1, i2, idf);
+    StepT c1 = load_step(e1d, e2d, phd, L, n, n > 1 ? 1 : 0, i1, i2, idf);
     for (int j = 0; j < n; ++j) {
-        if (j + kPrefetchSteps < n) {
-            const int64_t jp = j + kPrefetchSteps;
-            prefetch_l1(e1d + (jp * L.n1 + i1) * 2);
-            prefetch_l1(e2d + (jp * L.n2 + i2) * 2);
-            prefetch_l1(phd + (jp * L.ndf + idf) * 4);
-            if (const void* e = extra(static_cast<int>(jp))) prefetch_l1(e);
+        // one prefetch per 128-byte line: every 4 steps (the 32-byte phasor
+        // rows; the 16-byte rows are touched twice per line)
+        if ((j & 3) == 0 && j + kPrefetchSteps < n) {
+            const int jp = j + kPrefetchSteps;
+            prefetch_l1(p1 + jp * 2);
+            prefetch_l1(p2 + jp * 2);
+            prefetch_l1(pd + jp * 4);
+            if (const void* e = extra(jp)) prefetch_l1(e);
         }
-        const StepT c2 = load_step(e1d, e2d, phd, L, j + 2 < n ? j + 2 : n - 1, i1, i2, idf);
+        const StepT c2 = load_step(e1d, e2d, phd, L, n, j + 2 < n ? j + 2 : n - 1, i1, i2, idf);
         rf_apply64(rf + 9 * j, x, y, z);
         relax64(x, y, z, c0.e1t, c0.e2t, c0.ct, c0.st);
         at(j, x, y);

@@ -11,13 +11,23 @@
 // reads count as evaluations ("unique acquisitions", zoom.cpp:94-123), so
 // answers, scores and evaluation counts are the reference's.
 //
-// Each evaluation is the reference's FP64 pipeline: simulate (sim64.cuh,
-// host-libm tables => bit-identical fingerprint), FP64 normalize, FP64 CC and
-// Euclidean score (zoom.cpp:74-92), clamp at 1.
+// Certified screening.  A point is first evaluated by a single FP32 pass
+// (zsim32, float host-libm tables; |error| <= 6e-8 measured against the FP64
+// pipeline).  Every decision the reference takes on objective values (a > b,
+// a < threshold, the plateau spread) is taken on those screening values only
+// when they differ by more than a margin eps (1e-5, ~150x the error bound);
+// otherwise the points involved are evaluated exactly -- the reference's FP64
+// pipeline (simulate with host-libm tables => bit-identical fingerprint, FP64
+// normalize, FP64 CC/Euclidean score, zoom.cpp:74-92, clamp at 1) -- and the
+// decision is taken on exact values.  The decision sequence, the answer and
+// the evaluation count are therefore the reference's; the reported score and
+// PD are always exact.  MRFG_ZOOM_EPS=-1 evaluates everything in FP64.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "mrfg_internal.cuh"
@@ -28,15 +38,23 @@ namespace {
 
 constexpr unsigned long long kEmpty = ~0ull;
 constexpr unsigned long long kAcq = 1ull << 63;  // "acquired" flag in the key word
+constexpr int kPendCap = 256;                    // deferred exact evaluations per warp
+constexpr int kEagerAfter = 6;                   // passes before certifying eagerly
 
+// Memo slot.  `acc`/`are` are the single-pass FP32 screening values (CC
+// magnitude and normalized real part); cc/euc/nrm2 are the reference's FP64
+// values, present once nrm2 >= 0 ("exact").
 struct ZSlot {
     unsigned long long key;
+    float acc, are;
     double cc, euc, nrm2;
 };
 
 struct ZParams {
     // tables
     const double *rf, *e1d, *e2d, *phd;
+    const float4 *rf32, *e1f, *phf;
+    const float2* e2f;
     double inv0[3];
     int n;
     Lattice L;
@@ -50,30 +68,62 @@ struct ZParams {
     long long init1, init2;  // snapped (not yet clamped) initial indices
     // speculation widths: 1-D flanks +-1..spec1d steps, 2-D (2*spec2d+1)^2 block
     long long spec1d, spec2d;
+    // certification margins: |FP32 value - FP64 value| < eps (CC), eps_euc
+    // (Euclidean); eps < 0 = every evaluation in FP64 (no screening)
+    double eps, eps_euc;
     // data
     const double* fps;  // nvox x 2N raw
-    double* q;          // nvox x 2N normalized scratch
-    ZSlot* tab;         // nvox x cap
+    // per-warp scratch (persistent warps, nwarps of them)
+    double* q;          // nwarps x 2N normalized query
+    float2* q32;        // nwarps x N normalized query, FP32
+    double2* fpx;       // nwarps x N x 32 exact-evaluation fingerprints
+    int* pend;          // nwarps x kPendCap deferred exact evaluations
+    ZSlot* tab;         // nwarps x cap memo tables
+    unsigned long long* next;  // voxel work counter
+    int smem_stage;            // rf32 + per-warp q32 staged in dynamic shared memory
+    // screening transcendentals: 0 float host-libm tables (default; audited
+    // max |error| 2.9e-7); 1 MUFU ex2 + sin/cos (experimental, MRFG_ZOOM_SCREEN=mufu:
+    // audited 4.5e-6, too close to eps to certify)
+    int screen_mode;
+    double t1_min, t1_step, t2_min, t2_step, df_min, df_step;  // lattice axes (ms, ms, Hz)
     unsigned int cap_mask;
     const long long* bounds;  // nvox x 6 or null (full bounds)
     const long long* inits;   // nvox x 2 or null
     int64_t nvox;
     mrfg_quant* out;
     int* err;
+    // [fp32 evals, fp64 evals, fp64 rounds, near ties, sum cycles, max cycles,
+    //  screening cycles, exact cycles, max |screening - exact| (double bits), passes] or null
+    unsigned long long* stats;
+    long long* vstats;  // nvox x 4: cycles, screening rounds' cycles, exact rounds, exact cycles
 };
 
 struct Z {
     const ZParams* p;
     ZSlot* tab;
     const double* q;
+    const float2* q32;  // shared memory when staged
+    const float4* rfs;  // FP32 RF rotations (3 float4 per step), shared memory when staged
+    double2* fpx;       // exact-evaluation scratch: n x 32 lanes
+    int* pend;          // deferred exact evaluations (memo slots), kPendCap
+    int npend;          // warp-uniform
+    int eager;          // 1: certify each close decision immediately
     int lane;
     long long evals;
+    long long cyc32, cyc64;  // stats: cycles in screening / exact rounds
+    long long r64;           // stats: exact rounds
     long long lo1, hi1, lo2, hi2, lodf, hidf;
 };
 
 __device__ __forceinline__ unsigned long long zkey(long long i1, long long i2, long long idf) {
     return (static_cast<unsigned long long>(i1) << 42) | (static_cast<unsigned long long>(i2) << 21) |
            static_cast<unsigned long long>(idf);
+}
+__device__ __forceinline__ void zunkey(unsigned long long k, int& i1, int& i2, int& idf) {
+    k &= ~kAcq;
+    i1 = static_cast<int>(k >> 42);
+    i2 = static_cast<int>((k >> 21) & 0x1FFFFF);
+    idf = static_cast<int>(k & 0x1FFFFF);
 }
 __device__ __forceinline__ unsigned int zhash(unsigned long long k) {
     k ^= k >> 33;
@@ -85,6 +135,14 @@ __device__ __forceinline__ unsigned int zhash(unsigned long long k) {
 }
 __device__ __forceinline__ long long clampll(long long v, long long lo, long long hi) {
     return v < lo ? lo : (v > hi ? hi : v);
+}
+__device__ __forceinline__ void zsync() {
+    __syncwarp();
+    __threadfence_block();
+    __syncwarp();
+}
+__device__ __forceinline__ void zstat(const Z& z, int k, unsigned long long v) {
+    if (z.p->stats && v) atomicAdd(z.p->stats + k, v);
 }
 
 __device__ int zfind(const Z& z, unsigned long long key) {
@@ -119,35 +177,187 @@ __device__ int zclaim(const Z& z, unsigned long long key, bool& fresh) {
     return -1;
 }
 
-// One objective evaluation: the reference's Objective::acquire +
+// One exact objective evaluation: the reference's Objective::acquire +
 // score_from_entry for both metrics, FP64, two passes (norm, then the
 // normalized entry against the query).
-__device__ void zsim(const Z& z, int i1, int i2, int idf, ZSlot& s) {
+__device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, ZSlot& s) {
     const ZParams& P = *z.p;
     const int n = P.n;
-    double acc = sim64_lattice<0>(P.rf, P.e1d, P.e2d, P.phd, P.inv0, n, P.L, i1, i2, idf, 0.0, nullptr);
+    // pass 1: the recursion, |s|^2 in the reference's order (fingerprint.cpp:14-18);
+    // the entries are kept (lane-interleaved scratch) for pass 2
+    double2* fx = z.fpx + z.lane;
+    double acc = 0.0;
+    sim64_walk(P.rf, P.e1d, P.e2d, P.phd, P.inv0, n, P.L, i1, i2, idf, [&](int j, double x, double y) {
+        acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
+        fx[32 * j] = make_double2(x, y);
+    });
     const double inv = 1.0 / sqrt(acc);  // fingerprint.cpp:30-32
+    // pass 2: the normalized entry against the query (zoom.cpp:74-92)
     double re = 0.0, im = 0.0, dd = 0.0;
     const bool euc = P.need_euc;
-    const double* q = z.q;
-    sim64_walk_pf(P.rf, P.e1d, P.e2d, P.phd, P.inv0, n, P.L, i1, i2, idf, [&](int j, double x, double y) {
-        const double er = __dmul_rn(x, inv), ei = __dmul_rn(y, inv);
-        const double qr = q[2 * j], qi = q[2 * j + 1];
-        re = __dadd_rn(re, __dadd_rn(__dmul_rn(qr, er), __dmul_rn(qi, ei)));  // zoom.cpp:79
-        im = __dadd_rn(im, __dsub_rn(__dmul_rn(qi, er), __dmul_rn(qr, ei)));  // zoom.cpp:80
+    const double2* q = reinterpret_cast<const double2*>(z.q);
+    for (int j = 0; j < n; ++j) {
+        const double2 m = fx[32 * j];
+        const double er = __dmul_rn(m.x, inv), ei = __dmul_rn(m.y, inv);
+        const double2 qq = q[j];
+        re = __dadd_rn(re, __dadd_rn(__dmul_rn(qq.x, er), __dmul_rn(qq.y, ei)));  // zoom.cpp:79
+        im = __dadd_rn(im, __dsub_rn(__dmul_rn(qq.y, er), __dmul_rn(qq.x, ei)));  // zoom.cpp:80
         if (euc) {
-            const double dr = __dsub_rn(qr, er), di = __dsub_rn(qi, ei);  // zoom.cpp:87-89
+            const double dr = __dsub_rn(qq.x, er), di = __dsub_rn(qq.y, ei);  // zoom.cpp:87-89
             dd = __dadd_rn(dd, __dadd_rn(__dmul_rn(dr, dr), __dmul_rn(di, di)));
         }
-    }, [&](int jj) -> const void* { return q + 2 * jj; });
+    }
     const double v = sqrt(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
     s.cc = v < 1.0 ? v : 1.0;  // zoom.cpp:82-83
     s.euc = -sqrt(dd);          // zoom.cpp:91
     s.nrm2 = acc;
 }
 
-// Make sure the points pt(0..count-1) are in the memo (computed, not
+// One screening evaluation: single pass in FP32 over the host-libm float
+// tables (same recursion, unnormalized entry), FP32 partial sums folded into
+// FP64 every 16 steps.  Returns the CC magnitude and the normalized real
+// part (Euclidean score = -sqrt(2 - 2 re)).  Measured |error| vs the FP64
+// pipeline: <= 6e-8 (the certification margin eps is 1e-5).
+struct Apx {
+    float cc, re;
+};
+__device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
+    const ZParams& P = *z.p;
+    const int n = P.n;
+    // parameter-major tables: the walk streams n consecutive entries per
+    // lane (rows warp-uniform where the lanes share T1, T2 or df); the
+    // per-step uniform operands (RF rotation, query) come from shared memory
+    const float4* __restrict__ e1p = P.e1f + static_cast<int64_t>(i1) * n;
+    const float2* __restrict__ e2p = P.e2f + static_cast<int64_t>(i2) * n;
+    const float4* __restrict__ php = P.phf + static_cast<int64_t>(idf) * n;
+    const float4* rfp = z.rfs;
+    const float2* q = z.q32;
+    float x = static_cast<float>(P.inv0[0]), y = static_cast<float>(P.inv0[1]),
+          zz = static_cast<float>(P.inv0[2]);
+    double re = 0.0, im = 0.0, nn = 0.0;
+    // L1 prefetch one 128-byte line (8 float4 / 16 float2 steps) two lines ahead
+    for (int j = 0; j < 16 && j < n; j += 8) {
+        prefetch_l1(e1p + j);
+        prefetch_l1(php + j);
+    }
+    prefetch_l1(e2p);
+    // table entries one step ahead in registers
+    float4 e1 = __ldg(e1p), ph = __ldg(php);
+    float2 e2 = __ldg(e2p);
+    for (int jb = 0; jb < n; jb += 16) {
+        float pr = 0.f, pi = 0.f, pn = 0.f;
+        const int je = min(n, jb + 16);
+        if (jb + 16 < n) prefetch_l1(e2p + jb + 16);
+        for (int j = jb; j < je; ++j) {
+            if ((j & 7) == 0 && j + 16 < n) {
+                prefetch_l1(e1p + j + 16);
+                prefetch_l1(php + j + 16);
+            }
+            const int jn = j + 1 < n ? j + 1 : j;
+            const float4 e1n = __ldg(e1p + jn), phn = __ldg(php + jn);
+            const float2 e2n = __ldg(e2p + jn);
+            const float4 ra = rfp[3 * j], rb = rfp[3 * j + 1], rc = rfp[3 * j + 2];
+            const float2 qq = q[j];
+            // RF rotation (bloch.hpp:34-38)
+            const float nx = fmaf(ra.x, x, fmaf(ra.y, y, ra.z * zz));
+            const float ny = fmaf(ra.w, x, fmaf(rb.x, y, rb.y * zz));
+            const float nz = fmaf(rb.z, x, fmaf(rb.w, y, rc.x * zz));
+            // relax/precess over te (bloch.cpp:22-26): z' = z E1 + (1 - E1)
+            x = (nx * ph.x - ny * ph.y) * e2.x;
+            y = (nx * ph.y + ny * ph.x) * e2.x;
+            zz = fmaf(nz, e1.x, e1.y);
+            pr = fmaf(qq.x, x, fmaf(qq.y, y, pr));
+            pi = fmaf(qq.y, x, fmaf(-qq.x, y, pi));
+            pn = fmaf(x, x, fmaf(y, y, pn));
+            // over the rest of TR
+            const float rx = (x * ph.z - y * ph.w) * e2.y;
+            const float ry = (x * ph.w + y * ph.z) * e2.y;
+            x = rx;
+            y = ry;
+            zz = fmaf(zz, e1.z, e1.w);
+            e1 = e1n;
+            e2 = e2n;
+            ph = phn;
+        }
+        re += pr;
+        im += pi;
+        nn += pn;
+    }
+    const double inv = rsqrt(nn);
+    Apx a;
+    a.cc = static_cast<float>(fmin(sqrt(re * re + im * im) * inv, 1.0));
+    a.re = static_cast<float>(re * inv);
+    return a;
+}
+
+// The same screening evaluation with the per-step transcendentals computed
+// in registers instead of gathered (no per-lane memory streams): E = ex2(-dt
+// log2(e) / T) (MUFU.EX2), phasors from the range-reduced turn count df*dt
+// (MUFU.SIN/COS).  te/rest come from the staged RF rows (pad floats 9, 10).
+__device__ __noinline__ Apx zsim32_mufu(const Z& z, int i1, int i2, int idf) {
+    const ZParams& P = *z.p;
+    const int n = P.n;
+    const float4* rfp = z.rfs;
+    const float2* q = z.q32;
+    const float k1 = static_cast<float>(-1.4426950408889634 / ((P.t1_min + i1 * P.t1_step) * 1e-3));
+    const float k2 = static_cast<float>(-1.4426950408889634 / ((P.t2_min + i2 * P.t2_step) * 1e-3));
+    const float df = static_cast<float>(P.df_min + idf * P.df_step);
+    float x = static_cast<float>(P.inv0[0]), y = static_cast<float>(P.inv0[1]),
+          zz = static_cast<float>(P.inv0[2]);
+    double re = 0.0, im = 0.0, nn = 0.0;
+    for (int jb = 0; jb < n; jb += 16) {
+        float pr = 0.f, pi = 0.f, pn = 0.f;
+        const int je = min(n, jb + 16);
+        for (int j = jb; j < je; ++j) {
+            const float4 ra = rfp[3 * j], rb = rfp[3 * j + 1], rc = rfp[3 * j + 2];
+            const float2 qq = q[j];
+            const float te = rc.y, rest = rc.z;
+            const float e1t = exp2f(te * k1), e1r = exp2f(rest * k1);
+            const float e2t = exp2f(te * k2), e2r = exp2f(rest * k2);
+            // turn counts df*dt as exact two-products (hi + lo), reduced to [-0.5, 0.5]
+            const float tth = df * te, trh = df * rest;
+            const float tt = (tth - rintf(tth)) + fmaf(df, te, -tth);
+            const float tr = (trh - rintf(trh)) + fmaf(df, rest, -trh);
+            float st, ct, sr, cr;
+            __sincosf(6.283185307179586f * tt, &st, &ct);
+            __sincosf(6.283185307179586f * tr, &sr, &cr);
+            // RF rotation (bloch.hpp:34-38)
+            const float nx = fmaf(ra.x, x, fmaf(ra.y, y, ra.z * zz));
+            const float ny = fmaf(ra.w, x, fmaf(rb.x, y, rb.y * zz));
+            const float nz = fmaf(rb.z, x, fmaf(rb.w, y, rc.x * zz));
+            // relax/precess over te (bloch.cpp:22-26)
+            x = (nx * ct - ny * st) * e2t;
+            y = (nx * st + ny * ct) * e2t;
+            zz = fmaf(nz - 1.f, e1t, 1.f);
+            pr = fmaf(qq.x, x, fmaf(qq.y, y, pr));
+            pi = fmaf(qq.y, x, fmaf(-qq.x, y, pi));
+            pn = fmaf(x, x, fmaf(y, y, pn));
+            // over the rest of TR
+            const float rx = (x * cr - y * sr) * e2r;
+            const float ry = (x * sr + y * cr) * e2r;
+            x = rx;
+            y = ry;
+            zz = fmaf(zz - 1.f, e1r, 1.f);
+        }
+        re += pr;
+        im += pi;
+        nn += pn;
+    }
+    const double inv = rsqrt(nn);
+    Apx a;
+    a.cc = static_cast<float>(fmin(sqrt(re * re + im * im) * inv, 1.0));
+    a.re = static_cast<float>(re * inv);
+    return a;
+}
+
+__device__ __forceinline__ Apx zsim32(const Z& z, int i1, int i2, int idf) {
+    const int m = z.p->screen_mode;
+    return m == 1 ? zsim32_mufu(z, i1, i2, idf) : zsim32_tab(z, i1, i2, idf);
+}
+
+// Make sure the points pt(0..count-1) are in the memo (screened, not
 // acquired).  Lanes split the missing points; duplicates are claimed once.
+// With eps < 0 the points are evaluated exactly instead.
 template <class PT>
 __device__ void zensure(Z& z, long long count, PT pt) {
     for (long long base = 0; base < count; base += 32) {
@@ -165,25 +375,102 @@ __device__ void zensure(Z& z, long long count, PT pt) {
                 }
             }
         }
+        const long long t0 = z.p->stats ? clock64() : 0;
         if (mine) {
-            ZSlot s;
-            zsim(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c), s);
-            z.tab[slot].cc = s.cc;
-            z.tab[slot].euc = s.euc;
-            z.tab[slot].nrm2 = s.nrm2;
+            if (z.p->eps < 0) {
+                ZSlot s;
+                zsim(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c), s);
+                z.tab[slot].cc = s.cc;
+                z.tab[slot].euc = s.euc;
+                z.tab[slot].nrm2 = s.nrm2;
+                z.tab[slot].acc = static_cast<float>(s.cc);
+                z.tab[slot].are = 0.f;
+            } else {
+                const Apx v = zsim32(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c));
+                z.tab[slot].acc = v.cc;
+                z.tab[slot].are = v.re;
+                z.tab[slot].nrm2 = -1.0;
+                if (z.p->stats && (zhash(zkey(a, b, c) * 0x9E3779B97F4A7C15ull) & 63) == 0) {
+                    // audit (stats mode only): exact value of a random 1/64 of
+                    // all screened points, |error| into stats[10]
+                    ZSlot r;
+                    zsim(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c), r);
+                    const double e = fabs(static_cast<double>(v.cc) - r.cc);
+                    atomicMax(z.p->stats + 10, static_cast<unsigned long long>(__double_as_longlong(e)));
+                    atomicAdd(z.p->stats + 11, 1ull);
+                }
+            }
         }
-        __syncwarp();
-        __threadfence_block();
-        __syncwarp();
+        if (z.p->stats) {
+            const unsigned int m = __ballot_sync(0xffffffffu, mine);
+            if (z.lane == 0) zstat(z, z.p->eps < 0 ? 1 : 0, __popc(m));
+            __syncwarp();
+            if (m) z.cyc32 += clock64() - t0;
+        }
+        zsync();
     }
 }
 
+// Exact (FP64) evaluation of the memo slots named by slot_of(0..count-1)
+// (-1 = none) that are still screened-only, one warp round per 32 slots.
+template <class SL>
+__device__ void zexact(Z& z, int count, SL slot_of) {
+    for (int base = 0; base < count; base += 32) {
+        const int k = base + z.lane;
+        const int s = k < count ? slot_of(k) : -1;
+        const bool work = s >= 0 && *reinterpret_cast<volatile double*>(&z.tab[s].nrm2) < 0.0;
+        const unsigned int m = __ballot_sync(0xffffffffu, work);
+        if (!m) continue;
+        const long long t0 = z.p->stats ? clock64() : 0;
+        if (work) {
+            int i1, i2, idf;
+            zunkey(*reinterpret_cast<volatile unsigned long long*>(&z.tab[s].key), i1, i2, idf);
+            ZSlot r;
+            zsim(z, i1, i2, idf, r);
+            if (z.p->stats) {
+                const double e = fabs(static_cast<double>(z.tab[s].acc) - r.cc);
+                atomicMax(z.p->stats + 8, static_cast<unsigned long long>(__double_as_longlong(e)));
+            }
+            z.tab[s].cc = r.cc;
+            z.tab[s].euc = r.euc;
+            __threadfence_block();
+            z.tab[s].nrm2 = r.nrm2;
+        }
+        if (z.lane == 0) {
+            zstat(z, 1, __popc(m));
+            zstat(z, 2, 1);
+        }
+        if (z.p->stats) {
+            __syncwarp();
+            z.cyc64 += clock64() - t0;
+            ++z.r64;
+        }
+        zsync();
+    }
+}
+
+// A decision value: the memo slot it came from and whether it is the exact
+// (reference) value or the FP32 screening value.
+struct V {
+    double v;
+    int slot;
+    int exact;
+};
+
+__device__ __forceinline__ V zread(const Z& z, int s, int metric) {
+    const volatile ZSlot* vs = &z.tab[s];
+    if (vs->nrm2 >= 0.0) return {metric == MRFG_METRIC_CC ? vs->cc : vs->euc, s, 1};
+    if (metric == MRFG_METRIC_CC) return {static_cast<double>(vs->acc), s, 0};
+    const double d = 2.0 - 2.0 * static_cast<double>(vs->are);
+    return {-sqrt(d > 0.0 ? d : 0.0), s, 0};
+}
+
 // Objective::eval (zoom.cpp:125-138): range check, memo read, acquisition count.
-__device__ double zf(Z& z, long long i1, long long i2, long long idf, int metric) {
+__device__ V zf(Z& z, long long i1, long long i2, long long idf, int metric) {
     const ZParams& P = *z.p;
     if (i1 < 0 || i2 < 0 || idf < 0 || i1 >= P.L.n1 || i2 >= P.L.n2 || idf >= P.L.ndf) {
         atomicExch(P.err, 1);
-        return -1e300;
+        return {-1e300, -1, 1};
     }
     const unsigned long long key = zkey(i1, i2, idf);
     int s = zfind(z, key);
@@ -194,27 +481,94 @@ __device__ double zf(Z& z, long long i1, long long i2, long long idf, int metric
             c = idf;
         });
         s = zfind(z, key);
-        if (s < 0) return -1e300;
+        if (s < 0) return {-1e300, -1, 1};
     }
     const unsigned long long kk = *reinterpret_cast<volatile unsigned long long*>(&z.tab[s].key);
     if (!(kk & kAcq)) {
         __syncwarp();
         if (z.lane == 0) z.tab[s].key = kk | kAcq;
-        __syncwarp();
-        __threadfence_block();
-        __syncwarp();
+        zsync();
         ++z.evals;
     }
-    const volatile ZSlot* vs = &z.tab[s];
-    return metric == MRFG_METRIC_CC ? vs->cc : vs->euc;
+    return zread(z, s, metric);
+}
+
+__device__ __forceinline__ double zmargin(const Z& z, int metric) {
+    return metric == MRFG_METRIC_CC ? z.p->eps : z.p->eps_euc;
+}
+
+// Make a value exact (FP64) in place.
+__device__ void zmake_exact(Z& z, V& a, int metric) {
+    if (a.exact) return;
+    const int s = a.slot;
+    zexact(z, 1, [&](int) { return s; });
+    a = zread(z, s, metric);
+}
+
+// Evaluate every deferred slot exactly, 32 per warp round.
+__device__ void zflush(Z& z) {
+    zsync();
+    const int* pend = z.pend;
+    zexact(z, z.npend, [&](int k) { return pend[k]; });
+    z.npend = 0;
+}
+
+// Queue a screened-only slot for exact evaluation (nrm2 -1 -> -2 marks it
+// queued, so it is queued once).
+__device__ void zdefer(Z& z, const V& a) {
+    if (a.exact || a.slot < 0) return;
+    volatile double* nr = &z.tab[a.slot].nrm2;
+    if (*nr != -1.0) return;
+    __syncwarp();
+    if (z.lane == 0) {
+        *nr = -2.0;
+        z.pend[z.npend] = a.slot;
+    }
+    zsync();
+    if (++z.npend == kPendCap) zflush(z);
+}
+
+// The reference's `a > b` on objective values.  Screening values decide when
+// the two differ by more than the certification margin (the FP64 values are
+// then ordered the same way).  A closer decision is uncertified: eagerly, both
+// points are evaluated exactly first; optimistically (the default), the
+// screening order is used for now and both points are queued -- the search is
+// then replayed once they are exact (zoom_voxel), until a pass takes every
+// decision certified.
+__device__ bool gt(Z& z, V& a, V& b, int metric) {
+    if (!(a.exact && b.exact) && fabs(a.v - b.v) <= zmargin(z, metric)) {
+        if (z.lane == 0) zstat(z, 3, 1);
+        if (!z.eager) {
+            zdefer(z, a);
+            zdefer(z, b);
+            return a.v > b.v;
+        }
+        const int sa = a.exact ? -1 : a.slot, sb = b.exact ? -1 : b.slot;
+        zexact(z, 2, [&](int k) { return k == 0 ? sa : sb; });
+        if (sa >= 0) a = zread(z, sa, metric);
+        if (sb >= 0) b = zread(z, sb, metric);
+    }
+    return a.v > b.v;
+}
+// `a < c` against a constant threshold.
+__device__ bool lt_const(Z& z, V& a, double c, int metric) {
+    if (!a.exact && fabs(a.v - c) <= zmargin(z, metric)) {
+        if (!z.eager) {
+            zdefer(z, a);
+            return a.v < c;
+        }
+        zmake_exact(z, a, metric);
+    }
+    return a.v < c;
 }
 
 struct Best {
     long long idx;
-    double val;
+    V val;
 };
-__device__ __forceinline__ void offer(Best& b, long long i, double v) {
-    if (v > b.val) {
+__device__ __forceinline__ Best best_init() { return {-1, {-1e300, -1, 1}}; }
+__device__ __forceinline__ void offer(Z& z, Best& b, long long i, V v, int metric) {
+    if (gt(z, v, b.val, metric)) {
         b.val = v;
         b.idx = i;
     }
@@ -228,31 +582,55 @@ __device__ void df_scan(Z& z, long long i1, long long i2, long long a, long long
     b = clampll(b, z.lodf, z.hidf);
     const long long cnt = b >= a ? (b - a) / step + 1 : 0;
     const bool extra = b >= a && (b - a) % step != 0;
-    zensure(z, cnt + (extra ? 1 : 0), [&](long long k, long long& p1, long long& p2, long long& pd) {
+    auto pt = [&](long long k, long long& p1, long long& p2, long long& pd) {
         p1 = i1;
         p2 = i2;
         pd = k < cnt ? a + k * step : b;
-    });
-    for (long long x = a; x <= b; x += step) offer(bst, x, zf(z, i1, i2, x, z.p->metric));
-    if (extra) offer(bst, b, zf(z, i1, i2, b, z.p->metric));
+    };
+    const int metric = z.p->metric;
+    zensure(z, cnt + (extra ? 1 : 0), pt);
+    for (long long x = a; x <= b; x += step) offer(z, bst, x, zf(z, i1, i2, x, metric), metric);
+    if (extra) offer(z, bst, b, zf(z, i1, i2, b, metric), metric);
 }
 
-__device__ bool plateau(const double* marks, int nm, double eps) {
+// zoom.cpp:199-204: the last three marks span less than eps.  The screening
+// spread is within 2 margins of the exact one; closer than that to the
+// threshold the three marks are evaluated exactly.
+__device__ bool plateau(Z& z, V* marks, int nm, double eps) {
     if (nm < 3) return false;
-    double mn = marks[nm - 3], mx = mn;
-    for (int j = nm - 3; j < nm; ++j) {
-        mn = fmin(mn, marks[j]);
-        mx = fmax(mx, marks[j]);
+    const int metric = z.p->metric;
+    auto spread = [&]() {
+        double mn = marks[nm - 3].v, mx = mn;
+        for (int j = nm - 3; j < nm; ++j) {
+            mn = fmin(mn, marks[j].v);
+            mx = fmax(mx, marks[j].v);
+        }
+        return mx - mn;
+    };
+    double s = spread();
+    const bool all_exact = marks[nm - 3].exact && marks[nm - 2].exact && marks[nm - 1].exact;
+    if (!all_exact && fabs(s - eps) <= 2.0 * zmargin(z, metric)) {
+        if (!z.eager) {
+            for (int j = nm - 3; j < nm; ++j) zdefer(z, marks[j]);
+            return s < eps;
+        }
+        const int a = marks[nm - 3].exact ? -1 : marks[nm - 3].slot;
+        const int b = marks[nm - 2].exact ? -1 : marks[nm - 2].slot;
+        const int c = marks[nm - 1].exact ? -1 : marks[nm - 1].slot;
+        zexact(z, 3, [&](int k) { return k == 0 ? a : (k == 1 ? b : c); });
+        for (int j = nm - 3; j < nm; ++j)
+            if (marks[j].slot >= 0) marks[j] = zread(z, marks[j].slot, metric);
+        s = spread();
     }
-    return mx - mn < eps;
+    return s < eps;
 }
 
 // zoom.cpp:189-241
 __device__ Best df_run(Z& z, long long i1, long long i2, long long coarse, long long wh) {
     const ZParams& P = *z.p;
-    double marks[16];
+    V marks[16];
     int nm = 0;
-    Best cur{-1, -1e300};
+    Best cur = best_init();
     df_scan(z, i1, i2, z.lodf, z.hidf, coarse, cur);
     marks[nm++] = cur.val;
     {
@@ -266,27 +644,28 @@ __device__ Best df_run(Z& z, long long i1, long long i2, long long coarse, long 
         const long long nf = cur.idx + P.omega <= z.hidf ? (z.hidf - cur.idx) / P.omega : 0;
         const long long nb = cur.idx - P.omega >= z.lodf ? (cur.idx - z.lodf) / P.omega : 0;
         const long long c0 = cur.idx;
-        zensure(z, nf + nb, [&](long long k, long long& p1, long long& p2, long long& pd) {
+        auto hop = [&](long long k, long long& p1, long long& p2, long long& pd) {
             p1 = i1;
             p2 = i2;
             pd = k < nf ? c0 + (k + 1) * P.omega : c0 - (k - nf + 1) * P.omega;
-        });
+        };
+        zensure(z, nf + nb, hop);
         for (long long k = 1; cur.idx + k * P.omega <= z.hidf; ++k) {
             const long long q = cur.idx + k * P.omega;
-            offer(t, q, zf(z, i1, i2, q, P.metric));
+            offer(z, t, q, zf(z, i1, i2, q, P.metric), P.metric);
         }
         for (long long k = 1; cur.idx - k * P.omega >= z.lodf; ++k) {
             const long long q = cur.idx - k * P.omega;
-            offer(t, q, zf(z, i1, i2, q, P.metric));
+            offer(z, t, q, zf(z, i1, i2, q, P.metric), P.metric);
         }
         if (t.idx == cur.idx) break;
         Best r = t;
         df_scan(z, i1, i2, t.idx - wh, t.idx + wh, P.df_refine, r);
         cur = r;
         marks[nm++] = cur.val;
-        if (plateau(marks, nm, P.plateau_eps)) return cur;
+        if (plateau(z, marks, nm, P.plateau_eps)) return cur;
     }
-    if (plateau(marks, nm, P.plateau_eps)) return cur;
+    if (plateau(z, marks, nm, P.plateau_eps)) return cur;
     Best fin = cur;
     df_scan(z, i1, i2, cur.idx - P.omega / 2, cur.idx + P.omega / 2, 1, fin);
     return fin;
@@ -296,36 +675,37 @@ __device__ Best df_run(Z& z, long long i1, long long i2, long long coarse, long 
 __device__ long long search_df(Z& z, long long i1, long long i2) {
     const ZParams& P = *z.p;
     Best mainb = df_run(z, i1, i2, P.df_coarse, P.df_window_half);
-    if (mainb.val < P.heavy_cc) {
+    if (lt_const(z, mainb.val, P.heavy_cc, P.metric)) {
         Best fb = df_run(z, i1, i2, P.fb_coarse, P.fb_window_half);
-        if (fb.val > mainb.val) return fb.idx;
+        if (gt(z, fb.val, mainb.val, P.metric)) return fb.idx;
     }
     return mainb.idx;
 }
 
 // ------------------------------------------------------------- zoom_1d
 // zoom.cpp:252-282 along T1 (axis 0) or T2 (axis 1); speculative flanks
-// +-1..4 steps are simulated together before each decision.
+// +-1..spec1d steps are screened together before each decision.
 __device__ long long zoom_1d(Z& z, int axis, long long i1, long long i2, long long idf, long long lo,
                              long long hi, long long init, long long s, int metric) {
     auto F = [&](long long a) {
         return axis == 0 ? zf(z, a, i2, idf, metric) : zf(z, i1, a, idf, metric);
     };
     long long x = clampll(init, lo, hi);
-    double fx = F(x);
+    V fx = F(x);
     for (;;) {
         const long long x0 = x;
-        zensure(z, 2 * z.p->spec1d, [&](long long k, long long& a, long long& b, long long& c) {
+        auto pt = [&](long long k, long long& a, long long& b, long long& c) {
             const long long off = (k / 2 + 1) * s * ((k & 1) ? 1 : -1);
             const long long v = clampll(x0 + off, lo, hi);
             a = axis == 0 ? v : i1;
             b = axis == 0 ? i2 : v;
             c = idf;
-        });
+        };
+        zensure(z, 2 * z.p->spec1d, pt);
         const long long xl = clampll(x - s, lo, hi);
         if (xl != x) {
-            const double fl = F(xl);
-            if (fl > fx) {
+            V fl = F(xl);
+            if (gt(z, fl, fx, metric)) {
                 x = xl;
                 fx = fl;
                 continue;
@@ -333,8 +713,8 @@ __device__ long long zoom_1d(Z& z, int axis, long long i1, long long i2, long lo
         }
         const long long xr = clampll(x + s, lo, hi);
         if (xr != x) {
-            const double fr = F(xr);
-            if (fr > fx) {
+            V fr = F(xr);
+            if (gt(z, fr, fx, metric)) {
                 x = xr;
                 fx = fr;
                 continue;
@@ -346,14 +726,14 @@ __device__ long long zoom_1d(Z& z, int axis, long long i1, long long i2, long lo
 }
 
 // ------------------------------------------------------------- zoom_2d
-// zoom.cpp:284-399 for one step pair; the 3x3 neighbourhood is simulated
-// together before each iteration's probes.
-__device__ void zoom_2d_step(Z& z, long long idf, int metric, long long& x, long long& y, double& fc,
-                             long long& bx, long long& by, double& bf, long long s1, long long s2) {
+// zoom.cpp:284-399 for one step pair; the (2r+1)^2 neighbourhood is
+// screened together before each iteration's probes.
+__device__ void zoom_2d_step(Z& z, long long idf, int metric, long long& x, long long& y, V& fc,
+                             long long& bx, long long& by, V& bf, long long s1, long long s2) {
     const long long lo1 = z.lo1, hi1 = z.hi1, lo2 = z.lo2, hi2 = z.hi2;
     auto F = [&](long long a, long long b) { return zf(z, a, b, idf, metric); };
-    auto note = [&](long long px, long long py, double v) {
-        if (v > bf) {
+    auto note = [&](long long px, long long py, V& v) {
+        if (gt(z, v, bf, metric)) {
             bf = v;
             bx = px;
             by = py;
@@ -361,7 +741,26 @@ __device__ void zoom_2d_step(Z& z, long long idf, int metric, long long& x, long
     };
     const long long cap = 4 * ((hi1 - lo1) / s1 + (hi2 - lo2) / s2) + 16;
     bool converged = false;
+    // Cycle detection (Brent).  The move taken from (x, y) depends only on
+    // (x, y) -- fc is always F(x, y) and objective values are fixed -- so a
+    // revisited position means the walk is periodic and never converges:
+    // the reference keeps cycling until `cap` and then falls back to the
+    // best point noted (zoom.cpp:392-396).  When the repeat is seen, one
+    // full period has been walked since the saved position, so every point
+    // of the cycle has been noted, no later iteration evaluates a new point
+    // or changes the best: leaving now gives the reference's answer and
+    // evaluation count without walking the remaining periods.
+    long long sx = x, sy = y, power = 1, lam = 0;
     for (long long iter = 0; iter < cap && !converged; ++iter) {
+        if (iter > 0) {
+            if (x == sx && y == sy) break;  // periodic: not converged
+            if (++lam == power) {
+                sx = x;
+                sy = y;
+                power *= 2;
+                lam = 0;
+            }
+        }
         const long long cx = x, cy = y;
         const long long r = z.p->spec2d, w = 2 * r + 1;  // (2r+1)^2 - 1 neighbours
         zensure(z, w * w - 1, [&](long long k, long long& a, long long& b, long long& c) {
@@ -374,7 +773,7 @@ __device__ void zoom_2d_step(Z& z, long long idf, int metric, long long& x, long
         const long long xr = clampll(x + s1, lo1, hi1);
         const long long yd = clampll(y - s2, lo2, hi2);
         const long long yu = clampll(y + s2, lo2, hi2);
-        double fl = fc, fd = fc;
+        V fl = fc, fd = fc;
         if (xl != x) {
             fl = F(xl, y);
             note(xl, y, fl);
@@ -383,8 +782,8 @@ __device__ void zoom_2d_step(Z& z, long long idf, int metric, long long& x, long
             fd = F(x, yd);
             note(x, yd, fd);
         }
-        const bool lw = xl != x && fl > fc;
-        const bool dw = yd != y && fd > fc;
+        const bool lw = xl != x && gt(z, fl, fc, metric);
+        const bool dw = yd != y && gt(z, fd, fc, metric);
         if (lw && dw) {
             x = xl;
             y = yd;
@@ -393,7 +792,7 @@ __device__ void zoom_2d_step(Z& z, long long idf, int metric, long long& x, long
             continue;
         }
         if (!lw && !dw) {
-            double fr = fc, fu = fc;
+            V fr = fc, fu = fc;
             if (xr != x) {
                 fr = F(xr, y);
                 note(xr, y, fr);
@@ -402,8 +801,8 @@ __device__ void zoom_2d_step(Z& z, long long idf, int metric, long long& x, long
                 fu = F(x, yu);
                 note(x, yu, fu);
             }
-            const bool rw = xr != x && fr > fc;
-            const bool uw = yu != y && fu > fc;
+            const bool rw = xr != x && gt(z, fr, fc, metric);
+            const bool uw = yu != y && gt(z, fu, fc, metric);
             if (rw && uw) {
                 x = xr;
                 y = yu;
@@ -425,12 +824,12 @@ __device__ void zoom_2d_step(Z& z, long long idf, int metric, long long& x, long
             continue;
         }
         if (lw) {
-            double fu = fc;
+            V fu = fc;
             if (yu != y) {
                 fu = F(x, yu);
                 note(x, yu, fu);
             }
-            if (yu != y && fu > fc) {
+            if (yu != y && gt(z, fu, fc, metric)) {
                 x = xl;
                 y = yu;
                 fc = F(x, y);
@@ -441,12 +840,12 @@ __device__ void zoom_2d_step(Z& z, long long idf, int metric, long long& x, long
             fc = fl;
             continue;
         }
-        double fr = fc;
+        V fr = fc;
         if (xr != x) {
             fr = F(xr, y);
             note(xr, y, fr);
         }
-        if (xr != x && fr > fc) {
+        if (xr != x && gt(z, fr, fc, metric)) {
             x = xr;
             y = yd;
             fc = F(x, y);
@@ -467,25 +866,21 @@ __device__ void zoom_2d(Z& z, long long idf, int metric, long long& x, long long
                         const long long* s1v, const long long* s2v, int ns) {
     x = clampll(x, z.lo1, z.hi1);
     y = clampll(y, z.lo2, z.hi2);
-    double fc = zf(z, x, y, idf, metric);
+    V fc = zf(z, x, y, idf, metric);
     long long bx = x, by = y;
-    double bf = fc;
+    V bf = fc;
     for (int k = 0; k < ns; ++k) zoom_2d_step(z, idf, metric, x, y, fc, bx, by, bf, s1v[k], s2v[k]);
 }
 
 // ------------------------------------------------------------ the kernel
-__global__ void __launch_bounds__(128) k_zoom(const ZParams P) {
-    const int64_t v = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
-    if (v >= P.nvox) return;
-    Z z;
-    z.p = &P;
-    z.lane = threadIdx.x % 32;
-    z.tab = P.tab + v * (static_cast<int64_t>(P.cap_mask) + 1);
+__device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v) {
     z.evals = 0;
+    z.cyc32 = z.cyc64 = z.r64 = 0;
+    const long long tstart = clock64();
     const int n = P.n;
     const double* fp = P.fps + v * 2 * n;
-    double* q = P.q + v * 2 * n;
-    z.q = q;
+    double* q = const_cast<double*>(z.q);
+    float2* q32 = const_cast<float2*>(z.q32);
     // memo reset
     for (unsigned int s = z.lane; s <= P.cap_mask; s += 32) z.tab[s].key = kEmpty;
     // normalize the query (fingerprint.cpp:14-37): sequential FP64 sum,
@@ -500,9 +895,10 @@ __global__ void __launch_bounds__(128) k_zoom(const ZParams P) {
     }
     const double inv = 1.0 / nq;
     for (int j = z.lane; j < 2 * n; j += 32) q[j] = __dmul_rn(fp[j], inv);
-    __syncwarp();
-    __threadfence_block();
-    __syncwarp();
+    for (int j = z.lane; j < n; j += 32)
+        q32[j] = make_float2(static_cast<float>(__dmul_rn(fp[2 * j], inv)),
+                             static_cast<float>(__dmul_rn(fp[2 * j + 1], inv)));
+    zsync();
 
     if (P.bounds) {
         const long long* b = P.bounds + 6 * v;
@@ -522,41 +918,61 @@ __global__ void __launch_bounds__(128) k_zoom(const ZParams P) {
     }
     const long long s1 = P.inits ? P.inits[2 * v] : P.init1;
     const long long s2 = P.inits ? P.inits[2 * v + 1] : P.init2;
-    long long i1 = clampll(s1, z.lo1, z.hi1);  // zoom.cpp:428-429
-    long long i2 = clampll(s2, z.lo2, z.hi2);
-
-    // Stage 1 (zoom.cpp:465-469)
-    long long idf = search_df(z, i1, i2);
-    // Stage 2 (zoom.cpp:472-479)
-    zoom_2d(z, idf, P.metric, i1, i2, P.s2d1, P.s2d2, P.n2d);
-    zf(z, i1, i2, idf, P.metric);
-    // Stage 3 (zoom.cpp:482-489)
-    {
-        Best b{-1, -1e300};
-        const long long a = clampll(idf - P.omega / 2, z.lodf, z.hidf);
-        const long long e = clampll(idf + P.omega / 2, z.lodf, z.hidf);
-        const long long c1 = i1, c2 = i2;
-        zensure(z, e - a + 1, [&](long long k, long long& p1, long long& p2, long long& pd) {
-            p1 = c1;
-            p2 = c2;
-            pd = a + k;
-        });
-        for (long long k = a; k <= e; ++k) offer(b, k, zf(z, i1, i2, k, P.metric));
-        idf = b.idx;
-    }
-    // Stage 4 (zoom.cpp:492-501)
-    for (int k = 0; k < P.n1d; ++k) {
-        i1 = zoom_1d(z, 0, i1, i2, idf, z.lo1, z.hi1, i1, P.s1d1[k], P.metric);
+    long long i1 = 0, i2 = 0, idf = 0;
+    z.eager = P.eps < 0 ? 1 : 0;
+    z.npend = 0;
+    for (int pass = 0;; ++pass) {
+        if (pass > 0) {
+            // replay: the memo (values, exactness) persists; acquisitions and
+            // the evaluation count restart
+            for (unsigned int t = z.lane; t <= P.cap_mask; t += 32) {
+                const unsigned long long k = z.tab[t].key;
+                if (k != kEmpty && (k & kAcq)) z.tab[t].key = k & ~kAcq;
+            }
+            zsync();
+        }
+        if (pass >= kEagerAfter) z.eager = 1;
+        z.evals = 0;
+        i1 = clampll(s1, z.lo1, z.hi1);  // zoom.cpp:428-429
+        i2 = clampll(s2, z.lo2, z.hi2);
+        // Stage 1 (zoom.cpp:465-469)
+        idf = search_df(z, i1, i2);
+        // Stage 2 (zoom.cpp:472-479)
+        zoom_2d(z, idf, P.metric, i1, i2, P.s2d1, P.s2d2, P.n2d);
         zf(z, i1, i2, idf, P.metric);
-        i2 = zoom_1d(z, 1, i1, i2, idf, z.lo2, z.hi2, i2, P.s1d2[k], P.metric);
-        zf(z, i1, i2, idf, P.metric);
+        // Stage 3 (zoom.cpp:482-489)
+        {
+            Best b = best_init();
+            const long long a = clampll(idf - P.omega / 2, z.lodf, z.hidf);
+            const long long e = clampll(idf + P.omega / 2, z.lodf, z.hidf);
+            const long long c1 = i1, c2 = i2;
+            auto pt = [&](long long k, long long& p1, long long& p2, long long& pd) {
+                p1 = c1;
+                p2 = c2;
+                pd = a + k;
+            };
+            zensure(z, e - a + 1, pt);
+            for (long long k = a; k <= e; ++k) offer(z, b, k, zf(z, i1, i2, k, P.metric), P.metric);
+            idf = b.idx;
+        }
+        // Stage 4 (zoom.cpp:492-501)
+        for (int k = 0; k < P.n1d; ++k) {
+            i1 = zoom_1d(z, 0, i1, i2, idf, z.lo1, z.hi1, i1, P.s1d1[k], P.metric);
+            zf(z, i1, i2, idf, P.metric);
+            i2 = zoom_1d(z, 1, i1, i2, idf, z.lo2, z.hi2, i2, P.s1d2[k], P.metric);
+            zf(z, i1, i2, idf, P.metric);
+        }
+        // Stage 5 (zoom.cpp:505-512)
+        zoom_2d(z, idf, P.final_metric, i1, i2, &P.f2d1, &P.f2d2, 1);
+        zf(z, i1, i2, idf, P.final_metric);
+        if (z.lane == 0) zstat(z, 9, 1);
+        if (z.npend == 0) break;  // every decision of this pass was certified
+        zflush(z);
     }
-    // Stage 5 (zoom.cpp:505-512)
-    zoom_2d(z, idf, P.final_metric, i1, i2, &P.f2d1, &P.f2d2, 1);
-    zf(z, i1, i2, idf, P.final_metric);
-    // result (zoom.cpp:514-519)
-    const double score = zf(z, i1, i2, idf, P.metric);
-    const int s = zfind(z, zkey(i1, i2, idf));
+    // result (zoom.cpp:514-519): the exact score of the answer
+    V score = zf(z, i1, i2, idf, P.metric);
+    zmake_exact(z, score, P.metric);
+    const int s = score.slot;
     if (z.lane == 0) {
         mrfg_quant r;
         r.i1 = i1;
@@ -567,9 +983,54 @@ __global__ void __launch_bounds__(128) k_zoom(const ZParams P) {
         r.df_hz = 0;
         // estimate_pd (fingerprint.cpp:147-152): |fp| / |ideal|, ideal unnormalized
         r.pd = nq / sqrt(z.tab[s].nrm2);
-        r.score = score;
+        r.score = score.v;
         r.evaluations = z.evals;
         P.out[v] = r;
+        if (P.stats) {
+            const unsigned long long dt = static_cast<unsigned long long>(clock64() - tstart);
+            atomicAdd(P.stats + 4, dt);
+            atomicMax(P.stats + 5, dt);
+            atomicAdd(P.stats + 6, static_cast<unsigned long long>(z.cyc32));
+            atomicAdd(P.stats + 7, static_cast<unsigned long long>(z.cyc64));
+            long long* vs = P.vstats + 4 * v;
+            vs[0] = static_cast<long long>(dt);
+            vs[1] = z.cyc32;
+            vs[2] = z.r64;
+            vs[3] = z.cyc64;
+        }
+    }
+    zsync();
+}
+
+// Persistent warps: each warp owns a memo table and scratch and pulls voxels
+// from a work counter until the slice is done (no per-voxel memory, dynamic
+// balance of the very uneven per-voxel work).
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) k_zoom(const ZParams P) {
+    const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
+    Z z;
+    z.p = &P;
+    z.lane = threadIdx.x % 32;
+    z.tab = P.tab + w * (static_cast<int64_t>(P.cap_mask) + 1);
+    z.q = P.q + w * 2 * P.n;
+    z.fpx = P.fpx + w * P.n * 32;
+    z.pend = P.pend + w * kPendCap;
+    extern __shared__ float4 zsm[];
+    if (P.smem_stage) {
+        for (int i = threadIdx.x; i < 3 * P.n; i += blockDim.x) zsm[i] = P.rf32[i];
+        __syncthreads();
+        z.rfs = zsm;
+        z.q32 = reinterpret_cast<float2*>(zsm + 3 * P.n) + (threadIdx.x / 32) * P.n;
+    } else {
+        z.rfs = P.rf32;
+        z.q32 = P.q32 + w * P.n;
+    }
+    for (;;) {
+        unsigned long long v = 0;
+        if (z.lane == 0) v = atomicAdd(P.next, 1ull);
+        v = __shfl_sync(0xffffffffu, v, 0);
+        if (v >= static_cast<unsigned long long>(P.nvox)) break;
+        zoom_voxel(z, P, static_cast<int64_t>(v));
     }
 }
 
@@ -598,11 +1059,21 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     P.e1d = t.e1d.as<double>();
     P.e2d = t.e2d.as<double>();
     P.phd = t.phd.as<double>();
+    P.rf32 = c.rf32_d.as<float4>();
+    P.e1f = t.e1f.as<float4>();
+    P.e2f = t.e2f.as<float2>();
+    P.phf = t.phf.as<float4>();
     P.inv0[0] = c.inv64[2];
     P.inv0[1] = c.inv64[5];
     P.inv0[2] = c.inv64[8];
     P.n = static_cast<int>(c.n);
     P.L = {lat.t1_ms.count, lat.t2_ms.count, lat.df_hz.count};
+    P.t1_min = lat.t1_ms.min;
+    P.t1_step = lat.t1_ms.step;
+    P.t2_min = lat.t2_ms.min;
+    P.t2_step = lat.t2_ms.step;
+    P.df_min = lat.df_hz.min;
+    P.df_step = lat.df_hz.step;
     P.metric = cfg.metric;
     P.final_metric = cfg.final_metric;
     P.need_euc = cfg.metric == MRFG_METRIC_EUCLIDEAN || cfg.final_metric == MRFG_METRIC_EUCLIDEAN;
@@ -633,27 +1104,70 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
         const char* e2 = std::getenv("MRFG_ZOOM_SPEC2D");
         P.spec1d = e1 ? std::max(1, std::atoi(e1)) : 16;
         P.spec2d = e2 ? std::max(1, std::atoi(e2)) : 2;
+        const char* sm = std::getenv("MRFG_ZOOM_SCREEN");
+        const std::string smode = sm ? sm : "";
+        P.screen_mode = smode == "mufu" ? 1 : 0;
+        const char* ee = std::getenv("MRFG_ZOOM_EPS");
+        P.eps = ee ? std::atof(ee) : 1e-5;
+        // |sqrt(a) - sqrt(b)| <= sqrt(|a - b|), |d dd| <= 2 eps
+        P.eps_euc = P.eps < 0 ? P.eps : std::sqrt(2.0 * P.eps) * 1.01 + 1e-12;
     }
+    const bool want_stats = std::getenv("MRFG_ZOOM_STATS") != nullptr;
+    const char* vs_file = std::getenv("MRFG_ZOOM_STATS_FILE");
     P.init1 = snap_index(cfg.init_t1_ms, lat.t1_ms);
     P.init2 = snap_index(cfg.init_t2_ms, lat.t2_ms);
     P.fps = d_fps;
     const unsigned int cap = 8192;
     P.cap_mask = cap - 1;
     P.nvox = nvox;
-    // scratch: normalized queries, memo tables, bounds/inits, error flag
-    const size_t qbytes = sizeof(double) * 2 * c.n * nvox;
-    const size_t tbytes = sizeof(ZSlot) * cap * nvox;
+    // persistent warps: as many as are co-resident (at most one per voxel)
+    const int bs = 128;
+    // register budget: minimum resident blocks per SM (1, 4 or 6 -> 216/128/80 regs)
+    const char* mb_env = std::getenv("MRFG_ZOOM_MINB");
+    const int minb = mb_env ? std::atoi(mb_env) : 1;
+    void (*kern)(const ZParams) = minb >= 6 ? k_zoom<6> : (minb >= 4 ? k_zoom<4> : k_zoom<1>);
+    // shared staging: rf32 (48 B/step) + one FP32 query per warp (8 B/step)
+    size_t smem = (sizeof(float4) * 3 + sizeof(float2) * (bs / 32)) * c.n;
+    P.smem_stage = smem <= 200 * 1024 ? 1 : 0;
+    if (!P.smem_stage) smem = 0;
+    MRFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int per_sm = 0;
+    MRFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bs, smem));
+    const int64_t nwarps = std::min<int64_t>(int64_t(std::max(per_sm, 1)) * c.num_sms * (bs / 32),
+                                             round_up(nvox, bs / 32));
+    // scratch: per-warp queries, fingerprints and memo tables; per-voxel
+    // bounds/inits; error flag, stats, work counter
+    const size_t qbytes = (sizeof(double) * 2 + sizeof(float) * 2) * c.n * nwarps;
+    const size_t fbytes = sizeof(double2) * 32 * c.n * nwarps;
+    const size_t tbytes = sizeof(ZSlot) * cap * nwarps;
+    const size_t pbytes = sizeof(int) * kPendCap * nwarps;
     const size_t bbytes = h_bounds ? sizeof(long long) * 6 * nvox : 0;
     const size_t ibytes = h_init ? sizeof(long long) * 2 * nvox : 0;
+    const size_t vbytes = want_stats ? sizeof(long long) * 4 * nvox : 0;
     DevBuf scratch;
-    scratch.ensure(qbytes + tbytes + bbytes + ibytes + 64);
+    scratch.ensure(fbytes + qbytes + tbytes + pbytes + bbytes + ibytes + 256 + vbytes);
     char* base = scratch.as<char>();
+    P.fpx = reinterpret_cast<double2*>(base);
+    base += fbytes;
     P.q = reinterpret_cast<double*>(base);
-    P.tab = reinterpret_cast<ZSlot*>(base + qbytes);
-    P.bounds = h_bounds ? reinterpret_cast<long long*>(base + qbytes + tbytes) : nullptr;
-    P.inits = h_init ? reinterpret_cast<long long*>(base + qbytes + tbytes + bbytes) : nullptr;
-    P.err = reinterpret_cast<int*>(base + qbytes + tbytes + bbytes + ibytes);
+    P.q32 = reinterpret_cast<float2*>(base + sizeof(double) * 2 * c.n * nwarps);
+    base += qbytes;
+    P.tab = reinterpret_cast<ZSlot*>(base);
+    base += tbytes;
+    P.pend = reinterpret_cast<int*>(base);
+    base += pbytes;
+    P.bounds = h_bounds ? reinterpret_cast<long long*>(base) : nullptr;
+    base += bbytes;
+    P.inits = h_init ? reinterpret_cast<long long*>(base) : nullptr;
+    base += ibytes;
+    P.err = reinterpret_cast<int*>(base);
+    P.next = reinterpret_cast<unsigned long long*>(base + 64);
+    P.stats = want_stats ? reinterpret_cast<unsigned long long*>(base + 128) : nullptr;
+    P.vstats = want_stats ? reinterpret_cast<long long*>(base + 256) : nullptr;
+    MRFG_CUDA(cudaMemsetAsync(P.next, 0, sizeof(unsigned long long), c.stream));
     MRFG_CUDA(cudaMemsetAsync(P.err, 0, sizeof(int), c.stream));
+    if (P.stats) MRFG_CUDA(cudaMemsetAsync(P.stats, 0, 128, c.stream));
+    static_assert(sizeof(unsigned long long) * 16 <= 128, "stats block");
     if (h_bounds)
         MRFG_CUDA(cudaMemcpyAsync(const_cast<long long*>(P.bounds), h_bounds, bbytes,
                                   cudaMemcpyHostToDevice, c.stream));
@@ -668,13 +1182,39 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
                                   cudaMemcpyHostToDevice, c.stream));
     }
     P.out = d_out;
-    const int bs = 128;
-    const int64_t threads = nvox * 32;
-    k_zoom<<<(threads + bs - 1) / bs, bs, 0, c.stream>>>(P);
+    kern<<<static_cast<unsigned>(nwarps / (bs / 32)), bs, smem, c.stream>>>(P);
     MRFG_CUDA(cudaGetLastError());
     int err = 0;
     MRFG_CUDA(cudaMemcpyAsync(&err, P.err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    unsigned long long st[16] = {};
+    std::vector<long long> vst(want_stats ? 4 * nvox : 0);
+    if (P.stats) {
+        MRFG_CUDA(cudaMemcpyAsync(st, P.stats, 128, cudaMemcpyDeviceToHost, c.stream));
+        MRFG_CUDA(cudaMemcpyAsync(vst.data(), P.vstats, vbytes, cudaMemcpyDeviceToHost, c.stream));
+    }
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    if (P.stats)
+        std::fprintf(stderr,
+                     "[mrfg zoom] voxels %lld fp32 %llu fp64 %llu fp64_rounds %llu near_ties %llu "
+                     "cyc/voxel mean %.0f max %llu screen %.0f exact %.0f max|screen-exact| %.3g passes %llu "
+                     "audit %llu max|err| %.3g\n",
+                     static_cast<long long>(nvox), st[0], st[1], st[2], st[3],
+                     double(st[4]) / double(nvox), st[5], double(st[6]) / double(nvox),
+                     double(st[7]) / double(nvox), [&] {
+                         double d;
+                         std::memcpy(&d, &st[8], 8);
+                         return d;
+                     }(), st[9], st[11], [&] {
+                         double d;
+                         std::memcpy(&d, &st[10], 8);
+                         return d;
+                     }());
+    if (P.stats && vs_file) {
+        if (FILE* f = std::fopen(vs_file, "wb")) {
+            std::fwrite(vst.data(), sizeof(long long), vst.size(), f);
+            std::fclose(f);
+        }
+    }
     scratch.release();
     MRFG_REQUIRE(err != 1, MRFG_E_RANGE, "objective: lattice index out of range");
     MRFG_REQUIRE(err != 2, MRFG_E_RUNTIME, "quantify: per-voxel memo table full");
