@@ -221,67 +221,93 @@ __device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, ZSlot& s)
 struct Apx {
     float cc, re;
 };
+// One step of the FP32 screening recursion (bloch.hpp:34-38, bloch.cpp:22-26)
+// and the CC partial sums.
+__device__ __forceinline__ void zstep32(const float4 ra, const float4 rb, const float4 rc,
+                                        const float2 qq, const float4 e1, const float2 e2,
+                                        const float4 ph, float& x, float& y, float& zz, float& pr,
+                                        float& pi, float& pn) {
+    const float nx = fmaf(ra.x, x, fmaf(ra.y, y, ra.z * zz));
+    const float ny = fmaf(ra.w, x, fmaf(rb.x, y, rb.y * zz));
+    const float nz = fmaf(rb.z, x, fmaf(rb.w, y, rc.x * zz));
+    // relax/precess over te: z' = z E1 + (1 - E1)
+    x = (nx * ph.x - ny * ph.y) * e2.x;
+    y = (nx * ph.y + ny * ph.x) * e2.x;
+    zz = fmaf(nz, e1.x, e1.y);
+    pr = fmaf(qq.x, x, fmaf(qq.y, y, pr));
+    pi = fmaf(qq.y, x, fmaf(-qq.x, y, pi));
+    pn = fmaf(x, x, fmaf(y, y, pn));
+    // over the rest of TR
+    const float rx = (x * ph.z - y * ph.w) * e2.y;
+    const float ry = (x * ph.w + y * ph.z) * e2.y;
+    x = rx;
+    y = ry;
+    zz = fmaf(zz, e1.z, e1.w);
+}
+
+// Parameter-major tables: the walk streams n consecutive entries per lane
+// (rows warp-uniform where the lanes share T1, T2 or df).  The per-step
+// uniform operands (RF rotation, query) come from shared memory (SMEM) or
+// global.  Software pipeline: two register blocks of kB steps in ping-pong --
+// the table entries of block b+1 load while block b computes, and no register
+// copy consumes a load early.
+template <bool SMEM>
 __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
+    constexpr int kB = 4;
     const ZParams& P = *z.p;
     const int n = P.n;
-    // parameter-major tables: the walk streams n consecutive entries per
-    // lane (rows warp-uniform where the lanes share T1, T2 or df); the
-    // per-step uniform operands (RF rotation, query) come from shared memory
     const float4* __restrict__ e1p = P.e1f + static_cast<int64_t>(i1) * n;
     const float2* __restrict__ e2p = P.e2f + static_cast<int64_t>(i2) * n;
     const float4* __restrict__ php = P.phf + static_cast<int64_t>(idf) * n;
-    const float4* rfp = z.rfs;
-    const float2* q = z.q32;
+    extern __shared__ float4 zsm[];
+    const float4* rfp = SMEM ? zsm : z.rfs;
+    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + 3 * n) + (threadIdx.x / 32) * n : z.q32;
     float x = static_cast<float>(P.inv0[0]), y = static_cast<float>(P.inv0[1]),
           zz = static_cast<float>(P.inv0[2]);
     double re = 0.0, im = 0.0, nn = 0.0;
-    // L1 prefetch one 128-byte line (8 float4 / 16 float2 steps) two lines ahead
-    for (int j = 0; j < 16 && j < n; j += 8) {
+    for (int j = 0; j < 24 && j < n; j += 8) {
         prefetch_l1(e1p + j);
         prefetch_l1(php + j);
     }
     prefetch_l1(e2p);
-    // table entries one step ahead in registers
-    float4 e1 = __ldg(e1p), ph = __ldg(php);
-    float2 e2 = __ldg(e2p);
-    for (int jb = 0; jb < n; jb += 16) {
+    prefetch_l1(e2p + 16 < e2p + n ? e2p + 16 : e2p);
+    float4 A1[kB], AP[kB], B1[kB], BP[kB];
+    float2 A2[kB], B2[kB];
+    auto load = [&](float4* E1, float2* E2, float4* PH, int jb) {
+#pragma unroll
+        for (int m = 0; m < kB; ++m) {
+            const int j = min(jb + m, n - 1);
+            E1[m] = __ldg(e1p + j);
+            PH[m] = __ldg(php + j);
+            E2[m] = __ldg(e2p + j);
+        }
+    };
+    auto run = [&](const float4* E1, const float2* E2, const float4* PH, int jb) {
         float pr = 0.f, pi = 0.f, pn = 0.f;
-        const int je = min(n, jb + 16);
-        if (jb + 16 < n) prefetch_l1(e2p + jb + 16);
-        for (int j = jb; j < je; ++j) {
-            if ((j & 7) == 0 && j + 16 < n) {
-                prefetch_l1(e1p + j + 16);
-                prefetch_l1(php + j + 16);
-            }
-            const int jn = j + 1 < n ? j + 1 : j;
-            const float4 e1n = __ldg(e1p + jn), phn = __ldg(php + jn);
-            const float2 e2n = __ldg(e2p + jn);
-            const float4 ra = rfp[3 * j], rb = rfp[3 * j + 1], rc = rfp[3 * j + 2];
-            const float2 qq = q[j];
-            // RF rotation (bloch.hpp:34-38)
-            const float nx = fmaf(ra.x, x, fmaf(ra.y, y, ra.z * zz));
-            const float ny = fmaf(ra.w, x, fmaf(rb.x, y, rb.y * zz));
-            const float nz = fmaf(rb.z, x, fmaf(rb.w, y, rc.x * zz));
-            // relax/precess over te (bloch.cpp:22-26): z' = z E1 + (1 - E1)
-            x = (nx * ph.x - ny * ph.y) * e2.x;
-            y = (nx * ph.y + ny * ph.x) * e2.x;
-            zz = fmaf(nz, e1.x, e1.y);
-            pr = fmaf(qq.x, x, fmaf(qq.y, y, pr));
-            pi = fmaf(qq.y, x, fmaf(-qq.x, y, pi));
-            pn = fmaf(x, x, fmaf(y, y, pn));
-            // over the rest of TR
-            const float rx = (x * ph.z - y * ph.w) * e2.y;
-            const float ry = (x * ph.w + y * ph.z) * e2.y;
-            x = rx;
-            y = ry;
-            zz = fmaf(zz, e1.z, e1.w);
-            e1 = e1n;
-            e2 = e2n;
-            ph = phn;
+#pragma unroll
+        for (int m = 0; m < kB; ++m) {
+            const int j = jb + m;
+            if (j < n)
+                zstep32(rfp[3 * j], rfp[3 * j + 1], rfp[3 * j + 2], q[j], E1[m], E2[m], PH[m], x, y, zz,
+                        pr, pi, pn);
         }
         re += pr;
         im += pi;
         nn += pn;
+    };
+    load(A1, A2, AP, 0);
+    for (int jb = 0; jb < n; jb += 2 * kB) {
+        if ((jb & 15) == 0 && jb + 24 < n) {  // one L1 prefetch per 128-byte line, 3 lines ahead
+            prefetch_l1(e1p + jb + 24);
+            prefetch_l1(e1p + jb + 32 < e1p + n ? e1p + jb + 32 : e1p + n - 1);
+            prefetch_l1(php + jb + 24);
+            prefetch_l1(php + jb + 32 < php + n ? php + jb + 32 : php + n - 1);
+            prefetch_l1(e2p + jb + 32 < e2p + n ? e2p + jb + 32 : e2p + n - 1);
+        }
+        load(B1, B2, BP, jb + kB);
+        run(A1, A2, AP, jb);
+        load(A1, A2, AP, jb + 2 * kB);
+        run(B1, B2, BP, jb + kB);
     }
     const double inv = rsqrt(nn);
     Apx a;
@@ -352,7 +378,8 @@ __device__ __noinline__ Apx zsim32_mufu(const Z& z, int i1, int i2, int idf) {
 
 __device__ __forceinline__ Apx zsim32(const Z& z, int i1, int i2, int idf) {
     const int m = z.p->screen_mode;
-    return m == 1 ? zsim32_mufu(z, i1, i2, idf) : zsim32_tab(z, i1, i2, idf);
+    if (m == 1) return zsim32_mufu(z, i1, i2, idf);
+    return z.p->smem_stage ? zsim32_tab<true>(z, i1, i2, idf) : zsim32_tab<false>(z, i1, i2, idf);
 }
 
 // Make sure the points pt(0..count-1) are in the memo (screened, not
@@ -404,6 +431,10 @@ __device__ void zensure(Z& z, long long count, PT pt) {
         if (z.p->stats) {
             const unsigned int m = __ballot_sync(0xffffffffu, mine);
             if (z.lane == 0) zstat(z, z.p->eps < 0 ? 1 : 0, __popc(m));
+            if (z.lane == 0 && m) {  // rounds / lanes in batches > 32 points (12, 13) or <= 32 (14, 15)
+                zstat(z, count > 32 ? 12 : 14, 1);
+                zstat(z, count > 32 ? 13 : 15, __popc(m));
+            }
             __syncwarp();
             if (m) z.cyc32 += clock64() - t0;
         }
@@ -574,6 +605,52 @@ __device__ __forceinline__ void offer(Z& z, Best& b, long long i, V v, int metri
     }
 }
 
+// Offer the points pt(0..count-1) to bst in order: the reference's
+// per-point eval + offer (zoom.cpp:125-138, 182-187) with the memo reads done
+// 32 points at a time -- each lane looks up one point and takes its
+// acquisition (atomic, so a point is counted once), then the offers run in
+// order over the lanes' values (warp shuffles).  Decisions and counts are
+// those of the one-at-a-time loop.
+template <class PT>
+__device__ void offer_batch(Z& z, Best& bst, long long count, PT pt, int metric) {
+    const ZParams& P = *z.p;
+    for (long long base = 0; base < count; base += 32) {
+        const long long k = base + z.lane;
+        const bool valid = k < count;
+        long long a = 0, b = 0, c = 0;
+        int s = -1;
+        bool inrange = false;
+        if (valid) {
+            pt(k, a, b, c);
+            inrange = a >= 0 && b >= 0 && c >= 0 && a < P.L.n1 && b < P.L.n2 && c < P.L.ndf;
+            if (!inrange) atomicExch(P.err, 1);
+            else s = zfind(z, zkey(a, b, c));
+        }
+        if (__ballot_sync(0xffffffffu, valid && inrange && s < 0)) {  // not screened yet
+            zensure(z, count - base < 32 ? count - base : 32,
+                    [&](long long kk, long long& p1, long long& p2, long long& p3) { pt(base + kk, p1, p2, p3); });
+            if (valid && inrange) s = zfind(z, zkey(a, b, c));
+        }
+        bool newly = false;
+        V v{-1e300, -1, 1};
+        if (s >= 0) {
+            const unsigned long long old = atomicOr(&z.tab[s].key, kAcq);
+            newly = !(old & kAcq);
+            v = zread(z, s, metric);
+        }
+        z.evals += __popc(__ballot_sync(0xffffffffu, newly));
+        zsync();
+        const int nv = count - base < 32 ? static_cast<int>(count - base) : 32;
+        for (int l = 0; l < nv; ++l) {
+            V vl;
+            vl.v = __shfl_sync(0xffffffffu, v.v, l);
+            vl.slot = __shfl_sync(0xffffffffu, v.slot, l);
+            vl.exact = __shfl_sync(0xffffffffu, v.exact, l);
+            offer(z, bst, __shfl_sync(0xffffffffu, c, l), vl, metric);
+        }
+    }
+}
+
 // ------------------------------------------------------------ search_df
 // zoom.cpp:182-187 (scan: also evaluates the clamped end)
 __device__ void df_scan(Z& z, long long i1, long long i2, long long a, long long b, long long step,
@@ -589,8 +666,7 @@ __device__ void df_scan(Z& z, long long i1, long long i2, long long a, long long
     };
     const int metric = z.p->metric;
     zensure(z, cnt + (extra ? 1 : 0), pt);
-    for (long long x = a; x <= b; x += step) offer(z, bst, x, zf(z, i1, i2, x, metric), metric);
-    if (extra) offer(z, bst, b, zf(z, i1, i2, b, metric), metric);
+    offer_batch(z, bst, cnt + (extra ? 1 : 0), pt, metric);
 }
 
 // zoom.cpp:199-204: the last three marks span less than eps.  The screening
@@ -650,14 +726,7 @@ __device__ Best df_run(Z& z, long long i1, long long i2, long long coarse, long 
             pd = k < nf ? c0 + (k + 1) * P.omega : c0 - (k - nf + 1) * P.omega;
         };
         zensure(z, nf + nb, hop);
-        for (long long k = 1; cur.idx + k * P.omega <= z.hidf; ++k) {
-            const long long q = cur.idx + k * P.omega;
-            offer(z, t, q, zf(z, i1, i2, q, P.metric), P.metric);
-        }
-        for (long long k = 1; cur.idx - k * P.omega >= z.lodf; ++k) {
-            const long long q = cur.idx - k * P.omega;
-            offer(z, t, q, zf(z, i1, i2, q, P.metric), P.metric);
-        }
+        offer_batch(z, t, nf + nb, hop, P.metric);  // forward hops, then backward (zoom.cpp:213-220)
         if (t.idx == cur.idx) break;
         Best r = t;
         df_scan(z, i1, i2, t.idx - wh, t.idx + wh, P.df_refine, r);
@@ -952,7 +1021,7 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v) {
                 pd = a + k;
             };
             zensure(z, e - a + 1, pt);
-            for (long long k = a; k <= e; ++k) offer(z, b, k, zf(z, i1, i2, k, P.metric), P.metric);
+            offer_batch(z, b, e - a + 1, pt, P.metric);
             idf = b.idx;
         }
         // Stage 4 (zoom.cpp:492-501)
@@ -1128,7 +1197,8 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     void (*kern)(const ZParams) = minb >= 6 ? k_zoom<6> : (minb >= 4 ? k_zoom<4> : k_zoom<1>);
     // shared staging: rf32 (48 B/step) + one FP32 query per warp (8 B/step)
     size_t smem = (sizeof(float4) * 3 + sizeof(float2) * (bs / 32)) * c.n;
-    P.smem_stage = smem <= 200 * 1024 ? 1 : 0;
+    const char* st_env = std::getenv("MRFG_ZOOM_SMEM");
+    P.smem_stage = smem <= 200 * 1024 && !(st_env && std::atoi(st_env) == 0) ? 1 : 0;
     if (!P.smem_stage) smem = 0;
     MRFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
@@ -1197,7 +1267,7 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
         std::fprintf(stderr,
                      "[mrfg zoom] voxels %lld fp32 %llu fp64 %llu fp64_rounds %llu near_ties %llu "
                      "cyc/voxel mean %.0f max %llu screen %.0f exact %.0f max|screen-exact| %.3g passes %llu "
-                     "audit %llu max|err| %.3g\n",
+                     "audit %llu max|err| %.3g rounds(big) %llu lanes %.1f rounds(small) %llu lanes %.1f\n",
                      static_cast<long long>(nvox), st[0], st[1], st[2], st[3],
                      double(st[4]) / double(nvox), st[5], double(st[6]) / double(nvox),
                      double(st[7]) / double(nvox), [&] {
@@ -1208,7 +1278,8 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
                          double d;
                          std::memcpy(&d, &st[10], 8);
                          return d;
-                     }());
+                     }(), st[12], double(st[13]) / double(st[12] ? st[12] : 1), st[14],
+                     double(st[15]) / double(st[14] ? st[14] : 1));
     if (P.stats && vs_file) {
         if (FILE* f = std::fopen(vs_file, "wb")) {
             std::fwrite(vst.data(), sizeof(long long), vst.size(), f);
