@@ -465,7 +465,7 @@ int mrfg_destroy(mrfg_ctx* h) {
         Ctx& c = h->c;
         cudaSetDevice(c.device);
         cudaStreamSynchronize(c.stream);
-        for (DevBuf* b : {&c.rf64_d, &c.rf32_d, &c.tab.e1f, &c.tab.e2f, &c.tab.phf, &c.tab.e1d,
+        for (DevBuf* b : {&c.zoom, &c.rf64_d, &c.rf32_d, &c.tab.e1f, &c.tab.e2f, &c.tab.phf, &c.tab.e1d,
                           &c.tab.e2d, &c.tab.phd, &c.q64, &c.qprime, &c.best, &c.cand,
                           &c.cand_count, &c.atoms_a, &c.inv2, &c.seed_a, &c.seed_inv2, &c.rerank,
                           &c.params, &c.out64, &c.misc})

@@ -91,6 +91,7 @@ struct Ctx {
     DevBuf rf64_d, rf32_d;          // n x 9 doubles; n x 12 floats (9 RF, te, rest, pad)
     GridTables tab;                 // cache for the last grid
     // scratch
+    DevBuf zoom;  // K5 per-warp scratch (grow-only: no allocation inside a timed call)
     DevBuf q64, qprime, best, cand, cand_count, atoms_a, inv2, seed_a, seed_inv2, rerank,
         params, out64, misc;
     // producer stream + events for the K1/K2 overlap (created on first use)

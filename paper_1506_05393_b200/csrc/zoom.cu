@@ -53,7 +53,7 @@ struct ZSlot {
 struct ZParams {
     // tables
     const double *rf, *e1d, *e2d, *phd;
-    const float4 *rf32, *e1f, *phf;
+    const float4 *su, *e1f, *phf;  // su: StepU rows (RF rotation, te, rest, one-df-step phasor)
     const float2* e2f;
     double inv0[3];
     int n;
@@ -80,7 +80,7 @@ struct ZParams {
     int* pend;          // nwarps x kPendCap deferred exact evaluations
     ZSlot* tab;         // nwarps x cap memo tables
     unsigned long long* next;  // voxel work counter
-    int smem_stage;            // rf32 + per-warp q32 staged in dynamic shared memory
+    int smem_stage;            // StepU rows + per-warp q32 staged in dynamic shared memory
     // screening transcendentals: 0 float host-libm tables (default; audited
     // max |error| 2.9e-7); 1 MUFU ex2 + sin/cos (experimental, MRFG_ZOOM_SCREEN=mufu:
     // audited 4.5e-6, too close to eps to certify)
@@ -103,7 +103,7 @@ struct Z {
     ZSlot* tab;
     const double* q;
     const float2* q32;  // shared memory when staged
-    const float4* rfs;  // FP32 RF rotations (3 float4 per step), shared memory when staged
+    const float4* rfs;  // StepU rows (4 float4 per step), shared memory when staged
     double2* fpx;       // exact-evaluation scratch: n x 32 lanes
     int* pend;          // deferred exact evaluations (memo slots), kPendCap
     int npend;          // warp-uniform
@@ -261,7 +261,7 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
     const float4* __restrict__ php = P.phf + static_cast<int64_t>(idf) * n;
     extern __shared__ float4 zsm[];
     const float4* rfp = SMEM ? zsm : z.rfs;
-    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + 3 * n) + (threadIdx.x / 32) * n : z.q32;
+    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + 4 * n) + (threadIdx.x / 32) * n : z.q32;
     float x = static_cast<float>(P.inv0[0]), y = static_cast<float>(P.inv0[1]),
           zz = static_cast<float>(P.inv0[2]);
     double re = 0.0, im = 0.0, nn = 0.0;
@@ -288,7 +288,7 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
         for (int m = 0; m < kB; ++m) {
             const int j = jb + m;
             if (j < n)
-                zstep32(rfp[3 * j], rfp[3 * j + 1], rfp[3 * j + 2], q[j], E1[m], E2[m], PH[m], x, y, zz,
+                zstep32(rfp[4 * j], rfp[4 * j + 1], rfp[4 * j + 2], q[j], E1[m], E2[m], PH[m], x, y, zz,
                         pr, pi, pn);
         }
         re += pr;
@@ -316,10 +316,97 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
     return a;
 }
 
+// Two adjacent off-resonance points (idf, idf + 1) of one (T1, T2) in one
+// lane: the second phasor is the first times the one-df-step phasor w of the
+// StepU row (complex multiply), so the pair costs one table stream and the
+// uniform operands are read once.  Same arithmetic otherwise as zsim32_tab.
+struct Apx2 {
+    Apx a, b;
+};
+template <bool SMEM>
+__device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
+    constexpr int kB = 2;
+    const ZParams& P = *z.p;
+    const int n = P.n;
+    const float4* __restrict__ e1p = P.e1f + static_cast<int64_t>(i1) * n;
+    const float2* __restrict__ e2p = P.e2f + static_cast<int64_t>(i2) * n;
+    const float4* __restrict__ php = P.phf + static_cast<int64_t>(idf) * n;
+    extern __shared__ float4 zsm[];
+    const float4* rfp = SMEM ? zsm : z.rfs;
+    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + 4 * n) + (threadIdx.x / 32) * n : z.q32;
+    const float x0 = static_cast<float>(P.inv0[0]), y0 = static_cast<float>(P.inv0[1]),
+                z0 = static_cast<float>(P.inv0[2]);
+    float xa = x0, ya = y0, za = z0, xb = x0, yb = y0, zb = z0;
+    double rea = 0.0, ima = 0.0, nna = 0.0, reb = 0.0, imb = 0.0, nnb = 0.0;
+    for (int j = 0; j < 24 && j < n; j += 8) {
+        prefetch_l1(e1p + j);
+        prefetch_l1(php + j);
+    }
+    prefetch_l1(e2p);
+    prefetch_l1(e2p + 16 < e2p + n ? e2p + 16 : e2p);
+    float4 A1[kB], AP[kB], B1[kB], BP[kB];
+    float2 A2[kB], B2[kB];
+    auto load = [&](float4* E1, float2* E2, float4* PH, int jb) {
+#pragma unroll
+        for (int m = 0; m < kB; ++m) {
+            const int j = min(jb + m, n - 1);
+            E1[m] = __ldg(e1p + j);
+            PH[m] = __ldg(php + j);
+            E2[m] = __ldg(e2p + j);
+        }
+    };
+    auto run = [&](const float4* E1, const float2* E2, const float4* PH, int jb) {
+        float pra = 0.f, pia = 0.f, pna = 0.f, prb = 0.f, pib = 0.f, pnb = 0.f;
+#pragma unroll
+        for (int m = 0; m < kB; ++m) {
+            const int j = jb + m;
+            if (j < n) {
+                const float4 ra = rfp[4 * j], rb = rfp[4 * j + 1], rc = rfp[4 * j + 2], rd = rfp[4 * j + 3];
+                const float2 qq = q[j];
+                const float4 pa = PH[m];
+                // w = (wtc, wts) for te, (wrc, wrs) for rest: rc.w, rd.x, rd.y, rd.z
+                float4 pb;
+                pb.x = fmaf(pa.x, rc.w, -pa.y * rd.x);
+                pb.y = fmaf(pa.y, rc.w, pa.x * rd.x);
+                pb.z = fmaf(pa.z, rd.y, -pa.w * rd.z);
+                pb.w = fmaf(pa.w, rd.y, pa.z * rd.z);
+                zstep32(ra, rb, rc, qq, E1[m], E2[m], pa, xa, ya, za, pra, pia, pna);
+                zstep32(ra, rb, rc, qq, E1[m], E2[m], pb, xb, yb, zb, prb, pib, pnb);
+            }
+        }
+        rea += pra;
+        ima += pia;
+        nna += pna;
+        reb += prb;
+        imb += pib;
+        nnb += pnb;
+    };
+    load(A1, A2, AP, 0);
+    for (int jb = 0; jb < n; jb += 2 * kB) {
+        if ((jb & 7) == 0 && jb + 24 < n) {  // one L1 prefetch per 128-byte line, 3 lines ahead
+            prefetch_l1(e1p + jb + 24);
+            prefetch_l1(php + jb + 24);
+            if ((jb & 15) == 0) prefetch_l1(e2p + jb + 32 < e2p + n ? e2p + jb + 32 : e2p + n - 1);
+        }
+        load(B1, B2, BP, jb + kB);
+        run(A1, A2, AP, jb);
+        load(A1, A2, AP, jb + 2 * kB);
+        run(B1, B2, BP, jb + kB);
+    }
+    Apx2 r;
+    double inv = rsqrt(nna);
+    r.a.cc = static_cast<float>(fmin(sqrt(rea * rea + ima * ima) * inv, 1.0));
+    r.a.re = static_cast<float>(rea * inv);
+    inv = rsqrt(nnb);
+    r.b.cc = static_cast<float>(fmin(sqrt(reb * reb + imb * imb) * inv, 1.0));
+    r.b.re = static_cast<float>(reb * inv);
+    return r;
+}
+
 // The same screening evaluation with the per-step transcendentals computed
 // in registers instead of gathered (no per-lane memory streams): E = ex2(-dt
 // log2(e) / T) (MUFU.EX2), phasors from the range-reduced turn count df*dt
-// (MUFU.SIN/COS).  te/rest come from the staged RF rows (pad floats 9, 10).
+// (MUFU.SIN/COS).  te/rest come from the StepU rows.
 __device__ __noinline__ Apx zsim32_mufu(const Z& z, int i1, int i2, int idf) {
     const ZParams& P = *z.p;
     const int n = P.n;
@@ -335,7 +422,7 @@ __device__ __noinline__ Apx zsim32_mufu(const Z& z, int i1, int i2, int idf) {
         float pr = 0.f, pi = 0.f, pn = 0.f;
         const int je = min(n, jb + 16);
         for (int j = jb; j < je; ++j) {
-            const float4 ra = rfp[3 * j], rb = rfp[3 * j + 1], rc = rfp[3 * j + 2];
+            const float4 ra = rfp[4 * j], rb = rfp[4 * j + 1], rc = rfp[4 * j + 2];
             const float2 qq = q[j];
             const float te = rc.y, rest = rc.z;
             const float e1t = exp2f(te * k1), e1r = exp2f(rest * k1);
@@ -434,6 +521,78 @@ __device__ void zensure(Z& z, long long count, PT pt) {
             if (z.lane == 0 && m) {  // rounds / lanes in batches > 32 points (12, 13) or <= 32 (14, 15)
                 zstat(z, count > 32 ? 12 : 14, 1);
                 zstat(z, count > 32 ? 13 : 15, __popc(m));
+            }
+            __syncwarp();
+            if (m) z.cyc32 += clock64() - t0;
+        }
+        zsync();
+    }
+}
+
+// zensure for a stride-1 off-resonance run (i1, i2, a .. a + count - 1):
+// each lane screens two adjacent points (zsim32_df2), 64 per round.
+__device__ void zensure_df(Z& z, long long i1, long long i2, long long a, long long count) {
+    const ZParams& P = *z.p;
+    if (P.eps < 0 || P.screen_mode != 0) {
+        zensure(z, count, [&](long long k, long long& p1, long long& p2, long long& p3) {
+            p1 = i1;
+            p2 = i2;
+            p3 = a + k;
+        });
+        return;
+    }
+    for (long long base = 0; base < count; base += 64) {
+        const long long k0 = base + 2 * z.lane;
+        int slot[2] = {-1, -1};
+        bool mine[2] = {false, false};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const long long c = a + k0 + h;
+            if (k0 + h < count && c >= 0 && c < P.L.ndf && i1 >= 0 && i2 >= 0 && i1 < P.L.n1 && i2 < P.L.n2) {
+                const unsigned long long key = zkey(i1, i2, c);
+                if (zfind(z, key) < 0) {
+                    slot[h] = zclaim(z, key, mine[h]);
+                    if (slot[h] < 0) atomicExch(P.err, 2);  // memo full
+                }
+            }
+        }
+        const long long t0 = P.stats ? clock64() : 0;
+        if (mine[0] || mine[1]) {
+            const Apx2 v = P.smem_stage ? zsim32_df2<true>(z, static_cast<int>(i1), static_cast<int>(i2),
+                                                           static_cast<int>(a + k0))
+                                        : zsim32_df2<false>(z, static_cast<int>(i1), static_cast<int>(i2),
+                                                            static_cast<int>(a + k0));
+            if (mine[0]) {
+                z.tab[slot[0]].acc = v.a.cc;
+                z.tab[slot[0]].are = v.a.re;
+                z.tab[slot[0]].nrm2 = -1.0;
+            }
+            if (mine[1]) {
+                z.tab[slot[1]].acc = v.b.cc;
+                z.tab[slot[1]].are = v.b.re;
+                z.tab[slot[1]].nrm2 = -1.0;
+            }
+            if (P.stats) {  // audit (stats mode only), as in zensure
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const unsigned long long key = zkey(i1, i2, a + k0 + h);
+                    if (mine[h] && (zhash(key * 0x9E3779B97F4A7C15ull) & 63) == 0) {
+                        ZSlot r;
+                        zsim(z, static_cast<int>(i1), static_cast<int>(i2), static_cast<int>(a + k0 + h), r);
+                        const double e = fabs(static_cast<double>(h ? v.b.cc : v.a.cc) - r.cc);
+                        atomicMax(P.stats + 10, static_cast<unsigned long long>(__double_as_longlong(e)));
+                        atomicAdd(P.stats + 11, 1ull);
+                    }
+                }
+            }
+        }
+        if (P.stats) {
+            const unsigned int m0 = __ballot_sync(0xffffffffu, mine[0]), m1 = __ballot_sync(0xffffffffu, mine[1]);
+            const unsigned int m = m0 | m1;
+            if (z.lane == 0 && m) {
+                zstat(z, 0, __popc(m0) + __popc(m1));
+                zstat(z, 12, 1);
+                zstat(z, 13, __popc(m0) + __popc(m1));
             }
             __syncwarp();
             if (m) z.cyc32 += clock64() - t0;
@@ -665,7 +824,10 @@ __device__ void df_scan(Z& z, long long i1, long long i2, long long a, long long
         pd = k < cnt ? a + k * step : b;
     };
     const int metric = z.p->metric;
-    zensure(z, cnt + (extra ? 1 : 0), pt);
+    if (step == 1)
+        zensure_df(z, i1, i2, a, cnt);
+    else
+        zensure(z, cnt + (extra ? 1 : 0), pt);
     offer_batch(z, bst, cnt + (extra ? 1 : 0), pt, metric);
 }
 
@@ -1020,7 +1182,7 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v) {
                 p2 = c2;
                 pd = a + k;
             };
-            zensure(z, e - a + 1, pt);
+            zensure_df(z, c1, c2, a, e - a + 1);
             offer_batch(z, b, e - a + 1, pt, P.metric);
             idf = b.idx;
         }
@@ -1086,12 +1248,12 @@ __global__ void __launch_bounds__(128, MINB) k_zoom(const ZParams P) {
     z.pend = P.pend + w * kPendCap;
     extern __shared__ float4 zsm[];
     if (P.smem_stage) {
-        for (int i = threadIdx.x; i < 3 * P.n; i += blockDim.x) zsm[i] = P.rf32[i];
+        for (int i = threadIdx.x; i < 4 * P.n; i += blockDim.x) zsm[i] = P.su[i];
         __syncthreads();
         z.rfs = zsm;
-        z.q32 = reinterpret_cast<float2*>(zsm + 3 * P.n) + (threadIdx.x / 32) * P.n;
+        z.q32 = reinterpret_cast<float2*>(zsm + 4 * P.n) + (threadIdx.x / 32) * P.n;
     } else {
-        z.rfs = P.rf32;
+        z.rfs = P.su;
         z.q32 = P.q32 + w * P.n;
     }
     for (;;) {
@@ -1128,7 +1290,7 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     P.e1d = t.e1d.as<double>();
     P.e2d = t.e2d.as<double>();
     P.phd = t.phd.as<double>();
-    P.rf32 = c.rf32_d.as<float4>();
+    P.su = t.stepu.as<float4>();
     P.e1f = t.e1f.as<float4>();
     P.e2f = t.e2f.as<float2>();
     P.phf = t.phf.as<float4>();
@@ -1195,8 +1357,8 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     const char* mb_env = std::getenv("MRFG_ZOOM_MINB");
     const int minb = mb_env ? std::atoi(mb_env) : 1;
     void (*kern)(const ZParams) = minb >= 6 ? k_zoom<6> : (minb >= 4 ? k_zoom<4> : k_zoom<1>);
-    // shared staging: rf32 (48 B/step) + one FP32 query per warp (8 B/step)
-    size_t smem = (sizeof(float4) * 3 + sizeof(float2) * (bs / 32)) * c.n;
+    // shared staging: StepU rows (64 B/step) + one FP32 query per warp (8 B/step)
+    size_t smem = (sizeof(StepU) + sizeof(float2) * (bs / 32)) * c.n;
     const char* st_env = std::getenv("MRFG_ZOOM_SMEM");
     P.smem_stage = smem <= 200 * 1024 && !(st_env && std::atoi(st_env) == 0) ? 1 : 0;
     if (!P.smem_stage) smem = 0;
@@ -1214,7 +1376,7 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     const size_t bbytes = h_bounds ? sizeof(long long) * 6 * nvox : 0;
     const size_t ibytes = h_init ? sizeof(long long) * 2 * nvox : 0;
     const size_t vbytes = want_stats ? sizeof(long long) * 4 * nvox : 0;
-    DevBuf scratch;
+    DevBuf& scratch = c.zoom;
     scratch.ensure(fbytes + qbytes + tbytes + pbytes + bbytes + ibytes + 256 + vbytes);
     char* base = scratch.as<char>();
     P.fpx = reinterpret_cast<double2*>(base);
@@ -1286,7 +1448,6 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
             std::fclose(f);
         }
     }
-    scratch.release();
     MRFG_REQUIRE(err != 1, MRFG_E_RANGE, "objective: lattice index out of range");
     MRFG_REQUIRE(err != 2, MRFG_E_RUNTIME, "quantify: per-voxel memo table full");
     MRFG_REQUIRE(err != 3, MRFG_E_INVALID, "normalize: zero fingerprint");

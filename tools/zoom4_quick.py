@@ -42,16 +42,20 @@ def main():
             os.environ["MRFG_ZOOM_EPS"] = eps
             c.quantify_device(d_q.data_ptr(), nq, wl.grid, cfg, d_o.data_ptr())  # warm (tables)
             torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            c.quantify_device(d_q.data_ptr(), nq, wl.grid, cfg, d_o.data_ptr())
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1)
+            reps = int(os.environ.get("ZOOM_REPS", "5"))
+            times = []
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                c.quantify_device(d_q.data_ptr(), nq, wl.grid, cfg, d_o.data_ptr())
+                e1.record(stream)
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
+            ms = float(np.median(times))
             rec = d_o.cpu().numpy().view(P.dgs.QUANT_DTYPE).copy()
             recs[eps] = rec
             np.save(os.path.join(ROOT, "gpurun_out", f"zoom4_rec_{eps}.npy"), rec)
-            out[eps] = {"ms": ms, "voxels_per_s": nq / (ms * 1e-3),
+            out[eps] = {"ms": ms, "ms_all": [round(t, 1) for t in times], "voxels_per_s": nq / (ms * 1e-3),
                         "evals_per_voxel": float(rec["evaluations"].mean())}
     if len(recs) > 1:
         b = recs[epss[-1]]
