@@ -55,10 +55,13 @@ def main():
                           "evals_per_voxel_mean": float(rec["evaluations"].mean())}
         mask = np.ones(nq, dtype=np.uint8)
         res, secs = c.quantify_slice(wl.fps, mask, 64, 64, wl.grid, cfg, use_prior=2)
+        same = (res["i1"] == rec["i1"]) & (res["i2"] == rec["i2"]) & (res["idf"] == rec["idf"])
         out["prior_wavefront"] = {"slice_s": secs, "evals_per_voxel_mean": float(res["evaluations"].mean()),
-                                  "maps_equal_noprior": bool(
-                                      (res["i1"] == rec["i1"]).all() and (res["i2"] == rec["i2"]).all()
-                                      and (res["idf"] == rec["idf"]).all())}
+                                  "maps_equal_noprior": bool(same.all()),
+                                  "voxels_equal_noprior": int(same.sum()),
+                                  "score_prior_minus_noprior_mean": float((res["score"] - rec["score"]).mean()),
+                                  "prior_score_higher": int((res["score"] > rec["score"]).sum()),
+                                  "prior_score_lower": int((res["score"] < rec["score"]).sum())}
         truth_hit = (rec["i1"] == wl.truth[:, 0]) & (rec["i2"] == wl.truth[:, 1]) & (rec["idf"] == wl.truth[:, 2])
         out["exact_truth_fraction"] = float(truth_hit.mean())
         out["df_truth_fraction"] = float((rec["idf"] == wl.truth[:, 2]).mean())
