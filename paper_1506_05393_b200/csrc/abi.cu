@@ -134,8 +134,11 @@ const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
     }
     GridTables& t = c.tab;
     t.valid = false;
+    // 1 KB of zeroed tail padding: table walkers may load a few steps past the
+    // last row's end (look-ahead of the final block; the values are unused)
     auto up = [&](DevBuf& b, const void* src, size_t bytes) {
-        b.ensure(bytes);
+        b.ensure(bytes + 1024);
+        MRFG_CUDA(cudaMemsetAsync(static_cast<char*>(b.p) + bytes, 0, 1024, c.stream));
         MRFG_CUDA(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, c.stream));
     };
     up(t.e1d, e1.data(), e1.size() * 8);

@@ -247,10 +247,12 @@ __device__ __forceinline__ void zstep32(const float4 ra, const float4 rb, const 
 
 // Parameter-major tables: the walk streams n consecutive entries per lane
 // (rows warp-uniform where the lanes share T1, T2 or df).  The per-step
-// uniform operands (RF rotation, query) come from shared memory (SMEM) or
-// global.  Software pipeline: two register blocks of kB steps in ping-pong --
-// the table entries of block b+1 load while block b computes, and no register
-// copy consumes a load early.
+// uniform operands (StepU rows, query) come from shared memory (SMEM) or
+// global.  Software pipeline: blocks of 4 steps in ping-pong register sets --
+// the table entries of block b+1 load while block b computes.  The main loop
+// runs whole 8-step pairs without guards (per-block pointers, immediate
+// offsets; the tables carry tail padding for the last look-ahead), a guarded
+// loop finishes n % 8 steps.
 template <bool SMEM>
 __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
     constexpr int kB = 4;
@@ -265,49 +267,54 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
     float x = static_cast<float>(P.inv0[0]), y = static_cast<float>(P.inv0[1]),
           zz = static_cast<float>(P.inv0[2]);
     double re = 0.0, im = 0.0, nn = 0.0;
-    for (int j = 0; j < 24 && j < n; j += 8) {
+    for (int j = 0; j < 24; j += 8) {
         prefetch_l1(e1p + j);
         prefetch_l1(php + j);
     }
     prefetch_l1(e2p);
-    prefetch_l1(e2p + 16 < e2p + n ? e2p + 16 : e2p);
+    prefetch_l1(e2p + 16);
     float4 A1[kB], AP[kB], B1[kB], BP[kB];
     float2 A2[kB], B2[kB];
-    auto load = [&](float4* E1, float2* E2, float4* PH, int jb) {
+    auto load = [&](float4* E1, float2* E2, float4* PH, const float4* p1, const float2* p2, const float4* pp) {
 #pragma unroll
         for (int m = 0; m < kB; ++m) {
-            const int j = min(jb + m, n - 1);
-            E1[m] = __ldg(e1p + j);
-            PH[m] = __ldg(php + j);
-            E2[m] = __ldg(e2p + j);
+            E1[m] = __ldg(p1 + m);
+            PH[m] = __ldg(pp + m);
+            E2[m] = __ldg(p2 + m);
         }
     };
-    auto run = [&](const float4* E1, const float2* E2, const float4* PH, int jb) {
+    auto run = [&](const float4* E1, const float2* E2, const float4* PH, const float4* r, const float2* qb) {
         float pr = 0.f, pi = 0.f, pn = 0.f;
 #pragma unroll
-        for (int m = 0; m < kB; ++m) {
-            const int j = jb + m;
-            if (j < n)
-                zstep32(rfp[4 * j], rfp[4 * j + 1], rfp[4 * j + 2], q[j], E1[m], E2[m], PH[m], x, y, zz,
-                        pr, pi, pn);
-        }
+        for (int m = 0; m < kB; ++m)
+            zstep32(r[4 * m], r[4 * m + 1], r[4 * m + 2], qb[m], E1[m], E2[m], PH[m], x, y, zz, pr, pi, pn);
         re += pr;
         im += pi;
         nn += pn;
     };
-    load(A1, A2, AP, 0);
-    for (int jb = 0; jb < n; jb += 2 * kB) {
-        if ((jb & 15) == 0 && jb + 24 < n) {  // one L1 prefetch per 128-byte line, 3 lines ahead
+    const int nmain = n & ~(2 * kB - 1);
+    load(A1, A2, AP, e1p, e2p, php);
+    for (int jb = 0; jb < nmain; jb += 2 * kB) {
+        if ((jb & 15) == 0) {  // one L1 prefetch per 128-byte line, 3 lines ahead
             prefetch_l1(e1p + jb + 24);
-            prefetch_l1(e1p + jb + 32 < e1p + n ? e1p + jb + 32 : e1p + n - 1);
+            prefetch_l1(e1p + jb + 32);
             prefetch_l1(php + jb + 24);
-            prefetch_l1(php + jb + 32 < php + n ? php + jb + 32 : php + n - 1);
-            prefetch_l1(e2p + jb + 32 < e2p + n ? e2p + jb + 32 : e2p + n - 1);
+            prefetch_l1(php + jb + 32);
+            prefetch_l1(e2p + jb + 32);
         }
-        load(B1, B2, BP, jb + kB);
-        run(A1, A2, AP, jb);
-        load(A1, A2, AP, jb + 2 * kB);
-        run(B1, B2, BP, jb + kB);
+        load(B1, B2, BP, e1p + jb + kB, e2p + jb + kB, php + jb + kB);
+        run(A1, A2, AP, rfp + 4 * jb, q + jb);
+        load(A1, A2, AP, e1p + jb + 2 * kB, e2p + jb + 2 * kB, php + jb + 2 * kB);
+        run(B1, B2, BP, rfp + 4 * (jb + kB), q + jb + kB);
+    }
+    {  // tail: n % 8 steps
+        float pr = 0.f, pi = 0.f, pn = 0.f;
+        for (int j = nmain; j < n; ++j)
+            zstep32(rfp[4 * j], rfp[4 * j + 1], rfp[4 * j + 2], q[j], __ldg(e1p + j), __ldg(e2p + j),
+                    __ldg(php + j), x, y, zz, pr, pi, pn);
+        re += pr;
+        im += pi;
+        nn += pn;
     }
     const double inv = rsqrt(nn);
     Apx a;
@@ -338,42 +345,38 @@ __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
                 z0 = static_cast<float>(P.inv0[2]);
     float xa = x0, ya = y0, za = z0, xb = x0, yb = y0, zb = z0;
     double rea = 0.0, ima = 0.0, nna = 0.0, reb = 0.0, imb = 0.0, nnb = 0.0;
-    for (int j = 0; j < 24 && j < n; j += 8) {
+    for (int j = 0; j < 24; j += 8) {
         prefetch_l1(e1p + j);
         prefetch_l1(php + j);
     }
     prefetch_l1(e2p);
-    prefetch_l1(e2p + 16 < e2p + n ? e2p + 16 : e2p);
+    prefetch_l1(e2p + 16);
     float4 A1[kB], AP[kB], B1[kB], BP[kB];
     float2 A2[kB], B2[kB];
-    auto load = [&](float4* E1, float2* E2, float4* PH, int jb) {
+    auto load = [&](float4* E1, float2* E2, float4* PH, const float4* p1, const float2* p2, const float4* pp) {
 #pragma unroll
         for (int m = 0; m < kB; ++m) {
-            const int j = min(jb + m, n - 1);
-            E1[m] = __ldg(e1p + j);
-            PH[m] = __ldg(php + j);
-            E2[m] = __ldg(e2p + j);
+            E1[m] = __ldg(p1 + m);
+            PH[m] = __ldg(pp + m);
+            E2[m] = __ldg(p2 + m);
         }
     };
-    auto run = [&](const float4* E1, const float2* E2, const float4* PH, int jb) {
+    // one step of both points; w = (wtc, wts) for te, (wrc, wrs) for rest: rc.w, rd.x, rd.y, rd.z
+    auto step2 = [&](const float4* r, const float2 qq, const float4 e1, const float2 e2, const float4 pa, float& pra,
+                     float& pia, float& pna, float& prb, float& pib, float& pnb) {
+        const float4 ra = r[0], rb = r[1], rc = r[2], rd = r[3];
+        float4 pb;
+        pb.x = fmaf(pa.x, rc.w, -pa.y * rd.x);
+        pb.y = fmaf(pa.y, rc.w, pa.x * rd.x);
+        pb.z = fmaf(pa.z, rd.y, -pa.w * rd.z);
+        pb.w = fmaf(pa.w, rd.y, pa.z * rd.z);
+        zstep32(ra, rb, rc, qq, e1, e2, pa, xa, ya, za, pra, pia, pna);
+        zstep32(ra, rb, rc, qq, e1, e2, pb, xb, yb, zb, prb, pib, pnb);
+    };
+    auto run = [&](const float4* E1, const float2* E2, const float4* PH, const float4* r, const float2* qb) {
         float pra = 0.f, pia = 0.f, pna = 0.f, prb = 0.f, pib = 0.f, pnb = 0.f;
 #pragma unroll
-        for (int m = 0; m < kB; ++m) {
-            const int j = jb + m;
-            if (j < n) {
-                const float4 ra = rfp[4 * j], rb = rfp[4 * j + 1], rc = rfp[4 * j + 2], rd = rfp[4 * j + 3];
-                const float2 qq = q[j];
-                const float4 pa = PH[m];
-                // w = (wtc, wts) for te, (wrc, wrs) for rest: rc.w, rd.x, rd.y, rd.z
-                float4 pb;
-                pb.x = fmaf(pa.x, rc.w, -pa.y * rd.x);
-                pb.y = fmaf(pa.y, rc.w, pa.x * rd.x);
-                pb.z = fmaf(pa.z, rd.y, -pa.w * rd.z);
-                pb.w = fmaf(pa.w, rd.y, pa.z * rd.z);
-                zstep32(ra, rb, rc, qq, E1[m], E2[m], pa, xa, ya, za, pra, pia, pna);
-                zstep32(ra, rb, rc, qq, E1[m], E2[m], pb, xb, yb, zb, prb, pib, pnb);
-            }
-        }
+        for (int m = 0; m < kB; ++m) step2(r + 4 * m, qb[m], E1[m], E2[m], PH[m], pra, pia, pna, prb, pib, pnb);
         rea += pra;
         ima += pia;
         nna += pna;
@@ -381,17 +384,29 @@ __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
         imb += pib;
         nnb += pnb;
     };
-    load(A1, A2, AP, 0);
-    for (int jb = 0; jb < n; jb += 2 * kB) {
-        if ((jb & 7) == 0 && jb + 24 < n) {  // one L1 prefetch per 128-byte line, 3 lines ahead
+    const int nmain = n & ~(2 * kB - 1);
+    load(A1, A2, AP, e1p, e2p, php);
+    for (int jb = 0; jb < nmain; jb += 2 * kB) {
+        if ((jb & 7) == 0) {  // one L1 prefetch per 128-byte line, 3 lines ahead
             prefetch_l1(e1p + jb + 24);
             prefetch_l1(php + jb + 24);
-            if ((jb & 15) == 0) prefetch_l1(e2p + jb + 32 < e2p + n ? e2p + jb + 32 : e2p + n - 1);
+            if ((jb & 15) == 0) prefetch_l1(e2p + jb + 32);
         }
-        load(B1, B2, BP, jb + kB);
-        run(A1, A2, AP, jb);
-        load(A1, A2, AP, jb + 2 * kB);
-        run(B1, B2, BP, jb + kB);
+        load(B1, B2, BP, e1p + jb + kB, e2p + jb + kB, php + jb + kB);
+        run(A1, A2, AP, rfp + 4 * jb, q + jb);
+        load(A1, A2, AP, e1p + jb + 2 * kB, e2p + jb + 2 * kB, php + jb + 2 * kB);
+        run(B1, B2, BP, rfp + 4 * (jb + kB), q + jb + kB);
+    }
+    {  // tail: n % 4 steps
+        float pra = 0.f, pia = 0.f, pna = 0.f, prb = 0.f, pib = 0.f, pnb = 0.f;
+        for (int j = nmain; j < n; ++j)
+            step2(rfp + 4 * j, q[j], __ldg(e1p + j), __ldg(e2p + j), __ldg(php + j), pra, pia, pna, prb, pib, pnb);
+        rea += pra;
+        ima += pia;
+        nna += pna;
+        reb += prb;
+        imb += pib;
+        nnb += pnb;
     }
     Apx2 r;
     double inv = rsqrt(nna);
@@ -1236,8 +1251,8 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v) {
 // Persistent warps: each warp owns a memo table and scratch and pulls voxels
 // from a work counter until the slice is done (no per-voxel memory, dynamic
 // balance of the very uneven per-voxel work).
-template <int MINB>
-__global__ void __launch_bounds__(128, MINB) k_zoom(const ZParams P) {
+template <int BS, int MINB>
+__global__ void __launch_bounds__(BS, MINB) k_zoom(const ZParams P) {
     const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
     Z z;
     z.p = &P;
@@ -1352,11 +1367,17 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     P.cap_mask = cap - 1;
     P.nvox = nvox;
     // persistent warps: as many as are co-resident (at most one per voxel)
-    const int bs = 128;
-    // register budget: minimum resident blocks per SM (1, 4 or 6 -> 216/128/80 regs)
+    // block size: 8 warps (one StepU copy per SM, so L1 keeps room for the
+    // per-lane table streams) or 4 warps (MRFG_ZOOM_BS=128)
+    const char* bs_env = std::getenv("MRFG_ZOOM_BS");
+    const int bs = bs_env && std::atoi(bs_env) == 128 ? 128 : 256;
+    // register budget: minimum resident blocks per SM (128 threads: 1, 4 or 6;
+    // 256 threads: 1 or 2)
     const char* mb_env = std::getenv("MRFG_ZOOM_MINB");
     const int minb = mb_env ? std::atoi(mb_env) : 1;
-    void (*kern)(const ZParams) = minb >= 6 ? k_zoom<6> : (minb >= 4 ? k_zoom<4> : k_zoom<1>);
+    void (*kern)(const ZParams) =
+        bs == 256 ? (minb >= 2 ? k_zoom<256, 2> : k_zoom<256, 1>)
+                  : (minb >= 6 ? k_zoom<128, 6> : (minb >= 4 ? k_zoom<128, 4> : k_zoom<128, 1>));
     // shared staging: StepU rows (64 B/step) + one FP32 query per warp (8 B/step)
     size_t smem = (sizeof(StepU) + sizeof(float2) * (bs / 32)) * c.n;
     const char* st_env = std::getenv("MRFG_ZOOM_SMEM");
