@@ -504,6 +504,7 @@ __device__ void zensure(Z& z, long long count, PT pt) {
                 }
             }
         }
+        __syncwarp();
         const long long t0 = z.p->stats ? clock64() : 0;
         if (mine) {
             if (z.p->eps < 0) {
@@ -571,6 +572,9 @@ __device__ void zensure_df(Z& z, long long i1, long long i2, long long a, long l
                 }
             }
         }
+        // reconverge the warp before the evaluation: lanes leave the probe
+        // loops above at different iterations
+        __syncwarp();
         const long long t0 = P.stats ? clock64() : 0;
         if (mine[0] || mine[1]) {
             const Apx2 v = P.smem_stage ? zsim32_df2<true>(z, static_cast<int>(i1), static_cast<int>(i2),
@@ -1370,14 +1374,16 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     // block size: 8 warps (one StepU copy per SM, so L1 keeps room for the
     // per-lane table streams) or 4 warps (MRFG_ZOOM_BS=128)
     const char* bs_env = std::getenv("MRFG_ZOOM_BS");
-    const int bs = bs_env && std::atoi(bs_env) == 128 ? 128 : 256;
+    const int bs_req = bs_env ? std::atoi(bs_env) : 256;
+    const int bs = bs_req == 128 ? 128 : (bs_req == 512 ? 512 : 256);
     // register budget: minimum resident blocks per SM (128 threads: 1, 4 or 6;
     // 256 threads: 1 or 2)
     const char* mb_env = std::getenv("MRFG_ZOOM_MINB");
     const int minb = mb_env ? std::atoi(mb_env) : 1;
     void (*kern)(const ZParams) =
-        bs == 256 ? (minb >= 2 ? k_zoom<256, 2> : k_zoom<256, 1>)
-                  : (minb >= 6 ? k_zoom<128, 6> : (minb >= 4 ? k_zoom<128, 4> : k_zoom<128, 1>));
+        bs == 512   ? k_zoom<512, 1>
+        : bs == 256 ? (minb >= 2 ? k_zoom<256, 2> : k_zoom<256, 1>)
+                    : (minb >= 6 ? k_zoom<128, 6> : (minb >= 4 ? k_zoom<128, 4> : k_zoom<128, 1>));
     // shared staging: StepU rows (64 B/step) + one FP32 query per warp (8 B/step)
     size_t smem = (sizeof(StepU) + sizeof(float2) * (bs / 32)) * c.n;
     const char* st_env = std::getenv("MRFG_ZOOM_SMEM");
