@@ -189,10 +189,12 @@ std::pair<long, long> zoom_2d(const std::function<double(long, long)>& f, long l
 QuantResult quantify(const Fingerprint& fp, const SearchRanges& ranges, const ZoomConfig& cfg,
                      const Schedule& sched, const Dictionary* df_dict = nullptr,
                      const Dictionary* full_dict = nullptr);            // zoom.hpp:148-151
-// Batched form (GPU-native): one call, many fingerprints.
+// Batched form (GPU-native): one call, many fingerprints; same dictionary
+// options and validation as quantify.
 std::vector<QuantResult> quantify_batch(const std::vector<Fingerprint>& fps,
                                         const SearchRanges& ranges, const ZoomConfig& cfg,
-                                        const Schedule& sched);
+                                        const Schedule& sched, const Dictionary* df_dict = nullptr,
+                                        const Dictionary* full_dict = nullptr);
 Dictionary make_df_dictionary(const SearchRanges& ranges, const ZoomConfig& cfg,
                               const Schedule& sched, int workers = 1);  // zoom.hpp:157-158
 struct SliceResult {

@@ -71,9 +71,17 @@ typedef struct {
     double screen_err_max;     /* max |screen CC - exact CC| over re-ranked candidates (cc) */
 } mrfg_scan_stats;
 
-/* ZoomConfig (zoom.hpp:23-52) as a POD; the step lists hold up to 8 values. */
+/* ZoomConfig (zoom.hpp:23-52) as a POD; the step lists hold up to 8 values.
+ * dict_mode selects the reference's dictionary lookups (zoom.cpp:94-123):
+ * 0 = every entry simulated (FP64); 1 = df dictionary: entries first acquired
+ * during the off-resonance search (stage 1) are the dictionary's float
+ * entries (quantify's df_dict, built by make_df_dictionary); 2 = full
+ * dictionary: every entry is a float dictionary entry (quantify's full_dict).
+ * The dictionary itself is not needed: its entries are float(normalize(
+ * simulate)) of the lattice point (dictionary.cpp:37-53), reproduced
+ * bit-exactly; the caller validates it against the schedule and lattice. */
 typedef struct {
-    int32_t metric, final_metric, smooth_k, n2d, n1d, pad0;
+    int32_t metric, final_metric, smooth_k, n2d, n1d, dict_mode;
     double omega_hz, df_coarse_hz, df_refine_hz, df_window_hz, plateau_eps, heavy_noise_cc,
         fallback_coarse_hz, fallback_window_hz;
     double t1t2_2d_steps_ms[8];

@@ -42,7 +42,7 @@ class Sched(C.Structure):
 
 class ZoomCfg(C.Structure):
     _fields_ = [("metric", C.c_int32), ("final_metric", C.c_int32), ("smooth_k", C.c_int32),
-                ("n2d", C.c_int32), ("n1d", C.c_int32), ("pad0", C.c_int32),
+                ("n2d", C.c_int32), ("n1d", C.c_int32), ("dict_mode", C.c_int32),
                 ("omega_hz", C.c_double), ("df_coarse_hz", C.c_double),
                 ("df_refine_hz", C.c_double), ("df_window_hz", C.c_double),
                 ("plateau_eps", C.c_double), ("heavy_noise_cc", C.c_double),

@@ -481,6 +481,9 @@ typedef struct {
     int64_t cap, size;
     int64_t evals;
     int err;
+    int dict_mode; /* 0 none, 1 df dictionary during stage 1, 2 full dictionary */
+    int in_stage1;
+    double* buf3;
 } Obj;
 
 static uint64_t key_of(int64_t i1, int64_t i2, int64_t idf) {
@@ -521,13 +524,27 @@ static double obj_eval(Obj* o, int64_t i1, int64_t i2, int64_t idf, int metric) 
         int64_t n = o->n;
         sim_run(o->sim, axis_value(&o->g->t1_ms, i1) * 1e-3, axis_value(&o->g->t2_ms, i2) * 1e-3,
                 axis_value(&o->g->df_hz, idf), o->buf);
-        const double* src = o->buf;
-        if (o->smooth_k) {
-            smooth(o->buf, n, o->smooth_k, o->buf2);
-            src = o->buf2;
+        const double* e;
+        if (o->dict_mode == 2 || (o->dict_mode == 1 && o->in_stage1)) {
+            /* dictionary entry (zoom.cpp:101-110): the generated float entry
+             * float(normalize(simulate)) (dictionary.cpp:44-51), then, with
+             * smoothing, normalize(smooth(entry)) */
+            normalize(o->buf, n, o->buf3);
+            for (int64_t j = 0; j < 2 * n; ++j) o->buf3[j] = (double)(float)o->buf3[j];
+            if (o->smooth_k) {
+                smooth(o->buf3, n, o->smooth_k, o->buf2);
+                normalize(o->buf2, n, o->buf3);
+            }
+            e = o->buf3;
+        } else {
+            const double* src = o->buf;
+            if (o->smooth_k) {
+                smooth(o->buf, n, o->smooth_k, o->buf2);
+                src = o->buf2;
+            }
+            normalize(src, n, o->buf);
+            e = o->buf;
         }
-        normalize(src, n, o->buf);
-        const double* e = o->buf;
         double re = 0, im = 0, acc = 0;
         for (int64_t j = 0; j < n; ++j) {
             re += o->query[2 * j] * e[2 * j] + o->query[2 * j + 1] * e[2 * j + 1];
@@ -838,6 +855,8 @@ static int quantify_impl(const Sim* sim, const orc_grid* g, const Bounds* b,
     o.query = malloc(sizeof(double) * 2 * (size_t)n);
     o.buf = malloc(sizeof(double) * 2 * (size_t)n);
     o.buf2 = malloc(sizeof(double) * 2 * (size_t)n);
+    o.buf3 = malloc(sizeof(double) * 2 * (size_t)n);
+    o.dict_mode = cfg->dict_mode;
     o.cap = 4096;
     o.tab = calloc((size_t)o.cap, sizeof(Slot));
     int rc = 0;
@@ -866,7 +885,9 @@ static int quantify_impl(const Sim* sim, const orc_grid* g, const Bounds* b,
         prm.allow_fallback = 1;
         /* Stage 1 (zoom.cpp:465-469) */
         DfCtx dc = {&o, i1, i2, metric};
+        o.in_stage1 = 1;
         int64_t idf = search_df(&dc, b->lodf, b->hidf, &prm);
+        o.in_stage1 = 0;
         /* Stage 2 (zoom.cpp:472-479) */
         int64_t s1v[8], s2v[8];
         for (int k = 0; k < cfg->n2d; ++k) {
@@ -919,6 +940,7 @@ static int quantify_impl(const Sim* sim, const orc_grid* g, const Bounds* b,
     free(o.query);
     free(o.buf);
     free(o.buf2);
+    free(o.buf3);
     free(o.tab);
     return rc;
 }

@@ -33,7 +33,8 @@ typedef struct {
 
 /* ZoomConfig (zoom.hpp:23-52) as a POD; step lists hold up to 8 entries. */
 typedef struct {
-    int32_t metric, final_metric, smooth_k, n2d, n1d, pad0;
+    int32_t metric, final_metric, smooth_k, n2d, n1d;
+    int32_t dict_mode; /* 0 none, 1 df dictionary (stage 1), 2 full dictionary (zoom.cpp:94-123) */
     double omega_hz, df_coarse_hz, df_refine_hz, df_window_hz, plateau_eps, heavy_noise_cc,
         fallback_coarse_hz, fallback_window_hz;
     double t1t2_2d_steps_ms[8];

@@ -215,7 +215,20 @@ int orc_quantify(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg
     return guard([&] {
         mrf::SearchRanges r{to_range(lattice->t1_ms), to_range(lattice->t2_ms),
                             to_range(lattice->df_hz)};
-        mrf::QuantResult q = mrf::quantify(to_fp(fp, s->n), r, to_cfg(cfg), to_sched(s));
+        // dictionary lookup modes: the reference's own dictionaries
+        // (make_df_dictionary, zoom.cpp:541-553; generate over the lattice)
+        const mrf::Schedule sc = to_sched(s);
+        const mrf::ZoomConfig zc = to_cfg(cfg);
+        mrf::Dictionary dict;
+        const mrf::Dictionary *df = nullptr, *full = nullptr;
+        if (cfg->dict_mode == 1) {
+            dict = mrf::make_df_dictionary(r, zc, sc, 1);
+            df = &dict;
+        } else if (cfg->dict_mode == 2) {
+            dict = mrf::generate(mrf::grid_from_ranges(r.t1_ms, r.t2_ms, r.df_hz), sc, 1);
+            full = &dict;
+        }
+        mrf::QuantResult q = mrf::quantify(to_fp(fp, s->n), r, zc, sc, df, full);
         fill_quant(lattice, q.params.t1 * 1e3, q.params.t2 * 1e3, q.params.df, q.params.pd,
                    q.score, q.evaluations, out);
     });
@@ -231,8 +244,12 @@ int orc_quantify_slice(const orc_sched* s, const orc_grid* g, const orc_zoom_cfg
         for (std::size_t i = 0; i < nv; ++i)
             if (m[i]) v[i] = to_fp(fps + i * 2 * s->n, s->n);
         mrf::SearchRanges r{to_range(g->t1_ms), to_range(g->t2_ms), to_range(g->df_hz)};
-        mrf::SliceResult res =
-            mrf::quantify_slice(v, m, nx, ny, r, to_cfg(cfg), to_sched(s), use_prior != 0, threads);
+        const mrf::Schedule sc = to_sched(s);
+        const mrf::ZoomConfig zc = to_cfg(cfg);
+        mrf::Dictionary dfd;
+        if (cfg->dict_mode == 1) dfd = mrf::make_df_dictionary(r, zc, sc, 1);
+        mrf::SliceResult res = mrf::quantify_slice(v, m, nx, ny, r, zc, sc, use_prior != 0, threads,
+                                                   cfg->dict_mode == 1 ? &dfd : nullptr);
         std::memset(out, 0, sizeof(orc_quant) * nv);
         for (std::size_t i = 0; i < nv; ++i)
             if (m[i])

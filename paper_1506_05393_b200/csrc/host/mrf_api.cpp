@@ -151,9 +151,11 @@ QuantResult to_result(const ParameterGrid& lat, const mrfg_quant& q, double seco
     return r;
 }
 
-// df_dict validation of zoom.cpp:61-69 and :430-437.  A valid slab changes
-// nothing but the cost of stage 1 (its entries equal the generated ones), so
-// the GPU path simply simulates.
+// df_dict validation of zoom.cpp:61-69 and :430-437.  A valid slab's entries
+// are float(normalize(simulate)) of the lattice points at the initial T1/T2
+// (generate, dictionary.cpp:37-53), which the GPU path reproduces bit-exactly,
+// so it only switches the objective to dictionary entries for stage-1
+// acquisitions (mrfg_zoom_config.dict_mode = 1) instead of reading the slab.
 void check_df_dict(const Dictionary* d, const ParameterGrid& lat, const ZoomConfig& cfg,
                    const Schedule& sched) {
     if (!d) return;
@@ -176,6 +178,25 @@ void check_df_dict(const Dictionary* d, const ParameterGrid& lat, const ZoomConf
         throw std::invalid_argument("lattice mismatch: df dictionary T1 vs initial value");
     if (!close(d->grid.t2_ms.value(0), lat.t2_ms.value(static_cast<std::size_t>(i2))))
         throw std::invalid_argument("lattice mismatch: df dictionary T2 vs initial value");
+}
+
+// full_dict validation (zoom.cpp:50-58); entries reproduced like df_dict's
+// (mrfg_zoom_config.dict_mode = 2).
+void check_full_dict(const Dictionary* d, const ParameterGrid& lat, const Schedule& sched) {
+    if (!d) return;
+    auto close = [](double a, double b) {
+        return std::abs(a - b) <= 1e-9 * std::max({1.0, std::abs(a), std::abs(b)});
+    };
+    auto axis = [&](const AxisSpec& a, const AxisSpec& b, const char* what) {
+        if (!close(a.min, b.min) || !close(a.step, b.step) || a.count != b.count)
+            throw std::invalid_argument(std::string("lattice mismatch: ") + what);
+    };
+    if (d->digest != schedule_digest(sched))
+        throw std::invalid_argument("objective: dictionary built from another schedule");
+    axis(d->grid.t1_ms, lat.t1_ms, "t1 axis");
+    axis(d->grid.t2_ms, lat.t2_ms, "t2 axis");
+    axis(d->grid.df_hz, lat.df_hz, "df axis");
+    if (d->entry_len != sched.size()) throw std::invalid_argument("objective: dictionary entry length mismatch");
 }
 
 }  // namespace
@@ -610,8 +631,11 @@ std::pair<long, long> zoom_2d(const std::function<double(long, long)>& f, long l
 }
 
 std::vector<QuantResult> quantify_batch(const std::vector<Fingerprint>& fps, const SearchRanges& ranges,
-                                        const ZoomConfig& cfg, const Schedule& sched) {
+                                        const ZoomConfig& cfg, const Schedule& sched, const Dictionary* df_dict,
+                                        const Dictionary* full_dict) {
     const ParameterGrid lat = grid_from_ranges(ranges.t1_ms, ranges.t2_ms, ranges.df_hz);
+    check_full_dict(full_dict, lat, sched);
+    check_df_dict(df_dict, lat, cfg, sched);
     for (const auto& fp : fps)
         if (fp.size() != sched.size())
             throw std::invalid_argument("objective: query length does not match schedule");
@@ -622,7 +646,8 @@ std::vector<QuantResult> quantify_batch(const std::vector<Fingerprint>& fps, con
     std::vector<double> flat(2 * n * fps.size());
     for (std::size_t k = 0; k < fps.size(); ++k) std::memcpy(&flat[2 * n * k], interleaved(fps[k]), 16 * n);
     const mrfg_grid g = to_grid(lat);
-    const mrfg_zoom_config zc = to_cfg(cfg);
+    mrfg_zoom_config zc = to_cfg(cfg);
+    zc.dict_mode = full_dict ? 2 : (df_dict ? 1 : 0);
     std::vector<mrfg_quant> q(fps.size());
     const auto t0 = std::chrono::steady_clock::now();
     check(mrfg_quantify(c.h, &g, &zc, flat.data(), static_cast<int64_t>(fps.size()), q.data()));
@@ -633,11 +658,7 @@ std::vector<QuantResult> quantify_batch(const std::vector<Fingerprint>& fps, con
 
 QuantResult quantify(const Fingerprint& fp, const SearchRanges& ranges, const ZoomConfig& cfg,
                      const Schedule& sched, const Dictionary* df_dict, const Dictionary* full_dict) {
-    const ParameterGrid lat = grid_from_ranges(ranges.t1_ms, ranges.t2_ms, ranges.df_hz);
-    check_df_dict(df_dict, lat, cfg, sched);
-    if (full_dict)
-        throw std::invalid_argument("quantify: full-dictionary lookup mode is not provided by the B200 backend");
-    return quantify_batch({fp}, ranges, cfg, sched).at(0);
+    return quantify_batch({fp}, ranges, cfg, sched, df_dict, full_dict).at(0);
 }
 
 Dictionary make_df_dictionary(const SearchRanges& ranges, const ZoomConfig& cfg, const Schedule& sched,
@@ -669,7 +690,8 @@ SliceResult quantify_slice(const std::vector<Fingerprint>& fps, const std::vecto
             std::memcpy(&flat[2 * n * i], interleaved(fps[i]), 16 * n);
         }
     const mrfg_grid g = to_grid(lat);
-    const mrfg_zoom_config zc = to_cfg(cfg);
+    mrfg_zoom_config zc = to_cfg(cfg);
+    zc.dict_mode = df_dict ? 1 : 0;
     std::vector<mrfg_quant> q(nv);
     double secs = 0;
     check(mrfg_quantify_slice(c.h, &g, &zc, flat.data(), mask.data(), nx, ny, use_prior ? 1 : 0, q.data(), &secs));

@@ -48,7 +48,20 @@ struct ZSlot {
     unsigned long long key;
     float acc, are;
     double cc, euc, nrm2;
+    // entry types (zoom.cpp:94-123): 0 = FP64 simulation, 1 = float
+    // dictionary entry.  atype is fixed by this pass's first acquisition;
+    // (cc, euc) are exact when computed for xtype == atype (0xFF: none yet).
+    union {
+        struct {
+            unsigned int xtype;
+            unsigned short atype, queued;
+        };
+        unsigned long long meta;  // one load for the exactness test
+    };
 };
+__device__ __forceinline__ bool meta_exact(unsigned long long m) {
+    return static_cast<unsigned int>(m) == static_cast<unsigned int>((m >> 32) & 0xFFFFu);
+}
 
 struct ZParams {
     // tables
@@ -81,6 +94,7 @@ struct ZParams {
     ZSlot* tab;         // nwarps x cap memo tables
     unsigned long long* next;  // voxel work counter
     int smem_stage;            // StepU rows + per-warp q32 staged in dynamic shared memory
+    int dict_mode;             // 0 none, 1 df dictionary (stage-1 acquisitions), 2 full dictionary
     // screening transcendentals: 0 float host-libm tables (default; audited
     // max |error| 2.9e-7); 1 MUFU ex2 + sin/cos (experimental, MRFG_ZOOM_SCREEN=mufu:
     // audited 4.5e-6, too close to eps to certify)
@@ -108,6 +122,7 @@ struct Z {
     int* pend;          // deferred exact evaluations (memo slots), kPendCap
     int npend;          // warp-uniform
     int eager;          // 1: certify each close decision immediately
+    int stage1;         // inside search_df (df-dictionary acquisitions)
     int lane;
     long long evals;
     long long cyc32, cyc64;  // stats: cycles in screening / exact rounds
@@ -180,7 +195,7 @@ __device__ int zclaim(const Z& z, unsigned long long key, bool& fresh) {
 // One exact objective evaluation: the reference's Objective::acquire +
 // score_from_entry for both metrics, FP64, two passes (norm, then the
 // normalized entry against the query).
-__device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, ZSlot& s) {
+__device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, bool dict, ZSlot& s) {
     const ZParams& P = *z.p;
     const int n = P.n;
     // pass 1: the recursion, |s|^2 in the reference's order (fingerprint.cpp:14-18);
@@ -198,7 +213,11 @@ __device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, ZSlot& s)
     const double2* q = reinterpret_cast<const double2*>(z.q);
     for (int j = 0; j < n; ++j) {
         const double2 m = fx[32 * j];
-        const double er = __dmul_rn(m.x, inv), ei = __dmul_rn(m.y, inv);
+        double er = __dmul_rn(m.x, inv), ei = __dmul_rn(m.y, inv);
+        if (dict) {  // dictionary entry: float(normalized) (dictionary.cpp:44-51, zoom.cpp:106-108)
+            er = static_cast<double>(__double2float_rn(er));
+            ei = static_cast<double>(__double2float_rn(ei));
+        }
         const double2 qq = q[j];
         re = __dadd_rn(re, __dadd_rn(__dmul_rn(qq.x, er), __dmul_rn(qq.y, ei)));  // zoom.cpp:79
         im = __dadd_rn(im, __dsub_rn(__dmul_rn(qq.y, er), __dmul_rn(qq.x, ei)));  // zoom.cpp:80
@@ -509,22 +528,28 @@ __device__ void zensure(Z& z, long long count, PT pt) {
         if (mine) {
             if (z.p->eps < 0) {
                 ZSlot s;
-                zsim(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c), s);
+                zsim(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c), false, s);
                 z.tab[slot].cc = s.cc;
                 z.tab[slot].euc = s.euc;
                 z.tab[slot].nrm2 = s.nrm2;
                 z.tab[slot].acc = static_cast<float>(s.cc);
                 z.tab[slot].are = 0.f;
+                z.tab[slot].xtype = 0;
+                z.tab[slot].atype = 0;
+                z.tab[slot].queued = 0;
             } else {
                 const Apx v = zsim32(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c));
                 z.tab[slot].acc = v.cc;
                 z.tab[slot].are = v.re;
                 z.tab[slot].nrm2 = -1.0;
+                z.tab[slot].xtype = 0xFFu;
+                z.tab[slot].atype = 0;
+                z.tab[slot].queued = 0;
                 if (z.p->stats && (zhash(zkey(a, b, c) * 0x9E3779B97F4A7C15ull) & 63) == 0) {
                     // audit (stats mode only): exact value of a random 1/64 of
                     // all screened points, |error| into stats[10]
                     ZSlot r;
-                    zsim(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c), r);
+                    zsim(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c), false, r);
                     const double e = fabs(static_cast<double>(v.cc) - r.cc);
                     atomicMax(z.p->stats + 10, static_cast<unsigned long long>(__double_as_longlong(e)));
                     atomicAdd(z.p->stats + 11, 1ull);
@@ -581,15 +606,17 @@ __device__ void zensure_df(Z& z, long long i1, long long i2, long long a, long l
                                                            static_cast<int>(a + k0))
                                         : zsim32_df2<false>(z, static_cast<int>(i1), static_cast<int>(i2),
                                                             static_cast<int>(a + k0));
-            if (mine[0]) {
-                z.tab[slot[0]].acc = v.a.cc;
-                z.tab[slot[0]].are = v.a.re;
-                z.tab[slot[0]].nrm2 = -1.0;
-            }
-            if (mine[1]) {
-                z.tab[slot[1]].acc = v.b.cc;
-                z.tab[slot[1]].are = v.b.re;
-                z.tab[slot[1]].nrm2 = -1.0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (mine[h]) {
+                    ZSlot& t = z.tab[slot[h]];
+                    t.acc = h ? v.b.cc : v.a.cc;
+                    t.are = h ? v.b.re : v.a.re;
+                    t.nrm2 = -1.0;
+                    t.xtype = 0xFFu;
+                    t.atype = 0;
+                    t.queued = 0;
+                }
             }
             if (P.stats) {  // audit (stats mode only), as in zensure
 #pragma unroll
@@ -597,7 +624,7 @@ __device__ void zensure_df(Z& z, long long i1, long long i2, long long a, long l
                     const unsigned long long key = zkey(i1, i2, a + k0 + h);
                     if (mine[h] && (zhash(key * 0x9E3779B97F4A7C15ull) & 63) == 0) {
                         ZSlot r;
-                        zsim(z, static_cast<int>(i1), static_cast<int>(i2), static_cast<int>(a + k0 + h), r);
+                        zsim(z, static_cast<int>(i1), static_cast<int>(i2), static_cast<int>(a + k0 + h), false, r);
                         const double e = fabs(static_cast<double>(h ? v.b.cc : v.a.cc) - r.cc);
                         atomicMax(P.stats + 10, static_cast<unsigned long long>(__double_as_longlong(e)));
                         atomicAdd(P.stats + 11, 1ull);
@@ -627,23 +654,27 @@ __device__ void zexact(Z& z, int count, SL slot_of) {
     for (int base = 0; base < count; base += 32) {
         const int k = base + z.lane;
         const int s = k < count ? slot_of(k) : -1;
-        const bool work = s >= 0 && *reinterpret_cast<volatile double*>(&z.tab[s].nrm2) < 0.0;
+        const volatile ZSlot* vs = s >= 0 ? &z.tab[s] : nullptr;
+        const bool work = vs && !meta_exact(vs->meta);
         const unsigned int m = __ballot_sync(0xffffffffu, work);
         if (!m) continue;
         const long long t0 = z.p->stats ? clock64() : 0;
         if (work) {
             int i1, i2, idf;
             zunkey(*reinterpret_cast<volatile unsigned long long*>(&z.tab[s].key), i1, i2, idf);
+            const unsigned int ty = vs->atype;
             ZSlot r;
-            zsim(z, i1, i2, idf, r);
+            zsim(z, i1, i2, idf, ty == 1, r);
             if (z.p->stats) {
                 const double e = fabs(static_cast<double>(z.tab[s].acc) - r.cc);
                 atomicMax(z.p->stats + 8, static_cast<unsigned long long>(__double_as_longlong(e)));
             }
             z.tab[s].cc = r.cc;
             z.tab[s].euc = r.euc;
-            __threadfence_block();
             z.tab[s].nrm2 = r.nrm2;
+            z.tab[s].queued = 0;
+            __threadfence_block();
+            z.tab[s].xtype = ty;
         }
         if (z.lane == 0) {
             zstat(z, 1, __popc(m));
@@ -668,10 +699,16 @@ struct V {
 
 __device__ __forceinline__ V zread(const Z& z, int s, int metric) {
     const volatile ZSlot* vs = &z.tab[s];
-    if (vs->nrm2 >= 0.0) return {metric == MRFG_METRIC_CC ? vs->cc : vs->euc, s, 1};
+    if (meta_exact(vs->meta)) return {metric == MRFG_METRIC_CC ? vs->cc : vs->euc, s, 1};
     if (metric == MRFG_METRIC_CC) return {static_cast<double>(vs->acc), s, 0};
     const double d = 2.0 - 2.0 * static_cast<double>(vs->are);
     return {-sqrt(d > 0.0 ? d : 0.0), s, 0};
+}
+
+// Entry type of an acquisition now (zoom.cpp:101-113): dictionary entries in
+// full-dictionary mode, and in df-dictionary mode during search_df.
+__device__ __forceinline__ int zentry_type(const Z& z) {
+    return z.p->dict_mode == 2 || (z.p->dict_mode == 1 && z.stage1) ? 1 : 0;
 }
 
 // Objective::eval (zoom.cpp:125-138): range check, memo read, acquisition count.
@@ -695,9 +732,13 @@ __device__ V zf(Z& z, long long i1, long long i2, long long idf, int metric) {
     const unsigned long long kk = *reinterpret_cast<volatile unsigned long long*>(&z.tab[s].key);
     if (!(kk & kAcq)) {
         __syncwarp();
-        if (z.lane == 0) z.tab[s].key = kk | kAcq;
+        if (z.lane == 0) {
+            z.tab[s].atype = static_cast<unsigned short>(zentry_type(z));
+            z.tab[s].key = kk | kAcq;
+        }
         zsync();
         ++z.evals;
+        if (P.eps < 0) zexact(z, 1, [&](int) { return s; });  // all-FP64 mode: entry type may differ
     }
     return zread(z, s, metric);
 }
@@ -722,15 +763,15 @@ __device__ void zflush(Z& z) {
     z.npend = 0;
 }
 
-// Queue a screened-only slot for exact evaluation (nrm2 -1 -> -2 marks it
-// queued, so it is queued once).
+// Queue a slot without an exact value for exact evaluation (once).
 __device__ void zdefer(Z& z, const V& a) {
     if (a.exact || a.slot < 0) return;
-    volatile double* nr = &z.tab[a.slot].nrm2;
-    if (*nr != -1.0) return;
+    volatile ZSlot* vs = &z.tab[a.slot];
+    const unsigned long long m = vs->meta;
+    if ((m >> 48) || meta_exact(m)) return;
     __syncwarp();
     if (z.lane == 0) {
-        *nr = -2.0;
+        vs->queued = 1;
         z.pend[z.npend] = a.slot;
     }
     zsync();
@@ -810,14 +851,16 @@ __device__ void offer_batch(Z& z, Best& bst, long long count, PT pt, int metric)
             if (valid && inrange) s = zfind(z, zkey(a, b, c));
         }
         bool newly = false;
-        V v{-1e300, -1, 1};
         if (s >= 0) {
             const unsigned long long old = atomicOr(&z.tab[s].key, kAcq);
             newly = !(old & kAcq);
-            v = zread(z, s, metric);
+            if (newly) z.tab[s].atype = static_cast<unsigned short>(zentry_type(z));
         }
         z.evals += __popc(__ballot_sync(0xffffffffu, newly));
         zsync();
+        if (P.eps < 0) zexact(z, 32, [&](int) { return s; });  // all-FP64 mode: entry type may differ
+        V v{-1e300, -1, 1};
+        if (s >= 0) v = zread(z, s, metric);
         const int nv = count - base < 32 ? static_cast<int>(count - base) : 32;
         for (int l = 0; l < nv; ++l) {
             V vl;
@@ -1186,7 +1229,9 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v) {
         i1 = clampll(s1, z.lo1, z.hi1);  // zoom.cpp:428-429
         i2 = clampll(s2, z.lo2, z.hi2);
         // Stage 1 (zoom.cpp:465-469)
+        z.stage1 = 1;
         idf = search_df(z, i1, i2);
+        z.stage1 = 0;
         // Stage 2 (zoom.cpp:472-479)
         zoom_2d(z, idf, P.metric, i1, i2, P.s2d1, P.s2d2, P.n2d);
         zf(z, i1, i2, idf, P.metric);
@@ -1265,6 +1310,7 @@ __global__ void __launch_bounds__(BS, MINB) k_zoom(const ZParams P) {
     z.q = P.q + w * 2 * P.n;
     z.fpx = P.fpx + w * P.n * 32;
     z.pend = P.pend + w * kPendCap;
+    z.stage1 = 0;
     extern __shared__ float4 zsm[];
     if (P.smem_stage) {
         for (int i = threadIdx.x; i < 4 * P.n; i += blockDim.x) zsm[i] = P.su[i];
@@ -1324,6 +1370,8 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     P.t2_step = lat.t2_ms.step;
     P.df_min = lat.df_hz.min;
     P.df_step = lat.df_hz.step;
+    MRFG_REQUIRE(cfg.dict_mode >= 0 && cfg.dict_mode <= 2, MRFG_E_INVALID, "quantify: bad dictionary mode");
+    P.dict_mode = cfg.dict_mode;
     P.metric = cfg.metric;
     P.final_metric = cfg.final_metric;
     P.need_euc = cfg.metric == MRFG_METRIC_EUCLIDEAN || cfg.final_metric == MRFG_METRIC_EUCLIDEAN;

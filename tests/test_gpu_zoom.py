@@ -178,3 +178,38 @@ def test_zoom_slice_wavefront_prior(orc):
     for k in ("i1", "i2", "idf"):
         np.testing.assert_array_equal(a[k][m], b[k][m])
     assert b["evaluations"].sum() < a["evaluations"].sum()
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_zoom_dictionary_modes(orc, mode):
+    """dict_mode 1 (df dictionary, zoom.cpp:101-113 in stage 1) and 2 (full
+    dictionary): float dictionary entries, reproduced on the GPU, give the
+    oracle's answers, scores, PD and evaluation counts; the certified path and
+    the all-FP64 path agree."""
+    import os
+    s = P.baseline_schedule(300, 1)
+    g = P.grid_from_ranges((300.0, 1500.0, 20.0), (40.0, 240.0, 5.0), (-50.0, 51.0, 1.0))
+    kw = dict(df_coarse_hz=10, df_refine_hz=2, df_window_hz=10, omega_hz=82,
+              t1t2_2d_steps_ms=[200, 40], t1t2_1d_steps_ms=[100, 20], final_2d_step_ms=20)
+    cfg = P.zoom_config(dict_mode=mode, **kw)
+    rng = np.random.default_rng(3)
+    os_ = to_oracle_sched(s)
+    fps = []
+    for k in range(6):
+        fp = orc.simulate(os_, rng.uniform(0.4, 1.4), rng.uniform(0.06, 0.22), rng.uniform(-40, 40))
+        fps.append(orc.add_noise(fp, float(np.linalg.norm(fp)) / np.sqrt(300) / 20, 100 + k))
+    fps = np.stack(fps)
+    with P.Context(s) as c:
+        got = c.quantify(fps, g, cfg)
+        check_same(got, orc, s, g, cfg, fps)
+        old = os.environ.get("MRFG_ZOOM_EPS")
+        os.environ["MRFG_ZOOM_EPS"] = "-1"
+        try:
+            exact = c.quantify(fps, g, cfg)
+        finally:
+            if old is None:
+                del os.environ["MRFG_ZOOM_EPS"]
+            else:
+                os.environ["MRFG_ZOOM_EPS"] = old
+        for k in ("i1", "i2", "idf", "score", "pd", "evaluations"):
+            np.testing.assert_array_equal(got[k], exact[k])

@@ -99,6 +99,34 @@ def test_quantify_vs_reference(orc, ref):
                    (b.i1, b.i2, b.idf, b.score, b.pd, b.evaluations)
 
 
+@pytest.mark.parametrize("mode", [1, 2])
+def test_quantify_dictionary_modes_vs_reference(orc, ref, mode):
+    """zoom.cpp:94-123: df-dictionary (stage-1 acquisitions) and full-dictionary
+    lookups read float entries; the reference wrapper passes the reference's
+    own make_df_dictionary / generate dictionaries, the restatement
+    synthesizes float(normalize(simulate)).  Answers usually equal the plain
+    objective's (test_zoom.cpp:384-400); scores read from float entries differ."""
+    s = orc.baseline_schedule(300, 1)
+    g = oracle.make_grid((300.0, 20.0, 60), (40.0, 5.0, 40), (-50.0, 1.0, 101))
+    cfg = oracle.zoom_cfg(df_coarse_hz=10, df_refine_hz=2, df_window_hz=10, omega_hz=82,
+                          t1t2_2d_steps_ms=[200, 40], t1t2_1d_steps_ms=[100, 20], final_2d_step_ms=20)
+    cfg.dict_mode = mode
+    plain = oracle.zoom_cfg(df_coarse_hz=10, df_refine_hz=2, df_window_hz=10, omega_hz=82,
+                            t1t2_2d_steps_ms=[200, 40], t1t2_1d_steps_ms=[100, 20], final_2d_step_ms=20)
+    rng = np.random.default_rng(3)
+    changed = 0
+    for k in range(6):
+        fp = orc.simulate(s, rng.uniform(0.4, 1.4), rng.uniform(0.06, 0.22), rng.uniform(-40, 40))
+        fp = orc.add_noise(fp, float(np.linalg.norm(fp)) / np.sqrt(300) / 20, 100 + k)
+        a, b = orc.quantify(s, g, cfg, fp), ref.quantify(s, g, cfg, fp)
+        assert (a.i1, a.i2, a.idf, a.score, a.pd, a.evaluations) == \
+               (b.i1, b.i2, b.idf, b.score, b.pd, b.evaluations)
+        c = ref.quantify(s, g, plain, fp)
+        changed += c.score != b.score
+    if mode == 2:
+        assert changed > 0  # every score comes from a float entry
+
+
 def test_quantify_slice_prior_vs_reference(orc, ref):
     s = orc.build_schedule(60, 15)
     g = oracle.make_grid((600, 10, 40), (80, 5, 16), (-20, 2, 25))
