@@ -95,6 +95,10 @@ struct ZParams {
     unsigned long long* next;  // voxel work counter
     int smem_stage;            // StepU rows + per-warp q32 staged in dynamic shared memory
     int dict_mode;             // 0 none, 1 df dictionary (stage-1 acquisitions), 2 full dictionary
+    // smoothing (fingerprint.cpp:122-145): k = 0 (off), 3 or 5 taps, host-libm weights
+    int smooth_k;
+    double sw[5];
+    float swf[5];
     // screening transcendentals: 0 float host-libm tables (default; audited
     // max |error| 2.9e-7); 1 MUFU ex2 + sin/cos (experimental, MRFG_ZOOM_SCREEN=mufu:
     // audited 4.5e-6, too close to eps to certify)
@@ -195,6 +199,38 @@ __device__ int zclaim(const Z& z, unsigned long long key, bool& fresh) {
 // One exact objective evaluation: the reference's Objective::acquire +
 // score_from_entry for both metrics, FP64, two passes (norm, then the
 // normalized entry against the query).
+// smooth (fingerprint.cpp:122-145) in place over v[0], v[st], ..., v[(n-1) st]
+// (raw neighbours kept in a register window), the reference's tap order,
+// edge truncation and division by the summed weights; returns sum |out|^2 in
+// normalize's order (fingerprint.cpp:14-18).
+__device__ double zsmooth64(const ZParams& P, double2* v, int st, int n) {
+    const int h = P.smooth_k / 2;
+    double2 win[5];  // raw values at i-h .. i+h
+    for (int t = 0; t < 2 * h + 1; ++t) {
+        const int idx = t - h;
+        win[t] = idx >= 0 && idx < n ? v[static_cast<int64_t>(idx) * st] : make_double2(0.0, 0.0);
+    }
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) {
+        double re = 0.0, im = 0.0, ws = 0.0;
+        for (int j = -h; j <= h; ++j) {
+            const int t = i + j;
+            if (t < 0 || t >= n) continue;
+            const double w = P.sw[j + h];
+            re = __dadd_rn(re, __dmul_rn(w, win[j + h].x));
+            im = __dadd_rn(im, __dmul_rn(w, win[j + h].y));
+            ws = __dadd_rn(ws, w);
+        }
+        const double2 o = make_double2(__ddiv_rn(re, ws), __ddiv_rn(im, ws));
+        v[static_cast<int64_t>(i) * st] = o;
+        acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(o.x, o.x), __dmul_rn(o.y, o.y)));
+        for (int t = 0; t < 2 * h; ++t) win[t] = win[t + 1];
+        const int nx = i + h + 1;
+        win[2 * h] = nx < n ? v[static_cast<int64_t>(nx) * st] : make_double2(0.0, 0.0);
+    }
+    return acc;
+}
+
 __device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, bool dict, ZSlot& s) {
     const ZParams& P = *z.p;
     const int n = P.n;
@@ -206,7 +242,20 @@ __device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, bool dict
         acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
         fx[32 * j] = make_double2(x, y);
     });
-    const double inv = 1.0 / sqrt(acc);  // fingerprint.cpp:30-32
+    double inv = 1.0 / sqrt(acc);  // fingerprint.cpp:30-32
+    bool cast = dict;
+    if (P.smooth_k) {
+        // entry = normalize(smooth(e)), e the raw simulation (zoom.cpp:116-118)
+        // or the float dictionary entry (zoom.cpp:106-110)
+        if (dict)
+            for (int j = 0; j < n; ++j) {
+                const double2 m = fx[32 * j];
+                fx[32 * j] = make_double2(static_cast<double>(__double2float_rn(__dmul_rn(m.x, inv))),
+                                          static_cast<double>(__double2float_rn(__dmul_rn(m.y, inv))));
+            }
+        inv = 1.0 / sqrt(zsmooth64(P, fx, 32, n));
+        cast = false;
+    }
     // pass 2: the normalized entry against the query (zoom.cpp:74-92)
     double re = 0.0, im = 0.0, dd = 0.0;
     const bool euc = P.need_euc;
@@ -214,7 +263,7 @@ __device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, bool dict
     for (int j = 0; j < n; ++j) {
         const double2 m = fx[32 * j];
         double er = __dmul_rn(m.x, inv), ei = __dmul_rn(m.y, inv);
-        if (dict) {  // dictionary entry: float(normalized) (dictionary.cpp:44-51, zoom.cpp:106-108)
+        if (cast) {  // dictionary entry: float(normalized) (dictionary.cpp:44-51, zoom.cpp:106-108)
             er = static_cast<double>(__double2float_rn(er));
             ei = static_cast<double>(__double2float_rn(ei));
         }
@@ -497,8 +546,85 @@ __device__ __noinline__ Apx zsim32_mufu(const Z& z, int i1, int i2, int idf) {
     return a;
 }
 
+// Screening with smoothing (zoom.cpp:116-118): the FP32 recursion's raw echoes
+// pass through a register window; the smoothed sample i - h (taps i-2h .. i,
+// edge-truncated like fingerprint.cpp:133-143) is scored at step i, the last h
+// samples after the walk.  Plain loop: smoothing is an analysis option.
+__device__ __noinline__ Apx zsim32_smooth(const Z& z, int i1, int i2, int idf) {
+    const ZParams& P = *z.p;
+    const int n = P.n, h = P.smooth_k / 2;
+    const float4* __restrict__ e1p = P.e1f + static_cast<int64_t>(i1) * n;
+    const float2* __restrict__ e2p = P.e2f + static_cast<int64_t>(i2) * n;
+    const float4* __restrict__ php = P.phf + static_cast<int64_t>(idf) * n;
+    const float4* rfp = z.rfs;
+    const float2* q = z.q32;
+    float x = static_cast<float>(P.inv0[0]), y = static_cast<float>(P.inv0[1]),
+          zz = static_cast<float>(P.inv0[2]);
+    float2 win[5];
+    for (int t = 0; t < 5; ++t) win[t] = make_float2(0.f, 0.f);
+    double re = 0.0, im = 0.0, nn = 0.0;
+    float pr = 0.f, pi = 0.f, pn = 0.f;
+    auto emit = [&](int i) {  // window holds raw i-h .. i+h
+        float sr = 0.f, si = 0.f, ws = 0.f;
+        for (int t = -h; t <= h; ++t) {
+            const int idx = i + t;
+            if (idx < 0 || idx >= n) continue;
+            sr = fmaf(P.swf[t + h], win[t + h].x, sr);
+            si = fmaf(P.swf[t + h], win[t + h].y, si);
+            ws += P.swf[t + h];
+        }
+        sr /= ws;
+        si /= ws;
+        const float2 qq = q[i];
+        pr = fmaf(qq.x, sr, fmaf(qq.y, si, pr));
+        pi = fmaf(qq.y, sr, fmaf(-qq.x, si, pi));
+        pn = fmaf(sr, sr, fmaf(si, si, pn));
+        if ((i & 15) == 15) {
+            re += pr;
+            im += pi;
+            nn += pn;
+            pr = pi = pn = 0.f;
+        }
+    };
+    auto push = [&](float2 v) {
+        for (int t = 0; t < 2 * h; ++t) win[t] = win[t + 1];
+        win[2 * h] = v;
+    };
+    for (int j = 0; j < n; ++j) {
+        const float4 ra = rfp[4 * j], rb = rfp[4 * j + 1], rc = rfp[4 * j + 2];
+        const float4 e1 = __ldg(e1p + j), ph = __ldg(php + j);
+        const float2 e2 = __ldg(e2p + j);
+        const float nx = fmaf(ra.x, x, fmaf(ra.y, y, ra.z * zz));
+        const float ny = fmaf(ra.w, x, fmaf(rb.x, y, rb.y * zz));
+        const float nz = fmaf(rb.z, x, fmaf(rb.w, y, rc.x * zz));
+        x = (nx * ph.x - ny * ph.y) * e2.x;
+        y = (nx * ph.y + ny * ph.x) * e2.x;
+        zz = fmaf(nz, e1.x, e1.y);
+        push(make_float2(x, y));
+        if (j >= h) emit(j - h);
+        const float rx = (x * ph.z - y * ph.w) * e2.y;
+        const float ry = (x * ph.w + y * ph.z) * e2.y;
+        x = rx;
+        y = ry;
+        zz = fmaf(zz, e1.z, e1.w);
+    }
+    for (int i = n - h > 0 ? n - h : 0; i < n; ++i) {
+        push(make_float2(0.f, 0.f));
+        emit(i);
+    }
+    re += pr;
+    im += pi;
+    nn += pn;
+    const double inv = rsqrt(nn);
+    Apx a;
+    a.cc = static_cast<float>(fmin(sqrt(re * re + im * im) * inv, 1.0));
+    a.re = static_cast<float>(re * inv);
+    return a;
+}
+
 __device__ __forceinline__ Apx zsim32(const Z& z, int i1, int i2, int idf) {
     const int m = z.p->screen_mode;
+    if (z.p->smooth_k) return zsim32_smooth(z, i1, i2, idf);
     if (m == 1) return zsim32_mufu(z, i1, i2, idf);
     return z.p->smem_stage ? zsim32_tab<true>(z, i1, i2, idf) : zsim32_tab<false>(z, i1, i2, idf);
 }
@@ -574,7 +700,7 @@ __device__ void zensure(Z& z, long long count, PT pt) {
 // each lane screens two adjacent points (zsim32_df2), 64 per round.
 __device__ void zensure_df(Z& z, long long i1, long long i2, long long a, long long count) {
     const ZParams& P = *z.p;
-    if (P.eps < 0 || P.screen_mode != 0) {
+    if (P.eps < 0 || P.screen_mode != 0 || P.smooth_k) {
         zensure(z, count, [&](long long k, long long& p1, long long& p2, long long& p3) {
             p1 = i1;
             p2 = i2;
@@ -1186,11 +1312,26 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v) {
         if (z.lane == 0) atomicExch(P.err, 3);
         return;
     }
-    const double inv = 1.0 / nq;
-    for (int j = z.lane; j < 2 * n; j += 32) q[j] = __dmul_rn(fp[j], inv);
-    for (int j = z.lane; j < n; j += 32)
-        q32[j] = make_float2(static_cast<float>(__dmul_rn(fp[2 * j], inv)),
-                             static_cast<float>(__dmul_rn(fp[2 * j + 1], inv)));
+    if (P.smooth_k) {
+        // query = normalize(smooth(fp)) (zoom.cpp:49-50); pd keeps |fp| (zoom.cpp:518)
+        for (int j = z.lane; j < 2 * n; j += 32) q[j] = fp[j];
+        zsync();
+        double accs = 0.0;
+        if (z.lane == 0) accs = zsmooth64(P, reinterpret_cast<double2*>(q), 1, n);
+        accs = __shfl_sync(0xffffffffu, accs, 0);
+        zsync();
+        const double invs = 1.0 / sqrt(accs);
+        for (int j = z.lane; j < 2 * n; j += 32) q[j] = __dmul_rn(q[j], invs);
+        zsync();
+        for (int j = z.lane; j < n; j += 32)
+            q32[j] = make_float2(static_cast<float>(q[2 * j]), static_cast<float>(q[2 * j + 1]));
+    } else {
+        const double inv = 1.0 / nq;
+        for (int j = z.lane; j < 2 * n; j += 32) q[j] = __dmul_rn(fp[j], inv);
+        for (int j = z.lane; j < n; j += 32)
+            q32[j] = make_float2(static_cast<float>(__dmul_rn(fp[2 * j], inv)),
+                                 static_cast<float>(__dmul_rn(fp[2 * j + 1], inv)));
+    }
     zsync();
 
     if (P.bounds) {
@@ -1345,8 +1486,8 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     for (const mrfg_axis* ax : {&lat.t1_ms, &lat.t2_ms, &lat.df_hz})
         MRFG_REQUIRE(ax->count > 0 && ax->count < (int64_t(1) << 21), MRFG_E_INVALID,
                      "objective: lattice axis empty or too fine");  // zoom.cpp:46-48
-    MRFG_REQUIRE(cfg.smooth_k == 0, MRFG_E_INVALID,
-                 "quantify: smooth_k is not supported by the GPU MRF-ZOOM kernel");
+    MRFG_REQUIRE(cfg.smooth_k == 0 || cfg.smooth_k == 3 || cfg.smooth_k == 5, MRFG_E_INVALID,
+                 "smooth: kernel must be 3 or 5");  // fingerprint.cpp:123
     MRFG_REQUIRE(cfg.n2d >= 0 && cfg.n2d <= 8 && cfg.n1d >= 0 && cfg.n1d <= 8, MRFG_E_INVALID,
                  "quantify: at most 8 zoom steps per stage");
     const GridTables& t = ensure_tables(c, lat, true);
@@ -1372,6 +1513,15 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     P.df_step = lat.df_hz.step;
     MRFG_REQUIRE(cfg.dict_mode >= 0 && cfg.dict_mode <= 2, MRFG_E_INVALID, "quantify: bad dictionary mode");
     P.dict_mode = cfg.dict_mode;
+    P.smooth_k = cfg.smooth_k;
+    if (cfg.smooth_k) {  // fingerprint.cpp:125-129, host libm
+        const double sigma = cfg.smooth_k == 3 ? 0.85 : 1.0;
+        const int h = cfg.smooth_k / 2;
+        for (int j = -h; j <= h; ++j) {
+            P.sw[j + h] = std::exp(-0.5 * j * j / (sigma * sigma));
+            P.swf[j + h] = static_cast<float>(P.sw[j + h]);
+        }
+    }
     P.metric = cfg.metric;
     P.final_metric = cfg.final_metric;
     P.need_euc = cfg.metric == MRFG_METRIC_EUCLIDEAN || cfg.final_metric == MRFG_METRIC_EUCLIDEAN;

@@ -136,7 +136,7 @@ def test_zoom_errors():
         with pytest.raises(ValueError):
             c.quantify(np.zeros((1, 32), dtype=np.complex128), g)
         with pytest.raises(ValueError):
-            c.quantify(np.ones((1, 32), dtype=np.complex128), g, P.zoom_config(smooth_k=3))
+            c.quantify(np.ones((1, 32), dtype=np.complex128), g, P.zoom_config(smooth_k=4))  # fingerprint.cpp:123
 
 
 def _slice_problem(orc):
@@ -213,3 +213,24 @@ def test_zoom_dictionary_modes(orc, mode):
                 os.environ["MRFG_ZOOM_EPS"] = old
         for k in ("i1", "i2", "idf", "score", "pd", "evaluations"):
             np.testing.assert_array_equal(got[k], exact[k])
+
+
+@pytest.mark.parametrize("k,mode", [(3, 0), (5, 0), (3, 1), (3, 2)])
+def test_zoom_smoothing(orc, k, mode):
+    """smooth_k (fingerprint.cpp:122-145; zoom.cpp:49-50, 106-118): smoothed
+    query and entries (dictionary entries float-cast before smoothing), PD from
+    the raw fingerprints; oracle answers, scores, PD and counts."""
+    s = P.baseline_schedule(300, 1)
+    g = P.grid_from_ranges((300.0, 1500.0, 20.0), (40.0, 240.0, 5.0), (-50.0, 51.0, 1.0))
+    cfg = P.zoom_config(smooth_k=k, dict_mode=mode, df_coarse_hz=10, df_refine_hz=2, df_window_hz=10,
+                        omega_hz=82, t1t2_2d_steps_ms=[200, 40], t1t2_1d_steps_ms=[100, 20],
+                        final_2d_step_ms=20)
+    rng = np.random.default_rng(5)
+    os_ = to_oracle_sched(s)
+    fps = []
+    for j in range(5):
+        fp = orc.simulate(os_, rng.uniform(0.4, 1.4), rng.uniform(0.06, 0.22), rng.uniform(-40, 40))
+        fps.append(orc.add_noise(fp, float(np.linalg.norm(fp)) / np.sqrt(300) / 15, 300 + j))
+    fps = np.stack(fps)
+    with P.Context(s) as c:
+        check_same(c.quantify(fps, g, cfg), orc, s, g, cfg, fps)

@@ -127,6 +127,23 @@ def test_quantify_dictionary_modes_vs_reference(orc, ref, mode):
         assert changed > 0  # every score comes from a float entry
 
 
+@pytest.mark.parametrize("k,mode", [(3, 0), (5, 0), (3, 1), (3, 2)])
+def test_quantify_smoothing_vs_reference(orc, ref, k, mode):
+    """smooth_k with and without dictionary entries (zoom.cpp:49-50, 106-118)."""
+    s = orc.baseline_schedule(300, 1)
+    g = oracle.make_grid((300.0, 20.0, 60), (40.0, 5.0, 40), (-50.0, 1.0, 101))
+    cfg = oracle.zoom_cfg(smooth_k=k, df_coarse_hz=10, df_refine_hz=2, df_window_hz=10, omega_hz=82,
+                          t1t2_2d_steps_ms=[200, 40], t1t2_1d_steps_ms=[100, 20], final_2d_step_ms=20)
+    cfg.dict_mode = mode
+    rng = np.random.default_rng(5)
+    for j in range(3):
+        fp = orc.simulate(s, rng.uniform(0.4, 1.4), rng.uniform(0.06, 0.22), rng.uniform(-40, 40))
+        fp = orc.add_noise(fp, float(np.linalg.norm(fp)) / np.sqrt(300) / 15, 300 + j)
+        a, b = orc.quantify(s, g, cfg, fp), ref.quantify(s, g, cfg, fp)
+        assert (a.i1, a.i2, a.idf, a.score, a.pd, a.evaluations) == \
+               (b.i1, b.i2, b.idf, b.score, b.pd, b.evaluations)
+
+
 def test_quantify_slice_prior_vs_reference(orc, ref):
     s = orc.build_schedule(60, 15)
     g = oracle.make_grid((600, 10, 40), (80, 5, 16), (-20, 2, 25))
