@@ -212,6 +212,12 @@ class Context:
                                      _dp(out.view(np.float64))))
         return out
 
+    def simulate_device(self, d_params_ptr: int, count: int, d_out_ptr: int, precision: int = 64,
+                        normalize: bool = False) -> None:
+        """Device form of simulate: d_params (count, 3) float64 -> d_out (count, 2N) float64."""
+        check(self.lib.mrfg_simulate_dev(self.h, C.c_void_p(d_params_ptr), count, precision,
+                                         int(normalize), C.c_void_p(d_out_ptr)))
+
     def generate(self, g: Grid, first: int = 0, count: int | None = None,
                  precision: int = 64) -> np.ndarray:
         """generate (dictionary.cpp:184-194): unit-norm float32 entries, (count, 2N)."""
