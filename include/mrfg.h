@@ -60,6 +60,11 @@ typedef struct {
     int64_t chunk_atoms;   /* atoms simulated per streamed chunk (default 524288) */
     int64_t cand_capacity; /* candidate buffer entries (default 1<<25) */
     int64_t seed_atoms;    /* strided pre-pass atoms that seed the running max (default 16384) */
+    /* Optional (device, *_dev calls, metric cc): nq matches of an earlier scan
+     * over OTHER atoms (another B1 slab, another shard).  Their scores seed the
+     * screening maxima, so only atoms that can still win are re-ranked; a
+     * query with no atom above its floor returns flat -1 (merge skips it). */
+    const mrfg_match* floor_matches;
 } mrfg_scan_opts;
 
 /* What one scan did (device-timed with CUDA events on the ctx stream). */

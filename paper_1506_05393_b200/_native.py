@@ -29,7 +29,7 @@ class Match(C.Structure):
 
 class ScanOpts(C.Structure):
     _fields_ = [("delta", C.c_double), ("chunk_atoms", C.c_int64), ("cand_capacity", C.c_int64),
-                ("seed_atoms", C.c_int64)]
+                ("seed_atoms", C.c_int64), ("floor_matches", C.c_void_p)]
 
 
 class ScanStats(C.Structure):

@@ -159,6 +159,15 @@ __global__ void k_fill(float* p, int64_t n, float v) {
     if (i < n) p[i] = v;
 }
 
+// Screening maxima from an earlier scan's exact CC scores, rounded down
+// (a kept atom then still satisfies s >= e - eps >= floor - delta).
+__global__ void k_floor(const mrfg_match* __restrict__ m, int64_t nq, float* __restrict__ best) {
+    const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (v >= nq || m[v].flat < 0) return;
+    const float f = __double2float_rd(m[v].score);
+    if (f > best[v]) best[v] = f;
+}
+
 static void fill(Ctx& c, float* p, int64_t n, float v) {
     if (n <= 0) return;
     k_fill<<<(n + 255) / 256, 256, 0, c.stream>>>(p, n, v);
@@ -224,6 +233,11 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
     MRFG_REQUIRE(!h_bad, MRFG_E_INVALID, "normalize: zero fingerprint");
     float* best = c.best.as<float>();
     fill(c, best, nq, -3.0f);
+    const bool floored = o && o->floor_matches && metric == MRFG_METRIC_CC;
+    if (floored) {  // earlier scans' exact scores (rounded down) seed the maxima
+        k_floor<<<static_cast<unsigned>((nq + 255) / 256), 256, 0, c.stream>>>(o->floor_matches, nq, best);
+        MRFG_CUDA(cudaGetLastError());
+    }
 
     const int64_t arows = round_up(std::min(crows * ndf, round_up(range, ndf) + ndf), 256);  // pair tiles
     c.atoms_a.ensure(sizeof(__half) * 2 * arows * kp);  // double-buffered operand
@@ -348,7 +362,7 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
     int r0 = tm.mark();
     int64_t nsel = rerank_and_select(c, tp, d_dict, c.q64.as<double>(), nq, metric, best,
                                      static_cast<float>(delta), c.cand.as<CandRec>(),
-                                     static_cast<int64_t>(ncand), d_out, &err_max);
+                                     static_cast<int64_t>(ncand), d_out, &err_max, floored);
     int r1 = tm.mark();
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
     if (st) {

@@ -265,10 +265,11 @@ void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qro
 }
 
 // Returns the number of re-ranked candidates; throws when a voxel ends
-// without any (cannot happen unless the candidate buffer overflowed).
+// without any (cannot happen unless the candidate buffer overflowed), unless
+// allow_missing (a score floor from another scan was applied).
 int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, const double* d_q64,
                           int64_t nq, int metric, const float* d_best, float delta, CandRec* d_cand,
-                          int64_t ncand, mrfg_match* d_out, double* err_max) {
+                          int64_t ncand, mrfg_match* d_out, double* err_max, bool allow_missing) {
     // scratch layout: list (ncand i64) | score (ncand f64) | vkey (nq u64) |
     //                 vflat (nq u64) | counters
     size_t need = sizeof(int64_t) * ncand + sizeof(double) * ncand + 16 * nq + 64;
@@ -317,7 +318,9 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
         std::memcpy(&e, &h_missing[1], sizeof e);
         *err_max = e;
     }
-    MRFG_REQUIRE(!h_missing[0], MRFG_E_RUNTIME, "scan: a query ended without candidates");
+    // without a floor every query keeps its best atom (unless the candidate
+    // buffer overflowed); with one, flat -1 marks "nothing above the floor"
+    MRFG_REQUIRE(!h_missing[0] || allow_missing, MRFG_E_RUNTIME, "scan: a query ended without candidates");
     return static_cast<int64_t>(nsel);
 }
 

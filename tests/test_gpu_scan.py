@@ -191,3 +191,31 @@ def test_scan_single_cta_kernel(small, small_ref, monkeypatch):
     with P.Context(small.schedule) as c:
         flat, score, _ = c.scan_grid(small.grid, small.fps)
     assert_parity(flat, score, oflat, oscore, osecond)
+
+
+def test_scan_floor_from_other_atoms(small, small_ref):
+    """floor_matches: scanning the second half of the grid with the first half's
+    matches as the screening floor, then merging (max score, lowest flat), gives
+    the full scan's answer; voxels whose best lies in the first half may return
+    flat -1 from the second scan (nothing above the floor)."""
+    import torch
+    g, fps = small.grid, small.fps
+    total = P.grid_total(g)
+    half = total // 2
+    nq, n = fps.shape
+    dev = torch.device("cuda", 0)
+    d_q = torch.from_numpy(np.ascontiguousarray(fps).view(np.float64).reshape(nq, 2 * n)).to(dev)
+    d_all = torch.empty((2, nq, 2), dtype=torch.int64, device=dev)
+    d_out = torch.empty((nq, 2), dtype=torch.int64, device=dev)
+    with P.Context(small.schedule) as c:
+        c.scan_grid_device(g, d_q.data_ptr(), nq, d_all[0].data_ptr(), flat_range=(0, half))
+        opts = ScanOpts(0.0, 0, 0, 0, d_all[0].data_ptr())
+        st = c.scan_grid_device(g, d_q.data_ptr(), nq, d_all[1].data_ptr(), flat_range=(half, total), opts=opts)
+        c.merge_matches_device(d_all.data_ptr(), 2, nq, d_out.data_ptr())
+        torch.cuda.synchronize()
+        # without the floor, for comparison of re-rank work
+        st0 = c.scan_grid_device(g, d_q.data_ptr(), nq, d_all[1].data_ptr(), flat_range=(half, total))
+    out = d_out.cpu().numpy()
+    flat, score = out[:, 0], out[:, 1].view(np.float64)
+    assert_parity(flat, score, *small_ref)
+    assert st.reranked <= st0.reranked
