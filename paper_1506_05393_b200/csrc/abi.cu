@@ -915,8 +915,9 @@ int mrfg_quantify_slice(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_c
                 have = true;
             }
         } else {
-            // row wavefront: step s runs, for every row y, its (s - rank(y))-th
-            // masked voxel, where rank counts rows that hold masked voxels.
+            // row relaxation of the raster prior: rows of masked
+            // voxels; a row's first voxel is seeded by the first voxel of the
+            // previous non-empty row, every other voxel by its left neighbour.
             std::vector<std::vector<int64_t>> rows;
             for (int y = 0; y < ny; ++y) {
                 std::vector<int64_t> r;
@@ -924,30 +925,28 @@ int mrfg_quantify_slice(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_c
                     if (mask[static_cast<int64_t>(y) * nx + x]) r.push_back(static_cast<int64_t>(y) * nx + x);
                 if (!r.empty()) rows.push_back(std::move(r));
             }
+            // one launch: warp r walks row r, seeded on the device (k_zoom_rows)
             const int64_t R = static_cast<int64_t>(rows.size());
-            int64_t steps = 0;
-            for (int64_t r = 0; r < R; ++r) steps = std::max<int64_t>(steps, r + static_cast<int64_t>(rows[r].size()));
-            for (int64_t s = 0; s < steps; ++s) {
-                std::vector<int64_t> vox, b;
-                std::vector<double> init;
-                for (int64_t r = 0; r < R; ++r) {
-                    const int64_t k = s - r;
-                    if (k < 0 || k >= static_cast<int64_t>(rows[r].size())) continue;
-                    int64_t bb[6];
-                    double ii[2];
-                    const int64_t prev = k > 0 ? rows[r][k - 1] : (r > 0 ? rows[r - 1][0] : -1);
-                    if (prev >= 0) {
-                        prior_of(*lattice, *cfg, out[prev], bb, ii);
-                    } else {
-                        full_bounds(*lattice, bb);
-                        ii[0] = cfg->init_t1_ms;
-                        ii[1] = cfg->init_t2_ms;
-                    }
-                    vox.push_back(rows[r][k]);
-                    b.insert(b.end(), bb, bb + 6);
-                    init.insert(init.end(), ii, ii + 2);
+            std::vector<int64_t> row_start(1, 0), vox;
+            for (const auto& r : rows) {
+                vox.insert(vox.end(), r.begin(), r.end());
+                row_start.push_back(static_cast<int64_t>(vox.size()));
+            }
+            if (R > 0) {
+                DevBuf d_fps, d_res;
+                d_fps.ensure(sizeof(double) * n2 * nv);
+                d_res.ensure(sizeof(mrfg_quant) * nv);
+                MRFG_CUDA(cudaMemcpyAsync(d_fps.p, fps, sizeof(double) * n2 * nv, cudaMemcpyHostToDevice, c.stream));
+                MRFG_CUDA(cudaMemsetAsync(d_res.p, 0, sizeof(mrfg_quant) * nv, c.stream));
+                run_quantify(c, *lattice, *cfg, d_fps.as<double>(), nv, nullptr, nullptr, d_res.as<mrfg_quant>(), R,
+                             row_start.data(), vox.data());
+                MRFG_CUDA(cudaMemcpyAsync(out, d_res.p, sizeof(mrfg_quant) * nv, cudaMemcpyDeviceToHost, c.stream));
+                MRFG_CUDA(cudaStreamSynchronize(c.stream));
+                for (int64_t v : vox) {  // AxisSpec::value (dictionary.hpp:22)
+                    out[v].t1_ms = lattice->t1_ms.min + static_cast<double>(out[v].i1) * lattice->t1_ms.step;
+                    out[v].t2_ms = lattice->t2_ms.min + static_cast<double>(out[v].i2) * lattice->t2_ms.step;
+                    out[v].df_hz = lattice->df_hz.min + static_cast<double>(out[v].idf) * lattice->df_hz.step;
                 }
-                if (!vox.empty()) run(vox, &b, &init);
             }
         }
         if (seconds)

@@ -182,6 +182,10 @@ void launch_cc_map(Ctx& c, const GridTables& t, const double* d_q64, int64_t fir
 // K5 (zoom.cu)
 void run_quantify(Ctx& c, const mrfg_grid& lattice, const mrfg_zoom_config& cfg,
                   const double* d_fps, int64_t nvox, const int64_t* h_bounds /* nvox x 6 or null */,
-                  const double* h_init /* nvox x 2 or null */, mrfg_quant* d_out);
+                  const double* h_init /* nvox x 2 or null */, mrfg_quant* d_out,
+                  // neighbour-seeded slice (d_fps/d_out: the raster): nrows rows of
+                  // masked voxels, vox_list[row_start[r] .. row_start[r+1])
+                  int64_t nrows = 0, const int64_t* h_row_start = nullptr,
+                  const int64_t* h_vox_list = nullptr);
 
 }  // namespace mrfg

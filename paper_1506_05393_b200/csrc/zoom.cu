@@ -93,6 +93,13 @@ struct ZParams {
     int* pend;          // nwarps x kPendCap deferred exact evaluations
     ZSlot* tab;         // nwarps x cap memo tables
     unsigned long long* next;  // voxel work counter
+    // neighbour-seeded slice (row wavefront): rows of masked
+    // raster voxels, row r = vox_list[row_start[r] .. row_start[r+1]); done[v]
+    // flags finished voxels; prior windows in lattice units (zoom.cpp:600-605)
+    int64_t nrows;
+    const int64_t *row_start, *vox_list;
+    int* done;
+    long long pw1, pw2, pwdf;
     int smem_stage;            // StepU rows + per-warp q32 staged in dynamic shared memory
     int dict_mode;             // 0 none, 1 df dictionary (stage-1 acquisitions), 2 full dictionary
     // smoothing (fingerprint.cpp:122-145): k = 0 (off), 3 or 5 taps, host-libm weights
@@ -1292,7 +1299,10 @@ __device__ void zoom_2d(Z& z, long long idf, int metric, long long& x, long long
 }
 
 // ------------------------------------------------------------ the kernel
-__device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v) {
+// b6: (lo1, hi1, lo2, hi2, lodf, hidf) or null (full lattice); s1, s2: the
+// snapped, not yet clamped initial indices (zoom.cpp:428-429).
+__device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v, const long long* b6, long long s1,
+                           long long s2) {
     z.evals = 0;
     z.cyc32 = z.cyc64 = z.r64 = 0;
     const long long tstart = clock64();
@@ -1334,14 +1344,13 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v) {
     }
     zsync();
 
-    if (P.bounds) {
-        const long long* b = P.bounds + 6 * v;
-        z.lo1 = b[0];
-        z.hi1 = b[1];
-        z.lo2 = b[2];
-        z.hi2 = b[3];
-        z.lodf = b[4];
-        z.hidf = b[5];
+    if (b6) {
+        z.lo1 = b6[0];
+        z.hi1 = b6[1];
+        z.lo2 = b6[2];
+        z.hi2 = b6[3];
+        z.lodf = b6[4];
+        z.hidf = b6[5];
     } else {
         z.lo1 = 0;
         z.hi1 = P.L.n1 - 1;
@@ -1350,8 +1359,6 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v) {
         z.lodf = 0;
         z.hidf = P.L.ndf - 1;
     }
-    const long long s1 = P.inits ? P.inits[2 * v] : P.init1;
-    const long long s2 = P.inits ? P.inits[2 * v + 1] : P.init2;
     long long i1 = 0, i2 = 0, idf = 0;
     z.eager = P.eps < 0 ? 1 : 0;
     z.npend = 0;
@@ -1441,10 +1448,9 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v) {
 // Persistent warps: each warp owns a memo table and scratch and pulls voxels
 // from a work counter until the slice is done (no per-voxel memory, dynamic
 // balance of the very uneven per-voxel work).
-template <int BS, int MINB>
-__global__ void __launch_bounds__(BS, MINB) k_zoom(const ZParams P) {
-    const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
-    Z z;
+// Per-warp state and scratch; stages the StepU rows in shared memory (every
+// thread of the block takes part).
+__device__ void zwarp_setup(Z& z, const ZParams& P, int64_t w) {
     z.p = &P;
     z.lane = threadIdx.x % 32;
     z.tab = P.tab + w * (static_cast<int64_t>(P.cap_mask) + 1);
@@ -1462,12 +1468,77 @@ __global__ void __launch_bounds__(BS, MINB) k_zoom(const ZParams P) {
         z.rfs = P.su;
         z.q32 = P.q32 + w * P.n;
     }
+}
+
+template <int BS, int MINB>
+__global__ void __launch_bounds__(BS, MINB) k_zoom(const ZParams P) {
+    const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
+    Z z;
+    zwarp_setup(z, P, w);
     for (;;) {
         unsigned long long v = 0;
         if (z.lane == 0) v = atomicAdd(P.next, 1ull);
         v = __shfl_sync(0xffffffffu, v, 0);
         if (v >= static_cast<unsigned long long>(P.nvox)) break;
-        zoom_voxel(z, P, static_cast<int64_t>(v));
+        const int64_t vv = static_cast<int64_t>(v);
+        zoom_voxel(z, P, vv, P.bounds ? P.bounds + 6 * vv : nullptr, P.inits ? P.inits[2 * vv] : P.init1,
+                   P.inits ? P.inits[2 * vv + 1] : P.init2);
+    }
+}
+
+// Prior window around a finished voxel (zoom.cpp:595-610; the host
+// restatement is prior_of in abi.cu): parameters round-trip through seconds
+// like QuantResult::params, snap, intersect with the full lattice.
+__device__ void zprior(const ZParams& P, int64_t prev, long long* b, long long& s1, long long& s2) {
+    const volatile mrfg_quant* pr = P.out + prev;
+    const long long i1 = pr->i1, i2 = pr->i2, idf = pr->idf;
+    const double t1 = __dmul_rn(__dmul_rn(__dadd_rn(P.t1_min, __dmul_rn(static_cast<double>(i1), P.t1_step)), 1e-3), 1e3);
+    const double t2 = __dmul_rn(__dmul_rn(__dadd_rn(P.t2_min, __dmul_rn(static_cast<double>(i2), P.t2_step)), 1e-3), 1e3);
+    const double df = __dadd_rn(P.df_min, __dmul_rn(static_cast<double>(idf), P.df_step));
+    const long long p1 = llround(__ddiv_rn(__dsub_rn(t1, P.t1_min), P.t1_step));
+    const long long p2 = llround(__ddiv_rn(__dsub_rn(t2, P.t2_min), P.t2_step));
+    const long long pd = llround(__ddiv_rn(__dsub_rn(df, P.df_min), P.df_step));
+    s1 = p1;  // snap_index(init_t1_ms = t1) (zoom.cpp:596, 428)
+    s2 = p2;
+    b[0] = max(0ll, p1 - P.pw1);
+    b[1] = min(static_cast<long long>(P.L.n1 - 1), p1 + P.pw1);
+    b[2] = max(0ll, p2 - P.pw2);
+    b[3] = min(static_cast<long long>(P.L.n2 - 1), p2 + P.pw2);
+    b[4] = max(0ll, pd - P.pwdf);
+    b[5] = min(static_cast<long long>(P.L.ndf - 1), pd + P.pwdf);
+}
+
+// Neighbour-seeded slice in one launch: warp r walks raster row r left to
+// right, each voxel seeded by its left neighbour; a row's first voxel by the
+// first voxel of the row above (the permitted relaxation of the raster
+// order).  Rows wait only on lower rows' first voxels, and all
+// rows are co-resident (host check), so the spin-waits always finish.
+template <int BS>
+__global__ void __launch_bounds__(BS, 1) k_zoom_rows(const ZParams P) {
+    const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
+    Z z;
+    zwarp_setup(z, P, w);
+    if (w >= P.nrows) return;
+    const int64_t r = w, k0 = P.row_start[r], k1 = P.row_start[r + 1];
+    for (int64_t k = k0; k < k1; ++k) {
+        const int64_t v = P.vox_list[k];
+        const int64_t prev = k > k0 ? P.vox_list[k - 1] : (r > 0 ? P.vox_list[P.row_start[r - 1]] : -1);
+        long long b[6], s1 = P.init1, s2 = P.init2;
+        const long long* bp = nullptr;
+        if (prev >= 0) {
+            if (z.lane == 0)
+                while (*reinterpret_cast<volatile int*>(P.done + prev) == 0) __nanosleep(256);
+            __syncwarp();
+            __threadfence();
+            zprior(P, prev, b, s1, s2);
+            bp = b;
+        }
+        zoom_voxel(z, P, v, bp, s1, s2);
+        if (z.lane == 0) {
+            __threadfence();
+            *reinterpret_cast<volatile int*>(P.done + v) = 1;
+        }
+        __syncwarp();
     }
 }
 
@@ -1482,7 +1553,8 @@ long long step_units(double step_value, double finest) {  // zoom.cpp:411-414
 }  // namespace
 
 void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, const double* d_fps,
-                  int64_t nvox, const int64_t* h_bounds, const double* h_init, mrfg_quant* d_out) {
+                  int64_t nvox, const int64_t* h_bounds, const double* h_init, mrfg_quant* d_out,
+                  int64_t nrows, const int64_t* h_row_start, const int64_t* h_vox_list) {
     for (const mrfg_axis* ax : {&lat.t1_ms, &lat.t2_ms, &lat.df_hz})
         MRFG_REQUIRE(ax->count > 0 && ax->count < (int64_t(1) << 21), MRFG_E_INVALID,
                      "objective: lattice axis empty or too fine");  // zoom.cpp:46-48
@@ -1578,20 +1650,26 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     // 256 threads: 1 or 2)
     const char* mb_env = std::getenv("MRFG_ZOOM_MINB");
     const int minb = mb_env ? std::atoi(mb_env) : 1;
+    const bool rows = nrows > 0;
+    // rows mode: one warp per block (a row's voxels are a latency chain: one
+    // row per SM)
     void (*kern)(const ZParams) =
-        bs == 512   ? k_zoom<512, 1>
+        rows        ? k_zoom_rows<32>
+        : bs == 512 ? k_zoom<512, 1>
         : bs == 256 ? (minb >= 2 ? k_zoom<256, 2> : k_zoom<256, 1>)
                     : (minb >= 6 ? k_zoom<128, 6> : (minb >= 4 ? k_zoom<128, 4> : k_zoom<128, 1>));
+    const int bsk = rows ? 32 : bs;
     // shared staging: StepU rows (64 B/step) + one FP32 query per warp (8 B/step)
-    size_t smem = (sizeof(StepU) + sizeof(float2) * (bs / 32)) * c.n;
+    size_t smem = (sizeof(StepU) + sizeof(float2) * (bsk / 32)) * c.n;
     const char* st_env = std::getenv("MRFG_ZOOM_SMEM");
     P.smem_stage = smem <= 200 * 1024 && !(st_env && std::atoi(st_env) == 0) ? 1 : 0;
     if (!P.smem_stage) smem = 0;
     MRFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
-    MRFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bs, smem));
-    const int64_t nwarps = std::min<int64_t>(int64_t(std::max(per_sm, 1)) * c.num_sms * (bs / 32),
-                                             round_up(nvox, bs / 32));
+    MRFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bsk, smem));
+    const int64_t resident = int64_t(std::max(per_sm, 1)) * c.num_sms * (bsk / 32);
+    MRFG_REQUIRE(!rows || nrows <= resident, MRFG_E_RUNTIME, "quantify_slice: more raster rows than resident warps");
+    const int64_t nwarps = rows ? nrows : std::min<int64_t>(resident, round_up(nvox, bs / 32));
     // scratch: per-warp queries, fingerprints and memo tables; per-voxel
     // bounds/inits; error flag, stats, work counter
     const size_t qbytes = (sizeof(double) * 2 + sizeof(float) * 2) * c.n * nwarps;
@@ -1599,10 +1677,11 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     const size_t tbytes = sizeof(ZSlot) * cap * nwarps;
     const size_t pbytes = sizeof(int) * kPendCap * nwarps;
     const size_t bbytes = h_bounds ? sizeof(long long) * 6 * nvox : 0;
+    const size_t rbytes = rows ? sizeof(int64_t) * (nrows + 1 + h_row_start[nrows]) + sizeof(int) * nvox : 0;
     const size_t ibytes = h_init ? sizeof(long long) * 2 * nvox : 0;
     const size_t vbytes = want_stats ? sizeof(long long) * 4 * nvox : 0;
     DevBuf& scratch = c.zoom;
-    scratch.ensure(fbytes + qbytes + tbytes + pbytes + bbytes + ibytes + 256 + vbytes);
+    scratch.ensure(fbytes + qbytes + tbytes + pbytes + bbytes + ibytes + rbytes + 256 + vbytes);
     char* base = scratch.as<char>();
     P.fpx = reinterpret_cast<double2*>(base);
     base += fbytes;
@@ -1617,6 +1696,22 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     base += bbytes;
     P.inits = h_init ? reinterpret_cast<long long*>(base) : nullptr;
     base += ibytes;
+    P.nrows = rows ? nrows : 0;
+    if (rows) {
+        const int64_t m = h_row_start[nrows];
+        int64_t* rs = reinterpret_cast<int64_t*>(base);
+        int64_t* vl = rs + nrows + 1;
+        P.row_start = rs;
+        P.vox_list = vl;
+        P.done = reinterpret_cast<int*>(vl + m);
+        MRFG_CUDA(cudaMemcpyAsync(rs, h_row_start, sizeof(int64_t) * (nrows + 1), cudaMemcpyHostToDevice, c.stream));
+        MRFG_CUDA(cudaMemcpyAsync(vl, h_vox_list, sizeof(int64_t) * m, cudaMemcpyHostToDevice, c.stream));
+        MRFG_CUDA(cudaMemsetAsync(P.done, 0, sizeof(int) * nvox, c.stream));
+        P.pw1 = step_units(cfg.prior_window_t1_ms, lat.t1_ms.step);  // zoom.cpp:600-602
+        P.pw2 = step_units(cfg.prior_window_t2_ms, lat.t2_ms.step);
+        P.pwdf = step_units(cfg.prior_window_df_hz, lat.df_hz.step);
+    }
+    base += rbytes;
     P.err = reinterpret_cast<int*>(base);
     P.next = reinterpret_cast<unsigned long long*>(base + 64);
     P.stats = want_stats ? reinterpret_cast<unsigned long long*>(base + 128) : nullptr;
@@ -1639,7 +1734,7 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
                                   cudaMemcpyHostToDevice, c.stream));
     }
     P.out = d_out;
-    kern<<<static_cast<unsigned>(nwarps / (bs / 32)), bs, smem, c.stream>>>(P);
+    kern<<<static_cast<unsigned>((nwarps + bsk / 32 - 1) / (bsk / 32)), bsk, smem, c.stream>>>(P);
     MRFG_CUDA(cudaGetLastError());
     int err = 0;
     MRFG_CUDA(cudaMemcpyAsync(&err, P.err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));

@@ -234,3 +234,48 @@ def test_zoom_smoothing(orc, k, mode):
     fps = np.stack(fps)
     with P.Context(s) as c:
         check_same(c.quantify(fps, g, cfg), orc, s, g, cfg, fps)
+
+
+def _lround(x):  # std::lround: half away from zero
+    import math
+    return int(math.copysign(math.floor(abs(x) + 0.5), x))
+
+
+def _prior_of(g, cfg, r):
+    """Host restatement of the prior window (zoom.cpp:595-610)."""
+    t1 = (g.t1_ms.min + float(r["i1"]) * g.t1_ms.step) * 1e-3 * 1e3
+    t2 = (g.t2_ms.min + float(r["i2"]) * g.t2_ms.step) * 1e-3 * 1e3
+    df = g.df_hz.min + float(r["idf"]) * g.df_hz.step
+    units = lambda s, fine: max(1, _lround(s / fine))  # noqa: E731
+    p1, p2, pd = (_lround((t1 - g.t1_ms.min) / g.t1_ms.step), _lround((t2 - g.t2_ms.min) / g.t2_ms.step),
+                  _lround((df - g.df_hz.min) / g.df_hz.step))
+    w1, w2, wd = (units(cfg.prior_window_t1_ms, g.t1_ms.step), units(cfg.prior_window_t2_ms, g.t2_ms.step),
+                  units(cfg.prior_window_df_hz, g.df_hz.step))
+    b = [max(0, p1 - w1), min(g.t1_ms.count - 1, p1 + w1), max(0, p2 - w2), min(g.t2_ms.count - 1, p2 + w2),
+         max(0, pd - wd), min(g.df_hz.count - 1, pd + wd)]
+    return b, [t1, t2]
+
+
+def test_zoom_slice_row_relaxation_exact(orc):
+    """use_prior=2 runs the SPEC.md:449 row relaxation in one launch (device
+    seeding and completion flags); it must equal the same relaxation driven
+    voxel by voxel from the host through quantify_bounded (whose prior path is
+    the one pinned against the reference's raster mode)."""
+    s, g, cfg, nx, ny, mask, fps = _slice_problem(orc)
+    with P.Context(s) as c:
+        dev, _ = c.quantify_slice(fps, mask, nx, ny, g, cfg, use_prior=2)
+        rows = [[y * nx + x for x in range(nx) if mask[y * nx + x]] for y in range(ny)]
+        rows = [r for r in rows if r]
+        host = {}
+        for ri, r in enumerate(rows):
+            for k, v in enumerate(r):
+                prev = r[k - 1] if k > 0 else (rows[ri - 1][0] if ri > 0 else None)
+                if prev is None:
+                    res = c.quantify_bounded(fps[v:v + 1], g, cfg)
+                else:
+                    b, init = _prior_of(g, cfg, host[prev])
+                    res = c.quantify_bounded(fps[v:v + 1], g, cfg, bounds=[b], init_ms=[init])
+                host[v] = res[0]
+    for v, h in host.items():
+        for k in ("i1", "i2", "idf", "score", "pd", "evaluations"):
+            assert dev[k][v] == h[k], (v, k)
