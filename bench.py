@@ -273,33 +273,31 @@ def run_ours(args, world, rank, local):
     if not args.no_zoom:
         from paper_1506_05393_b200 import distributed as Dz
         zcfg = P.zoom_config(df_coarse_hz=5.0, omega_hz=82.0)
-        vb, ve = Dz.voxel_shard(nq, world, rank)
-        d_zq = torch.empty(max(ve - vb, 1) * P.dgs.QUANT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-        ctx.quantify_device(d_q[vb:ve].data_ptr(), ve - vb, g, zcfg, d_zq.data_ptr())  # warm-up
+        # voxel blocks per rank + one all_gather of the result structs
+        Dz.quantify_distributed(ctx, g, zcfg, d_q, nq)  # warm-up
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         z0.record(stream)
-        ctx.quantify_device(d_q[vb:ve].data_ptr(), ve - vb, g, zcfg, d_zq.data_ptr())
+        d_zq = Dz.quantify_distributed(ctx, g, zcfg, d_q, nq)
         z1.record(stream)
         torch.cuda.synchronize()
         zms = allmax(z0.elapsed_time(z1), world)
-        recs = d_zq[: (ve - vb) * P.dgs.QUANT_DTYPE.itemsize].cpu().numpy().view(P.dgs.QUANT_DTYPE)
+        recs = d_zq.cpu().numpy().view(P.dgs.QUANT_DTYPE)
         zoom = {"voxels_per_s": nq / (zms * 1e-3), "slice_ms": zms,
                 "evals_per_voxel_mean": float(recs["evaluations"].mean()),
-                "config": "df_coarse 5 Hz, omega 82 Hz, reference defaults otherwise; voxels sharded"}
+                "config": "df_coarse 5 Hz, omega 82 Hz, reference defaults otherwise; voxel blocks per rank + "
+                          "one all_gather of the result structs"}
         # BASELINE configs[3]: ZOOM only on the 1 ms / 0.5 ms / 0.1 Hz lattice
         # (9.7e10 points; brute force infeasible), same voxel sharding, median of 3
         wl4 = workloads.make(4, gpu_sim)
         g4, nq4 = wl4.grid, wl4.nvox
-        vb4, ve4 = Dz.voxel_shard(nq4, world, rank)
         z4cfg = P.zoom_config(**workloads.CONFIG4_ZOOM)
         with P.Context(wl4.schedule, local) as ctx4:
             ctx4.set_stream(stream.cuda_stream)
-            d_q4 = torch.from_numpy(wl4.fps.view(np.float64).reshape(nq4, 2 * n)[vb4:ve4].copy()).to(dev)
-            d_z4 = torch.empty(max(ve4 - vb4, 1) * P.dgs.QUANT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-            ctx4.quantify_device(d_q4.data_ptr(), ve4 - vb4, g4, z4cfg, d_z4.data_ptr())  # tables + warm-up
+            d_q4 = torch.from_numpy(wl4.fps.view(np.float64).reshape(nq4, 2 * n)).to(dev)
+            Dz.quantify_distributed(ctx4, g4, z4cfg, d_q4, nq4)  # tables + warm-up
             times = []
             for _ in range(3):
                 torch.cuda.synchronize()
@@ -307,12 +305,12 @@ def run_ours(args, world, rank, local):
                     torch.distributed.barrier()
                 z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 z0.record(stream)
-                ctx4.quantify_device(d_q4.data_ptr(), ve4 - vb4, g4, z4cfg, d_z4.data_ptr())
+                d_z4 = Dz.quantify_distributed(ctx4, g4, z4cfg, d_q4, nq4)
                 z1.record(stream)
                 torch.cuda.synchronize()
                 times.append(allmax(z0.elapsed_time(z1), world))
             z4ms = float(np.median(times))
-            r4 = d_z4[: (ve4 - vb4) * P.dgs.QUANT_DTYPE.itemsize].cpu().numpy().view(P.dgs.QUANT_DTYPE)
+            r4 = d_z4.cpu().numpy().view(P.dgs.QUANT_DTYPE)
         def zoom_roofline(vps, evals):
             # reference-equivalent unique evaluations x N x (37 Bloch + 8 CC)
             # flop against the FP32 CUDA-core peak (148 SMs x 128 lanes x 2 x max clock)

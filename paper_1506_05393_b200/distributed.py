@@ -74,3 +74,50 @@ def scan_grid_distributed(ctx, grid, d_queries, nq: int, group=None, opts=None, 
     d_merged = torch.empty(nq * 16, dtype=torch.uint8, device=dev)
     ctx.merge_matches_device(d_all.data_ptr(), world, nq, d_merged.data_ptr())
     return d_merged, stats
+
+
+def gather_voxel_shards(local, nvox: int, rec_bytes: int, group=None):
+    """All-gather per-rank voxel blocks (voxel_shard order) of fixed-size
+    records into the full array on every rank (ZOOM shards voxels
+    and all-gathers the per-voxel result structs).  `local` is a uint8 tensor of
+    (ve - vb) * rec_bytes bytes on the process group's device; blocks are padded
+    to the largest shard for one all_gather_into_tensor.  Works with NCCL (CUDA
+    tensors) and gloo (CPU tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return local
+    cap = max(ve - vb for vb, ve in (voxel_shard(nvox, world, r) for r in range(world)))
+    pad = torch.zeros(cap * rec_bytes, dtype=torch.uint8, device=local.device)
+    pad[: local.numel()] = local
+    allb = torch.empty(world * cap * rec_bytes, dtype=torch.uint8, device=local.device)
+    if local.device.type == "cuda":
+        dist.all_gather_into_tensor(allb, pad, group=group)
+    else:
+        dist.all_gather(list(allb.view(world, cap * rec_bytes).unbind(0)), pad, group=group)
+    parts = []
+    for r in range(world):
+        vb, ve = voxel_shard(nvox, world, r)
+        parts.append(allb[r * cap * rec_bytes: (r * cap + (ve - vb)) * rec_bytes])
+    return torch.cat(parts)
+
+
+def quantify_distributed(ctx, lattice, cfg, d_fps, nvox: int, group=None):
+    """MRF-ZOOM over the process group (GPU): each rank quantifies its voxel
+    block (voxel_shard) with K5, then one all_gather gives every rank all
+    nvox mrfg_quant records (uint8 CUDA tensor, dgs.QUANT_DTYPE layout).
+    d_fps: CUDA float64 tensor (nvox, 2N) of raw fingerprints on this rank."""
+    import torch
+    import torch.distributed as dist
+    from . import dgs
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    vb, ve = voxel_shard(nvox, world, rank)
+    rb = dgs.QUANT_DTYPE.itemsize
+    local = torch.empty(max(ve - vb, 0) * rb, dtype=torch.uint8, device=d_fps.device)
+    if ve > vb:
+        ctx.quantify_device(d_fps[vb:ve].data_ptr(), ve - vb, lattice, cfg, local.data_ptr())
+    return gather_voxel_shards(local, nvox, rb, group)

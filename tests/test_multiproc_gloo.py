@@ -100,3 +100,46 @@ def test_shards_partition_the_grid():
         cuts = [D.shard_range(n1, 100, world, r) for r in range(world)]
         assert cuts[0][0] == 0 and cuts[-1][1] == n1 * 100
         assert all(cuts[r][1] == cuts[r + 1][0] for r in range(world - 1))
+
+
+def zoom_worker(rank, world, port, out_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    from paper_1506_05393_b200 import dgs
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc, s, (t1, t2, df), q = problem()
+    g = oracle.make_grid(t1, t2, df)
+    cfg = oracle.zoom_cfg(df_coarse_hz=10.0)
+    nq = len(q)
+    vb, ve = D.voxel_shard(nq, world, rank)
+    rec = np.zeros(ve - vb, dtype=dgs.QUANT_DTYPE)
+    for k, v in enumerate(range(vb, ve)):  # per-rank compute: the CPU oracle (K5 needs a B200)
+        r = orc.quantify(s, g, cfg, q[v])
+        rec[k] = (r.i1, r.i2, r.idf, r.t1_ms, r.t2_ms, r.df_hz, r.pd, r.score, r.evaluations)
+    local = torch.from_numpy(rec.view(np.uint8).copy())
+    full = D.gather_voxel_shards(local, nq, dgs.QUANT_DTYPE.itemsize)
+    if rank == 0:
+        np.save(out_path, full.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_zoom_voxel_shards_gather(tmp_path, world):
+    """ZOOM's N>1 exchange: voxel blocks quantified per rank,
+    ONE all_gather of the 72-byte result structs; rank 0 holds every voxel's
+    record, identical to the single-process results."""
+    import oracle
+    from paper_1506_05393_b200 import dgs
+    out = str(tmp_path / "zoom.npy")
+    mp.spawn(zoom_worker, args=(world, free_port(), out), nprocs=world, join=True)
+    got = np.load(out).view(dgs.QUANT_DTYPE)
+    orc, s, (t1, t2, df), q = problem()
+    g = oracle.make_grid(t1, t2, df)
+    cfg = oracle.zoom_cfg(df_coarse_hz=10.0)
+    for v in range(len(q)):
+        r = orc.quantify(s, g, cfg, q[v])
+        assert (got["i1"][v], got["i2"][v], got["idf"][v], got["score"][v], got["evaluations"][v]) == \
+               (r.i1, r.i2, r.idf, r.score, r.evaluations)
