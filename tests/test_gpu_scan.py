@@ -219,3 +219,24 @@ def test_scan_floor_from_other_atoms(small, small_ref):
     flat, score = out[:, 0], out[:, 1].view(np.float64)
     assert_parity(flat, score, *small_ref)
     assert st.reranked <= st0.reranked
+
+
+@pytest.mark.parametrize("n", [1, 2, 33])
+def test_scan_tiny_shapes(orc, n):
+    """Degenerate shapes: schedules of 1/2/33 TRs (K padded from 2N to 64),
+    single-valued axes, a 1-point lattice, one voxel; the reference library's
+    answers and scores (flat + score bit-identical)."""
+    s = P.reference_schedule(n, 3)
+    os_ = to_oracle_sched(s)
+    grids = [P.grid((700.0, 10.0, 1), (90.0, 5.0, 1), (0.0, 1.0, 1)),
+             P.grid((600.0, 50.0, 7), (80.0, 5.0, 1), (-10.0, 5.0, 5)),
+             P.grid((600.0, 50.0, 1), (80.0, 5.0, 9), (0.0, 1.0, 1))]
+    rng = np.random.default_rng(n)
+    for g in grids:
+        for nv in (1, 3):
+            fps = np.stack([orc.add_noise(orc.simulate(os_, 0.5 + rng.random(), 0.05 + 0.1 * rng.random(),
+                                                       10 * rng.random() - 5), 0.01, 40 + k) for k in range(nv)])
+            with P.Context(s) as c:
+                flat, score, _ = c.scan_grid(g, fps)
+            of, osc, osec = orc.scan_grid(os_, to_oracle_grid(g), fps)
+            assert_parity(flat, score, of, osc, osec)

@@ -279,3 +279,20 @@ def test_zoom_slice_row_relaxation_exact(orc):
     for v, h in host.items():
         for k in ("i1", "i2", "idf", "score", "pd", "evaluations"):
             assert dev[k][v] == h[k], (v, k)
+
+
+@pytest.mark.parametrize("n", [1, 2, 33])
+def test_zoom_tiny_shapes(orc, n):
+    """ZOOM on degenerate lattices (single-valued axes, one voxel, 1-2 TR
+    schedules): the oracle's answers, scores, PD and evaluation counts."""
+    s = P.reference_schedule(n, 3)
+    os_ = to_oracle_sched(s)
+    rng = np.random.default_rng(n)
+    for g in (P.grid((700.0, 10.0, 1), (90.0, 5.0, 1), (0.0, 1.0, 1)),
+              P.grid((600.0, 50.0, 7), (80.0, 5.0, 1), (-10.0, 5.0, 5)),
+              P.grid((600.0, 10.0, 30), (80.0, 5.0, 20), (0.0, 1.0, 1))):
+        fps = np.stack([orc.add_noise(orc.simulate(os_, 0.5 + rng.random(), 0.05 + 0.1 * rng.random(),
+                                                   10 * rng.random() - 5), 0.01, 60 + k) for k in range(2)])
+        cfg = P.zoom_config(df_coarse_hz=5.0)
+        with P.Context(s) as c:
+            check_same(c.quantify(fps, g, cfg), orc, s, g, cfg, fps)
