@@ -123,6 +123,13 @@ struct ZParams {
     long long* vstats;  // nvox x 4: cycles, screening rounds' cycles, exact rounds, exact cycles
 };
 
+constexpr int kQCap = 256;  // queued evaluations per dispatch
+struct ZItem {
+    int kind;  // 0: screen one point, 1: screen a stride-1 df pair, 2: exact
+    int s0, s1;
+    int a, b, c;
+};
+
 struct Z {
     const ZParams* p;
     ZSlot* tab;
@@ -134,6 +141,10 @@ struct Z {
     int npend;          // warp-uniform
     int eager;          // 1: certify each close decision immediately
     int stage1;         // inside search_df (df-dictionary acquisitions)
+    int qw;             // shared-memory query slot (the voxel's warp in the block)
+    int cta_w;          // CTA mode: warps evaluating this voxel's rounds (0 = own warp only)
+    ZItem* queue;       // CTA mode: shared work queue (kQCap) and control words
+    int* ctl;
     int lane;
     long long evals;
     long long cyc32, cyc64;  // stats: cycles in screening / exact rounds
@@ -338,7 +349,9 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
     const float4* __restrict__ php = P.phf + static_cast<int64_t>(idf) * n;
     extern __shared__ float4 zsm[];
     const float4* rfp = SMEM ? zsm : z.rfs;
-    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + 4 * n) + (threadIdx.x / 32) * n : z.q32;
+    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + 4 * n) +
+                                 (z.cta_w ? 0 : static_cast<int>(threadIdx.x / 32)) * n
+                           : z.q32;
     float x = static_cast<float>(P.inv0[0]), y = static_cast<float>(P.inv0[1]),
           zz = static_cast<float>(P.inv0[2]);
     double re = 0.0, im = 0.0, nn = 0.0;
@@ -415,7 +428,9 @@ __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
     const float4* __restrict__ php = P.phf + static_cast<int64_t>(idf) * n;
     extern __shared__ float4 zsm[];
     const float4* rfp = SMEM ? zsm : z.rfs;
-    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + 4 * n) + (threadIdx.x / 32) * n : z.q32;
+    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + 4 * n) +
+                                 (z.cta_w ? 0 : static_cast<int>(threadIdx.x / 32)) * n
+                           : z.q32;
     const float x0 = static_cast<float>(P.inv0[0]), y0 = static_cast<float>(P.inv0[1]),
                 z0 = static_cast<float>(P.inv0[2]);
     float xa = x0, ya = y0, za = z0, xb = x0, yb = y0, zb = z0;
@@ -636,11 +651,112 @@ __device__ __forceinline__ Apx zsim32(const Z& z, int i1, int i2, int idf) {
     return z.p->smem_stage ? zsim32_tab<true>(z, i1, i2, idf) : zsim32_tab<false>(z, i1, i2, idf);
 }
 
+// ---------------------------------------------------------- helper warps
+// CTA mode (z.cta_w > 0): warp 0 of the block runs the voxel's decision
+// logic; every screening / exact round it needs is written to a shared-memory
+// queue and evaluated by all cta_w warps between two named barriers (the
+// helpers wait in zhelper_loop).  Without CTA mode a warp evaluates its own
+// rounds in place.
+__device__ __forceinline__ void zbar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Screen (or, with eps < 0, evaluate exactly) lattice point (a, b, c) into a
+// freshly claimed memo slot.
+__device__ void zdo_screen(Z& z, int slot, int a, int b, int c) {
+    if (z.p->eps < 0) {
+        ZSlot s;
+        zsim(z, a, b, c, false, s);
+        z.tab[slot].cc = s.cc;
+        z.tab[slot].euc = s.euc;
+        z.tab[slot].nrm2 = s.nrm2;
+        z.tab[slot].acc = static_cast<float>(s.cc);
+        z.tab[slot].are = 0.f;
+        z.tab[slot].xtype = 0;
+        z.tab[slot].atype = 0;
+        z.tab[slot].queued = 0;
+        return;
+    }
+    const Apx v = zsim32(z, a, b, c);
+    z.tab[slot].acc = v.cc;
+    z.tab[slot].are = v.re;
+    z.tab[slot].nrm2 = -1.0;
+    z.tab[slot].xtype = 0xFFu;
+    z.tab[slot].atype = 0;
+    z.tab[slot].queued = 0;
+    if (z.p->stats && (zhash(zkey(a, b, c) * 0x9E3779B97F4A7C15ull) & 63) == 0) {
+        // audit (stats mode only): exact value of a random 1/64 of all
+        // screened points, |error| into stats[10]
+        ZSlot r;
+        zsim(z, a, b, c, false, r);
+        const double e = fabs(static_cast<double>(v.cc) - r.cc);
+        atomicMax(z.p->stats + 10, static_cast<unsigned long long>(__double_as_longlong(e)));
+        atomicAdd(z.p->stats + 11, 1ull);
+    }
+}
+
+__device__ void zdo_pair(Z& z, int s0, int s1, int i1, int i2, int idf0);
+__device__ void zdo_exact(Z& z, int s);
+
+// Evaluate queued items k = warp*32 + lane, stride 32 * cta_w.
+__device__ void zwork(Z& z, int m) {
+    for (int k = static_cast<int>(threadIdx.x / 32) * 32 + z.lane; k < m; k += 32 * z.cta_w) {
+        const ZItem it = z.queue[k];
+        if (it.kind == 0)
+            zdo_screen(z, it.s0, it.a, it.b, it.c);
+        else if (it.kind == 1)
+            zdo_pair(z, it.s0, it.s1, it.a, it.b, it.c);
+        else
+            zdo_exact(z, it.s0);
+    }
+    __threadfence_block();
+}
+
+// Controller: evaluate the m queued items with all warps of the block.
+__device__ void zdispatch(Z& z, int m) {
+    if (z.lane == 0) {
+        z.ctl[0] = 1;
+        z.ctl[1] = m;
+    }
+    __syncwarp();
+    zbar(1, 32 * z.cta_w);
+    zwork(z, m);
+    zbar(2, 32 * z.cta_w);
+}
+
+// Helper warps: evaluate dispatched rounds until the controller sends 0.
+__device__ void zhelper_loop(Z& z) {
+    for (;;) {
+        zbar(1, 32 * z.cta_w);
+        const int cmd = *reinterpret_cast<volatile int*>(z.ctl), m = *reinterpret_cast<volatile int*>(z.ctl + 1);
+        if (cmd == 0) break;
+        zwork(z, m);
+        zbar(2, 32 * z.cta_w);
+    }
+}
+__device__ void zhelpers_release(Z& z) {
+    if (z.lane == 0) z.ctl[0] = 0;
+    __syncwarp();
+    zbar(1, 32 * z.cta_w);
+}
+
+// Append this lane's item (if has) to the queue; dispatch when nearly full.
+__device__ __forceinline__ void zenqueue(Z& z, int& qn, bool has, const ZItem& it) {
+    const unsigned int mm = __ballot_sync(0xffffffffu, has);
+    if (has) z.queue[qn + __popc(mm & ((1u << z.lane) - 1u))] = it;
+    qn += __popc(mm);
+    if (qn > kQCap - 32) {
+        zdispatch(z, qn);
+        qn = 0;
+    }
+}
+
 // Make sure the points pt(0..count-1) are in the memo (screened, not
 // acquired).  Lanes split the missing points; duplicates are claimed once.
 // With eps < 0 the points are evaluated exactly instead.
 template <class PT>
 __device__ void zensure(Z& z, long long count, PT pt) {
+    int qn = 0;
     for (long long base = 0; base < count; base += 32) {
         const long long k = base + z.lane;
         bool mine = false;
@@ -657,38 +773,12 @@ __device__ void zensure(Z& z, long long count, PT pt) {
             }
         }
         __syncwarp();
-        const long long t0 = z.p->stats ? clock64() : 0;
-        if (mine) {
-            if (z.p->eps < 0) {
-                ZSlot s;
-                zsim(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c), false, s);
-                z.tab[slot].cc = s.cc;
-                z.tab[slot].euc = s.euc;
-                z.tab[slot].nrm2 = s.nrm2;
-                z.tab[slot].acc = static_cast<float>(s.cc);
-                z.tab[slot].are = 0.f;
-                z.tab[slot].xtype = 0;
-                z.tab[slot].atype = 0;
-                z.tab[slot].queued = 0;
-            } else {
-                const Apx v = zsim32(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c));
-                z.tab[slot].acc = v.cc;
-                z.tab[slot].are = v.re;
-                z.tab[slot].nrm2 = -1.0;
-                z.tab[slot].xtype = 0xFFu;
-                z.tab[slot].atype = 0;
-                z.tab[slot].queued = 0;
-                if (z.p->stats && (zhash(zkey(a, b, c) * 0x9E3779B97F4A7C15ull) & 63) == 0) {
-                    // audit (stats mode only): exact value of a random 1/64 of
-                    // all screened points, |error| into stats[10]
-                    ZSlot r;
-                    zsim(z, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c), false, r);
-                    const double e = fabs(static_cast<double>(v.cc) - r.cc);
-                    atomicMax(z.p->stats + 10, static_cast<unsigned long long>(__double_as_longlong(e)));
-                    atomicAdd(z.p->stats + 11, 1ull);
-                }
-            }
+        if (z.cta_w) {
+            zenqueue(z, qn, mine, ZItem{0, slot, -1, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c)});
+            continue;
         }
+        const long long t0 = z.p->stats ? clock64() : 0;
+        if (mine) zdo_screen(z, slot, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c));
         if (z.p->stats) {
             const unsigned int m = __ballot_sync(0xffffffffu, mine);
             if (z.lane == 0) zstat(z, z.p->eps < 0 ? 1 : 0, __popc(m));
@@ -701,6 +791,7 @@ __device__ void zensure(Z& z, long long count, PT pt) {
         }
         zsync();
     }
+    if (qn) zdispatch(z, qn);
 }
 
 // zensure for a stride-1 off-resonance run (i1, i2, a .. a + count - 1):
@@ -715,6 +806,7 @@ __device__ void zensure_df(Z& z, long long i1, long long i2, long long a, long l
         });
         return;
     }
+    int qn = 0;
     for (long long base = 0; base < count; base += 64) {
         const long long k0 = base + 2 * z.lane;
         int slot[2] = {-1, -1};
@@ -733,38 +825,14 @@ __device__ void zensure_df(Z& z, long long i1, long long i2, long long a, long l
         // reconverge the warp before the evaluation: lanes leave the probe
         // loops above at different iterations
         __syncwarp();
-        const long long t0 = P.stats ? clock64() : 0;
-        if (mine[0] || mine[1]) {
-            const Apx2 v = P.smem_stage ? zsim32_df2<true>(z, static_cast<int>(i1), static_cast<int>(i2),
-                                                           static_cast<int>(a + k0))
-                                        : zsim32_df2<false>(z, static_cast<int>(i1), static_cast<int>(i2),
-                                                            static_cast<int>(a + k0));
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (mine[h]) {
-                    ZSlot& t = z.tab[slot[h]];
-                    t.acc = h ? v.b.cc : v.a.cc;
-                    t.are = h ? v.b.re : v.a.re;
-                    t.nrm2 = -1.0;
-                    t.xtype = 0xFFu;
-                    t.atype = 0;
-                    t.queued = 0;
-                }
-            }
-            if (P.stats) {  // audit (stats mode only), as in zensure
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const unsigned long long key = zkey(i1, i2, a + k0 + h);
-                    if (mine[h] && (zhash(key * 0x9E3779B97F4A7C15ull) & 63) == 0) {
-                        ZSlot r;
-                        zsim(z, static_cast<int>(i1), static_cast<int>(i2), static_cast<int>(a + k0 + h), false, r);
-                        const double e = fabs(static_cast<double>(h ? v.b.cc : v.a.cc) - r.cc);
-                        atomicMax(P.stats + 10, static_cast<unsigned long long>(__double_as_longlong(e)));
-                        atomicAdd(P.stats + 11, 1ull);
-                    }
-                }
-            }
+        const int s0 = mine[0] ? slot[0] : -1, s1 = mine[1] ? slot[1] : -1;
+        if (z.cta_w) {
+            zenqueue(z, qn, s0 >= 0 || s1 >= 0,
+                     ZItem{1, s0, s1, static_cast<int>(i1), static_cast<int>(i2), static_cast<int>(a + k0)});
+            continue;
         }
+        const long long t0 = P.stats ? clock64() : 0;
+        if (s0 >= 0 || s1 >= 0) zdo_pair(z, s0, s1, static_cast<int>(i1), static_cast<int>(i2), static_cast<int>(a + k0));
         if (P.stats) {
             const unsigned int m0 = __ballot_sync(0xffffffffu, mine[0]), m1 = __ballot_sync(0xffffffffu, mine[1]);
             const unsigned int m = m0 | m1;
@@ -778,37 +846,75 @@ __device__ void zensure_df(Z& z, long long i1, long long i2, long long a, long l
         }
         zsync();
     }
+    if (qn) zdispatch(z, qn);
+}
+
+// Screen the stride-1 df pair (idf0, idf0 + 1) of (i1, i2) into the claimed
+// slots s0 / s1 (-1: not this lane's).
+__device__ void zdo_pair(Z& z, int s0, int s1, int i1, int i2, int idf0) {
+    const ZParams& P = *z.p;
+    // only row idf0 is read (the second point's phasor comes from the ladder)
+    const int c0 = static_cast<int>(clampll(idf0, 0, P.L.ndf - 1));
+    const Apx2 v = P.smem_stage ? zsim32_df2<true>(z, i1, i2, c0) : zsim32_df2<false>(z, i1, i2, c0);
+    const int sl[2] = {s0, s1};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (sl[h] < 0) continue;
+        ZSlot& t = z.tab[sl[h]];
+        t.acc = h ? v.b.cc : v.a.cc;
+        t.are = h ? v.b.re : v.a.re;
+        t.nrm2 = -1.0;
+        t.xtype = 0xFFu;
+        t.atype = 0;
+        t.queued = 0;
+        if (P.stats && (zhash(zkey(i1, i2, idf0 + h) * 0x9E3779B97F4A7C15ull) & 63) == 0) {
+            ZSlot r;  // audit (stats mode only), as in zdo_screen
+            zsim(z, i1, i2, idf0 + h, false, r);
+            const double e = fabs(static_cast<double>(h ? v.b.cc : v.a.cc) - r.cc);
+            atomicMax(P.stats + 10, static_cast<unsigned long long>(__double_as_longlong(e)));
+            atomicAdd(P.stats + 11, 1ull);
+        }
+    }
+}
+
+// Exact (reference FP64 pipeline) value of memo slot s for its entry type.
+__device__ void zdo_exact(Z& z, int s) {
+    volatile ZSlot* vs = &z.tab[s];
+    int i1, i2, idf;
+    zunkey(vs->key, i1, i2, idf);
+    const unsigned int ty = vs->atype;
+    ZSlot r;
+    zsim(z, i1, i2, idf, ty == 1, r);
+    if (z.p->stats) {
+        const double e = fabs(static_cast<double>(z.tab[s].acc) - r.cc);
+        atomicMax(z.p->stats + 8, static_cast<unsigned long long>(__double_as_longlong(e)));
+    }
+    z.tab[s].cc = r.cc;
+    z.tab[s].euc = r.euc;
+    z.tab[s].nrm2 = r.nrm2;
+    z.tab[s].queued = 0;
+    __threadfence_block();
+    z.tab[s].xtype = ty;
 }
 
 // Exact (FP64) evaluation of the memo slots named by slot_of(0..count-1)
 // (-1 = none) that are still screened-only, one warp round per 32 slots.
 template <class SL>
 __device__ void zexact(Z& z, int count, SL slot_of) {
+    int qn = 0;
     for (int base = 0; base < count; base += 32) {
         const int k = base + z.lane;
         const int s = k < count ? slot_of(k) : -1;
         const volatile ZSlot* vs = s >= 0 ? &z.tab[s] : nullptr;
         const bool work = vs && !meta_exact(vs->meta);
+        if (z.cta_w) {
+            zenqueue(z, qn, work, ZItem{2, s, -1, 0, 0, 0});
+            continue;
+        }
         const unsigned int m = __ballot_sync(0xffffffffu, work);
         if (!m) continue;
         const long long t0 = z.p->stats ? clock64() : 0;
-        if (work) {
-            int i1, i2, idf;
-            zunkey(*reinterpret_cast<volatile unsigned long long*>(&z.tab[s].key), i1, i2, idf);
-            const unsigned int ty = vs->atype;
-            ZSlot r;
-            zsim(z, i1, i2, idf, ty == 1, r);
-            if (z.p->stats) {
-                const double e = fabs(static_cast<double>(z.tab[s].acc) - r.cc);
-                atomicMax(z.p->stats + 8, static_cast<unsigned long long>(__double_as_longlong(e)));
-            }
-            z.tab[s].cc = r.cc;
-            z.tab[s].euc = r.euc;
-            z.tab[s].nrm2 = r.nrm2;
-            z.tab[s].queued = 0;
-            __threadfence_block();
-            z.tab[s].xtype = ty;
-        }
+        if (work) zdo_exact(z, s);
         if (z.lane == 0) {
             zstat(z, 1, __popc(m));
             zstat(z, 2, 1);
@@ -820,6 +926,7 @@ __device__ void zexact(Z& z, int count, SL slot_of) {
         }
         zsync();
     }
+    if (qn) zdispatch(z, qn);
 }
 
 // A decision value: the memo slot it came from and whether it is the exact
@@ -1458,12 +1565,16 @@ __device__ void zwarp_setup(Z& z, const ZParams& P, int64_t w) {
     z.fpx = P.fpx + w * P.n * 32;
     z.pend = P.pend + w * kPendCap;
     z.stage1 = 0;
+    z.qw = static_cast<int>(threadIdx.x / 32);
+    z.cta_w = 0;
+    z.queue = nullptr;
+    z.ctl = nullptr;
     extern __shared__ float4 zsm[];
     if (P.smem_stage) {
         for (int i = threadIdx.x; i < 4 * P.n; i += blockDim.x) zsm[i] = P.su[i];
         __syncthreads();
         z.rfs = zsm;
-        z.q32 = reinterpret_cast<float2*>(zsm + 4 * P.n) + (threadIdx.x / 32) * P.n;
+        z.q32 = reinterpret_cast<float2*>(zsm + 4 * P.n) + z.qw * P.n;
     } else {
         z.rfs = P.su;
         z.q32 = P.q32 + w * P.n;
@@ -1515,11 +1626,35 @@ __device__ void zprior(const ZParams& P, int64_t prev, long long* b, long long& 
 // rows are co-resident (host check), so the spin-waits always finish.
 template <int BS>
 __global__ void __launch_bounds__(BS, 1) k_zoom_rows(const ZParams P) {
-    const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
+    // one row per block: warp 0 decides, all BS/32 warps evaluate (CTA mode);
+    // memo, queries and deferred list are the controller's (scratch index
+    // r * W), the FP64 fingerprint scratch is per warp
+    constexpr int W = BS / 32;
+    const int warp = static_cast<int>(threadIdx.x / 32);
+    const int64_t r = blockIdx.x;
     Z z;
-    zwarp_setup(z, P, w);
-    if (w >= P.nrows) return;
-    const int64_t r = w, k0 = P.row_start[r], k1 = P.row_start[r + 1];
+    zwarp_setup(z, P, r * W + warp);
+    const int64_t ctrl = r * W;
+    z.tab = P.tab + ctrl * (static_cast<int64_t>(P.cap_mask) + 1);
+    z.q = P.q + ctrl * 2 * P.n;
+    z.pend = P.pend + ctrl * kPendCap;
+    extern __shared__ float4 zsm[];
+    z.qw = 0;
+    if (P.smem_stage)
+        z.q32 = reinterpret_cast<float2*>(zsm + 4 * P.n);
+    else
+        z.q32 = P.q32 + ctrl * P.n;
+    if (W > 1) {
+        z.cta_w = W;
+        z.queue = reinterpret_cast<ZItem*>(reinterpret_cast<float2*>(zsm + 4 * P.n) + P.n);
+        z.ctl = reinterpret_cast<int*>(z.queue + kQCap);
+    }
+    if (r >= P.nrows) return;  // whole block
+    if (warp != 0) {
+        zhelper_loop(z);
+        return;
+    }
+    const int64_t k0 = P.row_start[r], k1 = P.row_start[r + 1];
     for (int64_t k = k0; k < k1; ++k) {
         const int64_t v = P.vox_list[k];
         const int64_t prev = k > k0 ? P.vox_list[k - 1] : (r > 0 ? P.vox_list[P.row_start[r - 1]] : -1);
@@ -1540,6 +1675,7 @@ __global__ void __launch_bounds__(BS, 1) k_zoom_rows(const ZParams P) {
         }
         __syncwarp();
     }
+    if (W > 1) zhelpers_release(z);
 }
 
 long long snap_index(double value, const mrfg_axis& ax) {  // zoom.cpp:407-409
@@ -1653,23 +1789,33 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     const bool rows = nrows > 0;
     // rows mode: one warp per block (a row's voxels are a latency chain: one
     // row per SM)
+    // rows mode: one row per block of row_w warps (warp 0 decides, all warps
+    // evaluate; MRFG_ZOOM_ROWW = 1, 4 or 8)
+    const char* rw_env = std::getenv("MRFG_ZOOM_ROWW");
+    const int row_w = rw_env ? (std::atoi(rw_env) >= 8 ? 8 : (std::atoi(rw_env) >= 4 ? 4 : 1)) : 8;
     void (*kern)(const ZParams) =
-        rows        ? k_zoom_rows<32>
+        rows        ? (row_w == 8 ? k_zoom_rows<256> : (row_w == 4 ? k_zoom_rows<128> : k_zoom_rows<32>))
         : bs == 512 ? k_zoom<512, 1>
         : bs == 256 ? (minb >= 2 ? k_zoom<256, 2> : k_zoom<256, 1>)
                     : (minb >= 6 ? k_zoom<128, 6> : (minb >= 4 ? k_zoom<128, 4> : k_zoom<128, 1>));
-    const int bsk = rows ? 32 : bs;
+    const int bsk = rows ? 32 * row_w : bs;
     // shared staging: StepU rows (64 B/step) + one FP32 query per warp (8 B/step)
-    size_t smem = (sizeof(StepU) + sizeof(float2) * (bsk / 32)) * c.n;
+    size_t smem = rows ? sizeof(StepU) * c.n + sizeof(float2) * c.n + sizeof(ZItem) * kQCap + 16
+                       : (sizeof(StepU) + sizeof(float2) * (bsk / 32)) * c.n;
     const char* st_env = std::getenv("MRFG_ZOOM_SMEM");
     P.smem_stage = smem <= 200 * 1024 && !(st_env && std::atoi(st_env) == 0) ? 1 : 0;
-    if (!P.smem_stage) smem = 0;
+    // rows mode keeps its shared layout (the helper-warp queue follows the
+    // staged rows) whether or not the kernel reads the staged copies
+    MRFG_REQUIRE(!rows || smem <= 200 * 1024, MRFG_E_INVALID,
+                 "quantify_slice: schedule too long for the neighbour-seeded kernel");
+    if (!P.smem_stage && !rows) smem = 0;
     MRFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
     MRFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bsk, smem));
     const int64_t resident = int64_t(std::max(per_sm, 1)) * c.num_sms * (bsk / 32);
-    MRFG_REQUIRE(!rows || nrows <= resident, MRFG_E_RUNTIME, "quantify_slice: more raster rows than resident warps");
-    const int64_t nwarps = rows ? nrows : std::min<int64_t>(resident, round_up(nvox, bs / 32));
+    MRFG_REQUIRE(!rows || nrows * row_w <= resident, MRFG_E_RUNTIME,
+                 "quantify_slice: more raster rows than resident blocks");
+    const int64_t nwarps = rows ? nrows * row_w : std::min<int64_t>(resident, round_up(nvox, bs / 32));
     // scratch: per-warp queries, fingerprints and memo tables; per-voxel
     // bounds/inits; error flag, stats, work counter
     const size_t qbytes = (sizeof(double) * 2 + sizeof(float) * 2) * c.n * nwarps;
