@@ -81,6 +81,7 @@ struct ZParams {
     long long init1, init2;  // snapped (not yet clamped) initial indices
     // speculation widths: 1-D flanks +-1..spec1d steps, 2-D (2*spec2d+1)^2 block
     long long spec1d, spec2d;
+    long long spec1d_cta, spec2d_cta;  // the same with helper warps (CTA mode)
     // certification margins: |FP32 value - FP64 value| < eps (CC), eps_euc
     // (Euclidean); eps < 0 = every evaluation in FP64 (no screening)
     double eps, eps_euc;
@@ -1234,7 +1235,7 @@ __device__ long long zoom_1d(Z& z, int axis, long long i1, long long i2, long lo
             b = axis == 0 ? i2 : v;
             c = idf;
         };
-        zensure(z, 2 * z.p->spec1d, pt);
+        zensure(z, 2 * (z.cta_w ? z.p->spec1d_cta : z.p->spec1d), pt);
         const long long xl = clampll(x - s, lo, hi);
         if (xl != x) {
             V fl = F(xl);
@@ -1295,7 +1296,7 @@ __device__ void zoom_2d_step(Z& z, long long idf, int metric, long long& x, long
             }
         }
         const long long cx = x, cy = y;
-        const long long r = z.p->spec2d, w = 2 * r + 1;  // (2r+1)^2 - 1 neighbours
+        const long long r = z.cta_w ? z.p->spec2d_cta : z.p->spec2d, w = 2 * r + 1;  // (2r+1)^2 - 1 neighbours
         zensure(z, w * w - 1, [&](long long k, long long& a, long long& b, long long& c) {
             const long long kk = k < (w * w) / 2 ? k : k + 1;  // skip the centre
             a = clampll(cx + (kk % w - r) * s1, lo1, hi1);
@@ -1760,6 +1761,10 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
         const char* e2 = std::getenv("MRFG_ZOOM_SPEC2D");
         P.spec1d = e1 ? std::max(1, std::atoi(e1)) : 16;
         P.spec2d = e2 ? std::max(1, std::atoi(e2)) : 2;
+        const char* c1 = std::getenv("MRFG_ZOOM_SPEC1D_CTA");
+        const char* c2 = std::getenv("MRFG_ZOOM_SPEC2D_CTA");
+        P.spec1d_cta = c1 ? std::max(1, std::atoi(c1)) : P.spec1d;
+        P.spec2d_cta = c2 ? std::max(1, std::atoi(c2)) : P.spec2d;
         const char* sm = std::getenv("MRFG_ZOOM_SCREEN");
         const std::string smode = sm ? sm : "";
         P.screen_mode = smode == "mufu" ? 1 : 0;
