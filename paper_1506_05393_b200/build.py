@@ -45,8 +45,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    shared = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "mrfg.h"), __file__]
+    hdr_t = max(os.path.getmtime(f) for f in shared)
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
+        objs.append(obj)
+        # per-object staleness (zoom.cu alone takes ~15 min in ptxas): only
+        # recompile a source newer than its object or when a shared header changed
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(
+                hdr_t, os.path.getmtime(os.path.join(CSRC, src))):
+            continue
         cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off",
                "-ccbin", "g++", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c",
                os.path.join(CSRC, src), "-o", obj]
@@ -56,7 +64,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-I", os.path.join(ROOT, "include"),
                    "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
-        objs.append(obj)
     failed = False
     for cmd, p in procs:
         out = p.communicate()[0].decode()

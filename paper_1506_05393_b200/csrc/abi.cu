@@ -691,7 +691,11 @@ int mrfg_screen_scores(mrfg_ctx* h, const mrfg_grid* grid, int64_t first, int64_
                      MRFG_E_INVALID, "screen_scores: bad shape");
         const GridTables& t = ensure_tables(c, *grid, false);
         const int64_t n = c.n, kp = k_pad_of(n), qrows = round_up(2 * nq, 256);
-        const int64_t rows = round_up(count, 256);
+        // use_simt bit 0: CUDA-core screening GEMM; bit 1: the production
+        // row producer (launch_bloch_rows, K1) instead of the table producer
+        const bool prod = (use_simt & 2) != 0;
+        const int64_t base = prod ? first / grid->df_hz.count * grid->df_hz.count : first;
+        const int64_t rows = round_up(first + count - base, 256);
         DevBuf raw, q64, qp, best, a, inv, cand, cnt;
         raw.ensure(sizeof(double) * 2 * n * nq);
         q64.ensure(sizeof(double) * 2 * n * nq);
@@ -708,7 +712,13 @@ int mrfg_screen_scores(mrfg_ctx* h, const mrfg_grid* grid, int64_t first, int64_
         MRFG_CUDA(cudaMemsetAsync(cnt.p, 0, 16, c.stream));
         launch_prepare_queries(c, raw.as<double>(), nq, qrows, q64.as<double>(), qp.as<__half>(), bad);
         fill(c, best.as<float>(), nq, -3.0f);
-        launch_bloch_operand(c, t, first, 1, first + count, rows, metric, a.as<__half>(), inv.as<float>());
+        if (prod) {
+            const int64_t b2 = launch_bloch_rows(c, t, first, first + count, metric, 0, rows, a.as<__half>(),
+                                                 nullptr, inv.as<float>());
+            MRFG_REQUIRE(b2 == base, MRFG_E_RUNTIME, "screen_scores: producer base mismatch");
+        } else {
+            launch_bloch_operand(c, t, first, 1, first + count, rows, metric, a.as<__half>(), inv.as<float>());
+        }
         MatchParams mp{};
         mp.a = a.as<__half>();
         mp.inv2 = inv.as<float>();
@@ -716,9 +726,10 @@ int mrfg_screen_scores(mrfg_ctx* h, const mrfg_grid* grid, int64_t first, int64_
         mp.atoms = rows;
         mp.q_rows = qrows;
         mp.k_pad = kp;
-        mp.valid_atoms = count;
+        mp.valid_atoms = first + count - base;
+        mp.valid_begin = first - base;
         mp.nvox = nq;
-        mp.flat_base = 0;
+        mp.flat_base = base - first;
         mp.flat_stride = 1;
         mp.best = best.as<float>();
         mp.cand = cand.as<CandRec>();
@@ -726,7 +737,7 @@ int mrfg_screen_scores(mrfg_ctx* h, const mrfg_grid* grid, int64_t first, int64_
         mp.cand_cap = cap;
         mp.delta = 1e30f;  // every (atom, voxel) pair becomes a candidate
         mp.metric = metric;
-        if (use_simt)
+        if (use_simt & 1)
             launch_match_simt(c, mp);
         else
             launch_match(c, mp);

@@ -293,12 +293,16 @@ class Context:
         return st
 
     def screen_scores(self, g: Grid, queries, first: int, count: int, metric="cc",
-                      use_simt: bool = False) -> np.ndarray:
-        """Dense K2 screening scores (count, nq) -- test support."""
+                      use_simt: bool = False, producer: str = "table") -> np.ndarray:
+        """Dense K2 screening scores (count, nq) -- test support.
+
+        producer "table": the per-atom table producer; "rows": the production
+        K1 row producer used by scan_grid (MRFG_K1 selects its variant)."""
         q = np.ascontiguousarray(np.atleast_2d(queries), dtype=np.complex128)
         out = np.empty((count, q.shape[0]), dtype=np.float32)
         check(self.lib.mrfg_screen_scores(self.h, C.byref(g), first, count, _dp(q.view(np.float64)),
-                                          q.shape[0], METRIC.get(metric, metric), int(use_simt),
+                                          q.shape[0], METRIC.get(metric, metric),
+                                          int(use_simt) | (2 if producer == "rows" else 0),
                                           out.ctypes.data_as(C.POINTER(C.c_float))))
         return out
 

@@ -70,15 +70,27 @@ def test_generate_fp64_bit_identical(ctx, sched, orc, grid_spec):
     assert np.array_equal(got, want)
 
 
-def test_generate_fp32_close(ctx, sched, orc):
+# K1 variants: the frame-folded producer (MRFG_K1=fold, 2/4/8 T2 rows per thread)
+# and the phasor-ladder row producer (default, MRFG_K1=rows)
+K1_VARIANTS = [("fold", "2"), ("fold", "4"), ("fold", "8"), ("rows", "4")]
+
+
+@pytest.mark.parametrize("k1,apt", K1_VARIANTS)
+def test_generate_fp32_close(ctx, sched, orc, monkeypatch, k1, apt):
+    monkeypatch.setenv("MRFG_K1", k1)
+    monkeypatch.setenv("MRFG_K1_APT", apt)
     g = P.grid((100, 20, 96), (20, 10, 29), (-50, 5, 21))
-    got = ctx.generate(g, 1000, 300, precision=32)
-    want = orc.generate(to_oracle_sched(sched), to_oracle_grid(g), 1000, 300)
+    # 29 T2 rows: partial pencils at every T1; the range starts mid-row
+    got = ctx.generate(g, 1000, 1300, precision=32)
+    want = orc.generate(to_oracle_sched(sched), to_oracle_grid(g), 1000, 1300)
     errs = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
     assert errs.max() < 1e-4
 
 
-def test_generate_n3000_fp32(orc):
+@pytest.mark.parametrize("k1,apt", K1_VARIANTS)
+def test_generate_n3000_fp32(orc, monkeypatch, k1, apt):
+    monkeypatch.setenv("MRFG_K1", k1)
+    monkeypatch.setenv("MRFG_K1_APT", apt)
     s = P.baseline_schedule(3000, 1)
     with P.Context(s) as c:
         g = P.grid((100, 25, 117), (20, 10, 49), (-100, 10, 21))

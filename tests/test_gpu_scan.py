@@ -60,6 +60,26 @@ def test_screen_close_to_exact_cc2(orc, small):
     assert np.abs(np.sqrt(a) - cc).max() < 1e-3
 
 
+@pytest.mark.parametrize("k1,apt", [("fold", "2"), ("fold", "4"), ("fold", "8"), ("rows", "4"), ("rows", "8")])
+def test_screen_production_producer(orc, small, monkeypatch, k1, apt):
+    """The GEMM operand of the production K1 (scan_grid's producer) screens
+    within fp16 rounding of the exact CC; ranges start and end mid-row and
+    cut T2 pencils."""
+    monkeypatch.setenv("MRFG_K1", k1)
+    monkeypatch.setenv("MRFG_K1_APT", apt)
+    first, count = 4999, 1777
+    with P.Context(small.schedule) as c:
+        a = c.screen_scores(small.grid, small.fps[:48], first, count, producer="rows")
+        b = c.screen_scores(small.grid, small.fps[:48], first, count)
+    ent = orc.generate(to_oracle_sched(small.schedule), to_oracle_grid(small.grid), first, count)
+    e = ent[:, 0::2] + 1j * ent[:, 1::2]
+    q = small.fps[:48] / np.linalg.norm(small.fps[:48], axis=1, keepdims=True)
+    cc = np.abs(e @ q.conj().T)
+    assert np.isfinite(a).all()
+    assert np.abs(np.sqrt(a) - cc).max() < 1e-3
+    assert np.abs(a - b).max() < 1e-3
+
+
 def test_scan_grid_config1_slice(small, small_ref):
     oflat, oscore, osecond = small_ref
     with P.Context(small.schedule) as c:
