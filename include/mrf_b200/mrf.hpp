@@ -58,6 +58,16 @@ double cc(const Fingerprint& a, const Fingerprint& b);                  // finge
 double euclidean(const Fingerprint& a, const Fingerprint& b);           // fingerprint.hpp:43
 Fingerprint add_noise(const Fingerprint& fp, double sigma, std::uint64_t seed);  // :47
 double estimate_pd(const Fingerprint& acquired, const Fingerprint& matched_ideal);  // :71
+double calibrate_noise(const Fingerprint& fp, double target_cc, std::uint64_t seed);  // :45-50
+struct CalibratedNoise {                                                // :52-61
+    double sigma = 0;
+    std::uint64_t seed = 0;
+    Fingerprint noisy;
+};
+CalibratedNoise make_calibrated_noise(const Fingerprint& fp, double target_cc, std::uint64_t seed);
+Fingerprint smooth(const Fingerprint& fp, int k);                       // :63-66
+void save_csv(const Fingerprint& fp, const std::filesystem::path& path);  // :73-74
+Fingerprint load_fingerprint_csv(const std::filesystem::path& path);
 
 // ------------------------------------------------------------- bloch.hpp:79-102
 class BlochSimulator {
@@ -120,6 +130,13 @@ struct Dictionary {
     }
 };
 Dictionary generate(const ParameterGrid& grid, const Schedule& sched, int workers = 1);  // :85
+// .mrfd files (dictionary.hpp:87-96): save / load / save_generated (GPU generation
+// streamed to disk; byte-identical to the reference's files).
+void save(const Dictionary& dict, const std::filesystem::path& path);
+Dictionary load(const std::filesystem::path& path);
+void save_generated(const ParameterGrid& grid, const Schedule& sched,
+                    const std::filesystem::path& path, int workers = 1,
+                    std::size_t chunk_entries = 1 << 15);
 enum class Metric { cc, euclidean };
 struct Match {
     TissueParams params;
@@ -139,6 +156,8 @@ ScanOutcome scan_grid(const ParameterGrid& grid, const Schedule& sched,
 void cc_map(const Fingerprint& fp, const ParameterGrid& grid, const Schedule& sched,
             const std::function<void(std::size_t first_flat, std::span<const float>)>& sink,
             int workers = 1, std::size_t chunk_entries = 1 << 15);        // :127-129
+void cc_map_to_file(const Fingerprint& fp, const ParameterGrid& grid, const Schedule& sched,
+                    const std::filesystem::path& path, int workers = 1);  // :130-132
 
 // -------------------------------------------------------------- zoom.hpp:17-178
 struct SearchRanges {

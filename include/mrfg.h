@@ -197,6 +197,49 @@ int mrfg_screen_scores(mrfg_ctx* ctx, const mrfg_grid* grid, int64_t first, int6
 int mrfg_cc_map(mrfg_ctx* ctx, const mrfg_grid* grid, const double* query, int64_t first,
                 int64_t count, float* out);
 
+/* cc_map with a precision choice: 64 = the reference pipeline in FP64
+ * (bit-identical float scores, = mrfg_cc_map); 32 = the fused FP32
+ * simulate-and-correlate row kernel (K1 OUT 3: |score - reference| ~1e-5,
+ * about 1000x the FP64 throughput). */
+int mrfg_cc_map_ex(mrfg_ctx* ctx, const mrfg_grid* grid, const double* query, int64_t first,
+                   int64_t count, int precision, float* out);
+
+/* -------------------------------------------------------- .mrfd / .mrfc files
+ * Layout (README.md:160-170, dictionary.cpp:62-112): little-endian magic
+ * "MRFD"/"MRFC", u32 version 1, 32-byte schedule digest (SHA-256 of the
+ * schedule CSV, dictionary.cpp:163-171 -- the caller supplies it), three axes
+ * as (f64 min, f64 step, u64 count), u64 entry length, then the payload:
+ * float32 (re, im) unit entries (MRFD) or float32 scores (MRFC) in flat order.
+ * I/O failures -> MRFG_E_RUNTIME (std::runtime_error in the reference). */
+/* save_generated (dictionary.hpp:94-96, dictionary.cpp:216-239): streams the
+ * GPU-generated dictionary to `path` (device generation overlaps the disk
+ * writes); precision 64 = bit-identical entries.  The payload does not depend
+ * on chunk_entries (> 0 required, as in the reference). */
+int mrfg_save_generated(mrfg_ctx* ctx, const mrfg_grid* grid, const uint8_t* digest,
+                        const char* path, int64_t chunk_entries, int precision);
+/* cc_map_to_file (dictionary.hpp:130-132, dictionary.cpp:333-347): the whole
+ * lattice's cc_map as an .mrfc file (entry length = schedule length). */
+int mrfg_cc_map_to_file(mrfg_ctx* ctx, const mrfg_grid* grid, const double* query,
+                        const uint8_t* digest, const char* path, int precision);
+/* write_header (dictionary.cpp:72-82): creates/truncates `path`; the caller
+ * appends the payload (save, dictionary.cpp:196-203). */
+int mrfg_write_header(const char* path, const char* magic, const mrfg_grid* grid,
+                      const uint8_t* digest, int64_t entry_len);
+/* read_header (dictionary.cpp:90-112) with its errors (bad magic, version,
+ * truncated header, degenerate dimensions); *payload_offset = header bytes. */
+int mrfg_read_header(const char* path, const char* magic, mrfg_grid* grid, uint8_t* digest,
+                     int64_t* entry_len, int64_t* payload_offset);
+
+/* ---------------------------------------------------------------- noise
+ * Host restatements (fingerprint.cpp:80-145): calibrate_noise
+ * (fingerprint.hpp:45-50), make_calibrated_noise (:52-61), smooth (:63-66).
+ * fp/out: n interleaved complex samples. */
+int mrfg_calibrate_noise(const double* fp, int64_t n, double target_cc, uint64_t seed,
+                         double* sigma);
+int mrfg_make_calibrated_noise(const double* fp, int64_t n, double target_cc, uint64_t seed,
+                               double* sigma, uint64_t* seed_used, double* noisy);
+int mrfg_smooth(const double* fp, int64_t n, int k, double* out);
+
 /* ----------------------------------------------------------- K5 MRF-ZOOM
  * quantify_impl per voxel (zoom.cpp:416-523) on a lattice (the finest
  * search pitch, zoom.hpp:17-21).  mrfg_quantify: independent voxels with full

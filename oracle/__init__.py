@@ -145,6 +145,14 @@ class Oracle:
                                          C.POINTER(ZoomCfg), dp, C.POINTER(C.c_uint8),
                                          C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(Quant)]
 
+        u64 = C.c_uint64
+        L.orc_calibrate_noise.argtypes = [dp, i64, C.c_double, u64, dp]
+        L.orc_make_calibrated_noise.argtypes = [dp, i64, C.c_double, u64, dp, C.POINTER(u64), dp]
+        L.orc_smooth.argtypes = [dp, i64, C.c_int, dp]
+        if which == "reference":
+            L.orc_ref_save_generated.argtypes = [C.POINTER(Sched), C.POINTER(Grid), C.c_char_p]
+            L.orc_ref_cc_map_to_file.argtypes = [C.POINTER(Sched), C.POINTER(Grid), dp, C.c_char_p]
+
     def _check(self, rc: int) -> None:
         if rc != 0:
             raise RuntimeError(f"{self.which} oracle: {self.lib.orc_last_error().decode()}")
@@ -186,6 +194,46 @@ class Oracle:
         a = np.ascontiguousarray(a, dtype=np.complex128)
         b = np.ascontiguousarray(b, dtype=np.complex128)
         return self.lib.orc_cc_unit(self._dp(a.view(np.float64)), self._dp(b.view(np.float64)), len(a))
+
+    def calibrate_noise(self, fp: np.ndarray, target: float, seed: int):
+        """-> sigma, or None when the reference throws runtime_error (code -3)."""
+        fp = np.ascontiguousarray(fp, dtype=np.complex128)
+        sg = C.c_double()
+        rc = self.lib.orc_calibrate_noise(self._dp(fp.view(np.float64)), len(fp), target, seed, C.byref(sg))
+        if rc == -3:
+            return None
+        self._check(rc)
+        return sg.value
+
+    def make_calibrated_noise(self, fp: np.ndarray, target: float, seed: int):
+        fp = np.ascontiguousarray(fp, dtype=np.complex128)
+        sg, used = C.c_double(), C.c_uint64()
+        out = np.zeros_like(fp)
+        rc = self.lib.orc_make_calibrated_noise(self._dp(fp.view(np.float64)), len(fp), target, seed,
+                                                C.byref(sg), C.byref(used), self._dp(out.view(np.float64)))
+        if rc == -3:
+            return None
+        self._check(rc)
+        return sg.value, used.value, out
+
+    def smooth(self, fp: np.ndarray, k: int) -> np.ndarray:
+        fp = np.ascontiguousarray(fp, dtype=np.complex128)
+        out = np.zeros_like(fp)
+        self._check(self.lib.orc_smooth(self._dp(fp.view(np.float64)), len(fp), k,
+                                        self._dp(out.view(np.float64))))
+        return out
+
+    def save_generated(self, s: Schedule, g: Grid, path: str) -> None:
+        """Reference library only: mrf::save_generated (dictionary.cpp:216-239)."""
+        cs = s.c()
+        self._check(self.lib.orc_ref_save_generated(C.byref(cs), C.byref(g), str(path).encode()))
+
+    def cc_map_to_file(self, s: Schedule, g: Grid, fp: np.ndarray, path: str) -> None:
+        """Reference library only: mrf::cc_map_to_file (dictionary.cpp:333-347)."""
+        fp = np.ascontiguousarray(fp, dtype=np.complex128)
+        cs = s.c()
+        self._check(self.lib.orc_ref_cc_map_to_file(C.byref(cs), C.byref(g), self._dp(fp.view(np.float64)),
+                                                    str(path).encode()))
 
     def generate(self, s: Schedule, g: Grid, first: int, count: int) -> np.ndarray:
         out = np.zeros((count, 2 * s.n), dtype=np.float32)

@@ -324,6 +324,61 @@ static void smooth(const double* v, int64_t n, int k, double* out) {
     }
 }
 
+int orc_smooth(const double* fp, int64_t n, int k, double* out) {
+    if (k != 3 && k != 5) return fail("smooth: kernel must be 3 or 5");
+    if (n == 0) return fail("smooth: empty input");
+    smooth(fp, n, k, out);
+    return 0;
+}
+/* fingerprint.cpp:80-105.  Returns 0 (sigma set), -1 invalid argument,
+ * -3 (runtime: cannot bracket / no sigma in 60 steps). */
+static int calibrate(const double* fp, int64_t n, double target, uint64_t seed, double* sigma) {
+    if (!(target > 0 && target < 1)) return fail("calibrate_noise: target must be in (0,1)");
+    double* noisy = malloc(sizeof(double) * 2 * (size_t)n);
+    int rc = -3;
+    double lo = 0, hi = norm2(fp, n) / sqrt((double)n);
+    orc_add_noise(fp, n, hi, seed, noisy);
+    double c = orc_cc(fp, noisy, n);
+    int done = 0;
+    for (int i = 0; i < 80 && c > target; ++i) {
+        if (fabs(c - target) <= 0.02) { *sigma = hi; rc = 0; done = 1; break; }
+        hi *= 2;
+        orc_add_noise(fp, n, hi, seed, noisy);
+        c = orc_cc(fp, noisy, n);
+    }
+    if (!done && c > target) {
+        fail("calibrate_noise: cannot bracket target");
+        done = 1;
+        rc = -3;
+    }
+    for (int i = 0; !done && i < 60; ++i) {
+        double mid = 0.5 * (lo + hi);
+        orc_add_noise(fp, n, mid, seed, noisy);
+        double cm = orc_cc(fp, noisy, n);
+        if (fabs(cm - target) <= 0.02) { *sigma = mid; rc = 0; done = 1; break; }
+        if (cm > target) lo = mid; else hi = mid;
+    }
+    if (!done) fail("calibrate_noise: no sigma within tolerance after 60 steps");
+    free(noisy);
+    return rc;
+}
+int orc_calibrate_noise(const double* fp, int64_t n, double target, uint64_t seed, double* sigma) {
+    return calibrate(fp, n, target, seed, sigma);
+}
+/* fingerprint.cpp:107-120 */
+int orc_make_calibrated_noise(const double* fp, int64_t n, double target, uint64_t seed,
+                              double* sigma, uint64_t* seed_used, double* noisy) {
+    for (int attempt = 0;; ++attempt) {
+        uint64_t s = attempt == 0 ? seed : rng_at(seed, 99, (uint64_t)attempt);
+        int rc = calibrate(fp, n, target, s, sigma);
+        if (rc == 0) {
+            *seed_used = s;
+            return orc_add_noise(fp, n, *sigma, s, noisy);
+        }
+        if (rc != -3 || attempt >= 7) return rc;
+    }
+}
+
 /* --------------------------------------------------------- dictionary.cpp */
 /* dictionary.hpp:22, 51-56: value(k) = min + k*step; params_at converts ms->s. */
 static double axis_value(const orc_axis* a, int64_t k) { return a->min + (double)k * a->step; }

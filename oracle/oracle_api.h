@@ -72,6 +72,15 @@ int orc_generate(const orc_sched* s, const orc_grid* g, int64_t first, int64_t c
 int orc_scan_grid(const orc_sched* s, const orc_grid* g, const double* queries, int64_t nq,
                   int metric, int threads, int64_t* best_flat, double* best_score,
                   double* second_score);
+/* fingerprint.cpp:80-145: calibrate_noise, make_calibrated_noise, smooth. */
+int orc_calibrate_noise(const double* fp, int64_t n, double target, uint64_t seed, double* sigma);
+int orc_make_calibrated_noise(const double* fp, int64_t n, double target, uint64_t seed,
+                              double* sigma, uint64_t* seed_used, double* noisy);
+int orc_smooth(const double* fp, int64_t n, int k, double* out);
+/* Reference library only (oracle/_ref): the file writers of dictionary.cpp. */
+int orc_ref_save_generated(const orc_sched* s, const orc_grid* g, const char* path);
+int orc_ref_cc_map_to_file(const orc_sched* s, const orc_grid* g, const double* fp,
+                           const char* path);
 int orc_quantify(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg* cfg,
                  const double* fp, orc_quant* out);
 int orc_quantify_slice(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg* cfg,

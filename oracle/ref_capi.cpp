@@ -179,6 +179,51 @@ double orc_cc_unit(const double* a, const double* b, int64_t n) {
     }
 }
 
+int orc_calibrate_noise(const double* fp, int64_t n, double target, uint64_t seed, double* sigma) {
+    try {
+        *sigma = mrf::calibrate_noise(to_fp(fp, n), target, seed);
+        return 0;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return -3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+int orc_make_calibrated_noise(const double* fp, int64_t n, double target, uint64_t seed,
+                              double* sigma, uint64_t* seed_used, double* noisy) {
+    try {
+        mrf::CalibratedNoise r = mrf::make_calibrated_noise(to_fp(fp, n), target, seed);
+        *sigma = r.sigma;
+        *seed_used = r.seed;
+        std::memcpy(noisy, r.noisy.s.data(), sizeof(double) * 2 * static_cast<std::size_t>(n));
+        return 0;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return -3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+int orc_smooth(const double* fp, int64_t n, int k, double* out) {
+    return guard([&] {
+        mrf::Fingerprint r = mrf::smooth(to_fp(fp, n), k);
+        std::memcpy(out, r.s.data(), sizeof(double) * 2 * static_cast<std::size_t>(n));
+    });
+}
+
+int orc_ref_save_generated(const orc_sched* s, const orc_grid* g, const char* path) {
+    return guard([&] { mrf::save_generated(to_grid(g), to_sched(s), path, 8); });
+}
+
+int orc_ref_cc_map_to_file(const orc_sched* s, const orc_grid* g, const double* fp, const char* path) {
+    return guard([&] { mrf::cc_map_to_file(to_fp(fp, s->n), to_grid(g), to_sched(s), path, 8); });
+}
+
 int orc_generate(const orc_sched* s, const orc_grid* g, int64_t first, int64_t count, float* out) {
     return guard([&] {
         // The reference materializes the whole lattice; generate() of a grid

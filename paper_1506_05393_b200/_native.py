@@ -73,7 +73,9 @@ EXPORTS = [
     "mrfg_generate_dev", "mrfg_bloch_norms_dev", "mrfg_scan_grid", "mrfg_scan_grid_dev",
     "mrfg_scan_dict", "mrfg_scan_dict_dev",
     "mrfg_merge_matches_dev", "mrfg_screen_scores", "mrfg_cc_map", "mrfg_quantify", "mrfg_quantify_slice", "mrfg_quantify_bounded",
-    "mrfg_quantify_dev",
+    "mrfg_quantify_dev", "mrfg_cc_map_ex", "mrfg_save_generated", "mrfg_cc_map_to_file",
+    "mrfg_write_header", "mrfg_read_header", "mrfg_calibrate_noise", "mrfg_make_calibrated_noise",
+    "mrfg_smooth",
 ]
 
 _lib = None
@@ -126,6 +128,15 @@ def load() -> C.CDLL:
     L.mrfg_screen_scores.argtypes = [vp, C.POINTER(Grid), i64, i64, dp, i64, C.c_int, C.c_int,
                                      C.POINTER(C.c_float)]
     L.mrfg_cc_map.argtypes = [vp, C.POINTER(Grid), dp, i64, i64, C.POINTER(C.c_float)]
+    L.mrfg_cc_map_ex.argtypes = [vp, C.POINTER(Grid), dp, i64, i64, C.c_int, C.POINTER(C.c_float)]
+    u8p, cp = C.POINTER(C.c_uint8), C.c_char_p
+    L.mrfg_save_generated.argtypes = [vp, C.POINTER(Grid), u8p, cp, i64, C.c_int]
+    L.mrfg_cc_map_to_file.argtypes = [vp, C.POINTER(Grid), dp, u8p, cp, C.c_int]
+    L.mrfg_write_header.argtypes = [cp, cp, C.POINTER(Grid), u8p, i64]
+    L.mrfg_read_header.argtypes = [cp, cp, C.POINTER(Grid), u8p, C.POINTER(i64), C.POINTER(i64)]
+    L.mrfg_calibrate_noise.argtypes = [dp, i64, C.c_double, u64, dp]
+    L.mrfg_make_calibrated_noise.argtypes = [dp, i64, C.c_double, u64, dp, C.POINTER(u64), dp]
+    L.mrfg_smooth.argtypes = [dp, i64, C.c_int, dp]
     L.mrfg_quantify.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp, i64,
                                 C.POINTER(Quant)]
     L.mrfg_quantify_dev.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), vp, i64, vp]

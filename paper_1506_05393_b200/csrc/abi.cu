@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "mrfg_internal.cuh"
@@ -754,37 +755,313 @@ int mrfg_screen_scores(mrfg_ctx* h, const mrfg_grid* grid, int64_t first, int64_
     });
 }
 
+}  // extern "C"
+
+namespace mrfg {
+// cc_map over flats [first, first+count), results delivered in pieces of at
+// most `per` scores to sink(offset, device pointer, k) on the ctx stream.
+// precision 64: the reference pipeline in FP64 (bit-identical float scores);
+// 32: the fused FP32 simulate-and-correlate row kernel (K1 OUT 3).
+template <class Sink>
+static void cc_map_run(Ctx& c, const mrfg_grid* grid, const double* query, int64_t first, int64_t count,
+                       int precision, Sink&& sink) {
+    MRFG_REQUIRE(precision == 32 || precision == 64, MRFG_E_INVALID, "cc_map: precision must be 32 or 64");
+    MRFG_REQUIRE(first >= 0 && count >= 0 && first + count <= grid_total(*grid), MRFG_E_INVALID,
+                 "cc_map: flat range outside the grid");
+    const GridTables& t = ensure_tables(c, *grid, precision == 64);
+    const int64_t kp = k_pad_of(c.n);
+    DevBuf raw, q64, qp, flag, res, q32;
+    raw.ensure(sizeof(double) * 2 * c.n);
+    q64.ensure(sizeof(double) * 2 * c.n);
+    qp.ensure(sizeof(__half) * 256 * kp);
+    flag.ensure(sizeof(int));
+    const int64_t per = int64_t(1) << 24;
+    res.ensure(sizeof(float) * std::min(per, std::max<int64_t>(count, 1)));
+    MRFG_CUDA(cudaMemcpyAsync(raw.p, query, sizeof(double) * 2 * c.n, cudaMemcpyHostToDevice, c.stream));
+    MRFG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), c.stream));
+    launch_prepare_queries(c, raw.as<double>(), 1, 256, q64.as<double>(), qp.as<__half>(), flag.as<int>());
+    int bad = 0;
+    MRFG_CUDA(cudaMemcpyAsync(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    MRFG_REQUIRE(!bad, MRFG_E_INVALID, "normalize: zero fingerprint");
+    if (precision == 32) {  // the FP64 unit query (prep_query) rounded to FP32
+        std::vector<double> h64(2 * c.n);
+        MRFG_CUDA(cudaMemcpy(h64.data(), q64.p, sizeof(double) * 2 * c.n, cudaMemcpyDeviceToHost));
+        std::vector<float> h32(h64.begin(), h64.end());
+        q32.ensure(sizeof(float) * 2 * c.n);
+        MRFG_CUDA(cudaMemcpyAsync(q32.p, h32.data(), sizeof(float) * 2 * c.n, cudaMemcpyHostToDevice, c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    for (int64_t f = 0; f < count; f += per) {
+        const int64_t k = std::min(per, count - f);
+        if (precision == 64)
+            launch_cc_map(c, t, q64.as<double>(), first + f, k, res.as<float>());
+        else
+            launch_bloch_rows(c, t, first + f, first + f + k, MRFG_METRIC_CC, 3, k, nullptr, nullptr,
+                              res.as<float>(), q32.as<float2>());
+        MRFG_CUDA(cudaGetLastError());
+        sink(f, res.as<float>(), k);
+    }
+    for (DevBuf* b : {&raw, &q64, &qp, &flag, &res, &q32}) b->release();
+}
+
+// .mrfd / .mrfc header (dictionary.cpp:62-112): magic, u32 version 1, 32-byte
+// schedule digest, 3 x (f64 min, f64 step, u64 count), u64 entry length.
+static void write_header(FILE* f, const char magic[4], const uint8_t digest[32], const mrfg_grid& g,
+                         uint64_t entry_len) {
+    const uint32_t version = 1;
+    bool ok = fwrite(magic, 1, 4, f) == 4 && fwrite(&version, 4, 1, f) == 1 && fwrite(digest, 1, 32, f) == 32;
+    for (const mrfg_axis* ax : {&g.t1_ms, &g.t2_ms, &g.df_hz}) {
+        const uint64_t cnt = static_cast<uint64_t>(ax->count);
+        ok = ok && fwrite(&ax->min, 8, 1, f) == 1 && fwrite(&ax->step, 8, 1, f) == 1 && fwrite(&cnt, 8, 1, f) == 1;
+    }
+    ok = ok && fwrite(&entry_len, 8, 1, f) == 1;
+    MRFG_REQUIRE(ok, MRFG_E_RUNTIME, "write failed");
+}
+
+struct FileCloser {
+    FILE* f;
+    ~FileCloser() {
+        if (f) fclose(f);
+    }
+};
+
+// Payload writer overlapping the device with the disk: piece i is copied to
+// pinned buffer i % 2 on the stream while a host thread writes piece i - 1.
+struct PipelinedWriter {
+    FILE* f;
+    Ctx& c;
+    void* pin[2] = {nullptr, nullptr};
+    size_t cap = 0;
+    int cur = 0;
+    std::thread th;
+    bool failed = false;
+    PipelinedWriter(FILE* f_, Ctx& c_, size_t bytes) : f(f_), c(c_), cap(bytes) {
+        MRFG_CUDA(cudaMallocHost(&pin[0], bytes));
+        MRFG_CUDA(cudaMallocHost(&pin[1], bytes));
+    }
+    void put(const void* d_src, size_t bytes) {
+        MRFG_CUDA(cudaMemcpyAsync(pin[cur], d_src, bytes, cudaMemcpyDeviceToHost, c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        join();
+        void* buf = pin[cur];
+        th = std::thread([this, buf, bytes] { failed |= fwrite(buf, 1, bytes, f) != bytes; });
+        cur ^= 1;
+    }
+    void join() {
+        if (th.joinable()) th.join();
+    }
+    ~PipelinedWriter() {
+        join();
+        for (void* p : pin)
+            if (p) cudaFreeHost(p);
+    }
+};
+}  // namespace mrfg
+
+extern "C" {
+
 int mrfg_cc_map(mrfg_ctx* h, const mrfg_grid* grid, const double* query, int64_t first,
                 int64_t count, float* out) {
+    return mrfg_cc_map_ex(h, grid, query, first, count, 64, out);
+}
+
+int mrfg_cc_map_ex(mrfg_ctx* h, const mrfg_grid* grid, const double* query, int64_t first,
+                   int64_t count, int precision, float* out) {
     return guard([&] {
         Ctx& c = h->c;
         MRFG_CUDA(cudaSetDevice(c.device));
-        MRFG_REQUIRE(first >= 0 && count >= 0 && first + count <= grid_total(*grid), MRFG_E_INVALID,
-                     "cc_map: flat range outside the grid");
-        const GridTables& t = ensure_tables(c, *grid, true);
-        const int64_t kp = k_pad_of(c.n);
-        DevBuf raw, q64, qp, flag, res;
-        raw.ensure(sizeof(double) * 2 * c.n);
-        q64.ensure(sizeof(double) * 2 * c.n);
-        qp.ensure(sizeof(__half) * 256 * kp);
-        flag.ensure(sizeof(int));
-        const int64_t per = int64_t(1) << 24;
-        res.ensure(sizeof(float) * std::min(per, std::max<int64_t>(count, 1)));
-        MRFG_CUDA(cudaMemcpyAsync(raw.p, query, sizeof(double) * 2 * c.n, cudaMemcpyHostToDevice, c.stream));
-        MRFG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), c.stream));
-        launch_prepare_queries(c, raw.as<double>(), 1, 256, q64.as<double>(), qp.as<__half>(),
-                               flag.as<int>());
-        int bad = 0;
-        MRFG_CUDA(cudaMemcpyAsync(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-        MRFG_CUDA(cudaStreamSynchronize(c.stream));
-        MRFG_REQUIRE(!bad, MRFG_E_INVALID, "normalize: zero fingerprint");
-        for (int64_t f = 0; f < count; f += per) {
-            int64_t k = std::min(per, count - f);
-            launch_cc_map(c, t, q64.as<double>(), first + f, k, res.as<float>());
-            MRFG_CUDA(cudaMemcpyAsync(out + f, res.p, sizeof(float) * k, cudaMemcpyDeviceToHost, c.stream));
+        cc_map_run(c, grid, query, first, count, precision, [&](int64_t f, const float* d, int64_t k) {
+            MRFG_CUDA(cudaMemcpyAsync(out + f, d, sizeof(float) * k, cudaMemcpyDeviceToHost, c.stream));
             MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        });
+    });
+}
+
+int mrfg_cc_map_to_file(mrfg_ctx* h, const mrfg_grid* grid, const double* query, const uint8_t* digest,
+                        const char* path, int precision) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        check_grid(*grid);
+        FileCloser fc{fopen(path, "wb")};
+        MRFG_REQUIRE(fc.f, MRFG_E_RUNTIME, std::string("cannot open for write: ") + path);
+        write_header(fc.f, "MRFC", digest, *grid, static_cast<uint64_t>(c.n));
+        {
+            PipelinedWriter w(fc.f, c, sizeof(float) * (size_t(1) << 24));
+            cc_map_run(c, grid, query, 0, grid_total(*grid), precision,
+                       [&](int64_t, const float* d, int64_t k) { w.put(d, sizeof(float) * k); });
+            w.join();
+            MRFG_REQUIRE(!w.failed, MRFG_E_RUNTIME, std::string("write failed: ") + path);
         }
-        for (DevBuf* b : {&raw, &q64, &qp, &flag, &res}) b->release();
+        MRFG_REQUIRE(fflush(fc.f) == 0, MRFG_E_RUNTIME, std::string("write failed: ") + path);
+    });
+}
+
+int mrfg_save_generated(mrfg_ctx* h, const mrfg_grid* grid, const uint8_t* digest, const char* path,
+                        int64_t chunk_entries, int precision) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE(chunk_entries > 0, MRFG_E_INVALID, "chunk_entries must be > 0");
+        MRFG_REQUIRE(precision == 32 || precision == 64, MRFG_E_INVALID, "generate: precision must be 32 or 64");
+        check_grid(*grid);
+        FileCloser fc{fopen(path, "wb")};
+        MRFG_REQUIRE(fc.f, MRFG_E_RUNTIME, std::string("cannot open for write: ") + path);
+        write_header(fc.f, "MRFD", digest, *grid, static_cast<uint64_t>(c.n));
+        const GridTables& t = ensure_tables(c, *grid, precision == 64);
+        // the payload does not depend on chunk_entries (bit-identical entries);
+        // device pieces of <= 256 MB keep the disk busy while the GPU generates
+        const int64_t total = grid_total(*grid);
+        const int64_t per = std::max<int64_t>(1, (int64_t(256) << 20) / (8 * c.n));
+        const size_t piece = sizeof(float) * 2 * c.n * std::min(per, std::max<int64_t>(total, 1));
+        DevBuf dev[2];
+        dev[0].ensure(piece);
+        dev[1].ensure(piece);
+        {
+            PipelinedWriter w(fc.f, c, piece);
+            int b = 0;
+            for (int64_t f = 0; f < total; f += per, b ^= 1) {
+                const int64_t k = std::min(per, total - f);
+                launch_generate(c, t, f, k, precision, dev[b].as<float>());
+                MRFG_CUDA(cudaGetLastError());
+                w.put(dev[b].p, sizeof(float) * 2 * c.n * k);
+            }
+            w.join();
+            MRFG_REQUIRE(!w.failed, MRFG_E_RUNTIME, std::string("write failed: ") + path);
+        }
+        MRFG_REQUIRE(fflush(fc.f) == 0, MRFG_E_RUNTIME, std::string("write failed: ") + path);
+    });
+}
+
+// ---------------------------------------------------------------- noise
+// Host restatements of the Experiment-4 noise tooling (fingerprint.cpp:80-145),
+// operand order identical to the reference (bit-identical sigma / output).
+namespace {
+double fp_norm2(const double* v, int64_t n) {  // fingerprint.cpp:14-18
+    double acc = 0;
+    for (int64_t j = 0; j < n; ++j) acc += v[2 * j] * v[2 * j] + v[2 * j + 1] * v[2 * j + 1];
+    return std::sqrt(acc);
+}
+double fp_cc(const double* a, const double* b, int64_t n) {  // fingerprint.cpp:39-55 (not unit)
+    double re = 0, im = 0;
+    for (int64_t j = 0; j < n; ++j) {
+        re += a[2 * j] * b[2 * j] + a[2 * j + 1] * b[2 * j + 1];
+        im += a[2 * j + 1] * b[2 * j] - a[2 * j] * b[2 * j + 1];
+    }
+    double num = std::sqrt(re * re + im * im);
+    const double na = fp_norm2(a, n), nb = fp_norm2(b, n);
+    MRFG_REQUIRE(na != 0 && nb != 0, MRFG_E_INVALID, "cc: zero fingerprint");
+    num /= na * nb;
+    return num < 1.0 ? num : 1.0;
+}
+struct CalibrateFail {};
+double calibrate(const double* fp, int64_t n, double target, uint64_t seed) {  // fingerprint.cpp:80-105
+    MRFG_REQUIRE(target > 0 && target < 1, MRFG_E_INVALID, "calibrate_noise: target must be in (0,1)");
+    MRFG_REQUIRE(n > 0, MRFG_E_INVALID, "cc: empty input");
+    std::vector<double> noisy(2 * n);
+    auto cc_at = [&](double sigma) {
+        mrfg_add_noise(fp, n, sigma, seed, noisy.data());
+        return fp_cc(fp, noisy.data(), n);
+    };
+    double lo = 0;
+    double hi = fp_norm2(fp, n) / std::sqrt(static_cast<double>(n));
+    double c = cc_at(hi);
+    for (int i = 0; i < 80 && c > target; ++i) {
+        if (std::abs(c - target) <= 0.02) return hi;
+        hi *= 2;
+        c = cc_at(hi);
+    }
+    if (c > target) throw Error{MRFG_E_RUNTIME, "calibrate_noise: cannot bracket target"};
+    for (int i = 0; i < 60; ++i) {
+        double mid = 0.5 * (lo + hi);
+        double cm = cc_at(mid);
+        if (std::abs(cm - target) <= 0.02) return mid;
+        (cm > target ? lo : hi) = mid;
+    }
+    throw Error{MRFG_E_RUNTIME, "calibrate_noise: no sigma within tolerance after 60 steps"};
+}
+}  // namespace
+
+int mrfg_calibrate_noise(const double* fp, int64_t n, double target_cc, uint64_t seed, double* sigma) {
+    return guard([&] { *sigma = calibrate(fp, n, target_cc, seed); });
+}
+
+int mrfg_make_calibrated_noise(const double* fp, int64_t n, double target_cc, uint64_t seed,
+                               double* sigma, uint64_t* seed_used, double* noisy) {
+    return guard([&] {  // fingerprint.cpp:107-120: up to 8 deterministic realizations
+        for (int attempt = 0;; ++attempt) {
+            const uint64_t sd = attempt == 0 ? seed : mrfg_rng_at(seed, 99, attempt);
+            try {
+                const double sg = calibrate(fp, n, target_cc, sd);
+                *sigma = sg;
+                *seed_used = sd;
+                mrfg_add_noise(fp, n, sg, sd, noisy);
+                return;
+            } catch (const Error& e) {
+                if (e.code != MRFG_E_RUNTIME || attempt >= 7) throw;
+            }
+        }
+    });
+}
+
+int mrfg_smooth(const double* fp, int64_t n, int k, double* out) {
+    return guard([&] {  // fingerprint.cpp:122-145
+        MRFG_REQUIRE(k == 3 || k == 5, MRFG_E_INVALID, "smooth: kernel must be 3 or 5");
+        MRFG_REQUIRE(n > 0, MRFG_E_INVALID, "smooth: empty input");
+        const double sigma = (k == 3) ? 0.85 : 1.0;
+        const int hh = k / 2;
+        double w[5];
+        for (int j = -hh; j <= hh; ++j) w[j + hh] = std::exp(-0.5 * j * j / (sigma * sigma));
+        for (int64_t i = 0; i < n; ++i) {
+            double re = 0, im = 0, wsum = 0;
+            for (int j = -hh; j <= hh; ++j) {
+                const int64_t t = i + j;
+                if (t < 0 || t >= n) continue;
+                re += w[j + hh] * fp[2 * t];
+                im += w[j + hh] * fp[2 * t + 1];
+                wsum += w[j + hh];
+            }
+            out[2 * i] = re / wsum;
+            out[2 * i + 1] = im / wsum;
+        }
+    });
+}
+
+int mrfg_write_header(const char* path, const char* magic, const mrfg_grid* grid, const uint8_t* digest,
+                      int64_t entry_len) {
+    return guard([&] {
+        FileCloser fc{fopen(path, "wb")};
+        MRFG_REQUIRE(fc.f, MRFG_E_RUNTIME, std::string("cannot open for write: ") + path);
+        write_header(fc.f, magic, digest, *grid, static_cast<uint64_t>(entry_len));
+    });
+}
+
+int mrfg_read_header(const char* path, const char* magic, mrfg_grid* grid, uint8_t* digest,
+                     int64_t* entry_len, int64_t* payload_offset) {
+    return guard([&] {
+        FileCloser fc{fopen(path, "rb")};
+        MRFG_REQUIRE(fc.f, MRFG_E_RUNTIME, std::string("cannot open: ") + path);
+        char m[4];
+        uint32_t version = 0;
+        MRFG_REQUIRE(fread(m, 1, 4, fc.f) == 4 && std::memcmp(m, magic, 4) == 0, MRFG_E_RUNTIME,
+                     std::string("bad magic in ") + path);
+        MRFG_REQUIRE(fread(&version, 4, 1, fc.f) == 1 && version == 1, MRFG_E_RUNTIME,
+                     std::string("unsupported version in ") + path);
+        bool ok = fread(digest, 1, 32, fc.f) == 32;
+        for (mrfg_axis* ax : {&grid->t1_ms, &grid->t2_ms, &grid->df_hz}) {
+            uint64_t cnt = 0;
+            ok = ok && fread(&ax->min, 8, 1, fc.f) == 1 && fread(&ax->step, 8, 1, fc.f) == 1 &&
+                 fread(&cnt, 8, 1, fc.f) == 1;
+            ax->count = static_cast<int64_t>(cnt);
+        }
+        uint64_t el = 0;
+        ok = ok && fread(&el, 8, 1, fc.f) == 1;
+        MRFG_REQUIRE(ok, MRFG_E_RUNTIME, std::string("truncated header in ") + path);
+        MRFG_REQUIRE(grid_total(*grid) != 0 && el != 0, MRFG_E_RUNTIME,
+                     std::string("degenerate dimensions in ") + path);
+        *entry_len = static_cast<int64_t>(el);
+        if (payload_offset) *payload_offset = ftell(fc.f);
     });
 }
 

@@ -301,6 +301,60 @@ Fingerprint add_noise(const Fingerprint& fp, double sigma, std::uint64_t seed) {
     return out;
 }
 
+double calibrate_noise(const Fingerprint& fp, double target_cc, std::uint64_t seed) {
+    double sigma = 0;
+    check(mrfg_calibrate_noise(interleaved(fp), static_cast<int64_t>(fp.size()), target_cc, seed, &sigma));
+    return sigma;
+}
+
+CalibratedNoise make_calibrated_noise(const Fingerprint& fp, double target_cc, std::uint64_t seed) {
+    CalibratedNoise r;
+    r.noisy.s.resize(fp.size());
+    uint64_t used = 0;
+    check(mrfg_make_calibrated_noise(interleaved(fp), static_cast<int64_t>(fp.size()), target_cc, seed,
+                                     &r.sigma, &used, reinterpret_cast<double*>(r.noisy.s.data())));
+    r.seed = used;
+    return r;
+}
+
+Fingerprint smooth(const Fingerprint& fp, int k) {
+    Fingerprint out;
+    out.s.resize(fp.size());
+    check(mrfg_smooth(interleaved(fp), static_cast<int64_t>(fp.size()), k,
+                      reinterpret_cast<double*>(out.s.data())));
+    return out;
+}
+
+void save_csv(const Fingerprint& fp, const std::filesystem::path& path) {  // fingerprint.cpp:154-161
+    std::ofstream f(path, std::ios::binary);
+    if (!f) throw std::runtime_error("cannot open for write: " + path.string());
+    f << "idx,re,im\n";
+    for (std::size_t j = 0; j < fp.size(); ++j)
+        f << j << ',' << g9(fp.s[j].real()) << ',' << g9(fp.s[j].imag()) << '\n';
+    if (!f) throw std::runtime_error("write failed: " + path.string());
+}
+
+Fingerprint load_fingerprint_csv(const std::filesystem::path& path) {  // fingerprint.cpp:163-183
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw std::runtime_error("cannot open fingerprint: " + path.string());
+    std::string line;
+    if (!std::getline(f, line) || split_csv(line) != std::vector<std::string>{"idx", "re", "im"})
+        throw std::runtime_error("bad fingerprint header in " + path.string());
+    Fingerprint fp;
+    std::size_t expect = 0;
+    while (std::getline(f, line)) {
+        if (line.empty()) continue;
+        auto cols = split_csv(line);
+        if (cols.size() != 3) throw std::runtime_error("bad fingerprint row in " + path.string());
+        if (static_cast<std::size_t>(parse_num(cols[0])) != expect)
+            throw std::runtime_error("non-sequential idx in " + path.string());
+        fp.s.emplace_back(parse_num(cols[1]), parse_num(cols[2]));
+        ++expect;
+    }
+    if (fp.size() == 0) throw std::runtime_error("empty fingerprint: " + path.string());
+    return fp;
+}
+
 double estimate_pd(const Fingerprint& acquired, const Fingerprint& matched_ideal) {
     if (acquired.size() != matched_ideal.size()) throw std::invalid_argument("estimate_pd: length mismatch");
     if (acquired.size() == 0) throw std::invalid_argument("estimate_pd: empty input");
@@ -391,6 +445,43 @@ Dictionary generate(const ParameterGrid& grid, const Schedule& sched, int) {
     return d;
 }
 
+void save(const Dictionary& dict, const std::filesystem::path& path) {  // dictionary.cpp:196-203
+    const mrfg_grid g = to_grid(dict.grid);
+    check(mrfg_write_header(path.c_str(), "MRFD", &g, dict.digest.data(), static_cast<int64_t>(dict.entry_len)));
+    std::ofstream f(path, std::ios::binary | std::ios::app);
+    if (!f) throw std::runtime_error("cannot open for write: " + path.string());
+    f.write(reinterpret_cast<const char*>(dict.data.data()),
+            static_cast<std::streamsize>(dict.data.size() * sizeof(float)));
+    if (!f) throw std::runtime_error("write failed: " + path.string());
+}
+
+Dictionary load(const std::filesystem::path& path) {  // dictionary.cpp:205-220
+    mrfg_grid g{};
+    Dictionary d;
+    int64_t el = 0, off = 0;
+    check(mrfg_read_header(path.c_str(), "MRFD", &g, d.digest.data(), &el, &off));
+    auto axis = [](const mrfg_axis& a) { return AxisSpec{a.min, a.step, static_cast<std::size_t>(a.count)}; };
+    d.grid = {axis(g.t1_ms), axis(g.t2_ms), axis(g.df_hz)};
+    d.entry_len = static_cast<std::size_t>(el);
+    d.data.resize(d.grid.total() * 2 * d.entry_len);
+    std::ifstream f(path, std::ios::binary);
+    f.seekg(off);
+    f.read(reinterpret_cast<char*>(d.data.data()), static_cast<std::streamsize>(d.data.size() * sizeof(float)));
+    if (f.gcount() != static_cast<std::streamsize>(d.data.size() * sizeof(float)))
+        throw std::runtime_error("truncated payload in " + path.string());
+    return d;
+}
+
+void save_generated(const ParameterGrid& grid, const Schedule& sched, const std::filesystem::path& path,
+                    int, std::size_t chunk_entries) {  // dictionary.cpp:216-239
+    if (chunk_entries == 0) throw std::invalid_argument("chunk_entries must be > 0");
+    if (sched.size() == 0) throw std::invalid_argument("generate: empty schedule");
+    CtxGuard c{create(sched)};
+    const mrfg_grid g = to_grid(grid);
+    const Digest dg = schedule_digest(sched);
+    check(mrfg_save_generated(c.h, &g, dg.data(), path.c_str(), static_cast<int64_t>(chunk_entries), 64));
+}
+
 Match brute_force_search(const Fingerprint& fp, const Dictionary& dict, Metric metric) {
     if (fp.size() != dict.entry_len)
         throw std::invalid_argument("query length does not match dictionary entries");
@@ -447,6 +538,16 @@ void cc_map(const Fingerprint& fp, const ParameterGrid& grid, const Schedule& sc
                           static_cast<int64_t>(end - begin), scores.data()));
         sink(begin, {scores.data(), scores.size()});
     }
+}
+
+void cc_map_to_file(const Fingerprint& fp, const ParameterGrid& grid, const Schedule& sched,
+                    const std::filesystem::path& path, int) {  // dictionary.cpp:333-347
+    if (fp.size() != sched.size())
+        throw std::invalid_argument("query length does not match dictionary entries");
+    CtxGuard c{create(sched)};
+    const mrfg_grid g = to_grid(grid);
+    const Digest dg = schedule_digest(sched);
+    check(mrfg_cc_map_to_file(c.h, &g, interleaved(fp), dg.data(), path.c_str(), 64));
 }
 
 // ---------------------------------------------------------------------- zoom

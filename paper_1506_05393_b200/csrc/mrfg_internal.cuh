@@ -127,10 +127,12 @@ void launch_bloch_operand(Ctx& c, const GridTables& t, int64_t first, int64_t st
                           int64_t valid_end, int64_t rows, int metric, __half* d_a,
                           float* d_inv2);
 // Row-tiled K1 over flats [vb, ve) (out 0: fp16 operand + inv; 1: raw float
-// entries; 2: |s|^2).  Returns base_flat (operand row = flat - base_flat);
+// entries; 2: |s|^2; 3: FP32 cc_map score against the unit query d_q32 into
+// d_inv2[flat - vb]).  Returns base_flat (operand row = flat - base_flat);
 // for out 0 the buffer rows outside the range, up to `rows`, are zeroed.
 int64_t launch_bloch_rows(Ctx& c, const GridTables& t, int64_t vb, int64_t ve, int metric, int out,
-                          int64_t rows, __half* d_a, float* d_outf, float* d_inv2);
+                          int64_t rows, __half* d_a, float* d_outf, float* d_inv2,
+                          const float2* d_q32 = nullptr);
 void launch_bloch_norms(Ctx& c, const GridTables& t, int64_t first, int64_t count, float* d_norm2);
 
 // K2 (match_sm100.cu)

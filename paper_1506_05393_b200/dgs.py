@@ -13,9 +13,14 @@ BlochSimulator::simulate   Context.simulate (precision 64 or 32)
 generate                   Context.generate
 scan_grid                  Context.scan_grid (+ scan_grid_device)
 brute_force_search         Context.brute_force_search
-cc_map                     Context.cc_map
+cc_map                     Context.cc_map (precision 64 exact / 32 fused FP32)
+cc_map_to_file             Context.cc_map_to_file (.mrfc)
+save_generated             Context.save_generated (.mrfd, GPU-generated)
+save / load (Dictionary)   save_dictionary / load_dictionary / read_header
 quantify / quantify_slice  Context.quantify / Context.quantify_slice
 add_noise / rng            add_noise / rng_at / uniform01 / gaussian
+calibrate_noise            calibrate_noise / make_calibrated_noise
+smooth                     smooth
 =========================  ===============================================
 """
 from __future__ import annotations
@@ -145,6 +150,82 @@ def add_noise(fp: np.ndarray, sigma: float, seed: int) -> np.ndarray:
     check(N.load().mrfg_add_noise(_dp(fp.view(np.float64)), len(fp), sigma, seed,
                                   _dp(out.view(np.float64))))
     return out
+
+
+def calibrate_noise(fp: np.ndarray, target_cc: float, seed: int) -> float:
+    """calibrate_noise (fingerprint.cpp:80-105): sigma with cc(fp, noisy) within 0.02 of target."""
+    fp = np.ascontiguousarray(fp, dtype=np.complex128)
+    sigma = C.c_double()
+    check(N.load().mrfg_calibrate_noise(_dp(fp.view(np.float64)), len(fp), target_cc, seed,
+                                        C.byref(sigma)))
+    return sigma.value
+
+
+def make_calibrated_noise(fp: np.ndarray, target_cc: float, seed: int):
+    """make_calibrated_noise (fingerprint.cpp:107-120) -> (sigma, seed_used, noisy)."""
+    fp = np.ascontiguousarray(fp, dtype=np.complex128)
+    sigma, used = C.c_double(), C.c_uint64()
+    out = np.empty_like(fp)
+    check(N.load().mrfg_make_calibrated_noise(_dp(fp.view(np.float64)), len(fp), target_cc, seed,
+                                              C.byref(sigma), C.byref(used), _dp(out.view(np.float64))))
+    return sigma.value, used.value, out
+
+
+def smooth(fp: np.ndarray, k: int) -> np.ndarray:
+    """smooth (fingerprint.cpp:122-145): Gaussian k = 3 / 5 taps, edge-truncated."""
+    fp = np.ascontiguousarray(fp, dtype=np.complex128)
+    out = np.empty_like(fp)
+    check(N.load().mrfg_smooth(_dp(fp.view(np.float64)), len(fp), k, _dp(out.view(np.float64))))
+    return out
+
+
+MAGIC_DICT, MAGIC_MAP = b"MRFD", b"MRFC"
+
+
+def _digest_bytes(digest) -> "C.Array":
+    d = bytes.fromhex(digest) if isinstance(digest, str) else bytes(digest)
+    if len(d) != 32:
+        raise ValueError("digest must be 32 bytes")
+    return (C.c_uint8 * 32).from_buffer_copy(d)
+
+
+def read_header(path: str, magic: bytes = MAGIC_DICT):
+    """read_header (dictionary.cpp:90-112) -> (grid, digest hex, entry_len, payload offset)."""
+    g, dg = Grid(), (C.c_uint8 * 32)()
+    el, off = C.c_int64(), C.c_int64()
+    check(N.load().mrfg_read_header(str(path).encode(), magic, C.byref(g), dg, C.byref(el),
+                                    C.byref(off)))
+    return g, bytes(dg).hex(), el.value, off.value
+
+
+def save_dictionary(path: str, g: Grid, digest, entries: np.ndarray) -> None:
+    """save (dictionary.cpp:196-203): header + float32 (re, im) entries in flat order."""
+    entries = np.ascontiguousarray(entries, dtype=np.float32)
+    if entries.ndim != 2 or entries.shape[0] != grid_total(g) or entries.shape[1] % 2:
+        raise ValueError("save: entries must be (grid total, 2N) float32")
+    check(N.load().mrfg_write_header(str(path).encode(), MAGIC_DICT, C.byref(g), _digest_bytes(digest),
+                                     entries.shape[1] // 2))
+    with open(path, "ab") as f:
+        entries.tofile(f)
+
+
+def load_dictionary(path: str):
+    """load (dictionary.cpp:205-220) -> (grid, digest hex, entries (total, 2N) float32)."""
+    g, dg, el, off = read_header(path, MAGIC_DICT)
+    want = grid_total(g) * 2 * el
+    data = np.fromfile(path, dtype=np.float32, offset=off)
+    if data.size < want:
+        raise N.MrfgError(-3, f"truncated payload in {path}")  # MRFG_E_RUNTIME
+    return g, dg, data[:want].reshape(grid_total(g), 2 * el)
+
+
+def load_cc_map(path: str):
+    """An .mrfc file (cc_map_to_file, dictionary.cpp:333-347) -> (grid, digest hex, scores)."""
+    g, dg, el, off = read_header(path, MAGIC_MAP)
+    data = np.fromfile(path, dtype=np.float32, offset=off)
+    if data.size < grid_total(g):
+        raise N.MrfgError(-3, f"truncated payload in {path}")
+    return g, dg, data[:grid_total(g)]
 
 
 def zoom_config(**kw) -> ZoomConfig:
@@ -306,15 +387,31 @@ class Context:
                                           out.ctypes.data_as(C.POINTER(C.c_float))))
         return out
 
-    def cc_map(self, fp, g: Grid, first: int = 0, count: int | None = None) -> np.ndarray:
-        """cc_map (dictionary.cpp:310-331): float32 CC of fp vs flats [first, first+count)."""
+    def cc_map(self, fp, g: Grid, first: int = 0, count: int | None = None,
+               precision: int = 64) -> np.ndarray:
+        """cc_map (dictionary.cpp:310-331): float32 CC of fp vs flats [first, first+count).
+
+        precision 64: the reference pipeline (bit-identical); 32: fused FP32 kernel."""
         if count is None:
             count = grid_total(g) - first
         q = np.ascontiguousarray(fp, dtype=np.complex128)
         out = np.empty(count, dtype=np.float32)
-        check(self.lib.mrfg_cc_map(self.h, C.byref(g), _dp(q.view(np.float64)), first, count,
-                                   out.ctypes.data_as(C.POINTER(C.c_float))))
+        check(self.lib.mrfg_cc_map_ex(self.h, C.byref(g), _dp(q.view(np.float64)), first, count,
+                                      precision, out.ctypes.data_as(C.POINTER(C.c_float))))
         return out
+
+    def cc_map_to_file(self, fp, g: Grid, path: str, precision: int = 64) -> None:
+        """cc_map_to_file (dictionary.cpp:333-347): the lattice's cc_map as an .mrfc file."""
+        q = np.ascontiguousarray(fp, dtype=np.complex128)
+        check(self.lib.mrfg_cc_map_to_file(self.h, C.byref(g), _dp(q.view(np.float64)),
+                                           _digest_bytes(self.sched.digest()), str(path).encode(),
+                                           precision))
+
+    def save_generated(self, g: Grid, path: str, chunk_entries: int = 1 << 15,
+                       precision: int = 64) -> None:
+        """save_generated (dictionary.cpp:216-239): the GPU-generated dictionary as .mrfd."""
+        check(self.lib.mrfg_save_generated(self.h, C.byref(g), _digest_bytes(self.sched.digest()),
+                                           str(path).encode(), chunk_entries, precision))
 
     # -- K5
     def quantify(self, fps, lattice: Grid, cfg: ZoomConfig = None) -> "np.ndarray":

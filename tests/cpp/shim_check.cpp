@@ -93,6 +93,51 @@ int main() {
         threw = true;
     }
     EXPECT(threw);
+    // .mrfd / .mrfc files (dictionary.hpp:87-96, 130-132)
+    {
+        const std::filesystem::path dir = std::filesystem::temp_directory_path();
+        const auto pd = dir / "shim_check.mrfd", pc = dir / "shim_check.mrfc";
+        save_generated(grid, s, pd, 1, 777);
+        Dictionary back = load(pd);
+        EXPECT(back.digest == dict.digest && back.entry_len == dict.entry_len);
+        EXPECT(back.grid.total() == grid.total() && back.data == dict.data);
+        save(dict, dir / "shim_check2.mrfd");
+        EXPECT(load(dir / "shim_check2.mrfd").data == dict.data);
+        cc_map_to_file(q[0], grid, s, pc);
+        EXPECT(std::filesystem::file_size(pc) == 4 + 4 + 32 + 72 + 8 + 4 * grid.total());
+        threw = false;
+        try {
+            load(pc);  // an .mrfc is not a dictionary
+        } catch (const std::runtime_error&) {
+            threw = true;
+        }
+        EXPECT(threw);
+        std::filesystem::remove(pd);
+        std::filesystem::remove(pc);
+        std::filesystem::remove(dir / "shim_check2.mrfd");
+    }
+    // noise calibration, smoothing, fingerprint CSV (fingerprint.hpp:45-75)
+    {
+        Fingerprint f0 = sim.simulate(grid.params_at(12, 9, 4));
+        const double sg = calibrate_noise(f0, 0.5, 3);
+        EXPECT(std::abs(cc(f0, add_noise(f0, sg, 3)) - 0.5) <= 0.02);
+        CalibratedNoise cn = make_calibrated_noise(f0, 0.5, 3);
+        EXPECT(cn.sigma == sg && cn.seed == 3);
+        Fingerprint sm = smooth(f0, 5);
+        EXPECT(sm.size() == f0.size());
+        const auto pf = std::filesystem::temp_directory_path() / "shim_check_fp.csv";
+        save_csv(f0, pf);
+        Fingerprint rl = load_fingerprint_csv(pf);
+        EXPECT(rl.size() == f0.size() && std::abs(rl.s[7] - f0.s[7]) < 1e-8);
+        std::filesystem::remove(pf);
+        threw = false;
+        try {
+            smooth(f0, 4);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        EXPECT(threw);
+    }
     std::printf("%s (%d failures)\n", fails ? "FAILED" : "OK", fails);
     return fails ? 1 : 0;
 }
