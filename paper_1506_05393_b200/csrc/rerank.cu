@@ -7,8 +7,12 @@
 // FP64 (sim64.cuh, host-libm tables), so its scores are bit-identical to the
 // reference's and the argmax -- including the lowest-flat tie rule of
 // dictionary.cpp:291-294 -- is the reference's.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "mrfg_internal.cuh"
 #include "sim64.cuh"
@@ -65,6 +69,20 @@ __global__ void k_filter(const CandRec* __restrict__ cand, int64_t n, const floa
         unsigned long long k = atomicAdd(count, 1ull);
         list[k] = i;
     }
+}
+
+// Sort key of a selected candidate: voxel above flat, so a warp's lanes
+// re-rank one voxel's neighbouring atoms -- the query row is a broadcast load
+// and the parameter-major table rows are shared or adjacent (the gathers,
+// not the FP64 pipe, bound the walk).
+constexpr int kFlatBits = 40;
+__global__ void k_rerank_keys(const CandRec* __restrict__ cand, const int64_t* __restrict__ list,
+                              int64_t n, unsigned long long* __restrict__ keys) {
+    int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= n) return;
+    const CandRec r = cand[list[k]];
+    keys[k] = (static_cast<unsigned long long>(r.voxel) << kFlatBits) |
+              static_cast<unsigned long long>(r.flat);
 }
 
 __device__ __forceinline__ unsigned long long order_key(double x) {
@@ -270,19 +288,30 @@ void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qro
 int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, const double* d_q64,
                           int64_t nq, int metric, const float* d_best, float delta, CandRec* d_cand,
                           int64_t ncand, mrfg_match* d_out, double* err_max, bool allow_missing) {
-    // scratch layout: list (ncand i64) | score (ncand f64) | vkey (nq u64) |
-    //                 vflat (nq u64) | counters
-    size_t need = sizeof(int64_t) * ncand + sizeof(double) * ncand + 16 * nq + 64;
+    // scratch layout: list, list2 (ncand i64) | keys, keys2 (ncand u64) |
+    //                 score (ncand f64) | vkey, vflat (nq u64) | counters | sort temp
+    const int vbits = std::max(1, 64 - __builtin_clzll(static_cast<unsigned long long>(std::max<int64_t>(nq, 2) - 1)));
+    const int end_bit = kFlatBits + vbits;
+    size_t sort_tmp = 0;
+    MRFG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, static_cast<unsigned long long*>(nullptr),
+                                              static_cast<unsigned long long*>(nullptr),
+                                              static_cast<int64_t*>(nullptr), static_cast<int64_t*>(nullptr),
+                                              std::max<int64_t>(ncand, 1), 0, end_bit, c.stream));
+    const size_t head = 40 * static_cast<size_t>(ncand) + 16 * nq + 64;
+    size_t need = head + sort_tmp + 256;
     c.rerank.ensure(need);
     char* base = c.rerank.as<char>();
     int64_t* list = reinterpret_cast<int64_t*>(base);
-    double* score = reinterpret_cast<double*>(base + sizeof(int64_t) * ncand);
-    unsigned long long* vkey =
-        reinterpret_cast<unsigned long long*>(base + (sizeof(int64_t) + sizeof(double)) * ncand);
+    int64_t* list2 = list + ncand;
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(list2 + ncand);
+    unsigned long long* keys2 = keys + ncand;
+    double* score = reinterpret_cast<double*>(keys2 + ncand);
+    unsigned long long* vkey = reinterpret_cast<unsigned long long*>(score + ncand);
     unsigned long long* vflat = vkey + nq;
     unsigned long long* cnt = vflat + nq;
     int* missing = reinterpret_cast<int*>(cnt + 1);
     unsigned int* d_err = reinterpret_cast<unsigned int*>(missing + 1);
+    void* d_sort_tmp = base + (head + 255) / 256 * 256;
     MRFG_CUDA(cudaMemsetAsync(vkey, 0, sizeof(unsigned long long) * nq, c.stream));
     MRFG_CUDA(cudaMemsetAsync(vflat, 0xFF, sizeof(unsigned long long) * nq, c.stream));
     MRFG_CUDA(cudaMemsetAsync(cnt, 0, 16, c.stream));
@@ -295,6 +324,16 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
     MRFG_CUDA(cudaMemcpyAsync(&nsel, cnt, sizeof nsel, cudaMemcpyDeviceToHost, c.stream));
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
     const int rb = 64;
+    const char* sort_env = std::getenv("MRFG_RERANK_SORT");  // "0": keep screening order
+    if (nsel > 0 && !(sort_env && sort_env[0] == '0')) {
+        // (voxel, flat) order for the gathers; the argmax does not depend on it
+        k_rerank_keys<<<(nsel + bs - 1) / bs, bs, 0, c.stream>>>(d_cand, list, nsel, keys);
+        MRFG_CUDA(cudaGetLastError());
+        size_t tmp = sort_tmp;
+        MRFG_CUDA(cub::DeviceRadixSort::SortPairs(d_sort_tmp, tmp, keys, keys2, list, list2,
+                                                  static_cast<int64_t>(nsel), 0, end_bit, c.stream));
+        list = list2;
+    }
     if (nsel > 0) {
         if (d_dict) {
             k_rerank_dict<<<(nsel + rb - 1) / rb, rb, 0, c.stream>>>(
