@@ -4,6 +4,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp32_pipes fp32_pipes.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 constexpr int ITERS = 4096;
@@ -83,7 +84,30 @@ float time_it(F f) {
     return ms / 5;
 }
 
-int main() {
+// Sustained FFMA: back-to-back launches for `seconds` (power/thermal steady
+// state, like MEASURED_PEAKS.json's sustained bf16 figure); returns TF/s of
+// the last second.
+double sustained_ffma(int sms, float* out, float* ab, double seconds) {
+    const int blocks = sms * 8, threads = 256;
+    const double fl = double(blocks) * threads * ITERS * 8 * 2;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double elapsed = 0, last = 0;
+    while (elapsed < seconds) {
+        cudaEventRecord(e0);
+        for (int r = 0; r < 50; ++r) k_ffma_reg<<<blocks, threads>>>(out, ab);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        elapsed += ms * 1e-3;
+        last = 50 * fl / (ms * 1e-3) / 1e12;
+    }
+    return last;
+}
+
+int main(int argc, char** argv) {
     cudaDeviceProp p;
     cudaGetDeviceProperties(&p, 0);
     int sms = p.multiProcessorCount;
@@ -104,7 +128,10 @@ int main() {
     printf("\"ffma2_tflops\": %.2f, ", fl / t / 1e9);
     t = time_it([&] { k_ex2<<<blocks, threads>>>(out, 0.999f); });
     double ops = lanes * (ITERS / 4) * 8;
-    printf("\"ex2_gops\": %.1f, \"ex2_per_clk_per_sm_at_max\": %.2f}\n", ops / t / 1e6,
+    printf("\"ex2_gops\": %.1f, \"ex2_per_clk_per_sm_at_max\": %.2f", ops / t / 1e6,
            ops / (t * 1e-3) / sms / (p.clockRate * 1e3));
+    if (argc > 1) printf(", \"ffma_sustained_tflops\": %.2f, \"sustained_s\": %s",
+                         sustained_ffma(sms, out, ab, atof(argv[1])), argv[1]);
+    printf("}\n");
     return 0;
 }
