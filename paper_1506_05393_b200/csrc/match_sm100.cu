@@ -52,6 +52,7 @@ constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
 struct Dev {
     const float* inv2;
     int64_t n_at, n_vt, nkb, last_sub;
+    int64_t ga;  // tile raster: 1 = atom-major; > 1 = groups of ga atom tiles per query tile
     int64_t valid_atoms, valid_begin, nvox, flat_base, flat_stride;
     float* best;
     CandRec* cand;
@@ -60,6 +61,25 @@ struct Dev {
     float delta;
     int metric;
 };
+
+// Tile t -> (atom tile, query tile).  ga = 1: atom-major (the query operand
+// is L2-resident, each atom tile is read once).  ga > 1 (query operand far
+// larger than L2, configs 3/5): the ga concurrently running CTAs (pairs) take
+// ga different atom tiles of the SAME query tile, so every query tile is
+// fetched from HBM once per ga atom tiles and the group's atom tiles stay in
+// L2 while it sweeps the query tiles.
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t n_at, int64_t n_vt, int64_t ga, int64_t& at,
+                                            int64_t& vt) {
+    if (ga <= 1) {
+        at = t / n_vt;
+        vt = t % n_vt;
+        return;
+    }
+    const int64_t per = ga * n_vt, g0 = t / per * ga, rem = t % per;
+    const int64_t gsz = n_at - g0 < ga ? n_at - g0 : ga;  // the last group may be smaller
+    vt = rem / gsz;
+    at = g0 + rem % gsz;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -230,7 +250,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-                const int at = static_cast<int>(t / p.n_vt), vt = static_cast<int>(t % p.n_vt);
+                int64_t at64, vt64;
+                tile_coords(t, p.n_at, p.n_vt, p.ga, at64, vt64);
+                const int at = static_cast<int>(at64), vt = static_cast<int>(vt64);
                 for (int kb = 0; kb < p.nkb; ++kb) {
                     mbar_wait(&s.empty[stage], phase ^ 1);
                     mbar_expect_tx(&s.full[stage], A_BYTES + B_BYTES);
@@ -281,7 +303,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            const int64_t at = t / p.n_vt, vt = t % p.n_vt;
+            int64_t at, vt;
+            tile_coords(t, p.n_at, p.n_vt, p.ga, at, vt);
             {
                 const int64_t v = vt * 128 + row;
                 float b = v < p.nvox ? __ldcg(p.best + v) : 1e30f;
@@ -444,7 +467,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t t = cid; t < n_tiles; t += ncl) {
-                const int at = static_cast<int>(t / n_vt), vt = static_cast<int>(t % n_vt);
+                int64_t at64, vt64;
+                tile_coords(t, n_at, n_vt, p.ga, at64, vt64);
+                const int at = static_cast<int>(at64), vt = static_cast<int>(vt64);
                 for (int kb = 0; kb < p.nkb; ++kb) {
                     mbar_wait(&s.empty[stage], phase ^ 1);
                     if (leader)
@@ -499,7 +524,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int64_t t = cid; t < n_tiles; t += ncl) {
-            const int64_t at = t / n_vt, vt = t % n_vt;
+            int64_t at, vt;
+            tile_coords(t, n_at, n_vt, p.ga, at, vt);
             {
                 const int64_t v = vt * 128 + row;
                 float b = v < p.nvox ? __ldcg(p.best + v) : 1e30f;
@@ -625,7 +651,16 @@ Dev dev_of(const MatchParams& p, int64_t k_valid) {
     d.cand_cap = p.cand_cap;
     d.delta = p.delta;
     d.metric = p.metric;
+    d.ga = 1;
     return d;
+}
+
+// Raster group size (MRFG_K2_GROUP; default 1 = atom-major).  Measured on
+// config 3 (2.1 GB query operand): one group per wave of concurrent CTA pairs
+// (74) ran the GEMM at 802 vs 940 TFLOP/s atom-major, config 5 977 vs 1011.
+int64_t group_of(const MatchParams&, int64_t) {
+    if (const char* e = std::getenv("MRFG_K2_GROUP")) return std::max<int64_t>(1, std::atoll(e));
+    return 1;
 }
 
 }  // namespace
@@ -654,6 +689,7 @@ void launch_match(Ctx& c, const MatchParams& p) {
         CUtensorMap mb = make_map(c, p.b, p.q_rows, p.k_pad, BN / 2);
         const int64_t tiles = (p.atoms / 256) * d.n_vt;
         const int64_t pairs = std::min<int64_t>(tiles, c.num_sms / 2);
+        d.ga = group_of(p, pairs);
         k_match_sm100_2cta<<<static_cast<int>(2 * pairs), NTHREADS, SMEM2_BYTES, c.stream>>>(ma, mb, d);
         MRFG_CUDA(cudaGetLastError());
         return;
@@ -662,6 +698,7 @@ void launch_match(Ctx& c, const MatchParams& p) {
     CUtensorMap mb = make_map(c, p.b, p.q_rows, p.k_pad, BN);
     int64_t tiles = d.n_at * d.n_vt;
     int grid = static_cast<int>(tiles < c.num_sms ? tiles : c.num_sms);
+    d.ga = group_of(p, grid);
     k_match_sm100<<<grid, NTHREADS, SMEM_BYTES, c.stream>>>(ma, mb, d);
     MRFG_CUDA(cudaGetLastError());
 }

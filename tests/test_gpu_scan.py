@@ -80,6 +80,22 @@ def test_screen_production_producer(orc, small, monkeypatch, k1, apt):
     assert np.abs(a - b).max() < 1e-3
 
 
+@pytest.mark.parametrize("pair", ["1", "0"])
+@pytest.mark.parametrize("group", ["3", "7", "64"])
+def test_screen_grouped_raster(small, monkeypatch, pair, group):
+    """K2's grouped tile raster (query operand larger than L2) visits every
+    (atom tile, query tile) once: dense scores identical to atom-major order,
+    including a short last group."""
+    monkeypatch.setenv("MRFG_K2_PAIR", pair)
+    q = np.concatenate([small.fps] * 4)  # 640 voxels: 5 query tiles
+    with P.Context(small.schedule) as c:
+        monkeypatch.setenv("MRFG_K2_GROUP", "1")
+        a = c.screen_scores(small.grid, q, 1000, 9 * 256 + 17)
+        monkeypatch.setenv("MRFG_K2_GROUP", group)
+        b = c.screen_scores(small.grid, q, 1000, 9 * 256 + 17)
+    np.testing.assert_array_equal(a, b)
+
+
 def test_scan_grid_config1_slice(small, small_ref):
     oflat, oscore, osecond = small_ref
     with P.Context(small.schedule) as c:
