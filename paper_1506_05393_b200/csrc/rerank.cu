@@ -297,16 +297,28 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
                                               static_cast<unsigned long long*>(nullptr),
                                               static_cast<int64_t*>(nullptr), static_cast<int64_t*>(nullptr),
                                               std::max<int64_t>(ncand, 1), 0, end_bit, c.stream));
-    const size_t head = 40 * static_cast<size_t>(ncand) + 16 * nq + 64;
+    // Sized for the next power of two of the candidate count: the count
+    // varies by a few 1e4 between identical scans (the running maxima race
+    // the GEMM epilogue), and a regrow (cudaFree + cudaMalloc of ~0.5 GB in
+    // the timed scan) was measured to cost up to 200 ms.
+    int64_t cap = int64_t(1) << 20;
+    while (cap < ncand) cap *= 2;
+    size_t sort_cap_tmp = 0;
+    MRFG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_cap_tmp, static_cast<unsigned long long*>(nullptr),
+                                              static_cast<unsigned long long*>(nullptr),
+                                              static_cast<int64_t*>(nullptr), static_cast<int64_t*>(nullptr),
+                                              cap, 0, end_bit, c.stream));
+    sort_tmp = std::max(sort_tmp, sort_cap_tmp);
+    const size_t head = 40 * static_cast<size_t>(cap) + 16 * nq + 64;
     size_t need = head + sort_tmp + 256;
     c.rerank.ensure(need);
     char* base = c.rerank.as<char>();
     int64_t* list = reinterpret_cast<int64_t*>(base);
-    int64_t* list2 = list + ncand;
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(list2 + ncand);
-    unsigned long long* keys2 = keys + ncand;
-    double* score = reinterpret_cast<double*>(keys2 + ncand);
-    unsigned long long* vkey = reinterpret_cast<unsigned long long*>(score + ncand);
+    int64_t* list2 = list + cap;
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(list2 + cap);
+    unsigned long long* keys2 = keys + cap;
+    double* score = reinterpret_cast<double*>(keys2 + cap);
+    unsigned long long* vkey = reinterpret_cast<unsigned long long*>(score + cap);
     unsigned long long* vflat = vkey + nq;
     unsigned long long* cnt = vflat + nq;
     int* missing = reinterpret_cast<int*>(cnt + 1);
