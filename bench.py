@@ -47,6 +47,21 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def k2_traffic(args, n, nq):
+    """DRAM bytes (read + write) of one K2 launch from the committed ncu --set
+    full capture (profiles/r01_k2_traffic.json), when it was taken on this
+    workload shape; else None."""
+    p = os.path.join(ROOT, "profiles", "r01_k2_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None
+    if (d.get("chunk_atoms"), d.get("voxels"), d.get("timepoints")) != (args.chunk, nq, n):
+        return None
+    return d.get("dram_bytes_per_launch")
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -360,9 +375,10 @@ def run_ours(args, world, rank, local):
                                   "scan_total": sum(s.total_ms for s in stats) / len(stats)},
         "screen_err_max": max(s.screen_err_max for s in stats),
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
-                     "frac": gemm_tflops / peak_t, "traffic": None,
-                     "kernel": "k_match_sm100 (K2)", "peak_kind": f"{pk_kind} bf16 dense sustained",
-                     "avg_launch_ms": gemm_ms / max(launches, 1)},
+                     "frac": gemm_tflops / peak_t, "traffic": k2_traffic(args, n, nq),
+                     "kernel": "k_match_sm100_2cta (K2)", "peak_kind": f"{pk_kind} bf16 dense sustained",
+                     "avg_launch_ms": gemm_ms / max(launches, 1),
+                     "flop_per_launch": 8.0 * n * nq * args.chunk},
         "e2e": {"value": nq * total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nq * n * 16,
                 "d2h_bytes_per_step": nq * 16, "seconds_per_step": e2e_s},
         "gpu_launches": int(sum(2 * s.chunks + 8 for s in stats) + (args.steps if world > 1 else 0)),

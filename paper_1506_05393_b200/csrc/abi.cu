@@ -486,7 +486,7 @@ int mrfg_destroy(mrfg_ctx* h) {
         for (DevBuf* b : {&c.zoom, &c.rf64_d, &c.rf32_d, &c.tab.e1f, &c.tab.e2f, &c.tab.phf, &c.tab.e1d,
                           &c.tab.e2d, &c.tab.phd, &c.q64, &c.qprime, &c.best, &c.cand,
                           &c.cand_count, &c.atoms_a, &c.inv2, &c.seed_a, &c.seed_inv2, &c.rerank,
-                          &c.params, &c.out64, &c.misc})
+                          &c.params, &c.out64, &c.misc, &c.rerank_scratch})
             b->release();
         if (c.own_stream) cudaStreamDestroy(c.stream);
         if (c.aux) {

@@ -93,7 +93,7 @@ struct Ctx {
     // scratch
     DevBuf zoom;  // K5 per-warp scratch (grow-only: no allocation inside a timed call)
     DevBuf q64, qprime, best, cand, cand_count, atoms_a, inv2, seed_a, seed_inv2, rerank,
-        params, out64, misc;
+        params, out64, misc, rerank_scratch;
     // producer stream + events for the K1/K2 overlap (created on first use)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev[8] = {};

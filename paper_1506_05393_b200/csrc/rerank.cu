@@ -150,6 +150,76 @@ __global__ void k_rerank(Tab64 T, const double* __restrict__ q64, const CandRec*
     }
 }
 
+// Single-walk variant of k_rerank: the FP64 echoes of the one walk are kept
+// in a lane-interleaved scratch (a warp's 32 lanes store step j as 512
+// contiguous bytes, streaming cache hints), then the scoring pass reads them
+// back instead of re-walking: the walk -- L1-wavefront bound on its table
+// gathers -- runs once per candidate instead of twice.  Same operations in the
+// same order as exact_score, so the score is the same bits.  Persistent
+// threads (grid-stride over the sorted list) bound the scratch.
+__global__ void __launch_bounds__(64) k_rerank1(Tab64 T, const double* __restrict__ q64,
+                                                const CandRec* __restrict__ cand,
+                                                const int64_t* __restrict__ list, int64_t n, int metric,
+                                                double2* __restrict__ scratch, double* __restrict__ score,
+                                                unsigned long long* __restrict__ vkey,
+                                                unsigned int* __restrict__ err_max) {
+    const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    double2* my = scratch + (tid >> 5) * static_cast<int64_t>(T.n) * 32 + lane;
+    // whole warps iterate together (lanes past the end idle in the last round)
+    const int64_t rounds = (n + nthreads - 1) / nthreads;
+    for (int64_t rd = 0; rd < rounds; ++rd) {
+        const int64_t k = tid + rd * nthreads;
+        if (k >= n) break;
+        const CandRec r = cand[list[k]];
+        const double* q = q64 + static_cast<int64_t>(r.voxel) * 2 * T.n;
+        int i1, i2, idf;
+        unflatten(r.flat, T.L, i1, i2, idf);
+        double acc = 0.0;
+        sim64_walk(T.rf, T.e1d, T.e2d, T.phd, T.inv0, T.n, T.L, i1, i2, idf, [&](int j, double x, double y) {
+            acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
+            __stcs(my + static_cast<int64_t>(j) * 32, make_double2(x, y));
+        });
+        const double inv = 1.0 / sqrt(acc);
+        double re = 0.0, im = 0.0, dd = 0.0;
+        // scoring pass: the echoes stream back 8 steps per batch of loads
+        // (memory-level parallelism: the scratch is DRAM-resident at large N)
+        constexpr int U = 8;
+        for (int j0 = 0; j0 < T.n; j0 += U) {
+            double2 m[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                m[u] = j0 + u < T.n ? __ldcs(my + static_cast<int64_t>(j0 + u) * 32) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + u;
+                if (j >= T.n) break;
+                const double er = static_cast<double>(__double2float_rn(__dmul_rn(m[u].x, inv)));
+                const double ei = static_cast<double>(__double2float_rn(__dmul_rn(m[u].y, inv)));
+                const double qr = q[2 * j], qi = q[2 * j + 1];
+                if (metric == MRFG_METRIC_CC) {
+                    re = __dadd_rn(re, __dadd_rn(__dmul_rn(qr, er), __dmul_rn(qi, ei)));
+                    im = __dadd_rn(im, __dsub_rn(__dmul_rn(qi, er), __dmul_rn(qr, ei)));
+                } else {
+                    const double dr = __dsub_rn(qr, er), di = __dsub_rn(qi, ei);
+                    dd = __dadd_rn(dd, __dadd_rn(__dmul_rn(dr, dr), __dmul_rn(di, di)));
+                }
+            }
+        }
+        double sc;
+        if (metric == MRFG_METRIC_CC) {
+            const double v = sqrt(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
+            sc = v < 1.0 ? v : 1.0;
+        } else {
+            sc = -sqrt(dd);
+        }
+        score[k] = sc;
+        atomicMax(vkey + r.voxel, order_key(sc));
+        if (metric == MRFG_METRIC_CC) atomicMax(err_max, __float_as_uint(fabsf(sqrtf(r.s) - static_cast<float>(sc))));
+    }
+}
+
 // brute_force_search over a stored dictionary: the reference scores the
 // FP64 unit query against the stored float32 entry (dictionary.cpp:117-143).
 __device__ double exact_score_entry(const double* __restrict__ q, const float* __restrict__ e, int n,
@@ -351,8 +421,27 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
             k_rerank_dict<<<(nsel + rb - 1) / rb, rb, 0, c.stream>>>(
                 d_dict, static_cast<int>(c.n), d_q64, d_cand, list, nsel, metric, score, vkey, d_err);
         } else {
-            k_rerank<<<(nsel + rb - 1) / rb, rb, 0, c.stream>>>(tab64_of(c, *t), d_q64, d_cand, list,
-                                                                nsel, metric, score, vkey, d_err);
+            // one walk per candidate (k_rerank1) while its echo scratch stays
+            // small (measured: config 2, N = 1000, 1.5 GB: 91 -> 64 ms); at
+            // config 5's N = 3000 (4.5 GB, DRAM-resident) the re-walk is as fast
+            // (681 vs 703 ms), so k_rerank walks twice.  MRFG_RERANK_WALK=1/2 forces.
+            int per_sm = 0;
+            MRFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rerank1, rb, 0));
+            const int64_t blocks = std::min<int64_t>((nsel + rb - 1) / rb,
+                                                     int64_t(std::max(per_sm, 1)) * c.num_sms);
+            const size_t scratch = sizeof(double2) * c.n * blocks * rb;
+            const char* e = std::getenv("MRFG_RERANK_WALK");
+            const bool one = e ? e[0] == '1' : scratch <= (size_t(2) << 30);
+            if (!one) {
+                k_rerank<<<(nsel + rb - 1) / rb, rb, 0, c.stream>>>(tab64_of(c, *t), d_q64, d_cand, list,
+                                                                    nsel, metric, score, vkey, d_err);
+                MRFG_CUDA(cudaGetLastError());
+            } else {
+            c.rerank_scratch.ensure(scratch);
+            k_rerank1<<<static_cast<unsigned>(blocks), rb, 0, c.stream>>>(
+                tab64_of(c, *t), d_q64, d_cand, list, nsel, metric, c.rerank_scratch.as<double2>(), score, vkey,
+                d_err);
+            }
         }
         MRFG_CUDA(cudaGetLastError());
         k_select_flat<<<(nsel + bs - 1) / bs, bs, 0, c.stream>>>(d_cand, list, nsel, score, vkey,

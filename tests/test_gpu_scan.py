@@ -97,6 +97,18 @@ def test_screen_grouped_raster(small, monkeypatch, pair, group):
     np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("walk", ["1", "2"])
+@pytest.mark.parametrize("metric", ["cc", "euclidean"])
+def test_rerank_walk_modes(small, orc, monkeypatch, walk, metric):
+    """K3 with one walk + echo scratch (default) or two walks: identical bits."""
+    monkeypatch.setenv("MRFG_RERANK_WALK", walk)
+    with P.Context(small.schedule) as c:
+        flat, score, _ = c.scan_grid(small.grid, small.fps[:96], metric=metric)
+    oflat, oscore, osecond = orc.scan_grid(to_oracle_sched(small.schedule), to_oracle_grid(small.grid),
+                                           small.fps[:96], metric=1 if metric == "euclidean" else 0)
+    assert_parity(flat, score, oflat, oscore, osecond)
+
+
 def test_scan_grid_config1_slice(small, small_ref):
     oflat, oscore, osecond = small_ref
     with P.Context(small.schedule) as c:
