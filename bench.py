@@ -173,6 +173,29 @@ def cpu_sample(config: int, nvox_sample: int, which: str | None = None):
                       f"({n2 * nd} atoms, N={c['n']}), simulate+match, {dt:.2f} s"}
 
 
+def arm_config(args, world, nx, ny, n, nq, total):
+    """The workload description both arms print (config of the JSON line)."""
+    return {"workload": f"BASELINE configs[{args.config - 1}]: {nx}x{ny} slice, N={n}, "
+                        f"{total} atoms, brute-force streamed DGS",
+            "voxels": nq, "atoms": total, "timepoints": n, "chunk_atoms": args.chunk,
+            "delta": args.delta, "parallelism": f"atom-shard x{world}",
+            "l2": "256 MB flush per step; each step streams >100 GB of fp16 atoms"}
+
+
+def ref_config(args, world):
+    """Our arm's config for the same workload (the reference arm times a
+    bounded sample of it: cpu_baseline.sample says which)."""
+    from paper_1506_05393_b200 import workloads
+    c = workloads.CONFIGS[args.config]
+    axes = [int(round((c[k][1] - c[k][0]) / c[k][2])) + 1 for k in ("t1", "t2", "df")]
+    total = axes[0] * axes[1] * axes[2]
+    if args.atoms:
+        total = min(total, args.atoms)
+    nx, ny = c.get("nx", 0), c.get("ny", 0)
+    nq = args.nvox or (nx * ny)
+    return arm_config(args, world, nx, ny, c["n"], nq, total)
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -186,7 +209,7 @@ def run_reference(args, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"BASELINE configs[{args.config - 1}] brute-force DGS (CPU sample)"},
+            "config": ref_config(args, world),
             "cpu_baseline": r,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -360,11 +383,7 @@ def run_ours(args, world, rank, local):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "fp16 screen / fp32 accum / f64 rerank",
         "data": "synthetic (seeded BASELINE configs[1] phantom, SNR 30)",
-        "config": {"workload": f"BASELINE configs[{args.config - 1}]: {wl.nx}x{wl.ny} slice, N={n}, "
-                               f"{total} atoms, brute-force streamed DGS",
-                   "voxels": nq, "atoms": total, "timepoints": n, "chunk_atoms": args.chunk,
-                   "delta": args.delta, "parallelism": f"atom-shard x{world}",
-                   "l2": "256 MB flush per step; each step streams >100 GB of fp16 atoms"},
+        "config": arm_config(args, world, wl.nx, wl.ny, n, nq, total),
         "slice_dgs_wall_s": ms * 1e-3,
         "bloch_atom_steps_per_s": bloch_rate * world,
         "bloch_fp32_tflops": bloch_rate * BLOCH_FLOP_PER_STEP / 1e12,
