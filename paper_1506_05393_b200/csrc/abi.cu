@@ -300,7 +300,10 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
         // consumes chunk i (the persistent GEMM leaves room for one producer CTA
         // per SM).  Measured on B200: K2 runs under sw_power_cap, so concurrent
         // CUDA-core work lowers the SM clock and the GEMM loses what K1 gains
-        // (3.05 s vs 2.99 s per config-2 slice); the default is one stream.
+        // (3.05 s vs 2.99 s per config-2 slice with the scalar K1; with the
+        // packed-pair K1: 2.900 vs 2.940 s, but K1's own duration stretches to
+        // 355 ms, so the Bloch rate is no longer measurable per kernel); the
+        // default is one stream.
         static const bool overlap = [] {
             const char* e = std::getenv("MRFG_OVERLAP");
             return e && e[0] == '1';
