@@ -308,27 +308,59 @@ __device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, bool dict
 struct Apx {
     float cc, re;
 };
+// Packed f32x2 helpers: sm_100a executes fma/mul.rn.f32x2 as FFMA2/FMUL2 and
+// folds a scalar broadcast, a half swap and a one-half negation into the
+// operand selectors, so a complex product v*(c + i s) is 2 instructions.
+typedef unsigned long long zf2;
+__device__ __forceinline__ zf2 zpk(float a, float b) {
+    zf2 r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void zup(zf2 v, float& a, float& b) {
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ zf2 zfma2(zf2 a, zf2 b, zf2 c) {
+    zf2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ zf2 zmul2(zf2 a, zf2 b) {
+    zf2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// v*(c + i s) [+ acc]
+__device__ __forceinline__ zf2 zcmul(zf2 v, float c, float s) {
+    float x, y;
+    zup(v, x, y);
+    return zfma2(v, zpk(c, c), zmul2(zpk(y, x), zpk(-s, s)));
+}
+__device__ __forceinline__ zf2 zcmac(zf2 v, float c, float s, zf2 acc) {
+    float x, y;
+    zup(v, x, y);
+    return zfma2(v, zpk(c, c), zfma2(zpk(y, x), zpk(-s, s), acc));
+}
+
 // One step of the FP32 screening recursion (bloch.hpp:34-38, bloch.cpp:22-26)
-// and the CC partial sums.
+// and the CC partial sums.  The transverse state rotations and the query dot
+// are complex products on f32x2 pairs (FFMA2/FMUL2): 20 FMA-pipe instructions
+// per step instead of 29.  pq accumulates sum_j conj(q_j) s_j = (re, -im) of
+// sum_j q_j conj(s_j) (same magnitude and real part); pn the two halves of |s|^2.
 __device__ __forceinline__ void zstep32(const float4 ra, const float4 rb, const float4 rc,
                                         const float2 qq, const float4 e1, const float2 e2,
-                                        const float4 ph, float& x, float& y, float& zz, float& pr,
-                                        float& pi, float& pn) {
+                                        const float4 ph, float& x, float& y, float& zz, zf2& pq,
+                                        zf2& pn) {
     const float nx = fmaf(ra.x, x, fmaf(ra.y, y, ra.z * zz));
     const float ny = fmaf(ra.w, x, fmaf(rb.x, y, rb.y * zz));
     const float nz = fmaf(rb.z, x, fmaf(rb.w, y, rc.x * zz));
     // relax/precess over te: z' = z E1 + (1 - E1)
-    x = (nx * ph.x - ny * ph.y) * e2.x;
-    y = (nx * ph.y + ny * ph.x) * e2.x;
+    const zf2 v = zmul2(zcmul(zpk(nx, ny), ph.x, ph.y), zpk(e2.x, e2.x));
     zz = fmaf(nz, e1.x, e1.y);
-    pr = fmaf(qq.x, x, fmaf(qq.y, y, pr));
-    pi = fmaf(qq.y, x, fmaf(-qq.x, y, pi));
-    pn = fmaf(x, x, fmaf(y, y, pn));
+    pq = zcmac(v, qq.x, -qq.y, pq);
+    pn = zfma2(v, v, pn);
     // over the rest of TR
-    const float rx = (x * ph.z - y * ph.w) * e2.y;
-    const float ry = (x * ph.w + y * ph.z) * e2.y;
-    x = rx;
-    y = ry;
+    zup(zmul2(zcmul(v, ph.z, ph.w), zpk(e2.y, e2.y)), x, y);
     zz = fmaf(zz, e1.z, e1.w);
 }
 
@@ -372,14 +404,20 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
             E2[m] = __ldg(p2 + m);
         }
     };
-    auto run = [&](const float4* E1, const float2* E2, const float4* PH, const float4* r, const float2* qb) {
-        float pr = 0.f, pi = 0.f, pn = 0.f;
-#pragma unroll
-        for (int m = 0; m < kB; ++m)
-            zstep32(r[4 * m], r[4 * m + 1], r[4 * m + 2], qb[m], E1[m], E2[m], PH[m], x, y, zz, pr, pi, pn);
+    auto fold = [&](zf2 pq, zf2 pn) {  // FP32 partial sums into FP64
+        float pr, pi, na, nb;
+        zup(pq, pr, pi);
+        zup(pn, na, nb);
         re += pr;
         im += pi;
-        nn += pn;
+        nn += na + nb;
+    };
+    auto run = [&](const float4* E1, const float2* E2, const float4* PH, const float4* r, const float2* qb) {
+        zf2 pq = zpk(0.f, 0.f), pn = zpk(0.f, 0.f);
+#pragma unroll
+        for (int m = 0; m < kB; ++m)
+            zstep32(r[4 * m], r[4 * m + 1], r[4 * m + 2], qb[m], E1[m], E2[m], PH[m], x, y, zz, pq, pn);
+        fold(pq, pn);
     };
     const int nmain = n & ~(2 * kB - 1);
     load(A1, A2, AP, e1p, e2p, php);
@@ -397,13 +435,11 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
         run(B1, B2, BP, rfp + 4 * (jb + kB), q + jb + kB);
     }
     {  // tail: n % 8 steps
-        float pr = 0.f, pi = 0.f, pn = 0.f;
+        zf2 pq = zpk(0.f, 0.f), pn = zpk(0.f, 0.f);
         for (int j = nmain; j < n; ++j)
             zstep32(rfp[4 * j], rfp[4 * j + 1], rfp[4 * j + 2], q[j], __ldg(e1p + j), __ldg(e2p + j),
-                    __ldg(php + j), x, y, zz, pr, pi, pn);
-        re += pr;
-        im += pi;
-        nn += pn;
+                    __ldg(php + j), x, y, zz, pq, pn);
+        fold(pq, pn);
     }
     const double inv = rsqrt(nn);
     Apx a;
@@ -453,27 +489,35 @@ __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
         }
     };
     // one step of both points; w = (wtc, wts) for te, (wrc, wrs) for rest: rc.w, rd.x, rd.y, rd.z
-    auto step2 = [&](const float4* r, const float2 qq, const float4 e1, const float2 e2, const float4 pa, float& pra,
-                     float& pia, float& pna, float& prb, float& pib, float& pnb) {
+    auto step2 = [&](const float4* r, const float2 qq, const float4 e1, const float2 e2, const float4 pa, zf2& pra,
+                     zf2& pna, zf2& prb, zf2& pnb) {
         const float4 ra = r[0], rb = r[1], rc = r[2], rd = r[3];
         float4 pb;
         pb.x = fmaf(pa.x, rc.w, -pa.y * rd.x);
         pb.y = fmaf(pa.y, rc.w, pa.x * rd.x);
         pb.z = fmaf(pa.z, rd.y, -pa.w * rd.z);
         pb.w = fmaf(pa.w, rd.y, pa.z * rd.z);
-        zstep32(ra, rb, rc, qq, e1, e2, pa, xa, ya, za, pra, pia, pna);
-        zstep32(ra, rb, rc, qq, e1, e2, pb, xb, yb, zb, prb, pib, pnb);
+        zstep32(ra, rb, rc, qq, e1, e2, pa, xa, ya, za, pra, pna);
+        zstep32(ra, rb, rc, qq, e1, e2, pb, xb, yb, zb, prb, pnb);
+    };
+    auto fold = [&](zf2 pra, zf2 pna, zf2 prb, zf2 pnb) {
+        float r0, i0, n0, n1;
+        zup(pra, r0, i0);
+        zup(pna, n0, n1);
+        rea += r0;
+        ima += i0;
+        nna += n0 + n1;
+        zup(prb, r0, i0);
+        zup(pnb, n0, n1);
+        reb += r0;
+        imb += i0;
+        nnb += n0 + n1;
     };
     auto run = [&](const float4* E1, const float2* E2, const float4* PH, const float4* r, const float2* qb) {
-        float pra = 0.f, pia = 0.f, pna = 0.f, prb = 0.f, pib = 0.f, pnb = 0.f;
+        zf2 pra = zpk(0.f, 0.f), pna = pra, prb = pra, pnb = pra;
 #pragma unroll
-        for (int m = 0; m < kB; ++m) step2(r + 4 * m, qb[m], E1[m], E2[m], PH[m], pra, pia, pna, prb, pib, pnb);
-        rea += pra;
-        ima += pia;
-        nna += pna;
-        reb += prb;
-        imb += pib;
-        nnb += pnb;
+        for (int m = 0; m < kB; ++m) step2(r + 4 * m, qb[m], E1[m], E2[m], PH[m], pra, pna, prb, pnb);
+        fold(pra, pna, prb, pnb);
     };
     const int nmain = n & ~(2 * kB - 1);
     load(A1, A2, AP, e1p, e2p, php);
@@ -489,15 +533,10 @@ __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
         run(B1, B2, BP, rfp + 4 * (jb + kB), q + jb + kB);
     }
     {  // tail: n % 4 steps
-        float pra = 0.f, pia = 0.f, pna = 0.f, prb = 0.f, pib = 0.f, pnb = 0.f;
+        zf2 pra = zpk(0.f, 0.f), pna = pra, prb = pra, pnb = pra;
         for (int j = nmain; j < n; ++j)
-            step2(rfp + 4 * j, q[j], __ldg(e1p + j), __ldg(e2p + j), __ldg(php + j), pra, pia, pna, prb, pib, pnb);
-        rea += pra;
-        ima += pia;
-        nna += pna;
-        reb += prb;
-        imb += pib;
-        nnb += pnb;
+            step2(rfp + 4 * j, q[j], __ldg(e1p + j), __ldg(e2p + j), __ldg(php + j), pra, pna, prb, pnb);
+        fold(pra, pna, prb, pnb);
     }
     Apx2 r;
     double inv = rsqrt(nna);
