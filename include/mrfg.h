@@ -73,7 +73,10 @@ typedef struct {
     double bloch_ms, gemm_ms, rerank_ms, total_ms;
     double gemm_kernel_ms_avg; /* average duration of one K2 launch */
     int64_t gemm_launches;
-    double screen_err_max;     /* max |screen CC - exact CC| over re-ranked candidates (cc) */
+    double screen_err_max;     /* max |screen CC - exact CC| over re-ranked candidates (cc;
+                                  measured against the FP32 re-screen, +-1e-5, when it runs) */
+    int64_t rescreened32;      /* candidates scored by the certified FP32 walk before the
+                                  FP64 re-rank (0 when that stage is off); reranked = FP64 */
 } mrfg_scan_stats;
 
 /* ZoomConfig (zoom.hpp:23-52) as a POD; the step lists hold up to 8 values.

@@ -38,7 +38,7 @@ class ScanStats(C.Structure):
                 ("overflow_passes", C.c_int64), ("bloch_ms", C.c_double),
                 ("gemm_ms", C.c_double), ("rerank_ms", C.c_double), ("total_ms", C.c_double),
                 ("gemm_kernel_ms_avg", C.c_double), ("gemm_launches", C.c_int64),
-                ("screen_err_max", C.c_double)]
+                ("screen_err_max", C.c_double), ("rescreened32", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -364,9 +364,10 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
     }
     double err_max = 0;
     int r0 = tm.mark();
+    int64_t n32 = 0;
     int64_t nsel = rerank_and_select(c, tp, d_dict, c.q64.as<double>(), nq, metric, best,
                                      static_cast<float>(delta), c.cand.as<CandRec>(),
-                                     static_cast<int64_t>(ncand), d_out, &err_max, floored);
+                                     static_cast<int64_t>(ncand), d_out, &err_max, floored, &n32);
     int r1 = tm.mark();
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
     if (st) {
@@ -383,6 +384,7 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
         st->gemm_launches = gemm_launches;
         st->gemm_kernel_ms_avg = gemm_launches ? gemm_ms / gemm_launches : 0;
         st->screen_err_max = err_max;
+        st->rescreened32 = n32;
     }
 }
 

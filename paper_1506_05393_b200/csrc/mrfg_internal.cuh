@@ -172,7 +172,7 @@ void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qro
 int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, const double* d_q64,
                           int64_t nq, int metric, const float* d_best, float delta, CandRec* d_cand,
                           int64_t ncand, mrfg_match* d_out, double* err_max = nullptr,
-                          bool allow_missing = false);
+                          bool allow_missing = false, int64_t* stats_n32 = nullptr);
 // Stored float32 rows first + r*stride (r < count) -> fp16 operand (rows, zero
 // padded) + inv.
 void launch_dict_operand(Ctx& c, const float* d_dict, int64_t first, int64_t count, int64_t rows,

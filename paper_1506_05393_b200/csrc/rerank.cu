@@ -13,6 +13,7 @@
 #include <cstring>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 
 #include "mrfg_internal.cuh"
 #include "sim64.cuh"
@@ -76,6 +77,7 @@ __global__ void k_filter(const CandRec* __restrict__ cand, int64_t n, const floa
 // and the parameter-major table rows are shared or adjacent (the gathers,
 // not the FP64 pipe, bound the walk).
 constexpr int kFlatBits = 40;
+constexpr float kRescreenEps = 1e-5f;  // certification margin of the FP32 re-screen
 __global__ void k_rerank_keys(const CandRec* __restrict__ cand, const int64_t* __restrict__ list,
                               int64_t n, unsigned long long* __restrict__ keys) {
     int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -144,7 +146,7 @@ __global__ void k_rerank(Tab64 T, const double* __restrict__ q64, const CandRec*
     const double sc = exact_score(T, q64 + static_cast<int64_t>(r.voxel) * 2 * T.n, r.flat, metric);
     score[k] = sc;
     atomicMax(vkey + r.voxel, order_key(sc));
-    if (metric == MRFG_METRIC_CC) {
+    if (metric == MRFG_METRIC_CC && err_max) {
         const float e = fabsf(sqrtf(r.s) - static_cast<float>(sc));
         atomicMax(err_max, __float_as_uint(e));
     }
@@ -216,8 +218,93 @@ __global__ void __launch_bounds__(64) k_rerank1(Tab64 T, const double* __restric
         }
         score[k] = sc;
         atomicMax(vkey + r.voxel, order_key(sc));
-        if (metric == MRFG_METRIC_CC) atomicMax(err_max, __float_as_uint(fabsf(sqrtf(r.s) - static_cast<float>(sc))));
+        if (metric == MRFG_METRIC_CC && err_max)
+            atomicMax(err_max, __float_as_uint(fabsf(sqrtf(r.s) - static_cast<float>(sc))));
     }
+}
+
+// Certified FP32 re-screen (lattice scans, CC metric).  Every selected
+// candidate is walked once in FP32 over the float copies of the host-libm
+// tables (one thread per candidate, (voxel, flat) order), partial sums folded
+// into FP64 every 16 steps -- the K5 screening arithmetic, audited there at
+// <= 2.5e-7 from the exact score.  With eps = 1e-5 the exact argmax a* keeps
+// s32(a*) >= e(a*) - eps >= e(a) - eps >= s32(a) - 2 eps for every a, so only
+// candidates within 2 eps of their voxel's FP32 maximum go on to the FP64
+// re-rank (config 5: 7.1 M -> ~1e4).  The fp16 screening error is measured
+// against these scores.
+struct Tab32 {
+    const StepU* su;
+    const float4* e1f;
+    const float2* e2f;
+    const float4* phf;
+    float inv0[3];
+    int n;
+    Lattice L;
+};
+
+__global__ void __launch_bounds__(128) k_rescreen32(Tab32 T, const double* __restrict__ q64,
+                                                    const CandRec* __restrict__ cand,
+                                                    const int64_t* __restrict__ list, int64_t cnt,
+                                                    float* __restrict__ s32, unsigned* __restrict__ vmax,
+                                                    unsigned* __restrict__ err_max) {
+    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= cnt) return;
+    const CandRec r = cand[list[k]];
+    int i1, i2, idf;
+    unflatten(r.flat, T.L, i1, i2, idf);
+    const int n = T.n;
+    const float4* e1p = T.e1f + static_cast<int64_t>(i1) * n;
+    const float2* e2p = T.e2f + static_cast<int64_t>(i2) * n;
+    const float4* php = T.phf + static_cast<int64_t>(idf) * n;
+    const double2* q = reinterpret_cast<const double2*>(q64 + static_cast<int64_t>(r.voxel) * 2 * n);
+    float x = T.inv0[0], y = T.inv0[1], z = T.inv0[2];
+    double re = 0.0, im = 0.0, nn = 0.0;
+    float pr = 0.f, pi = 0.f, pn = 0.f;
+    for (int j = 0; j < n; ++j) {
+        const StepU& u = T.su[j];
+        const float4 ra = __ldg(reinterpret_cast<const float4*>(u.r));
+        const float4 rb = __ldg(reinterpret_cast<const float4*>(u.r) + 1);
+        const float r8 = __ldg(u.r + 8);
+        const float4 e1 = __ldg(e1p + j), ph = __ldg(php + j);
+        const float2 e2 = __ldg(e2p + j);
+        const double2 qd = __ldg(q + j);
+        const float qr = static_cast<float>(qd.x), qi = static_cast<float>(qd.y);
+        const float nx = fmaf(ra.x, x, fmaf(ra.y, y, ra.z * z));
+        const float ny = fmaf(ra.w, x, fmaf(rb.x, y, rb.y * z));
+        const float nz = fmaf(rb.z, x, fmaf(rb.w, y, r8 * z));
+        x = (nx * ph.x - ny * ph.y) * e2.x;
+        y = (nx * ph.y + ny * ph.x) * e2.x;
+        z = fmaf(nz, e1.x, e1.y);
+        pr = fmaf(qr, x, fmaf(qi, y, pr));
+        pi = fmaf(qi, x, fmaf(-qr, y, pi));
+        pn = fmaf(x, x, fmaf(y, y, pn));
+        const float rx = (x * ph.z - y * ph.w) * e2.y;
+        y = (x * ph.w + y * ph.z) * e2.y;
+        x = rx;
+        z = fmaf(z, e1.z, e1.w);
+        if ((j & 15) == 15) {
+            re += pr;
+            im += pi;
+            nn += pn;
+            pr = pi = pn = 0.f;
+        }
+    }
+    re += pr;
+    im += pi;
+    nn += pn;
+    const float sc = static_cast<float>(fmin(sqrt(re * re + im * im) / sqrt(nn), 1.0));
+    s32[k] = sc;
+    atomicMax(vmax + r.voxel, __float_as_uint(sc));  // scores >= 0: int order = float order
+    atomicMax(err_max, __float_as_uint(fabsf(sqrtf(r.s) - sc)));
+}
+
+__global__ void k_flag32(const CandRec* __restrict__ cand, const int64_t* __restrict__ list, int64_t cnt,
+                         const float* __restrict__ s32, const unsigned* __restrict__ vmax, float margin,
+                         unsigned char* __restrict__ flags) {
+    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= cnt) return;
+    const CandRec r = cand[list[k]];
+    flags[k] = s32[k] >= __uint_as_float(vmax[r.voxel]) - margin ? 1 : 0;
 }
 
 // brute_force_search over a stored dictionary: the reference scores the
@@ -357,7 +444,8 @@ void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qro
 // allow_missing (a score floor from another scan was applied).
 int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, const double* d_q64,
                           int64_t nq, int metric, const float* d_best, float delta, CandRec* d_cand,
-                          int64_t ncand, mrfg_match* d_out, double* err_max, bool allow_missing) {
+                          int64_t ncand, mrfg_match* d_out, double* err_max, bool allow_missing,
+                          int64_t* stats_n32) {
     // scratch layout: list, list2 (ncand i64) | keys, keys2 (ncand u64) |
     //                 score (ncand f64) | vkey, vflat (nq u64) | counters | sort temp
     const int vbits = std::max(1, 64 - __builtin_clzll(static_cast<unsigned long long>(std::max<int64_t>(nq, 2) - 1)));
@@ -379,7 +467,12 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
                                               static_cast<int64_t*>(nullptr), static_cast<int64_t*>(nullptr),
                                               cap, 0, end_bit, c.stream));
     sort_tmp = std::max(sort_tmp, sort_cap_tmp);
-    const size_t head = 40 * static_cast<size_t>(cap) + 16 * nq + 64;
+    size_t sel_tmp = 0;  // order-preserving compaction for the FP32 stage
+    MRFG_CUDA(cub::DeviceSelect::Flagged(nullptr, sel_tmp, static_cast<int64_t*>(nullptr),
+                                         static_cast<unsigned char*>(nullptr), static_cast<int64_t*>(nullptr),
+                                         static_cast<unsigned long long*>(nullptr), cap, c.stream));
+    sort_tmp = std::max(sort_tmp, sel_tmp);
+    const size_t head = 53 * static_cast<size_t>(cap) + 20 * nq + 64;
     size_t need = head + sort_tmp + 256;
     c.rerank.ensure(need);
     char* base = c.rerank.as<char>();
@@ -393,10 +486,14 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
     unsigned long long* cnt = vflat + nq;
     int* missing = reinterpret_cast<int*>(cnt + 1);
     unsigned int* d_err = reinterpret_cast<unsigned int*>(missing + 1);
+    unsigned long long* cnt32 = reinterpret_cast<unsigned long long*>(cnt + 2);
+    float* s32 = reinterpret_cast<float*>(base + 40 * static_cast<size_t>(cap) + 16 * nq + 64);
+    unsigned* vmax = reinterpret_cast<unsigned*>(s32 + cap);
+    unsigned char* flags = reinterpret_cast<unsigned char*>(vmax + nq);
     void* d_sort_tmp = base + (head + 255) / 256 * 256;
     MRFG_CUDA(cudaMemsetAsync(vkey, 0, sizeof(unsigned long long) * nq, c.stream));
     MRFG_CUDA(cudaMemsetAsync(vflat, 0xFF, sizeof(unsigned long long) * nq, c.stream));
-    MRFG_CUDA(cudaMemsetAsync(cnt, 0, 16, c.stream));
+    MRFG_CUDA(cudaMemsetAsync(cnt, 0, 24, c.stream));
     const int bs = 256;
     if (ncand > 0)
         k_filter<<<(ncand + bs - 1) / bs, bs, 0, c.stream>>>(d_cand, ncand, d_best, delta, metric,
@@ -416,6 +513,36 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
                                                   static_cast<int64_t>(nsel), 0, end_bit, c.stream));
         list = list2;
     }
+    // certified FP32 re-screen (lattice scans, CC): only near-ties go to FP64
+    const char* r32_env = std::getenv("MRFG_RERANK_FP32");  // "0": every candidate in FP64
+    int64_t n32 = 0;
+    if (nsel > 0 && t != nullptr && metric == MRFG_METRIC_CC && !(r32_env && r32_env[0] == '0')) {
+        n32 = static_cast<int64_t>(nsel);
+        Tab32 T32;
+        T32.su = t->stepu.as<StepU>();
+        T32.e1f = t->e1f.as<float4>();
+        T32.e2f = t->e2f.as<float2>();
+        T32.phf = t->phf.as<float4>();
+        T32.inv0[0] = static_cast<float>(c.inv64[2]);
+        T32.inv0[1] = static_cast<float>(c.inv64[5]);
+        T32.inv0[2] = static_cast<float>(c.inv64[8]);
+        T32.n = static_cast<int>(c.n);
+        T32.L = {t->grid.t1_ms.count, t->grid.t2_ms.count, t->grid.df_hz.count};
+        MRFG_CUDA(cudaMemsetAsync(vmax, 0, sizeof(unsigned) * nq, c.stream));
+        k_rescreen32<<<(nsel + 127) / 128, 128, 0, c.stream>>>(T32, d_q64, d_cand, list, nsel, s32, vmax, d_err);
+        MRFG_CUDA(cudaGetLastError());
+        k_flag32<<<(nsel + bs - 1) / bs, bs, 0, c.stream>>>(d_cand, list, nsel, s32, vmax, 2.0f * kRescreenEps,
+                                                            flags);
+        MRFG_CUDA(cudaGetLastError());
+        int64_t* out_list = list == list2 ? reinterpret_cast<int64_t*>(keys) : list2;
+        size_t tmp = sort_tmp;
+        MRFG_CUDA(cub::DeviceSelect::Flagged(d_sort_tmp, tmp, list, flags, out_list, cnt32,
+                                             static_cast<int64_t>(nsel), c.stream));
+        MRFG_CUDA(cudaMemcpyAsync(&nsel, cnt32, sizeof nsel, cudaMemcpyDeviceToHost, c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        list = out_list;
+    }
+    if (stats_n32) *stats_n32 = n32;
     if (nsel > 0) {
         if (d_dict) {
             k_rerank_dict<<<(nsel + rb - 1) / rb, rb, 0, c.stream>>>(
@@ -434,13 +561,14 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
             const bool one = e ? e[0] == '1' : scratch <= (size_t(2) << 30);
             if (!one) {
                 k_rerank<<<(nsel + rb - 1) / rb, rb, 0, c.stream>>>(tab64_of(c, *t), d_q64, d_cand, list,
-                                                                    nsel, metric, score, vkey, d_err);
+                                                                    nsel, metric, score, vkey,
+                                                                    n32 ? nullptr : d_err);
                 MRFG_CUDA(cudaGetLastError());
             } else {
             c.rerank_scratch.ensure(scratch);
             k_rerank1<<<static_cast<unsigned>(blocks), rb, 0, c.stream>>>(
                 tab64_of(c, *t), d_q64, d_cand, list, nsel, metric, c.rerank_scratch.as<double2>(), score, vkey,
-                d_err);
+                n32 ? nullptr : d_err);
             }
         }
         MRFG_CUDA(cudaGetLastError());

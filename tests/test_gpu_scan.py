@@ -109,6 +109,22 @@ def test_rerank_walk_modes(small, orc, monkeypatch, walk, metric):
     assert_parity(flat, score, oflat, oscore, osecond)
 
 
+@pytest.mark.parametrize("fp32", ["1", "0"])
+def test_rerank_fp32_rescreen(small, small_ref, monkeypatch, fp32):
+    """The certified FP32 re-screen only thins the FP64 re-rank: answers and
+    scores identical with and without it; near-ties still reach FP64."""
+    monkeypatch.setenv("MRFG_RERANK_FP32", fp32)
+    oflat, oscore, osecond = small_ref
+    with P.Context(small.schedule) as c:
+        flat, score, st = c.scan_grid(small.grid, small.fps)
+    assert_parity(flat, score, oflat, oscore, osecond)
+    if fp32 == "1":
+        assert st.rescreened32 >= st.reranked >= len(flat)
+        assert st.reranked < st.rescreened32
+    else:
+        assert st.rescreened32 == 0
+
+
 def test_scan_grid_config1_slice(small, small_ref):
     oflat, oscore, osecond = small_ref
     with P.Context(small.schedule) as c:

@@ -68,10 +68,10 @@ def main():
     ctxs = [P.Context(s) for s in scheds]
     for c in ctxs:
         c.set_stream(stream.cuda_stream)
-    # warm-up (like bench.py's W steps): one small scan per B1 context builds its
-    # schedule tables and loads every kernel before the timed region
+    # warm-up (like bench.py's W steps): one scan per B1 context builds its
+    # schedule tables, sizes its scratch and loads every kernel before the timed region
     for k, c in enumerate(ctxs):
-        c.scan_grid_device(g, d_q.data_ptr(), min(nvox, 512), d_all[k].data_ptr())
+        c.scan_grid_device(g, d_q.data_ptr(), nvox, d_all[k].data_ptr())
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
