@@ -8,8 +8,8 @@ timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err; echo "ref rc=$?"
 B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-zoom --atoms 4194304"
 timeout 600 $B > $O/short.json 2>&1; echo "short rc=$?"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
-    python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-zoom > /dev/null 2>&1; echo "launches rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file $O/launches.csv \
+    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-zoom > /dev/null 2>&1; echo "launches rc=$?"
 # gpurun copies back <= 64 MiB: export the pages as CSV on the box and keep
 # only small reports
 export_rep() {
@@ -19,7 +19,7 @@ export_rep() {
   gzip -f $O/$1_sass.csv $O/$1_raw.csv
   [ $(stat -c %s $O/$1.ncu-rep) -gt 12000000 ] && rm -f $O/$1.ncu-rep
 }
-for spec in "k2:regex:k_match_sm100_2cta:4" "k1:regex:k_bloch_rows2:4" "k3:regex:^k_rerank1\$:0"; do
+for spec in "k2:regex:k_match_sm100_2cta:4" "k1:regex:k_bloch_rows2:4" "k3:regex:^k_rescreen32\$:0"; do
   IFS=: read name kind pat skip <<< "$spec"
   timeout 900 ncu --set full --import-source on --clock-control none -k "regex:$pat" -s $skip -c 1 \
       -o $O/ncu_$name $B > $O/ncu_$name.log 2>&1; echo "ncu $name rc=$?"
