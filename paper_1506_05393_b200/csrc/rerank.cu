@@ -312,8 +312,8 @@ __global__ void k_flag32(const CandRec* __restrict__ cand, const int64_t* __rest
 __device__ double exact_score_entry(const double* __restrict__ q, const float* __restrict__ e, int n,
                                     int metric) {
     double re = 0.0, im = 0.0, dd = 0.0;
-    for (int j = 0; j < n; ++j) {
-        const double er = static_cast<double>(e[2 * j]), ei = static_cast<double>(e[2 * j + 1]);
+    auto acc = [&](int j, float erf, float eif) {
+        const double er = static_cast<double>(erf), ei = static_cast<double>(eif);
         const double qr = q[2 * j], qi = q[2 * j + 1];
         if (metric == MRFG_METRIC_CC) {
             re = __dadd_rn(re, __dadd_rn(__dmul_rn(qr, er), __dmul_rn(qi, ei)));
@@ -322,7 +322,22 @@ __device__ double exact_score_entry(const double* __restrict__ q, const float* _
             const double dr = __dsub_rn(qr, er), di = __dsub_rn(qi, ei);
             dd = __dadd_rn(dd, __dadd_rn(__dmul_rn(dr, dr), __dmul_rn(di, di)));
         }
+    };
+    int j = 0;
+    // whole 32-byte sectors per lane (4 steps = two float4 loads) when the
+    // entry row is 16-byte aligned (n even); the lanes of a warp read
+    // different rows, so 8-byte loads used a quarter of every sector
+    if ((reinterpret_cast<uintptr_t>(e) & 15) == 0) {
+        const float4* e4 = reinterpret_cast<const float4*>(e);
+        for (; j + 4 <= n; j += 4) {
+            const float4 a = __ldg(e4 + j / 2), b = __ldg(e4 + j / 2 + 1);
+            acc(j, a.x, a.y);
+            acc(j + 1, a.z, a.w);
+            acc(j + 2, b.x, b.y);
+            acc(j + 3, b.z, b.w);
+        }
     }
+    for (; j < n; ++j) acc(j, e[2 * j], e[2 * j + 1]);
     if (metric == MRFG_METRIC_CC) {
         const double v = sqrt(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
         return v < 1.0 ? v : 1.0;
