@@ -210,6 +210,43 @@ __device__ __noinline__ void record_hit(const Dev& p, float bst, int64_t v, int6
     if (su > bst) atomic_max_float(p.best + v, su);
 }
 
+// Warp-aggregated candidate append for one 32-column block of the epilogue:
+// lane l holds the hit mask of its atom over the block's 32 voxels.  One
+// atomicAdd per warp reserves the warp's slots (warp prefix sum of the
+// per-lane counts) instead of one contended atomic per hit on the single
+// global counter (config 3 records 1.2e8 candidates); returns this lane's
+// first slot.
+__device__ __noinline__ unsigned long long reserve_hits(const Dev& p, uint32_t hits) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int mine = __popc(hits);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(full, incl, o);
+        if (lane >= o) incl += t;
+    }
+    unsigned long long base = 0;
+    if (lane == 31 && p.cand != nullptr && incl > 0)
+        base = atomicAdd(p.cand_count, static_cast<unsigned long long>(incl));
+    base = __shfl_sync(full, base, 31);
+    return base + static_cast<unsigned long long>(incl - mine);
+}
+
+// One reserved hit: the candidate record and the running maximum.
+__device__ __noinline__ void store_hit(const Dev& p, float bst, int64_t v, int64_t atom, float sc,
+                                       unsigned long long idx) {
+    if (p.cand != nullptr && idx < static_cast<unsigned long long>(p.cand_cap)) {
+        CandRec rec;
+        rec.voxel = static_cast<uint32_t>(v);
+        rec.s = sc;
+        rec.flat = p.flat_base + atom * p.flat_stride;
+        p.cand[idx] = rec;
+    }
+    const float su = unsquare(sc, p.metric);
+    if (su > bst) atomic_max_float(p.best + v, su);
+}
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_match_sm100(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                   Dev p) {
@@ -335,9 +372,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 if (!avalid) hits = 0;
                 if (__any_sync(0xffffffffu, hits != 0)) {
+                    unsigned long long slot = reserve_hits(p, hits);
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
-                        if ((hits >> i) & 1u) record_hit(p, s.bst[acc][q * 32 + i], vt * 128 + q * 32 + i, atom, sc[i]);
+                        if ((hits >> i) & 1u)
+                            store_hit(p, s.bst[acc][q * 32 + i], vt * 128 + q * 32 + i, atom, sc[i], slot++);
                 }
             }
             tc_fence_before();
@@ -555,9 +594,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 }
                 if (!avalid) hits = 0;
                 if (__any_sync(0xffffffffu, hits != 0)) {
+                    unsigned long long slot = reserve_hits(p, hits);
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
-                        if ((hits >> i) & 1u) record_hit(p, s.bst[acc][q * 32 + i], vt * 128 + q * 32 + i, atom, sc[i]);
+                        if ((hits >> i) & 1u)
+                            store_hit(p, s.bst[acc][q * 32 + i], vt * 128 + q * 32 + i, atom, sc[i], slot++);
                 }
             }
             tc_fence_before();
