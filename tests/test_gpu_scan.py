@@ -61,7 +61,7 @@ def test_screen_close_to_exact_cc2(orc, small):
 
 
 @pytest.mark.parametrize("k1,apt", [("fold", "2"), ("fold", "4"), ("fold", "8"), ("rows", "4"), ("rows", "8"),
-                                    ("rows2", "4")])
+                                    ("rows2", "4"), ("rows2", "8")])
 def test_screen_production_producer(orc, small, monkeypatch, k1, apt):
     """The GEMM operand of the production K1 (scan_grid's producer) screens
     within fp16 rounding of the exact CC; ranges start and end mid-row and
