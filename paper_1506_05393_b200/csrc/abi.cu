@@ -261,6 +261,15 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
 
     double gemm_ms = 0, bloch_ms = 0;
     int64_t gemm_launches = 0, chunks = 0;
+    // Voxel batch: query rows of <= ~40 MB (L2 is 126 MB).  Measured on config 3
+    // (stored dictionary): the GEMM runs at 1,255 / 1,039 / 890 TFLOP/s with
+    // 33 MB / 134 MB / 2.1 GB of query rows.  MRFG_VOX_BATCH overrides (0 = all).
+    int64_t vox_batch = std::max<int64_t>(128, (int64_t(40) << 20) / (4 * kp) / 128 * 128);
+    if (const char* e = std::getenv("MRFG_VOX_BATCH")) {
+        const int64_t v = std::atoll(e);
+        vox_batch = v > 0 ? std::max<int64_t>(128, v / 128 * 128) : nq;
+    }
+    if (vox_batch >= nq) vox_batch = nq;
     // Seed pass: a strided sample of the range raises the running maxima
     // before the stream starts (no candidates are recorded).
     {
@@ -339,9 +348,20 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
             mp.valid_atoms = ve - base;
             mp.flat_base = base;
             mp.flat_stride = 1;
-            gm.push_back(tm.mark());
-            launch_match(c, mp);
-            gm.push_back(tm.mark());
+            // voxel batches whose query rows stay L2-resident (the chunk's atom
+            // operand is re-read from HBM per batch instead of every query
+            // tile per atom tile)
+            for (int64_t v0 = 0; v0 < nq; v0 += vox_batch) {
+                const int64_t nvb = std::min(vox_batch, nq - v0);
+                mp.b = c.qprime.as<__half>() + 2 * v0 * kp;
+                mp.q_rows = round_up(2 * nvb, 256);
+                mp.nvox = nvb;
+                mp.best = best + v0;
+                mp.vox_base = v0;
+                gm.push_back(tm.mark());
+                launch_match(c, mp);
+                gm.push_back(tm.mark());
+            }
             MRFG_CUDA(cudaEventRecord(c.ev[2 + b], S));
             ++chunks;
         }
@@ -355,6 +375,11 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
         }
         mp.a = c.atoms_a.as<__half>();
         mp.inv2 = c.inv2.as<float>();
+        mp.b = c.qprime.as<__half>();
+        mp.q_rows = qrows;
+        mp.nvox = nq;
+        mp.best = best;
+        mp.vox_base = 0;
         if (ncand <= static_cast<unsigned long long>(cap)) break;
         // Overflow: the running maxima are now final, so a second pass records
         // a subset of the first pass's candidates; size the buffer for all.

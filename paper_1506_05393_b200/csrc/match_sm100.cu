@@ -51,6 +51,7 @@ constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
 
 struct Dev {
     const float* inv2;
+    int64_t vox_base;  // global index of this launch's voxel 0 (candidate records)
     int64_t n_at, n_vt, nkb, last_sub;
     int64_t ga;  // tile raster: 1 = atom-major; > 1 = groups of ga atom tiles per query tile
     int64_t valid_atoms, valid_begin, nvox, flat_base, flat_stride;
@@ -196,7 +197,7 @@ __device__ __forceinline__ void push_candidate(const Dev& p, int64_t v, int64_t 
         unsigned long long idx = atomicAdd(p.cand_count, 1ull);
         if (idx < static_cast<unsigned long long>(p.cand_cap)) {
             CandRec rec;
-            rec.voxel = static_cast<uint32_t>(v);
+            rec.voxel = static_cast<uint32_t>(p.vox_base + v);
             rec.s = s;
             rec.flat = p.flat_base + atom * p.flat_stride;
             p.cand[idx] = rec;
@@ -238,7 +239,7 @@ __device__ __noinline__ void store_hit(const Dev& p, float bst, int64_t v, int64
                                        unsigned long long idx) {
     if (p.cand != nullptr && idx < static_cast<unsigned long long>(p.cand_cap)) {
         CandRec rec;
-        rec.voxel = static_cast<uint32_t>(v);
+        rec.voxel = static_cast<uint32_t>(p.vox_base + v);
         rec.s = sc;
         rec.flat = p.flat_base + atom * p.flat_stride;
         p.cand[idx] = rec;
@@ -675,6 +676,7 @@ CUtensorMap make_map(Ctx& c, const __half* base, int64_t rows, int64_t k_pad, in
 Dev dev_of(const MatchParams& p, int64_t k_valid) {
     Dev d;
     d.inv2 = p.inv2;
+    d.vox_base = p.vox_base;
     d.n_at = p.atoms / BM;
     d.n_vt = p.q_rows / BN;
     d.nkb = p.k_pad / BK;

@@ -152,6 +152,7 @@ struct MatchParams {
     int64_t valid_begin;
     int64_t nvox;
     int64_t flat_base, flat_stride;  // global flat of local atom r = flat_base + r*flat_stride
+    int64_t vox_base;   // global index of voxel 0 of b / best (voxel batches)
     float* best;        // nvox running max (screening units)
     CandRec* cand;      // may be null (seed pass)
     unsigned long long* cand_count;

@@ -125,6 +125,19 @@ def test_rerank_fp32_rescreen(small, small_ref, monkeypatch, fp32):
         assert st.rescreened32 == 0
 
 
+@pytest.mark.parametrize("batch", ["128", "256"])
+def test_scan_voxel_batches(small, small_ref, monkeypatch, batch):
+    """Voxel-batched screening (query rows kept L2-resident): same answers."""
+    monkeypatch.setenv("MRFG_VOX_BATCH", batch)
+    oflat, oscore, osecond = small_ref
+    with P.Context(small.schedule) as c:
+        flat, score, st = c.scan_grid(small.grid, small.fps)
+        dflat, dscore, _ = c.brute_force_search(small.fps, c.generate(small.grid, precision=64))
+    assert_parity(flat, score, oflat, oscore, osecond)
+    np.testing.assert_array_equal(dflat, flat)
+    np.testing.assert_array_equal(dscore, score)
+
+
 def test_scan_grid_config1_slice(small, small_ref):
     oflat, oscore, osecond = small_ref
     with P.Context(small.schedule) as c:
