@@ -400,7 +400,11 @@ def run_ours(args, world, rank, local):
                      "flop_per_launch": 8.0 * n * nq * args.chunk},
         "e2e": {"value": nq * total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nq * n * 16,
                 "d2h_bytes_per_step": nq * 16, "seconds_per_step": e2e_s},
-        "gpu_launches": int(sum(2 * s.chunks + 8 for s in stats) + (args.steps if world > 1 else 0)),
+        # our kernels per scan: per chunk K1 + K2 (+ k_zero_rows for the chunk's
+        # edge rows); seed pass (table producer + K2), k_fill, query prep;
+        # re-rank: filter, keys, FP32 re-screen, flag, FP64 re-rank, select,
+        # write (CUB sort/select kernels not counted); + k_merge when N > 1
+        "gpu_launches": int(sum(3 * s.chunks + 11 for s in stats) + (args.steps if world > 1 else 0)),
         "clocks": clk.summary(),
         "zoom": zoom,
     }
