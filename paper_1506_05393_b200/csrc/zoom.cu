@@ -1798,12 +1798,15 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     {
         const char* e1 = std::getenv("MRFG_ZOOM_SPEC1D");
         const char* e2 = std::getenv("MRFG_ZOOM_SPEC2D");
-        P.spec1d = e1 ? std::max(1, std::atoi(e1)) : 16;
-        P.spec2d = e2 ? std::max(1, std::atoi(e2)) : 2;
+        // speculation widths, re-measured after the packed screening step
+        // (ms, config 2 / config 4): 1-D/2-D 8/1: 17.4 / 66.6-67.1;
+        // 16/2: 19.1-19.3 / 67.6-68.3.  The helper-warp (rows) kernel keeps 16/2.
+        P.spec1d = e1 ? std::max(1, std::atoi(e1)) : 8;
+        P.spec2d = e2 ? std::max(1, std::atoi(e2)) : 1;
         const char* c1 = std::getenv("MRFG_ZOOM_SPEC1D_CTA");
         const char* c2 = std::getenv("MRFG_ZOOM_SPEC2D_CTA");
-        P.spec1d_cta = c1 ? std::max(1, std::atoi(c1)) : P.spec1d;
-        P.spec2d_cta = c2 ? std::max(1, std::atoi(c2)) : P.spec2d;
+        P.spec1d_cta = c1 ? std::max(1, std::atoi(c1)) : (e1 ? P.spec1d : 16);
+        P.spec2d_cta = c2 ? std::max(1, std::atoi(c2)) : (e2 ? P.spec2d : 2);
         const char* sm = std::getenv("MRFG_ZOOM_SCREEN");
         const std::string smode = sm ? sm : "";
         P.screen_mode = smode == "mufu" ? 1 : 0;
