@@ -107,6 +107,29 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: launch N NCCL ranks (one process
+    per GPU) through torch.distributed.run on 127.0.0.1 and relay rank 0's
+    line.  Fails when fewer than N GPUs are visible."""
+    import socket
+    try:
+        import torch
+        ngpu = torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        ngpu = 0
+    if ngpu < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {ngpu}"}),
+              flush=True)
+        return 1
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -137,7 +160,12 @@ def shard(total: int, world: int, rank: int):
 
 # ------------------------------------------------------------- CPU baseline
 def cpu_sample(config: int, nvox_sample: int, which: str | None = None):
-    """Reference CPU path on a bounded sample: nvox_sample voxels x one T1 slab."""
+    """Reference CPU path on a bounded sample: nvox_sample voxels x one T1 slab
+    (all T2 x df atoms at one T1 value), on ALL host cores: the reference's own
+    mrf::generate for the slab's rows (row-parallel) and mrf::brute_force_search
+    per voxel (voxel-parallel) -- SURVEY 8(d)'s plan, since scan_grid's own
+    scan loop is serial over queries (dictionary.cpp:283-299).  The C
+    restatement stands in where the reference library was not built."""
     import oracle
     from paper_1506_05393_b200 import workloads
     kind = which or ("reference" if oracle.available("reference") else "restatement")
@@ -149,8 +177,6 @@ def cpu_sample(config: int, nvox_sample: int, which: str | None = None):
     nd = int(round((c["df"][1] - c["df"][0]) / c["df"][2])) + 1
     i1 = n1 // 2
     t1v = c["t1"][0] + i1 * c["t1"][2]
-    slab = oracle.make_grid((t1v, c["t1"][2], 1), (c["t2"][0], c["t2"][2], n2),
-                            (c["df"][0], c["df"][2], nd))
     # queries: noisy on-grid fingerprints (uniform over the grid, SNR as configured)
     rng_idx = [(k * 7919) % (n1 * n2 * nd) for k in range(nvox_sample)]
     fps = []
@@ -163,14 +189,24 @@ def cpu_sample(config: int, nvox_sample: int, which: str | None = None):
         fps.append(orc.add_noise(fp, sigma, 1_000_000 + k))
     fps = np.stack(fps)
     threads = os.cpu_count() or 1
+    t2v = c["t2"][0] + np.arange(n2, dtype=np.float64) * c["t2"][2]
     t0 = time.perf_counter()
-    orc.scan_grid(s, slab, fps, threads=threads)
+    if kind == "reference":
+        orc.scan_rows(s, np.array([t1v]), t2v, (c["df"][0], c["df"][2], nd), fps, threads=threads)
+        how = "mrf::generate rows + mrf::brute_force_search, voxel-parallel"
+    else:
+        import concurrent.futures as cf
+        slab = oracle.make_grid((t1v, c["t1"][2], 1), (c["t2"][0], c["t2"][2], n2), (c["df"][0], c["df"][2], nd))
+        with cf.ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda b: orc.scan_grid(s, slab, fps[b], threads=1),
+                        np.array_split(np.arange(nvox_sample), threads)))
+        how = "C restatement scan_grid, voxel blocks in parallel"
     dt = time.perf_counter() - t0
     evals = nvox_sample * n2 * nd
     return {"value": evals / dt, "unit": UNIT, "cores": threads,
             "kind": "reference" if kind == "reference" else "port",
-            "sample": f"scan_grid of {nvox_sample} noisy config-{config} voxels over one T1 slab "
-                      f"({n2 * nd} atoms, N={c['n']}), simulate+match, {dt:.2f} s"}
+            "sample": f"{nvox_sample} noisy config-{config} voxels x one T1 slab ({n2 * nd} atoms, "
+                      f"N={c['n']}), simulate+match ({how}, {threads} threads), {dt:.2f} s"}
 
 
 def arm_config(args, world, nx, ny, n, nq, total):
@@ -178,7 +214,7 @@ def arm_config(args, world, nx, ny, n, nq, total):
     return {"workload": f"BASELINE configs[{args.config - 1}]: {nx}x{ny} slice, N={n}, "
                         f"{total} atoms, brute-force streamed DGS",
             "voxels": nq, "atoms": total, "timepoints": n, "chunk_atoms": args.chunk,
-            "delta": args.delta, "parallelism": f"atom-shard x{world}",
+            "delta": args.delta or 2.5e-3, "parallelism": f"atom-shard x{world}",
             "l2": "256 MB flush per step; each step streams >100 GB of fp16 atoms"}
 
 
@@ -300,7 +336,7 @@ def run_ours(args, world, rank, local):
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
-    e2e_steps = max(1, min(args.steps, 2))
+    e2e_steps = max(1, args.steps)
     for _ in range(e2e_steps):
         e2e_step()
     torch.cuda.synchronize()
@@ -393,6 +429,12 @@ def run_ours(args, world, rank, local):
                                   "rerank": sum(s.rerank_ms for s in stats) / len(stats),
                                   "scan_total": sum(s.total_ms for s in stats) / len(stats)},
         "screen_err_max": max(s.screen_err_max for s in stats),
+        "screen_audit": {"err_max": max(s.screen_err_audit_max for s in stats),
+                         "rescreen32_err_max": max(s.rescreen_err_audit_max for s in stats),
+                         "samples_per_step": stats[-1].audit_samples,
+                         "delta": stats[-1].delta_used, "rescans": sum(s.rescans for s in stats),
+                         "rule": "hash sample of ALL screened (voxel, atom) pairs, scored exactly; "
+                                 "certificate needs err_max <= delta/2"},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
                      "frac": gemm_tflops / peak_t, "traffic": k2_traffic(args, n, nq),
                      "kernel": "k_match_sm100_2cta (K2)", "peak_kind": f"{pk_kind} bf16 dense sustained",
@@ -403,8 +445,9 @@ def run_ours(args, world, rank, local):
         # our kernels per scan: per chunk K1 + K2 (+ k_zero_rows for the chunk's
         # edge rows); seed pass (table producer + K2), k_fill, query prep;
         # re-rank: filter, keys, FP32 re-screen, flag, FP64 re-rank, select,
-        # write (CUB sort/select kernels not counted); + k_merge when N > 1
-        "gpu_launches": int(sum(3 * s.chunks + 11 for s in stats) + (args.steps if world > 1 else 0)),
+        # FP32 error check, write (CUB sort/select kernels not counted); the
+        # screening audit; + seed pass and k_merge when N > 1
+        "gpu_launches": int(sum(3 * s.chunks + 13 for s in stats) + (3 * args.steps if world > 1 else 0)),
         "clocks": clk.summary(),
         "zoom": zoom,
     }
@@ -428,12 +471,16 @@ def main():
     ap.add_argument("--nvox", type=int, default=None)
     ap.add_argument("--atoms", type=int, default=0, help="limit atoms (debug only)")
     ap.add_argument("--chunk", type=int, default=524288)
-    ap.add_argument("--delta", type=float, default=1e-3)
-    ap.add_argument("--ref-voxels", type=int, default=16)
+    ap.add_argument("--delta", type=float, default=0.0, help="screening margin (0: library default 2.5e-3)")
+    ap.add_argument("--ref-voxels", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-zoom", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     world, rank, local = dist_setup(args)
+    if world != args.gpus and rank == 0:
+        print(f"[bench] note: --gpus {args.gpus} but WORLD_SIZE {world}; using {world}", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:

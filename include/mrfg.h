@@ -44,8 +44,16 @@ enum { MRFG_METRIC_CC = 0, MRFG_METRIC_EUCLIDEAN = 1 }; /* Metric, dictionary.hp
 
 typedef struct mrfg_ctx mrfg_ctx;
 
-/* AxisSpec (dictionary.hpp:17-24): values min + k*step, k < count. */
-typedef struct { double min, step; int64_t count; } mrfg_axis;
+/* AxisSpec (dictionary.hpp:17-24): values min + k*step, k < count.
+ * `values` (optional, may be NULL): count explicit axis values that replace
+ * min + k*step -- e.g. the log-spaced T1/T2 axes of BASELINE configs[2],
+ * which a ParameterGrid cannot express (the reference builds those
+ * dictionaries from explicit TissueParams, value[k] ms * 1e-3 s).  Supported
+ * on the T1 and T2 axes of generate / scan_grid / cc_map; the df axis and
+ * ZOOM lattices must be evenly spaced.  Tables are computed from the values
+ * with host libm, so FP64 entries equal the reference's simulate() of the
+ * same TissueParams bit for bit. */
+typedef struct { double min, step; int64_t count; const double* values; } mrfg_axis;
 /* ParameterGrid (dictionary.hpp:34-56): T1 outer, T2 middle, df inner;
  * flat = (i1*n2 + i2)*ndf + idf. */
 typedef struct { mrfg_axis t1_ms, t2_ms, df_hz; } mrfg_grid;
@@ -56,7 +64,8 @@ typedef struct { int64_t flat; double score; } mrfg_match;
 /* Screening/streaming knobs of the brute-force path (no reference analogue;
  * zero fields take defaults). */
 typedef struct {
-    double delta;          /* screening margin in CC units (default 1e-3) */
+    double delta;          /* screening margin in CC units (default 2.5e-3: twice the analytic
+                              bound on the fp16 screening error) */
     int64_t chunk_atoms;   /* atoms simulated per streamed chunk (default 524288) */
     int64_t cand_capacity; /* candidate buffer entries (default 1<<25) */
     int64_t seed_atoms;    /* strided pre-pass atoms that seed the running max (default 16384) */
@@ -65,6 +74,10 @@ typedef struct {
      * screening maxima, so only atoms that can still win are re-ranked; a
      * query with no atom above its floor returns flat -1 (merge skips it). */
     const mrfg_match* floor_matches;
+    /* Optional HOST array of nq flags: 1 = the query is already unit norm
+     * (Fingerprint::unit_norm) and is scored as given, without the FP64
+     * normalization of prep_query (dictionary.cpp:145-150). */
+    const uint8_t* unit_queries;
 } mrfg_scan_opts;
 
 /* What one scan did (device-timed with CUDA events on the ctx stream). */
@@ -77,6 +90,16 @@ typedef struct {
                                   measured against the FP32 re-screen, +-1e-5, when it runs) */
     int64_t rescreened32;      /* candidates scored by the certified FP32 walk before the
                                   FP64 re-rank (0 when that stage is off); reranked = FP64 */
+    /* Unbiased screening audit (metric cc): a hash-sampled subset of ALL
+     * screened (voxel, atom) pairs, whatever their screening score, is scored
+     * exactly.  screen_err_audit_max = max |fp16 screen CC - exact CC| over it;
+     * rescreen_err_audit_max = max |FP32 re-screen - exact| (lattice scans).
+     * A scan whose audit exceeds delta/2 is repeated with a wider margin
+     * (rescans); one whose FP32 re-screen error exceeds half its margin
+     * re-ranks every candidate in FP64. */
+    double screen_err_audit_max, rescreen_err_audit_max, delta_used;
+    int64_t audit_samples, rescans;
+    double rescreen_err_max;   /* max |FP32 re-screen - exact| over the FP64 survivors */
 } mrfg_scan_stats;
 
 /* ZoomConfig (zoom.hpp:23-52) as a POD; the step lists hold up to 8 values.
@@ -184,6 +207,17 @@ int mrfg_scan_dict(mrfg_ctx* ctx, const float* dict, int64_t natoms, const doubl
 int mrfg_scan_dict_dev(mrfg_ctx* ctx, const float* d_dict, int64_t natoms, int64_t flat_begin,
                        int64_t flat_end, const double* d_queries, int64_t nq, int metric,
                        const mrfg_scan_opts* opts, mrfg_match* d_out, mrfg_scan_stats* stats);
+/* Seed pass only (multi-GPU / multi-device sharding): the screening maxima
+ * (CC units, float, nq) of a strided sample of flats [flat_begin, flat_end)
+ * of the lattice (grid) or of a device dictionary (d_dict, natoms) -- the
+ * maxima a scan of that range starts from.  Maxima of all shards, reduced by
+ * max and passed back as floor_matches (flat 0, score = maximum), seed every
+ * shard's screening with the GLOBAL sample, so per-shard candidate and
+ * re-rank work does not grow with the number of shards; the screening
+ * certificate holds for any seed. */
+int mrfg_scan_seed_dev(mrfg_ctx* ctx, const mrfg_grid* grid, const float* d_dict, int64_t natoms,
+                       int64_t flat_begin, int64_t flat_end, const double* d_queries, int64_t nq, int metric,
+                       const mrfg_scan_opts* opts, float* d_seed, mrfg_scan_stats* stats);
 /* C1: merge per-rank matches gathered as d_in[rank*nq + q] (max score,
  * lowest flat on ties) -- the reduction after the NCCL allgather. */
 int mrfg_merge_matches_dev(mrfg_ctx* ctx, const mrfg_match* d_in, int nranks, int64_t nq,

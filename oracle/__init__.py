@@ -139,6 +139,8 @@ class Oracle:
                                    C.POINTER(C.c_float)]
         L.orc_scan_grid.argtypes = [C.POINTER(Sched), C.POINTER(Grid), dp, i64, C.c_int,
                                     C.c_int, C.POINTER(i64), dp, dp]
+        L.orc_scan_grid_ex.argtypes = [C.POINTER(Sched), C.POINTER(Grid), dp, C.POINTER(C.c_uint8), i64,
+                                       C.c_int, C.c_int, C.POINTER(i64), dp, dp]
         L.orc_quantify.argtypes = [C.POINTER(Sched), C.POINTER(Grid), C.POINTER(ZoomCfg), dp,
                                    C.POINTER(Quant)]
         L.orc_quantify_slice.argtypes = [C.POINTER(Sched), C.POINTER(Grid),
@@ -152,6 +154,8 @@ class Oracle:
         if which == "reference":
             L.orc_ref_save_generated.argtypes = [C.POINTER(Sched), C.POINTER(Grid), C.c_char_p]
             L.orc_ref_cc_map_to_file.argtypes = [C.POINTER(Sched), C.POINTER(Grid), dp, C.c_char_p]
+            L.orc_ref_scan_rows.argtypes = [C.POINTER(Sched), dp, i64, dp, i64, C.POINTER(Axis), dp, i64,
+                                            C.c_int, C.c_int, C.POINTER(i64), dp]
 
     def _check(self, rc: int) -> None:
         if rc != 0:
@@ -235,6 +239,25 @@ class Oracle:
         self._check(self.lib.orc_ref_cc_map_to_file(C.byref(cs), C.byref(g), self._dp(fp.view(np.float64)),
                                                     str(path).encode()))
 
+    def scan_rows(self, s: Schedule, t1_ms: np.ndarray, t2_ms: np.ndarray, df: tuple,
+                  queries: np.ndarray, metric: int = 0, threads: int = 0):
+        """Reference library only: argmax over explicit T1 x T2 values x a linear
+        df axis (min, step, count) with mrf::generate rows + mrf::brute_force_search
+        (ref_capi.cpp orc_ref_scan_rows).  -> (flat, score)."""
+        q = np.ascontiguousarray(queries, dtype=np.complex128)
+        t1 = np.ascontiguousarray(t1_ms, dtype=np.float64)
+        t2 = np.ascontiguousarray(t2_ms, dtype=np.float64)
+        nq = q.shape[0]
+        flat = np.zeros(nq, dtype=np.int64)
+        score = np.zeros(nq)
+        cs = s.c()
+        ax = Axis(*df)
+        self._check(self.lib.orc_ref_scan_rows(
+            C.byref(cs), self._dp(t1), len(t1), self._dp(t2), len(t2), C.byref(ax),
+            self._dp(q.view(np.float64)), nq, metric, threads or os.cpu_count() or 1,
+            flat.ctypes.data_as(C.POINTER(C.c_int64)), self._dp(score)))
+        return flat, score
+
     def generate(self, s: Schedule, g: Grid, first: int, count: int) -> np.ndarray:
         out = np.zeros((count, 2 * s.n), dtype=np.float32)
         cs = s.c()
@@ -243,7 +266,8 @@ class Oracle:
         return out
 
     def scan_grid(self, s: Schedule, g: Grid, queries: np.ndarray, metric: int = 0,
-                  threads: int = 0):
+                  threads: int = 0, unit_norm=None):
+        """unit_norm: None, or per-query flags (Fingerprint::unit_norm: used as given)."""
         q = np.ascontiguousarray(queries, dtype=np.complex128)
         nq = q.shape[0]
         flat = np.zeros(nq, dtype=np.int64)
@@ -251,10 +275,14 @@ class Oracle:
         second = np.zeros(nq)
         cs = s.c()
         threads = threads or os.cpu_count() or 1
-        self._check(self.lib.orc_scan_grid(C.byref(cs), C.byref(g), self._dp(q.view(np.float64)),
-                                           nq, metric, threads,
-                                           flat.ctypes.data_as(C.POINTER(C.c_int64)),
-                                           self._dp(score), self._dp(second)))
+        unit = None
+        if unit_norm is not None:
+            unit = np.ascontiguousarray(np.broadcast_to(np.asarray(unit_norm, dtype=np.uint8), (nq,)))
+        self._check(self.lib.orc_scan_grid_ex(C.byref(cs), C.byref(g), self._dp(q.view(np.float64)),
+                                              None if unit is None else unit.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                              nq, metric, threads,
+                                              flat.ctypes.data_as(C.POINTER(C.c_int64)),
+                                              self._dp(score), self._dp(second)))
         return flat, score, second
 
     def quantify(self, s: Schedule, g: Grid, cfg: ZoomCfg, fp: np.ndarray) -> Quant:

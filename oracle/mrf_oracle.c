@@ -447,6 +447,13 @@ static double dist_against_entry(const double* q, const float* e, int64_t n) {
 int orc_scan_grid(const orc_sched* s, const orc_grid* g, const double* queries, int64_t nq,
                   int metric, int threads, int64_t* best_flat, double* best_score,
                   double* second_score) {
+    return orc_scan_grid_ex(s, g, queries, NULL, nq, metric, threads, best_flat, best_score, second_score);
+}
+
+/* prep_query (dictionary.cpp:145-150): `fp.unit_norm ? fp : normalize(fp)`. */
+int orc_scan_grid_ex(const orc_sched* s, const orc_grid* g, const double* queries, const uint8_t* unit,
+                     int64_t nq, int metric, int threads, int64_t* best_flat, double* best_score,
+                     double* second_score) {
     if (nq <= 0) return fail("scan_grid: no queries");
     Sim sim;
     if (sim_init(&sim, s)) {
@@ -455,12 +462,17 @@ int orc_scan_grid(const orc_sched* s, const orc_grid* g, const double* queries, 
     }
     int64_t n = s->n;
     double* q = malloc(sizeof(double) * 2 * (size_t)(n * nq));
-    for (int64_t iq = 0; iq < nq; ++iq)
+    for (int64_t iq = 0; iq < nq; ++iq) {
+        if (unit && unit[iq]) {
+            memcpy(q + iq * 2 * n, queries + iq * 2 * n, sizeof(double) * 2 * (size_t)n);
+            continue;
+        }
         if (normalize(queries + iq * 2 * n, n, q + iq * 2 * n)) {
             free(q);
             sim_free(&sim);
             return -1;
         }
+    }
     double* best = malloc(sizeof(double) * (size_t)nq);
     double* second = malloc(sizeof(double) * (size_t)nq);
     for (int64_t iq = 0; iq < nq; ++iq) {

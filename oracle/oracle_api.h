@@ -72,6 +72,11 @@ int orc_generate(const orc_sched* s, const orc_grid* g, int64_t first, int64_t c
 int orc_scan_grid(const orc_sched* s, const orc_grid* g, const double* queries, int64_t nq,
                   int metric, int threads, int64_t* best_flat, double* best_score,
                   double* second_score);
+/* scan_grid with Fingerprint::unit_norm flags (unit may be NULL): flagged
+ * queries are used as given (prep_query, dictionary.cpp:145-150). */
+int orc_scan_grid_ex(const orc_sched* s, const orc_grid* g, const double* queries, const uint8_t* unit,
+                     int64_t nq, int metric, int threads, int64_t* best_flat, double* best_score,
+                     double* second_score);
 /* fingerprint.cpp:80-145: calibrate_noise, make_calibrated_noise, smooth. */
 int orc_calibrate_noise(const double* fp, int64_t n, double target, uint64_t seed, double* sigma);
 int orc_make_calibrated_noise(const double* fp, int64_t n, double target, uint64_t seed,
@@ -81,6 +86,12 @@ int orc_smooth(const double* fp, int64_t n, int k, double* out);
 int orc_ref_save_generated(const orc_sched* s, const orc_grid* g, const char* path);
 int orc_ref_cc_map_to_file(const orc_sched* s, const orc_grid* g, const double* fp,
                            const char* path);
+/* Reference library only: exhaustive argmax over T1 values x T2 values x a
+ * linear df axis, built from mrf::generate rows and mrf::brute_force_search
+ * (see ref_capi.cpp).  Flat order (i1*n2 + i2)*ndf + idf; lowest flat on ties. */
+int orc_ref_scan_rows(const orc_sched* s, const double* t1_ms, int64_t n1, const double* t2_ms,
+                      int64_t n2, const orc_axis* df, const double* queries, int64_t nq,
+                      int metric, int threads, int64_t* best_flat, double* best_score);
 int orc_quantify(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg* cfg,
                  const double* fp, orc_quant* out);
 int orc_quantify_slice(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg* cfg,

@@ -8,7 +8,11 @@
 // (proj/include/mrf/*.hpp); the only harness logic is unit conversion and the
 // BASELINE.json schedule formula (which the reference ingests through
 // load_schedule_csv in real use).
+#include <atomic>
 #include <cmath>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <complex>
 #include <cstring>
 #include <string>
@@ -237,9 +241,18 @@ int orc_generate(const orc_sched* s, const orc_grid* g, int64_t first, int64_t c
 int orc_scan_grid(const orc_sched* s, const orc_grid* g, const double* queries, int64_t nq,
                   int metric, int threads, int64_t* best_flat, double* best_score,
                   double* second_score) {
+    return orc_scan_grid_ex(s, g, queries, nullptr, nq, metric, threads, best_flat, best_score, second_score);
+}
+
+int orc_scan_grid_ex(const orc_sched* s, const orc_grid* g, const double* queries, const uint8_t* unit,
+                     int64_t nq, int metric, int threads, int64_t* best_flat, double* best_score,
+                     double* second_score) {
     return guard([&] {
         std::vector<mrf::Fingerprint> qs;
-        for (int64_t i = 0; i < nq; ++i) qs.push_back(to_fp(queries + i * 2 * s->n, s->n));
+        for (int64_t i = 0; i < nq; ++i) {
+            qs.push_back(to_fp(queries + i * 2 * s->n, s->n));
+            qs.back().unit_norm = unit != nullptr && unit[i] != 0;
+        }
         mrf::ParameterGrid grid = to_grid(g);
         mrf::ScanOutcome out = mrf::scan_grid(grid, to_sched(s), qs,
                                               metric ? mrf::Metric::euclidean : mrf::Metric::cc,
@@ -300,6 +313,83 @@ int orc_quantify_slice(const orc_sched* s, const orc_grid* g, const orc_zoom_cfg
             if (m[i])
                 fill_quant(g, res.t1_ms[i], res.t2_ms[i], res.df_hz[i], res.pd[i], res.score[i],
                            res.evaluations[i], &out[i]);
+    });
+}
+
+/* Reference answers at BASELINE scale (test infrastructure for the scale
+ * fixtures).  The lattice is T1 values x T2 values x a linear df axis, given
+ * as explicit value arrays (linear axes pass min + k*step, which is what
+ * AxisSpec::value computes; config 3 passes its log-spaced values).  Each
+ * (T1, T2) row of atoms is produced by the reference's own mrf::generate on
+ * the one-row subgrid {t1[i1], 1, 1} x {t2[i2], 1, 1} x df (value(0) = min
+ * exactly, so every TissueParams equals the full lattice's), rows are
+ * gathered into T1 slabs, and every query is scored by the reference's own
+ * mrf::brute_force_search over each slab (an index-space Dictionary).  Slabs
+ * are visited in flat order and a later slab wins only with a strictly higher
+ * score: the reference's lowest-flat tie rule (dictionary.cpp:241-255,
+ * :291-294).  Work is spread over `threads` host threads (rows for
+ * generation, queries for the search). */
+int orc_ref_scan_rows(const orc_sched* s, const double* t1_ms, int64_t n1, const double* t2_ms,
+                      int64_t n2, const orc_axis* df, const double* queries, int64_t nq,
+                      int metric, int threads, int64_t* best_flat, double* best_score) {
+    return guard([&] {
+        const mrf::Schedule sc = to_sched(s);
+        const std::size_t n = static_cast<std::size_t>(s->n);
+        const std::size_t ndf = static_cast<std::size_t>(df->count);
+        const std::size_t row = ndf * 2 * n;
+        std::vector<mrf::Fingerprint> qs;
+        for (int64_t i = 0; i < nq; ++i) qs.push_back(to_fp(queries + i * 2 * s->n, s->n));
+        std::vector<double> best(static_cast<std::size_t>(nq), -1e300);
+        std::vector<int64_t> bflat(static_cast<std::size_t>(nq), 0);
+        mrf::Dictionary slab;
+        slab.grid.t1_ms = {0.0, 1.0, 1};
+        slab.grid.t2_ms = {0.0, 1.0, static_cast<std::size_t>(n2)};
+        slab.grid.df_hz = {0.0, 1.0, ndf};
+        slab.entry_len = n;
+        slab.data.resize(static_cast<std::size_t>(n2) * row);
+        const int T = threads > 0 ? threads : 1;
+        auto pool = [&](int64_t count, auto&& fn) {
+            std::atomic<int64_t> next{0};
+            std::vector<std::thread> ts;
+            std::exception_ptr err;
+            std::mutex mu;
+            for (int t = 0; t < T; ++t)
+                ts.emplace_back([&] {
+                    try {
+                        for (int64_t k; (k = next.fetch_add(1)) < count;) fn(k);
+                    } catch (...) {
+                        std::lock_guard<std::mutex> lk(mu);
+                        if (!err) err = std::current_exception();
+                    }
+                });
+            for (auto& t : ts) t.join();
+            if (err) std::rethrow_exception(err);
+        };
+        const mrf::Metric m = metric ? mrf::Metric::euclidean : mrf::Metric::cc;
+        for (int64_t i1 = 0; i1 < n1; ++i1) {
+            pool(n2, [&](int64_t i2) {
+                mrf::ParameterGrid g;
+                g.t1_ms = {t1_ms[i1], 1.0, 1};
+                g.t2_ms = {t2_ms[i2], 1.0, 1};
+                g.df_hz = {df->min, df->step, ndf};
+                mrf::Dictionary d = mrf::generate(g, sc, 1);
+                std::memcpy(slab.data.data() + static_cast<std::size_t>(i2) * row, d.data.data(),
+                            row * sizeof(float));
+            });
+            pool(nq, [&](int64_t q) {
+                mrf::Match r = mrf::brute_force_search(qs[static_cast<std::size_t>(q)], slab, m);
+                if (r.score > best[q]) {
+                    best[q] = r.score;
+                    const int64_t i2 = std::lround(r.params.t2 * 1e3);
+                    const int64_t idf = std::lround(r.params.df);
+                    bflat[q] = (i1 * n2 + i2) * static_cast<int64_t>(ndf) + idf;
+                }
+            });
+        }
+        for (int64_t q = 0; q < nq; ++q) {
+            best_flat[q] = bflat[q];
+            best_score[q] = best[q];
+        }
     });
 }
 

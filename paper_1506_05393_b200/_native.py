@@ -15,7 +15,8 @@ LIB_PATH = os.path.join(HERE, "libmrfg.so")
 
 class Axis(C.Structure):
     """AxisSpec (reference dictionary.hpp:17-24)."""
-    _fields_ = [("min", C.c_double), ("step", C.c_double), ("count", C.c_int64)]
+    _fields_ = [("min", C.c_double), ("step", C.c_double), ("count", C.c_int64),
+                ("values", C.POINTER(C.c_double))]  # optional explicit values (log axes)
 
 
 class Grid(C.Structure):
@@ -29,7 +30,8 @@ class Match(C.Structure):
 
 class ScanOpts(C.Structure):
     _fields_ = [("delta", C.c_double), ("chunk_atoms", C.c_int64), ("cand_capacity", C.c_int64),
-                ("seed_atoms", C.c_int64), ("floor_matches", C.c_void_p)]
+                ("seed_atoms", C.c_int64), ("floor_matches", C.c_void_p),
+                ("unit_queries", C.POINTER(C.c_uint8))]
 
 
 class ScanStats(C.Structure):
@@ -38,7 +40,10 @@ class ScanStats(C.Structure):
                 ("overflow_passes", C.c_int64), ("bloch_ms", C.c_double),
                 ("gemm_ms", C.c_double), ("rerank_ms", C.c_double), ("total_ms", C.c_double),
                 ("gemm_kernel_ms_avg", C.c_double), ("gemm_launches", C.c_int64),
-                ("screen_err_max", C.c_double), ("rescreened32", C.c_int64)]
+                ("screen_err_max", C.c_double), ("rescreened32", C.c_int64),
+                ("screen_err_audit_max", C.c_double), ("rescreen_err_audit_max", C.c_double),
+                ("delta_used", C.c_double), ("audit_samples", C.c_int64), ("rescans", C.c_int64),
+                ("rescreen_err_max", C.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -71,7 +76,7 @@ EXPORTS = [
     "mrfg_rng_gaussian", "mrfg_axis_count", "mrfg_create", "mrfg_destroy", "mrfg_length",
     "mrfg_set_stream", "mrfg_synchronize", "mrfg_simulate", "mrfg_simulate_dev", "mrfg_generate",
     "mrfg_generate_dev", "mrfg_bloch_norms_dev", "mrfg_scan_grid", "mrfg_scan_grid_dev",
-    "mrfg_scan_dict", "mrfg_scan_dict_dev",
+    "mrfg_scan_dict", "mrfg_scan_dict_dev", "mrfg_scan_seed_dev",
     "mrfg_merge_matches_dev", "mrfg_screen_scores", "mrfg_cc_map", "mrfg_quantify", "mrfg_quantify_slice", "mrfg_quantify_bounded",
     "mrfg_quantify_dev", "mrfg_cc_map_ex", "mrfg_save_generated", "mrfg_cc_map_to_file",
     "mrfg_write_header", "mrfg_read_header", "mrfg_calibrate_noise", "mrfg_make_calibrated_noise",
@@ -123,6 +128,8 @@ def load() -> C.CDLL:
     L.mrfg_scan_dict.argtypes = [vp, C.POINTER(C.c_float), i64, dp, i64, C.c_int,
                                  C.POINTER(ScanOpts), C.POINTER(Match), C.POINTER(ScanStats)]
     L.mrfg_scan_dict_dev.argtypes = [vp, vp, i64, i64, i64, vp, i64, C.c_int,
+                                     C.POINTER(ScanOpts), vp, C.POINTER(ScanStats)]
+    L.mrfg_scan_seed_dev.argtypes = [vp, C.POINTER(Grid), vp, i64, i64, i64, vp, i64, C.c_int,
                                      C.POINTER(ScanOpts), vp, C.POINTER(ScanStats)]
     L.mrfg_merge_matches_dev.argtypes = [vp, vp, C.c_int, i64, vp]
     L.mrfg_screen_scores.argtypes = [vp, C.POINTER(Grid), i64, i64, dp, i64, C.c_int, C.c_int,

@@ -14,8 +14,14 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmrfg.so")
 SHIM = os.path.join(HERE, "libmrf_b200.so")  # the reference's C++ interface over LIB
-SOURCES = ["abi.cu", "bloch.cu", "match_sm100.cu", "rerank.cu", "zoom.cu", "synth.cpp"]
+# zoom_k_var.cu (experimental K5 variants) is the slowest object: listed
+# first so its ptxas starts first
+SOURCES = ["zoom_k_var.cu", "zoom_k_main.cu", "zoom_k_rows.cu", "zoom.cu", "abi.cu", "bloch.cu",
+           "match_sm100.cu", "rerank.cu", "synth.cpp"]
 HEADERS = ["mrfg_internal.cuh", "sim64.cuh"]
+# per-source extra dependencies
+EXTRA_DEPS = {s: ["zoom_dev.cuh", "zoom_launch.h"] for s in
+              ("zoom.cu", "zoom_k_main.cu", "zoom_k_rows.cu", "zoom_k_var.cu")}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -30,7 +36,7 @@ def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS + ["zoom_dev.cuh", "zoom_launch.h"]] + [
         os.path.join(ROOT, "include", "mrfg.h"), os.path.join(ROOT, "include", "mrf_b200", "mrf.hpp"),
         os.path.join(CSRC, "host", "mrf_api.cpp"), __file__]
     if not os.path.exists(SHIM):
@@ -52,8 +58,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
         # per-object staleness (zoom.cu alone takes ~15 min in ptxas): only
         # recompile a source newer than its object or when a shared header changed
+        own = [os.path.join(CSRC, f) for f in [src] + EXTRA_DEPS.get(src, [])]
         if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(
-                hdr_t, os.path.getmtime(os.path.join(CSRC, src))):
+                [hdr_t] + [os.path.getmtime(f) for f in own]):
             continue
         cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off",
                "-ccbin", "g++", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c",

@@ -58,22 +58,38 @@ void host_rf_matrix(double alpha, double phi, double out[9]) {
     mul3(ab, c, out);
 }
 
-static bool same_grid(const mrfg_grid& a, const mrfg_grid& b) {
-    return std::memcmp(&a, &b, sizeof(mrfg_grid)) == 0;
+static bool same_axis(const mrfg_axis& a, const mrfg_axis& b, const std::vector<double>& bv) {
+    if (a.min != b.min || a.step != b.step || a.count != b.count || (a.values == nullptr) != bv.empty())
+        return false;
+    return a.values == nullptr || std::memcmp(a.values, bv.data(), sizeof(double) * a.count) == 0;
+}
+static bool same_grid(const mrfg_grid& a, const GridTables& t) {
+    return same_axis(a.t1_ms, t.grid.t1_ms, t.v1) && same_axis(a.t2_ms, t.grid.t2_ms, t.v2) &&
+           a.df_hz.min == t.grid.df_hz.min && a.df_hz.step == t.grid.df_hz.step &&
+           a.df_hz.count == t.grid.df_hz.count && a.df_hz.values == nullptr;
 }
 
 static void check_grid(const mrfg_grid& g) {
     const mrfg_axis* ax[3] = {&g.t1_ms, &g.t2_ms, &g.df_hz};
     for (auto* a : ax) MRFG_REQUIRE(a->count > 0, MRFG_E_INVALID, "grid: empty axis");
-    MRFG_REQUIRE(g.t1_ms.min > 0 && g.t1_ms.min + (g.t1_ms.count - 1) * g.t1_ms.step > 0 &&
-                     g.t2_ms.min > 0 && g.t2_ms.min + (g.t2_ms.count - 1) * g.t2_ms.step > 0,
-                 MRFG_E_INVALID, "simulate: T1 and T2 must be positive");
+    MRFG_REQUIRE(g.df_hz.values == nullptr, MRFG_E_INVALID,
+                 "grid: explicit axis values are supported on the T1 and T2 axes only");
+    for (const mrfg_axis* a : {&g.t1_ms, &g.t2_ms}) {
+        if (a->values) {
+            for (int64_t i = 0; i < a->count; ++i)
+                MRFG_REQUIRE(a->values[i] > 0 && std::isfinite(a->values[i]), MRFG_E_INVALID,
+                             "simulate: T1 and T2 must be positive");
+        } else {
+            MRFG_REQUIRE(a->min > 0 && a->min + (a->count - 1) * a->step > 0, MRFG_E_INVALID,
+                         "simulate: T1 and T2 must be positive");
+        }
+    }
 }
 
 // Per-axis transcendental tables: host libm, reference operand order
 // (bloch.cpp:17-21).  Cached per context for the last grid.
 const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
-    if (c.tab.valid && same_grid(c.tab.grid, g)) return c.tab;
+    if (c.tab.valid && same_grid(g, c.tab)) return c.tab;
     check_grid(g);
     const int64_t n = c.n, n1 = g.t1_ms.count, n2 = g.t2_ms.count, nd = g.df_hz.count;
     std::vector<double> e1(n * n1 * 2), e2(n * n2 * 2), ph(n * nd * 4);
@@ -83,7 +99,7 @@ const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
     // so a walker over j streams memory (K3/K4/K5 gather scattered points).
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n1; ++i) {
-        const double inv = 1.0 / ((g.t1_ms.min + static_cast<double>(i) * g.t1_ms.step) * 1e-3);
+        const double inv = 1.0 / (axis_value(g.t1_ms, i) * 1e-3);
         for (int64_t j = 0; j < n; ++j) {
             const double a = std::exp(-c.te_s[j] * inv), b = std::exp(-c.rest_s[j] * inv);
             e1[(i * n + j) * 2] = a;
@@ -97,7 +113,7 @@ const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
     }
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n2; ++i) {
-        const double inv = 1.0 / ((g.t2_ms.min + static_cast<double>(i) * g.t2_ms.step) * 1e-3);
+        const double inv = 1.0 / (axis_value(g.t2_ms, i) * 1e-3);
         for (int64_t j = 0; j < n; ++j) {
             const double a = std::exp(-c.te_s[j] * inv), b = std::exp(-c.rest_s[j] * inv);
             e2[(i * n + j) * 2] = a;
@@ -149,8 +165,18 @@ const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
     up(t.e2f, e2f.data(), e2f.size() * 4);
     up(t.phf, phf.data(), phf.size() * 4);
     up(t.stepu, su.data(), su.size() * sizeof(StepU));
+    // K1 row producers: log2(e)/T per lattice index (ex2 arguments), FP64 -> FP32
+    std::vector<float> kt(n1 + n2);
+    for (int64_t i = 0; i < n1; ++i) kt[i] = static_cast<float>(1.4426950408889634 / (axis_value(g.t1_ms, i) * 1e-3));
+    for (int64_t i = 0; i < n2; ++i)
+        kt[n1 + i] = static_cast<float>(1.4426950408889634 / (axis_value(g.t2_ms, i) * 1e-3));
+    up(t.kt, kt.data(), kt.size() * sizeof(float));
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
     t.grid = g;
+    t.v1.assign(g.t1_ms.values ? g.t1_ms.values : nullptr, g.t1_ms.values ? g.t1_ms.values + n1 : nullptr);
+    t.v2.assign(g.t2_ms.values ? g.t2_ms.values : nullptr, g.t2_ms.values ? g.t2_ms.values + n2 : nullptr);
+    t.grid.t1_ms.values = t.v1.empty() ? nullptr : t.v1.data();  // owned copies, not the caller's
+    t.grid.t2_ms.values = t.v2.empty() ? nullptr : t.v2.data();
     t.valid = true;
     return t;
 }
@@ -199,9 +225,12 @@ struct EventTimer {
 // The streamed brute-force scan on device-resident queries.  Atoms come from
 // the lattice (grid != nullptr: K1 simulates them chunk by chunk) or from a
 // stored float32 dictionary (d_dict: converted to the fp16 operand per chunk).
-static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t dict_atoms,
-                     int64_t fb, int64_t fe, const double* d_raw, int64_t nq, int metric,
-                     const mrfg_scan_opts* o, mrfg_match* d_out, mrfg_scan_stats* st) {
+// Returns false (nothing written) when the unbiased audit finds a screening
+// error above delta/2: the caller repeats the scan with a wider margin.
+static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t dict_atoms,
+                          int64_t fb, int64_t fe, const double* d_raw, int64_t nq, int metric,
+                          const mrfg_scan_opts* o, double delta, mrfg_match* d_out, mrfg_scan_stats* st,
+                          float* seed_out = nullptr) {
     MRFG_REQUIRE(nq > 0, MRFG_E_INVALID, "scan_grid: no queries");  // dictionary.cpp:260
     MRFG_REQUIRE(metric == MRFG_METRIC_CC || metric == MRFG_METRIC_EUCLIDEAN, MRFG_E_INVALID,
                  "scan_grid: unknown metric");
@@ -209,7 +238,6 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
     if (fb == 0 && fe == 0) fe = total;
     MRFG_REQUIRE(0 <= fb && fb < fe && fe <= total, MRFG_E_INVALID, "scan_grid: bad flat range");
     const GridTables* tp = grid ? &ensure_tables(c, *grid, true) : nullptr;
-    const double delta = (o && o->delta > 0) ? o->delta : 1e-3;
     int64_t chunk = (o && o->chunk_atoms > 0) ? o->chunk_atoms : 524288;
     // K1 tiles whole lattice rows (ndf atoms): a chunk is crows rows.  A stored
     // dictionary is chunked in flat order directly (ndf = 1).
@@ -227,7 +255,14 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
     c.best.ensure(sizeof(float) * nq + 64);
     int* d_bad = reinterpret_cast<int*>(c.best.as<char>() + sizeof(float) * nq);
     MRFG_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), c.stream));
-    launch_prepare_queries(c, d_raw, nq, qrows, c.q64.as<double>(), c.qprime.as<__half>(), d_bad);
+    const uint8_t* d_unit = nullptr;
+    if (o && o->unit_queries) {  // Fingerprint::unit_norm flags (host) -> device
+        c.misc2.ensure(64 + nq);
+        d_unit = c.misc2.as<uint8_t>() + 64;
+        MRFG_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(d_unit), o->unit_queries, nq, cudaMemcpyHostToDevice,
+                                  c.stream));
+    }
+    launch_prepare_queries(c, d_raw, nq, qrows, c.q64.as<double>(), c.qprime.as<__half>(), d_bad, d_unit);
     int h_bad = 0;
     MRFG_CUDA(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
@@ -297,11 +332,39 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
         gemm_ms += tm.ms(a1, a2);
         ++gemm_launches;
     }
+    if (seed_out) {  // seed maxima only (mrfg_scan_seed_dev)
+        MRFG_CUDA(cudaMemcpyAsync(seed_out, best, sizeof(float) * nq, cudaMemcpyDeviceToDevice, c.stream));
+        if (st) {
+            st->atoms = range;
+            st->voxels = nq;
+            st->bloch_ms = bloch_ms;
+            st->gemm_ms = gemm_ms;
+            st->gemm_launches = gemm_launches;
+        }
+        return true;
+    }
+    // Unbiased audit: a hash sample of ALL screened pairs, about audit_target
+    // of them per scan (MRFG_AUDIT=0 disables, =k sets the target).
+    int64_t audit_target = 16384;
+    if (const char* e = std::getenv("MRFG_AUDIT")) audit_target = std::atoll(e);
+    const int64_t audit_cap = 4 * std::max<int64_t>(audit_target, 1024);
+    const bool audit_on = audit_target > 0 && metric == MRFG_METRIC_CC;
+    if (audit_on) {
+        c.audit.ensure(sizeof(CandRec) * audit_cap + 64);
+        const double pairs = static_cast<double>(nq) * static_cast<double>(range);
+        const double frac = std::min(1.0, static_cast<double>(audit_target) / pairs);
+        mp.audit = c.audit.as<CandRec>();
+        mp.audit_count = reinterpret_cast<unsigned long long*>(c.audit.as<char>() + sizeof(CandRec) * audit_cap);
+        mp.audit_cap = audit_cap;
+        mp.audit_thr = static_cast<uint32_t>(std::min(4294967295.0, std::floor(frac * 4294967296.0)));
+        if (mp.audit_thr == 0) mp.audit_thr = 1;
+    }
     int64_t overflow_passes = 0;
     unsigned long long ncand = 0;
     for (int pass = 0; pass < 2; ++pass) {
         c.cand.ensure(sizeof(CandRec) * cap);
         MRFG_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), c.stream));
+        if (audit_on) MRFG_CUDA(cudaMemsetAsync(mp.audit_count, 0, sizeof(unsigned long long), c.stream));
         mp.cand = c.cand.as<CandRec>();
         mp.cand_cap = cap;
         // Two operand buffers: with MRFG_OVERLAP=1 the producer (K1 or the
@@ -387,12 +450,33 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
         cap = static_cast<int64_t>(ncand);
         ++overflow_passes;
     }
-    double err_max = 0;
+    // the audit: exact scores of the sampled pairs (fp16 screen and FP32
+    // re-screen errors); a margin the sample contradicts is widened by a rescan
+    double a16 = 0, a32 = 0;
+    int64_t nsamp = 0;
+    int ra0 = tm.mark();
+    if (audit_on) {
+        unsigned long long h = 0;
+        MRFG_CUDA(cudaMemcpyAsync(&h, mp.audit_count, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+        nsamp = static_cast<int64_t>(std::min<unsigned long long>(h, static_cast<unsigned long long>(audit_cap)));
+        audit_screen(c, tp, d_dict, c.q64.as<double>(), mp.audit, nsamp, &a16, &a32);
+        if (a16 > 0.5 * delta) {
+            if (st) st->screen_err_audit_max = a16;
+            return false;
+        }
+    }
+    int ra1 = tm.mark();
+    double err_max = 0, err32 = 0;
     int r0 = tm.mark();
     int64_t n32 = 0;
+    // the FP32 stage certifies with margin kRescreenEps = 1e-5: needs its
+    // audited error below half of it, else every candidate is re-ranked in FP64
+    const bool fp32_ok = !audit_on || a32 <= 0.5e-5;
     int64_t nsel = rerank_and_select(c, tp, d_dict, c.q64.as<double>(), nq, metric, best,
                                      static_cast<float>(delta), c.cand.as<CandRec>(),
-                                     static_cast<int64_t>(ncand), d_out, &err_max, floored, &n32);
+                                     static_cast<int64_t>(ncand), d_out, &err_max, floored, &n32, fp32_ok,
+                                     &err32);
     int r1 = tm.mark();
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
     if (st) {
@@ -410,6 +494,34 @@ static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t
         st->gemm_kernel_ms_avg = gemm_launches ? gemm_ms / gemm_launches : 0;
         st->screen_err_max = err_max;
         st->rescreened32 = n32;
+        st->screen_err_audit_max = a16;
+        st->rescreen_err_audit_max = a32;
+        st->audit_samples = nsamp;
+        st->delta_used = delta;
+        st->rescreen_err_max = err32;
+        st->rerank_ms += tm.ms(ra0, ra1);
+    }
+    return true;
+}
+
+// Default screening margin: twice the analytic bound on |fp16 screen CC -
+// exact CC| (2u + u^2 + FP32 accumulation over 2N terms + the
+// K1 FP32 error, u = 2^-11).
+constexpr double kDefaultDelta = 2.5e-3;
+
+static void scan_dev(Ctx& c, const mrfg_grid* grid, const float* d_dict, int64_t dict_atoms, int64_t fb,
+                     int64_t fe, const double* d_raw, int64_t nq, int metric, const mrfg_scan_opts* o,
+                     mrfg_match* d_out, mrfg_scan_stats* st) {
+    double delta = (o && o->delta > 0) ? o->delta : kDefaultDelta;
+    for (int64_t rescans = 0;; ++rescans) {
+        mrfg_scan_stats tmp{};
+        mrfg_scan_stats* sp = st ? st : &tmp;
+        if (scan_dev_once(c, grid, d_dict, dict_atoms, fb, fe, d_raw, nq, metric, o, delta, d_out, sp)) {
+            sp->rescans = rescans;
+            return;
+        }
+        MRFG_REQUIRE(rescans < 3, MRFG_E_RUNTIME, "scan: screening audit failed after widening the margin");
+        delta = std::max(2 * delta, 4 * sp->screen_err_audit_max);
     }
 }
 
@@ -514,9 +626,10 @@ int mrfg_destroy(mrfg_ctx* h) {
         cudaSetDevice(c.device);
         cudaStreamSynchronize(c.stream);
         for (DevBuf* b : {&c.zoom, &c.rf64_d, &c.rf32_d, &c.tab.e1f, &c.tab.e2f, &c.tab.phf, &c.tab.e1d,
-                          &c.tab.e2d, &c.tab.phd, &c.q64, &c.qprime, &c.best, &c.cand,
-                          &c.cand_count, &c.atoms_a, &c.inv2, &c.seed_a, &c.seed_inv2, &c.rerank,
-                          &c.params, &c.out64, &c.misc, &c.rerank_scratch})
+                          &c.tab.e2d, &c.tab.phd, &c.tab.stepu, &c.tab.kt, &c.q64, &c.qprime, &c.best,
+                          &c.cand, &c.cand_count, &c.atoms_a, &c.inv2, &c.seed_a, &c.seed_inv2, &c.rerank,
+                          &c.params, &c.out64, &c.misc, &c.rerank_scratch, &c.misc2, &c.audit, &c.h_raw,
+                          &c.h_res, &c.h_dict})
             b->release();
         if (c.own_stream) cudaStreamDestroy(c.stream);
         if (c.aux) {
@@ -631,6 +744,20 @@ int mrfg_scan_grid_dev(mrfg_ctx* h, const mrfg_grid* grid, int64_t fb, int64_t f
     });
 }
 
+int mrfg_scan_seed_dev(mrfg_ctx* h, const mrfg_grid* grid, const float* d_dict, int64_t natoms, int64_t fb,
+                       int64_t fe, const double* d_queries, int64_t nq, int metric, const mrfg_scan_opts* o,
+                       float* d_seed, mrfg_scan_stats* st) {
+    return guard([&] {
+        Ctx& c = h->c;
+        MRFG_CUDA(cudaSetDevice(c.device));
+        MRFG_REQUIRE((grid != nullptr) != (d_dict != nullptr), MRFG_E_INVALID,
+                     "scan_seed: give either a grid or a dictionary");
+        const double delta = (o && o->delta > 0) ? o->delta : kDefaultDelta;
+        scan_dev_once(c, grid, d_dict, grid ? 0 : natoms, fb, fe, d_queries, nq, metric, o, delta, nullptr, st,
+                      d_seed);
+    });
+}
+
 int mrfg_scan_dict_dev(mrfg_ctx* h, const float* d_dict, int64_t natoms, int64_t fb, int64_t fe,
                        const double* d_queries, int64_t nq, int metric, const mrfg_scan_opts* o,
                        mrfg_match* d_out, mrfg_scan_stats* st) {
@@ -642,6 +769,8 @@ int mrfg_scan_dict_dev(mrfg_ctx* h, const float* d_dict, int64_t natoms, int64_t
     });
 }
 
+// The host-buffer entry points stage through per-context device buffers
+// (grow-only, kept between calls: no cudaMalloc/cudaFree per call).
 int mrfg_scan_dict(mrfg_ctx* h, const float* dict, int64_t natoms, const double* queries,
                    int64_t nq, int metric, const mrfg_scan_opts* o, mrfg_match* out,
                    mrfg_scan_stats* st) {
@@ -650,29 +779,17 @@ int mrfg_scan_dict(mrfg_ctx* h, const float* dict, int64_t natoms, const double*
         MRFG_CUDA(cudaSetDevice(c.device));
         MRFG_REQUIRE(nq > 0, MRFG_E_INVALID, "scan_grid: no queries");
         MRFG_REQUIRE(natoms > 0, MRFG_E_INVALID, "brute_force_search: empty dictionary");
-        DevBuf raw, res, dd;
-        raw.ensure(sizeof(double) * 2 * c.n * nq);
-        res.ensure(sizeof(mrfg_match) * nq);
-        dd.ensure(sizeof(float) * 2 * c.n * natoms);
-        try {
-            MRFG_CUDA(cudaMemcpyAsync(dd.p, dict, sizeof(float) * 2 * c.n * natoms,
-                                      cudaMemcpyHostToDevice, c.stream));
-            MRFG_CUDA(cudaMemcpyAsync(raw.p, queries, sizeof(double) * 2 * c.n * nq,
-                                      cudaMemcpyHostToDevice, c.stream));
-            scan_dev(c, nullptr, dd.as<float>(), natoms, 0, natoms, raw.as<double>(), nq, metric, o,
-                     res.as<mrfg_match>(), st);
-            MRFG_CUDA(cudaMemcpyAsync(out, res.p, sizeof(mrfg_match) * nq, cudaMemcpyDeviceToHost,
-                                      c.stream));
-            MRFG_CUDA(cudaStreamSynchronize(c.stream));
-        } catch (...) {
-            raw.release();
-            res.release();
-            dd.release();
-            throw;
-        }
-        raw.release();
-        res.release();
-        dd.release();
+        c.h_raw.ensure(sizeof(double) * 2 * c.n * nq);
+        c.h_res.ensure(sizeof(mrfg_match) * nq);
+        c.h_dict.ensure(sizeof(float) * 2 * c.n * natoms);
+        MRFG_CUDA(cudaMemcpyAsync(c.h_dict.p, dict, sizeof(float) * 2 * c.n * natoms, cudaMemcpyHostToDevice,
+                                  c.stream));
+        MRFG_CUDA(cudaMemcpyAsync(c.h_raw.p, queries, sizeof(double) * 2 * c.n * nq, cudaMemcpyHostToDevice,
+                                  c.stream));
+        scan_dev(c, nullptr, c.h_dict.as<float>(), natoms, 0, natoms, c.h_raw.as<double>(), nq, metric, o,
+                 c.h_res.as<mrfg_match>(), st);
+        MRFG_CUDA(cudaMemcpyAsync(out, c.h_res.p, sizeof(mrfg_match) * nq, cudaMemcpyDeviceToHost, c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
     });
 }
 
@@ -683,23 +800,13 @@ int mrfg_scan_grid(mrfg_ctx* h, const mrfg_grid* grid, int64_t fb, int64_t fe,
         Ctx& c = h->c;
         MRFG_CUDA(cudaSetDevice(c.device));
         MRFG_REQUIRE(nq > 0, MRFG_E_INVALID, "scan_grid: no queries");
-        DevBuf raw, res;
-        raw.ensure(sizeof(double) * 2 * c.n * nq);
-        res.ensure(sizeof(mrfg_match) * nq);
-        try {
-            MRFG_CUDA(cudaMemcpyAsync(raw.p, queries, sizeof(double) * 2 * c.n * nq,
-                                      cudaMemcpyHostToDevice, c.stream));
-            scan_dev(c, grid, nullptr, 0, fb, fe, raw.as<double>(), nq, metric, o, res.as<mrfg_match>(), st);
-            MRFG_CUDA(cudaMemcpyAsync(out, res.p, sizeof(mrfg_match) * nq, cudaMemcpyDeviceToHost,
-                                      c.stream));
-            MRFG_CUDA(cudaStreamSynchronize(c.stream));
-        } catch (...) {
-            raw.release();
-            res.release();
-            throw;
-        }
-        raw.release();
-        res.release();
+        c.h_raw.ensure(sizeof(double) * 2 * c.n * nq);
+        c.h_res.ensure(sizeof(mrfg_match) * nq);
+        MRFG_CUDA(cudaMemcpyAsync(c.h_raw.p, queries, sizeof(double) * 2 * c.n * nq, cudaMemcpyHostToDevice,
+                                  c.stream));
+        scan_dev(c, grid, nullptr, 0, fb, fe, c.h_raw.as<double>(), nq, metric, o, c.h_res.as<mrfg_match>(), st);
+        MRFG_CUDA(cudaMemcpyAsync(out, c.h_res.p, sizeof(mrfg_match) * nq, cudaMemcpyDeviceToHost, c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
     });
 }
 
@@ -914,6 +1021,8 @@ int mrfg_cc_map_to_file(mrfg_ctx* h, const mrfg_grid* grid, const double* query,
         Ctx& c = h->c;
         MRFG_CUDA(cudaSetDevice(c.device));
         check_grid(*grid);
+        MRFG_REQUIRE(!grid_explicit(*grid), MRFG_E_INVALID,
+                     "the .mrfd/.mrfc header stores evenly spaced axes only (explicit axis values)");
         FileCloser fc{fopen(path, "wb")};
         MRFG_REQUIRE(fc.f, MRFG_E_RUNTIME, std::string("cannot open for write: ") + path);
         write_header(fc.f, "MRFC", digest, *grid, static_cast<uint64_t>(c.n));
@@ -936,6 +1045,8 @@ int mrfg_save_generated(mrfg_ctx* h, const mrfg_grid* grid, const uint8_t* diges
         MRFG_REQUIRE(chunk_entries > 0, MRFG_E_INVALID, "chunk_entries must be > 0");
         MRFG_REQUIRE(precision == 32 || precision == 64, MRFG_E_INVALID, "generate: precision must be 32 or 64");
         check_grid(*grid);
+        MRFG_REQUIRE(!grid_explicit(*grid), MRFG_E_INVALID,
+                     "the .mrfd/.mrfc header stores evenly spaced axes only (explicit axis values)");
         FileCloser fc{fopen(path, "wb")};
         MRFG_REQUIRE(fc.f, MRFG_E_RUNTIME, std::string("cannot open for write: ") + path);
         write_header(fc.f, "MRFD", digest, *grid, static_cast<uint64_t>(c.n));
@@ -1108,24 +1219,13 @@ int mrfg_quantify_bounded(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom
                 MRFG_REQUIRE(bounds[6 * k] <= bounds[6 * k + 1] && bounds[6 * k + 2] <= bounds[6 * k + 3] &&
                                  bounds[6 * k + 4] <= bounds[6 * k + 5],
                              MRFG_E_INVALID, "zoom_2d: empty range");  // zoom.cpp:176,287
-        DevBuf d_fps, d_out;
-        d_fps.ensure(sizeof(double) * 2 * c.n * nvox);
-        d_out.ensure(sizeof(mrfg_quant) * nvox);
-        MRFG_CUDA(cudaMemcpyAsync(d_fps.p, fps, sizeof(double) * 2 * c.n * nvox,
-                                  cudaMemcpyHostToDevice, c.stream));
-        try {
-            run_quantify(c, *lattice, *cfg, d_fps.as<double>(), nvox, bounds, init_ms,
-                         d_out.as<mrfg_quant>());
-            MRFG_CUDA(cudaMemcpyAsync(out, d_out.p, sizeof(mrfg_quant) * nvox, cudaMemcpyDeviceToHost,
-                                      c.stream));
-            MRFG_CUDA(cudaStreamSynchronize(c.stream));
-        } catch (...) {
-            d_fps.release();
-            d_out.release();
-            throw;
-        }
-        d_fps.release();
-        d_out.release();
+        c.h_raw.ensure(sizeof(double) * 2 * c.n * nvox);
+        c.h_res.ensure(sizeof(mrfg_quant) * nvox);
+        MRFG_CUDA(cudaMemcpyAsync(c.h_raw.p, fps, sizeof(double) * 2 * c.n * nvox, cudaMemcpyHostToDevice,
+                                  c.stream));
+        run_quantify(c, *lattice, *cfg, c.h_raw.as<double>(), nvox, bounds, init_ms, c.h_res.as<mrfg_quant>());
+        MRFG_CUDA(cudaMemcpyAsync(out, c.h_res.p, sizeof(mrfg_quant) * nvox, cudaMemcpyDeviceToHost, c.stream));
+        MRFG_CUDA(cudaStreamSynchronize(c.stream));
         for (int64_t k = 0; k < nvox; ++k) {  // AxisSpec::value (dictionary.hpp:22)
             out[k].t1_ms = lattice->t1_ms.min + static_cast<double>(out[k].i1) * lattice->t1_ms.step;
             out[k].t2_ms = lattice->t2_ms.min + static_cast<double>(out[k].i2) * lattice->t2_ms.step;
@@ -1251,7 +1351,8 @@ int mrfg_quantify_slice(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_c
                 row_start.push_back(static_cast<int64_t>(vox.size()));
             }
             if (R > 0) {
-                DevBuf d_fps, d_res;
+                DevBuf& d_fps = c.h_raw;
+                DevBuf& d_res = c.h_res;
                 d_fps.ensure(sizeof(double) * n2 * nv);
                 d_res.ensure(sizeof(mrfg_quant) * nv);
                 MRFG_CUDA(cudaMemcpyAsync(d_fps.p, fps, sizeof(double) * n2 * nv, cudaMemcpyHostToDevice, c.stream));

@@ -68,7 +68,7 @@ mrfg_ctx* create_len(std::size_t n) {
     return create(s);
 }
 
-mrfg_axis to_axis(const AxisSpec& a) { return {a.min, a.step, static_cast<int64_t>(a.count)}; }
+mrfg_axis to_axis(const AxisSpec& a) { return {a.min, a.step, static_cast<int64_t>(a.count), nullptr}; }
 mrfg_grid to_grid(const ParameterGrid& g) { return {to_axis(g.t1_ms), to_axis(g.t2_ms), to_axis(g.df_hz)}; }
 
 mrfg_zoom_config to_cfg(const ZoomConfig& z) {
@@ -487,8 +487,12 @@ Match brute_force_search(const Fingerprint& fp, const Dictionary& dict, Metric m
         throw std::invalid_argument("query length does not match dictionary entries");
     CtxGuard c{create_len(dict.entry_len)};
     mrfg_match m;
+    // prep_query (dictionary.cpp:145-150): a unit_norm query is used as given
+    const uint8_t unit = fp.unit_norm ? 1 : 0;
+    mrfg_scan_opts o{};
+    o.unit_queries = &unit;
     check(mrfg_scan_dict(c.h, dict.data.data(), static_cast<int64_t>(dict.grid.total()), interleaved(fp), 1,
-                         metric == Metric::cc ? MRFG_METRIC_CC : MRFG_METRIC_EUCLIDEAN, nullptr, &m, nullptr));
+                         metric == Metric::cc ? MRFG_METRIC_CC : MRFG_METRIC_EUCLIDEAN, &o, &m, nullptr));
     const auto u = dict.grid.unflatten(static_cast<std::size_t>(m.flat));
     return {dict.grid.params_at(u.i1, u.i2, u.idf), m.score, dict.grid.total()};
 }
@@ -504,13 +508,18 @@ ScanOutcome scan_grid(const ParameterGrid& grid, const Schedule& sched,
     CtxGuard c{create(sched)};
     const std::size_t n = sched.size(), nq = queries.size();
     std::vector<double> flat(2 * n * nq);
-    for (std::size_t k = 0; k < nq; ++k) std::memcpy(&flat[2 * n * k], interleaved(queries[k]), 16 * n);
+    std::vector<uint8_t> unit(nq);  // prep_query: unit_norm queries are used as given
+    for (std::size_t k = 0; k < nq; ++k) {
+        std::memcpy(&flat[2 * n * k], interleaved(queries[k]), 16 * n);
+        unit[k] = queries[k].unit_norm ? 1 : 0;
+    }
     std::vector<mrfg_match> m(nq);
     mrfg_scan_stats st{};
+    mrfg_scan_opts o{};
+    o.unit_queries = unit.data();
     const mrfg_grid g = to_grid(grid);
     check(mrfg_scan_grid(c.h, &g, 0, 0, flat.data(), static_cast<int64_t>(nq),
-                         metric == Metric::cc ? MRFG_METRIC_CC : MRFG_METRIC_EUCLIDEAN, nullptr, m.data(),
-                         &st));
+                         metric == Metric::cc ? MRFG_METRIC_CC : MRFG_METRIC_EUCLIDEAN, &o, m.data(), &st));
     ScanOutcome out;
     for (std::size_t k = 0; k < nq; ++k) {
         const auto u = grid.unflatten(static_cast<std::size_t>(m[k].flat));

@@ -46,6 +46,7 @@ struct alignas(1024) Smem {
     uint32_t tmem_base;
     float thr[2][128];
     float bst[2][128];
+    uint32_t hv[2][128];
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
 
@@ -61,6 +62,10 @@ struct Dev {
     int64_t cand_cap;
     float delta;
     int metric;
+    CandRec* audit;
+    unsigned long long* audit_count;
+    int64_t audit_cap;
+    uint32_t audit_thr;
 };
 
 // Tile t -> (atom tile, query tile).  ga = 1: atom-major (the query operand
@@ -234,6 +239,19 @@ __device__ __noinline__ unsigned long long reserve_hits(const Dev& p, uint32_t h
     return base + static_cast<unsigned long long>(incl - mine);
 }
 
+// One audit-sampled pair (rare): recorded whatever its score, valid voxels only.
+__device__ __noinline__ void record_audit(const Dev& p, int64_t v, int64_t atom, float sc) {
+    if (v >= p.nvox) return;
+    const unsigned long long idx = atomicAdd(p.audit_count, 1ull);
+    if (idx < static_cast<unsigned long long>(p.audit_cap)) {
+        CandRec rec;
+        rec.voxel = static_cast<uint32_t>(p.vox_base + v);
+        rec.s = sc;
+        rec.flat = p.flat_base + atom * p.flat_stride;
+        p.audit[idx] = rec;
+    }
+}
+
 // One reserved hit: the candidate record and the running maximum.
 __device__ __noinline__ void store_hit(const Dev& p, float bst, int64_t v, int64_t atom, float sc,
                                        unsigned long long idx) {
@@ -349,6 +367,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // padding voxel columns can never screen in
                 s.thr[acc][row] = v < p.nvox ? threshold_of(b, p.delta, p.metric) : __int_as_float(0x7f800000);
                 s.bst[acc][row] = b;
+                s.hv[acc][row] = audit_hash_voxel(static_cast<uint64_t>(p.vox_base + v));
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
             mbar_wait(&s.tfull[acc], acc_phase);
@@ -356,6 +375,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int64_t atom = at * BM + row;
             const bool avalid = atom >= p.valid_begin && atom < p.valid_atoms;
             const float inv = __ldg(p.inv2 + atom);
+            const uint32_t ha = audit_hash_flat(static_cast<uint64_t>(p.flat_base + atom * p.flat_stride));
             const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
@@ -378,6 +398,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     for (int i = 0; i < 32; ++i)
                         if ((hits >> i) & 1u)
                             store_hit(p, s.bst[acc][q * 32 + i], vt * 128 + q * 32 + i, atom, sc[i], slot++);
+                }
+                if (p.audit_thr != 0u && avalid) {
+                    uint32_t samp = 0;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        samp |= (audit_mix(ha, s.hv[acc][q * 32 + i]) < p.audit_thr ? 1u : 0u) << i;
+                    if (samp) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if ((samp >> i) & 1u) record_audit(p, vt * 128 + q * 32 + i, atom, sc[i]);
+                    }
                 }
             }
             tc_fence_before();
@@ -413,6 +444,7 @@ struct alignas(1024) Smem2 {
     uint32_t tmem_base;
     float thr[2][128];
     float bst[2][128];
+    uint32_t hv[2][128];
 };
 constexpr size_t SMEM2_BYTES = sizeof(Smem2) + 1024;
 constexpr uint32_t IDESC2 = (1u << 4) | (static_cast<uint32_t>(BN >> 3) << 17) |
@@ -571,6 +603,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 float b = v < p.nvox ? __ldcg(p.best + v) : 1e30f;
                 s.thr[acc][row] = v < p.nvox ? threshold_of(b, p.delta, p.metric) : __int_as_float(0x7f800000);
                 s.bst[acc][row] = b;
+                s.hv[acc][row] = audit_hash_voxel(static_cast<uint64_t>(p.vox_base + v));
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
             mbar_wait(&s.tfull[acc], acc_phase);
@@ -578,6 +611,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             const int64_t atom = at * 256 + static_cast<int64_t>(rank) * 128 + row;
             const bool avalid = atom >= p.valid_begin && atom < p.valid_atoms;
             const float inv = __ldg(p.inv2 + atom);
+            const uint32_t ha = audit_hash_flat(static_cast<uint64_t>(p.flat_base + atom * p.flat_stride));
             const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
@@ -600,6 +634,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     for (int i = 0; i < 32; ++i)
                         if ((hits >> i) & 1u)
                             store_hit(p, s.bst[acc][q * 32 + i], vt * 128 + q * 32 + i, atom, sc[i], slot++);
+                }
+                if (p.audit_thr != 0u && avalid) {
+                    uint32_t samp = 0;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        samp |= (audit_mix(ha, s.hv[acc][q * 32 + i]) < p.audit_thr ? 1u : 0u) << i;
+                    if (samp) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if ((samp >> i) & 1u) record_audit(p, vt * 128 + q * 32 + i, atom, sc[i]);
+                    }
                 }
             }
             tc_fence_before();
@@ -695,6 +740,10 @@ Dev dev_of(const MatchParams& p, int64_t k_valid) {
     d.delta = p.delta;
     d.metric = p.metric;
     d.ga = 1;
+    d.audit = p.audit;
+    d.audit_count = p.audit_count;
+    d.audit_cap = p.audit_cap;
+    d.audit_thr = (p.audit != nullptr && p.audit_count != nullptr) ? p.audit_thr : 0u;
     return d;
 }
 
@@ -718,14 +767,12 @@ static bool use_pair_kernel() {
 void launch_match(Ctx& c, const MatchParams& p) {
     MRFG_REQUIRE(p.atoms % BM == 0 && p.q_rows % BN == 0 && p.k_pad % BK == 0, MRFG_E_INVALID,
                  "match: operand shapes not tile aligned");
-    static bool attr_set = false;
-    if (!attr_set) {
-        MRFG_CUDA(cudaFuncSetAttribute(k_match_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(SMEM_BYTES)));
-        MRFG_CUDA(cudaFuncSetAttribute(k_match_sm100_2cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(SMEM2_BYTES)));
-        attr_set = true;
-    }
+    // the shared-memory opt-in is per device (a process may drive several
+    // GPUs), so it is set on every launch, like the K1/K5 attributes
+    MRFG_CUDA(cudaFuncSetAttribute(k_match_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(SMEM_BYTES)));
+    MRFG_CUDA(cudaFuncSetAttribute(k_match_sm100_2cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(SMEM2_BYTES)));
     Dev d = dev_of(p, 2 * c.n);
     if (use_pair_kernel() && p.atoms % 256 == 0) {
         CUtensorMap ma = make_map(c, p.a, p.atoms, p.k_pad, 128);

@@ -30,9 +30,29 @@ void set_error(const std::string& msg);
     } while (0)
 
 // ---------------------------------------------------------- device buffers
+// Owning, move-only device allocation (grow-only via ensure).  The owner
+// frees on destruction; callers keep the right device current.
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            bytes = o.bytes;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
     void ensure(size_t n) {
         if (n <= bytes) return;
         if (p) cudaFree(p);
@@ -67,6 +87,8 @@ static_assert(sizeof(StepU) == 64, "StepU is 4 x 16 B");
 
 struct GridTables {
     mrfg_grid grid{};
+    std::vector<double> v1, v2;  // explicit T1/T2 values of the cached grid (empty: evenly spaced)
+    DevBuf kt;  // float log2(e)/T1 [n1] then log2(e)/T2 [n2], 1/s (K1 row producers)
     DevBuf stepu;  // n x StepU
     bool valid = false;
     // Parameter-major (lattice index i, step j):
@@ -93,7 +115,9 @@ struct Ctx {
     // scratch
     DevBuf zoom;  // K5 per-warp scratch (grow-only: no allocation inside a timed call)
     DevBuf q64, qprime, best, cand, cand_count, atoms_a, inv2, seed_a, seed_inv2, rerank,
-        params, out64, misc, rerank_scratch;
+        params, out64, misc, rerank_scratch, misc2, audit,
+        // persistent buffers of the host-buffer entry points (no per-call cudaMalloc)
+        h_raw, h_res, h_dict;
     // producer stream + events for the K1/K2 overlap (created on first use)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev[8] = {};
@@ -109,6 +133,13 @@ struct Ctx {
 // ------------------------------------------------------------ host helpers
 void host_rf_matrix(double alpha, double phi, double out[9]);  // bloch.cpp:63-66
 const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool need64);
+// AxisSpec::value (dictionary.hpp:22), or the explicit value
+inline double axis_value(const mrfg_axis& a, int64_t i) {
+    return a.values ? a.values[i] : a.min + static_cast<double>(i) * a.step;
+}
+inline bool grid_explicit(const mrfg_grid& g) {
+    return g.t1_ms.values || g.t2_ms.values || g.df_hz.values;
+}
 inline int64_t grid_total(const mrfg_grid& g) {
     return g.t1_ms.count * g.t2_ms.count * g.df_hz.count;
 }
@@ -160,20 +191,45 @@ struct MatchParams {
     float delta;
     int metric;
     float* debug_scores;  // optional dense atoms x nvox output (tests)
+    // Unbiased screening audit: every (voxel, atom) pair whose hash falls
+    // below audit_thr (a fraction audit_thr / 2^32 of all screened pairs,
+    // independent of its score) is appended here with its screening score.
+    CandRec* audit;
+    unsigned long long* audit_count;
+    int64_t audit_cap;
+    uint32_t audit_thr;
 };
+// The audit sample's hash: one mix of the pair's global flat and voxel.
+__host__ __device__ inline uint32_t audit_hash_voxel(uint64_t v) {
+    uint32_t h = static_cast<uint32_t>(v) * 0x85EBCA77u + 0x165667B1u;
+    return h ^ (h >> 13);
+}
+__host__ __device__ inline uint32_t audit_hash_flat(uint64_t f) {
+    uint32_t h = static_cast<uint32_t>(f) * 0x9E3779B1u ^ static_cast<uint32_t>(f >> 32) * 0xC2B2AE3Du;
+    return h ^ (h >> 16);
+}
+__host__ __device__ inline uint32_t audit_mix(uint32_t ha, uint32_t hv) {
+    uint32_t h = (ha ^ hv) * 0x7FEB352Du;
+    return h ^ (h >> 15);
+}
 void launch_match(Ctx& c, const MatchParams& p);
 // CUDA-core reference of the same fused screening (tests only, small sizes).
 void launch_match_simt(Ctx& c, const MatchParams& p);
 
 // K3 (rerank.cu)
 void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qrows, double* d_q64,
-                            __half* d_qprime, int* d_bad);
+                            __half* d_qprime, int* d_bad, const uint8_t* d_unit = nullptr);
 // Exact re-rank: lattice atoms re-simulated through the FP64 tables (t), or
 // stored float32 dictionary entries (d_dict != nullptr, flat = row).
 int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, const double* d_q64,
                           int64_t nq, int metric, const float* d_best, float delta, CandRec* d_cand,
                           int64_t ncand, mrfg_match* d_out, double* err_max = nullptr,
-                          bool allow_missing = false, int64_t* stats_n32 = nullptr);
+                          bool allow_missing = false, int64_t* stats_n32 = nullptr,
+                          bool allow_fp32 = true, double* err32_max = nullptr);
+// Unbiased screening audit over K2's sampled pairs (metric cc): max fp16
+// screening error and (lattice) max FP32 re-screen error against the exact scores.
+void audit_screen(Ctx& c, const GridTables* t, const float* d_dict, const double* d_q64, const CandRec* d_rec,
+                  int64_t n, double* err16, double* err32);
 // Stored float32 rows first + r*stride (r < count) -> fp16 operand (rows, zero
 // padded) + inv.
 void launch_dict_operand(Ctx& c, const float* d_dict, int64_t first, int64_t count, int64_t rows,

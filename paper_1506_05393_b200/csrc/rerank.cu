@@ -22,14 +22,18 @@ namespace mrfg {
 namespace {
 
 // prep_query (dictionary.cpp:145-150) -> normalize (fingerprint.cpp:28-37),
-// then the fp16 screening rows (see match_sm100.cu).
+// then the fp16 screening rows (see match_sm100.cu).  A query flagged
+// unit_norm (unit[v] != 0) is used as given (`fp.unit_norm ? fp :
+// normalize(fp)`); its screening rows are still scaled to unit length.
 __global__ void k_prepare_queries(const double* __restrict__ raw, int n, int64_t nq,
                                   int64_t k_pad, double* __restrict__ q64,
-                                  __half* __restrict__ qprime, int* __restrict__ bad) {
+                                  __half* __restrict__ qprime, int* __restrict__ bad,
+                                  const uint8_t* __restrict__ unit) {
     int64_t v = blockIdx.x;
     if (v >= nq) return;
     __shared__ double s_inv;
     const double* src = raw + v * 2 * n;
+    const bool as_is = unit != nullptr && unit[v] != 0;
     if (threadIdx.x == 0) {
         double acc = 0;  // sequential, the reference's summation order
         for (int j = 0; j < n; ++j)
@@ -44,13 +48,13 @@ __global__ void k_prepare_queries(const double* __restrict__ raw, int n, int64_t
     __half* re_row = qprime + (2 * v) * k_pad;
     __half* im_row = qprime + (2 * v + 1) * k_pad;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        double qr = __dmul_rn(src[2 * j], inv), qi = __dmul_rn(src[2 * j + 1], inv);
-        q64[v * 2 * n + 2 * j] = qr;
-        q64[v * 2 * n + 2 * j + 1] = qi;
-        re_row[2 * j] = __double2half(qr);
-        re_row[2 * j + 1] = __double2half(qi);
-        im_row[2 * j] = __double2half(qi);
-        im_row[2 * j + 1] = __double2half(-qr);
+        const double ur = __dmul_rn(src[2 * j], inv), ui = __dmul_rn(src[2 * j + 1], inv);
+        q64[v * 2 * n + 2 * j] = as_is ? src[2 * j] : ur;
+        q64[v * 2 * n + 2 * j + 1] = as_is ? src[2 * j + 1] : ui;
+        re_row[2 * j] = __double2half(ur);
+        re_row[2 * j + 1] = __double2half(ui);
+        im_row[2 * j] = __double2half(ui);
+        im_row[2 * j + 1] = __double2half(-ur);
     }
 }
 
@@ -242,21 +246,15 @@ struct Tab32 {
     Lattice L;
 };
 
-__global__ void __launch_bounds__(128) k_rescreen32(Tab32 T, const double* __restrict__ q64,
-                                                    const CandRec* __restrict__ cand,
-                                                    const int64_t* __restrict__ list, int64_t cnt,
-                                                    float* __restrict__ s32, unsigned* __restrict__ vmax,
-                                                    unsigned* __restrict__ err_max) {
-    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (k >= cnt) return;
-    const CandRec r = cand[list[k]];
+// One candidate's FP32 re-screen score (the K5 screening arithmetic).
+__device__ float rescreen32_score(const Tab32& T, const double* __restrict__ q64, int64_t flat) {
     int i1, i2, idf;
-    unflatten(r.flat, T.L, i1, i2, idf);
+    unflatten(flat, T.L, i1, i2, idf);
     const int n = T.n;
     const float4* e1p = T.e1f + static_cast<int64_t>(i1) * n;
     const float2* e2p = T.e2f + static_cast<int64_t>(i2) * n;
     const float4* php = T.phf + static_cast<int64_t>(idf) * n;
-    const double2* q = reinterpret_cast<const double2*>(q64 + static_cast<int64_t>(r.voxel) * 2 * n);
+    const double2* q = reinterpret_cast<const double2*>(q64);
     float x = T.inv0[0], y = T.inv0[1], z = T.inv0[2];
     double re = 0.0, im = 0.0, nn = 0.0;
     float pr = 0.f, pi = 0.f, pn = 0.f;
@@ -292,10 +290,29 @@ __global__ void __launch_bounds__(128) k_rescreen32(Tab32 T, const double* __res
     re += pr;
     im += pi;
     nn += pn;
-    const float sc = static_cast<float>(fmin(sqrt(re * re + im * im) / sqrt(nn), 1.0));
+    return static_cast<float>(fmin(sqrt(re * re + im * im) / sqrt(nn), 1.0));
+}
+
+__global__ void __launch_bounds__(128) k_rescreen32(Tab32 T, const double* __restrict__ q64,
+                                                    const CandRec* __restrict__ cand,
+                                                    const int64_t* __restrict__ list, int64_t cnt,
+                                                    float* __restrict__ s32, unsigned* __restrict__ vmax,
+                                                    unsigned* __restrict__ err_max) {
+    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= cnt) return;
+    const CandRec r = cand[list[k]];
+    const float sc = rescreen32_score(T, q64 + static_cast<int64_t>(r.voxel) * 2 * T.n, r.flat);
     s32[k] = sc;
     atomicMax(vmax + r.voxel, __float_as_uint(sc));  // scores >= 0: int order = float order
     atomicMax(err_max, __float_as_uint(fabsf(sqrtf(r.s) - sc)));
+}
+
+// max |s32 - exact| over the FP64 survivors of the FP32 stage (k: compacted index)
+__global__ void k_err32(const float* __restrict__ s32c, const double* __restrict__ score, int64_t n,
+                        unsigned* __restrict__ err) {
+    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= n) return;
+    atomicMax(err, __float_as_uint(static_cast<float>(fabs(static_cast<double>(s32c[k]) - score[k]))));
 }
 
 __global__ void k_flag32(const CandRec* __restrict__ cand, const int64_t* __restrict__ list, int64_t cnt,
@@ -429,6 +446,41 @@ __global__ void k_cc_map(Tab64 T, const double* __restrict__ q, int64_t first, i
     out[k] = static_cast<float>(exact_score(T, q, first + k, MRFG_METRIC_CC));  // dictionary.cpp:325-327
 }
 
+Tab32 tab32_of(Ctx& c, const GridTables& t) {
+    Tab32 T32;
+    T32.su = t.stepu.as<StepU>();
+    T32.e1f = t.e1f.as<float4>();
+    T32.e2f = t.e2f.as<float2>();
+    T32.phf = t.phf.as<float4>();
+    T32.inv0[0] = static_cast<float>(c.inv64[2]);
+    T32.inv0[1] = static_cast<float>(c.inv64[5]);
+    T32.inv0[2] = static_cast<float>(c.inv64[8]);
+    T32.n = static_cast<int>(c.n);
+    T32.L = {t.grid.t1_ms.count, t.grid.t2_ms.count, t.grid.df_hz.count};
+    return T32;
+}
+
+// Unbiased screening audit (metric cc): for every sampled (voxel, atom) pair,
+// whatever its screening score, the exact reference score, the fp16 screening
+// error |sqrt(s) - exact| and (lattice scans) the FP32 re-screen error
+// |s32 - exact|.  Errors are rounded up to float.
+__global__ void __launch_bounds__(64) k_audit(Tab64 T, Tab32 T32, const float* __restrict__ dict,
+                                              const double* __restrict__ q64, const CandRec* __restrict__ rec,
+                                              int64_t n, unsigned* __restrict__ err16,
+                                              unsigned* __restrict__ err32) {
+    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= n) return;
+    const CandRec r = rec[k];
+    const double* q = q64 + static_cast<int64_t>(r.voxel) * 2 * T.n;
+    const double ex = dict ? exact_score_entry(q, dict + r.flat * 2 * T.n, T.n, MRFG_METRIC_CC)
+                           : exact_score(T, q, r.flat, MRFG_METRIC_CC);
+    atomicMax(err16, __float_as_uint(__double2float_ru(fabs(sqrt(static_cast<double>(r.s)) - ex))));
+    if (!dict) {
+        const float s32 = rescreen32_score(T32, q, r.flat);
+        atomicMax(err32, __float_as_uint(__double2float_ru(fabs(static_cast<double>(s32) - ex))));
+    }
+}
+
 Tab64 tab64_of(Ctx& c, const GridTables& t) {
     Tab64 T;
     T.rf = c.rf64_d.as<double>();
@@ -446,11 +498,11 @@ Tab64 tab64_of(Ctx& c, const GridTables& t) {
 }  // namespace
 
 void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qrows, double* d_q64,
-                            __half* d_qprime, int* d_bad) {
+                            __half* d_qprime, int* d_bad, const uint8_t* d_unit) {
     const int64_t kp = k_pad_of(c.n);
     MRFG_CUDA(cudaMemsetAsync(d_qprime, 0, sizeof(__half) * qrows * kp, c.stream));
     k_prepare_queries<<<nq, 128, 0, c.stream>>>(d_raw, static_cast<int>(c.n), nq, kp, d_q64, d_qprime,
-                                                d_bad);
+                                                d_bad, d_unit);
     MRFG_CUDA(cudaGetLastError());
 }
 
@@ -460,7 +512,7 @@ void launch_prepare_queries(Ctx& c, const double* d_raw, int64_t nq, int64_t qro
 int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, const double* d_q64,
                           int64_t nq, int metric, const float* d_best, float delta, CandRec* d_cand,
                           int64_t ncand, mrfg_match* d_out, double* err_max, bool allow_missing,
-                          int64_t* stats_n32) {
+                          int64_t* stats_n32, bool allow_fp32, double* err32_max) {
     // scratch layout: list, list2 (ncand i64) | keys, keys2 (ncand u64) |
     //                 score (ncand f64) | vkey, vflat (nq u64) | counters | sort temp
     const int vbits = std::max(1, 64 - __builtin_clzll(static_cast<unsigned long long>(std::max<int64_t>(nq, 2) - 1)));
@@ -505,10 +557,12 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
     float* s32 = reinterpret_cast<float*>(base + 40 * static_cast<size_t>(cap) + 16 * nq + 64);
     unsigned* vmax = reinterpret_cast<unsigned*>(s32 + cap);
     unsigned char* flags = reinterpret_cast<unsigned char*>(vmax + nq);
+    float* s32c = reinterpret_cast<float*>(flags + cap);  // 4-byte aligned: cap, nq multiples of 4 apart
+    unsigned* d_err32 = reinterpret_cast<unsigned*>(cnt32 + 2);
     void* d_sort_tmp = base + (head + 255) / 256 * 256;
     MRFG_CUDA(cudaMemsetAsync(vkey, 0, sizeof(unsigned long long) * nq, c.stream));
     MRFG_CUDA(cudaMemsetAsync(vflat, 0xFF, sizeof(unsigned long long) * nq, c.stream));
-    MRFG_CUDA(cudaMemsetAsync(cnt, 0, 24, c.stream));
+    MRFG_CUDA(cudaMemsetAsync(cnt, 0, 40, c.stream));
     const int bs = 256;
     if (ncand > 0)
         k_filter<<<(ncand + bs - 1) / bs, bs, 0, c.stream>>>(d_cand, ncand, d_best, delta, metric,
@@ -531,18 +585,9 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
     // certified FP32 re-screen (lattice scans, CC): only near-ties go to FP64
     const char* r32_env = std::getenv("MRFG_RERANK_FP32");  // "0": every candidate in FP64
     int64_t n32 = 0;
-    if (nsel > 0 && t != nullptr && metric == MRFG_METRIC_CC && !(r32_env && r32_env[0] == '0')) {
+    if (nsel > 0 && t != nullptr && metric == MRFG_METRIC_CC && allow_fp32 && !(r32_env && r32_env[0] == '0')) {
         n32 = static_cast<int64_t>(nsel);
-        Tab32 T32;
-        T32.su = t->stepu.as<StepU>();
-        T32.e1f = t->e1f.as<float4>();
-        T32.e2f = t->e2f.as<float2>();
-        T32.phf = t->phf.as<float4>();
-        T32.inv0[0] = static_cast<float>(c.inv64[2]);
-        T32.inv0[1] = static_cast<float>(c.inv64[5]);
-        T32.inv0[2] = static_cast<float>(c.inv64[8]);
-        T32.n = static_cast<int>(c.n);
-        T32.L = {t->grid.t1_ms.count, t->grid.t2_ms.count, t->grid.df_hz.count};
+        const Tab32 T32 = tab32_of(c, *t);
         MRFG_CUDA(cudaMemsetAsync(vmax, 0, sizeof(unsigned) * nq, c.stream));
         k_rescreen32<<<(nsel + 127) / 128, 128, 0, c.stream>>>(T32, d_q64, d_cand, list, nsel, s32, vmax, d_err);
         MRFG_CUDA(cudaGetLastError());
@@ -552,6 +597,11 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
         int64_t* out_list = list == list2 ? reinterpret_cast<int64_t*>(keys) : list2;
         size_t tmp = sort_tmp;
         MRFG_CUDA(cub::DeviceSelect::Flagged(d_sort_tmp, tmp, list, flags, out_list, cnt32,
+                                             static_cast<int64_t>(nsel), c.stream));
+        // the survivors' FP32 scores, aligned with the compacted list (their
+        // error against the exact scores is checked after the FP64 re-rank)
+        tmp = sort_tmp;
+        MRFG_CUDA(cub::DeviceSelect::Flagged(d_sort_tmp, tmp, s32, flags, s32c, cnt32 + 1,
                                              static_cast<int64_t>(nsel), c.stream));
         MRFG_CUDA(cudaMemcpyAsync(&nsel, cnt32, sizeof nsel, cudaMemcpyDeviceToHost, c.stream));
         MRFG_CUDA(cudaStreamSynchronize(c.stream));
@@ -590,12 +640,23 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
         k_select_flat<<<(nsel + bs - 1) / bs, bs, 0, c.stream>>>(d_cand, list, nsel, score, vkey,
                                                                  vflat);
         MRFG_CUDA(cudaGetLastError());
+        if (n32) {
+            k_err32<<<(nsel + bs - 1) / bs, bs, 0, c.stream>>>(s32c, score, nsel, d_err32);
+            MRFG_CUDA(cudaGetLastError());
+        }
     }
     k_write_matches<<<(nq + bs - 1) / bs, bs, 0, c.stream>>>(vkey, vflat, nq, d_out, missing);
     MRFG_CUDA(cudaGetLastError());
     int h_missing[2] = {0, 0};
+    unsigned h_err32 = 0;
     MRFG_CUDA(cudaMemcpyAsync(h_missing, missing, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    MRFG_CUDA(cudaMemcpyAsync(&h_err32, d_err32, sizeof h_err32, cudaMemcpyDeviceToHost, c.stream));
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    if (err32_max) {
+        float e;
+        std::memcpy(&e, &h_err32, sizeof e);
+        *err32_max = e;
+    }
     if (err_max) {
         float e;
         std::memcpy(&e, &h_missing[1], sizeof e);
@@ -605,6 +666,34 @@ int64_t rerank_and_select(Ctx& c, const GridTables* t, const float* d_dict, cons
     // buffer overflowed); with one, flat -1 marks "nothing above the floor"
     MRFG_REQUIRE(!h_missing[0] || allow_missing, MRFG_E_RUNTIME, "scan: a query ended without candidates");
     return static_cast<int64_t>(nsel);
+}
+
+void audit_screen(Ctx& c, const GridTables* t, const float* d_dict, const double* d_q64, const CandRec* d_rec,
+                  int64_t n, double* err16, double* err32) {
+    *err16 = 0;
+    *err32 = 0;
+    if (n <= 0) return;
+    c.misc2.ensure(64);
+    unsigned* d_e = c.misc2.as<unsigned>();
+    MRFG_CUDA(cudaMemsetAsync(d_e, 0, 8, c.stream));
+    Tab64 T{};
+    Tab32 T32{};
+    if (t) {
+        T = tab64_of(c, *t);
+        T32 = tab32_of(c, *t);
+    } else {
+        T.n = static_cast<int>(c.n);
+    }
+    k_audit<<<static_cast<unsigned>((n + 63) / 64), 64, 0, c.stream>>>(T, T32, t ? nullptr : d_dict, d_q64, d_rec,
+                                                                        n, d_e, d_e + 1);
+    MRFG_CUDA(cudaGetLastError());
+    unsigned h[2] = {0, 0};
+    MRFG_CUDA(cudaMemcpyAsync(h, d_e, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+    MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    float f[2];
+    std::memcpy(f, h, sizeof f);
+    *err16 = f[0];
+    *err32 = f[1];
 }
 
 void launch_dict_operand(Ctx& c, const float* d_dict, int64_t first, int64_t count, int64_t rows,

@@ -93,6 +93,27 @@ def grid(t1, t2, df) -> Grid:
     return Grid(Axis(*t1), Axis(*t2), Axis(*df))
 
 
+def grid_values(t1_ms, t2_ms, df) -> Grid:
+    """Grid with EXPLICIT T1 and T2 values [ms] (e.g. log-spaced, BASELINE
+    configs[2]) and an evenly spaced df axis (min, step, count).  The arrays are
+    kept alive by the returned Grid.  generate / scan_grid / cc_map accept it;
+    the reference builds such dictionaries from explicit TissueParams."""
+    t1 = np.ascontiguousarray(t1_ms, dtype=np.float64)
+    t2 = np.ascontiguousarray(t2_ms, dtype=np.float64)
+    dp = C.POINTER(C.c_double)
+    g = Grid(Axis(float(t1[0]), 0.0, len(t1), t1.ctypes.data_as(dp)),
+             Axis(float(t2[0]), 0.0, len(t2), t2.ctypes.data_as(dp)), Axis(*df))
+    g._keep = (t1, t2)
+    return g
+
+
+def axis_values(ax: Axis) -> np.ndarray:
+    """AxisSpec::value over the axis (or its explicit values)."""
+    if ax.values:
+        return np.ctypeslib.as_array(ax.values, shape=(ax.count,)).copy()
+    return ax.min + np.arange(ax.count, dtype=np.float64) * ax.step
+
+
 def axis_count(lo: float, hi: float, step: float) -> int:
     c = C.c_int64()
     rc = N.load().mrfg_axis_count(lo, hi, step, C.byref(c))
@@ -125,9 +146,12 @@ def unflatten(g: Grid, flat):
 
 def params_at(g: Grid, i1, i2, idf):
     """ParameterGrid::params_at (dictionary.hpp:51-53): seconds, seconds, Hz."""
-    return ((g.t1_ms.min + np.asarray(i1, dtype=np.float64) * g.t1_ms.step) * 1e-3,
-            (g.t2_ms.min + np.asarray(i2, dtype=np.float64) * g.t2_ms.step) * 1e-3,
-            g.df_hz.min + np.asarray(idf, dtype=np.float64) * g.df_hz.step)
+    def val(ax, i):
+        i = np.asarray(i)
+        if ax.values:
+            return axis_values(ax)[i.astype(np.int64)]
+        return ax.min + i.astype(np.float64) * ax.step
+    return val(g.t1_ms, i1) * 1e-3, val(g.t2_ms, i2) * 1e-3, val(g.df_hz, idf)
 
 
 # -------------------------------------------------------------------- rng
@@ -310,11 +334,24 @@ class Context:
         return out
 
     # -- K2/K3
-    def scan_grid(self, g: Grid, queries, metric="cc", flat_range=(0, 0), opts: ScanOpts = None):
-        """scan_grid (dictionary.cpp:257-308) -> (best_flat, best_score, stats)."""
+    @staticmethod
+    def _unit_opts(opts, unit_norm, nq):
+        """Attach Fingerprint::unit_norm flags (bool or per-query array) to the options."""
+        if unit_norm is None or unit_norm is False:
+            return opts, None
+        flags = np.ascontiguousarray(np.broadcast_to(np.asarray(unit_norm, dtype=np.uint8), (nq,)))
+        o = ScanOpts() if opts is None else ScanOpts.from_buffer_copy(opts)
+        o.unit_queries = flags.ctypes.data_as(C.POINTER(C.c_uint8))
+        return o, flags
+
+    def scan_grid(self, g: Grid, queries, metric="cc", flat_range=(0, 0), opts: ScanOpts = None,
+                  unit_norm=None):
+        """scan_grid (dictionary.cpp:257-308) -> (best_flat, best_score, stats).
+        unit_norm: queries flagged Fingerprint::unit_norm are scored as given."""
         q = np.ascontiguousarray(np.atleast_2d(queries), dtype=np.complex128)
         if q.shape[-1] != self.n:
             raise N.InvalidArgument(-1, "query length does not match dictionary entries")
+        opts, _flags = self._unit_opts(opts, unit_norm, q.shape[0])
         out = (Match * q.shape[0])()
         st = ScanStats()
         check(self.lib.mrfg_scan_grid(self.h, C.byref(g), flat_range[0], flat_range[1],
@@ -336,6 +373,20 @@ class Context:
                                           C.c_void_p(d_out_ptr), C.byref(st)))
         return st
 
+    def scan_seed_device(self, g: Grid, d_queries_ptr: int, nq: int, d_seed_ptr: int, metric="cc",
+                         flat_range=(0, 0), opts: ScanOpts = None, d_dict_ptr: int = 0,
+                         natoms: int = 0) -> ScanStats:
+        """Seed pass only: float screening maxima (nq) of a strided sample of the
+        flat range (lattice g, or a device dictionary when d_dict_ptr is given)."""
+        st = ScanStats()
+        check(self.lib.mrfg_scan_seed_dev(self.h, None if d_dict_ptr else C.byref(g),
+                                          C.c_void_p(d_dict_ptr) if d_dict_ptr else None, natoms,
+                                          flat_range[0], flat_range[1], C.c_void_p(d_queries_ptr), nq,
+                                          METRIC.get(metric, metric),
+                                          C.byref(opts) if opts is not None else None,
+                                          C.c_void_p(d_seed_ptr), C.byref(st)))
+        return st
+
     def merge_matches_device(self, d_in_ptr: int, nranks: int, nq: int, d_out_ptr: int) -> None:
         check(self.lib.mrfg_merge_matches_dev(self.h, C.c_void_p(d_in_ptr), nranks, nq,
                                               C.c_void_p(d_out_ptr)))
@@ -345,7 +396,7 @@ class Context:
                                             C.c_void_p(d_out_ptr)))
 
     def brute_force_search(self, queries, dictionary: np.ndarray, metric="cc",
-                           opts: ScanOpts = None):
+                           opts: ScanOpts = None, unit_norm=None):
         """brute_force_search (dictionary.cpp:241-255) over a STORED dictionary.
 
         dictionary: (atoms, 2N) float32 unit entries in flat order (generate()'s
@@ -354,6 +405,7 @@ class Context:
         d = np.ascontiguousarray(dictionary, dtype=np.float32)
         if q.shape[-1] != self.n or d.shape[-1] != 2 * self.n:
             raise N.InvalidArgument(-1, "query length does not match dictionary entries")
+        opts, _flags = self._unit_opts(opts, unit_norm, q.shape[0])
         out = (Match * q.shape[0])()
         st = ScanStats()
         check(self.lib.mrfg_scan_dict(self.h, d.ctypes.data_as(C.POINTER(C.c_float)), d.shape[0],

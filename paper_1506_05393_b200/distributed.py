@@ -47,14 +47,38 @@ def merge_matches(flats: np.ndarray, scores: np.ndarray):
     return best_f, best_s
 
 
-def scan_grid_distributed(ctx, grid, d_queries, nq: int, group=None, opts=None, metric="cc"):
-    """Brute-force scan of the whole grid across the process group (GPU).
+def _all_gather(out, inp, group):
+    """all_gather_into_tensor (NCCL) or its list form (gloo, CPU tensors)."""
+    import torch.distributed as dist
+    if inp.device.type == "cuda":
+        dist.all_gather_into_tensor(out, inp, group=group)
+    else:
+        world = out.numel() // inp.numel()
+        dist.all_gather(list(out.view(world, -1).unbind(0)), inp.view(-1), group=group)
 
-    d_queries: CUDA float64 tensor (nq, 2N) resident on this rank's device.
-    Returns (CUDA uint8 tensor of nq mrfg_match records (flat i64, score f64),
+
+def scan_grid_distributed(ctx, grid, d_queries, nq: int, group=None, opts=None, metric="cc",
+                          global_seed: bool = True):
+    """Brute-force scan of the whole grid across the process group.
+
+    d_queries: float64 tensor (nq, 2N) on this rank's device (CUDA; CPU with
+    the test stub context).  Protocol:
+      1. (cc, global_seed) each rank's seed pass over its slab -> screening
+         maxima; one all_reduce(MAX) makes them global; they seed every rank's
+         screening (floor_matches), so per-rank candidates and re-rank work
+         do not grow with the world size;
+      2. each rank scans its contiguous T1 slab (K1 -> K2 -> K3), exact
+         (flat, score) per voxel, flat -1 where nothing on the slab reaches
+         the global seed;
+      3. ONE all_gather of the nq x 16 B match records and the merge (highest
+         score, lowest flat on ties; dictionary.cpp:291-294).
+    Returns (uint8 tensor of nq mrfg_match records (flat i64, score f64),
     identical on every rank; this rank's ScanStats or None)."""
+    import ctypes as C
+
     import torch
     import torch.distributed as dist
+    from ._native import ScanOpts
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -62,15 +86,28 @@ def scan_grid_distributed(ctx, grid, d_queries, nq: int, group=None, opts=None, 
     dev = d_queries.device
     d_out = torch.empty(nq * 16, dtype=torch.uint8, device=dev)
     stats = None
+    o = opts
+    if world > 1 and global_seed and metric == "cc":
+        seed = torch.full((nq,), -3.0, dtype=torch.float32, device=dev)
+        if fe > fb:
+            ctx.scan_seed_device(grid, d_queries.data_ptr(), nq, seed.data_ptr(), metric=metric,
+                                 flat_range=(fb, fe), opts=opts)
+        dist.all_reduce(seed, op=dist.ReduceOp.MAX, group=group)
+        floor = torch.zeros((nq, 2), dtype=torch.float64, device=dev)
+        floor[:, 1] = seed.double()
+        floor_rec = floor.view(torch.int64)
+        floor_rec[:, 0] = 0  # flat 0: "a floor is present"
+        o = ScanOpts() if opts is None else ScanOpts.from_buffer_copy(opts)
+        o.floor_matches = C.c_void_p(floor_rec.data_ptr())
     if fe > fb:
         stats = ctx.scan_grid_device(grid, d_queries.data_ptr(), nq, d_out.data_ptr(), metric=metric,
-                                     flat_range=(fb, fe), opts=opts)
+                                     flat_range=(fb, fe), opts=o)
     else:  # more ranks than T1 slabs: contribute "no atoms"
         d_out.view(torch.int64).view(nq, 2)[:, 0] = -1
     if world == 1:
         return d_out, stats
     d_all = torch.empty(world * nq * 16, dtype=torch.uint8, device=dev)
-    dist.all_gather_into_tensor(d_all, d_out, group=group)
+    _all_gather(d_all, d_out, group)
     d_merged = torch.empty(nq * 16, dtype=torch.uint8, device=dev)
     ctx.merge_matches_device(d_all.data_ptr(), world, nq, d_merged.data_ptr())
     return d_merged, stats
@@ -93,10 +130,7 @@ def gather_voxel_shards(local, nvox: int, rec_bytes: int, group=None):
     pad = torch.zeros(cap * rec_bytes, dtype=torch.uint8, device=local.device)
     pad[: local.numel()] = local
     allb = torch.empty(world * cap * rec_bytes, dtype=torch.uint8, device=local.device)
-    if local.device.type == "cuda":
-        dist.all_gather_into_tensor(allb, pad, group=group)
-    else:
-        dist.all_gather(list(allb.view(world, cap * rec_bytes).unbind(0)), pad, group=group)
+    _all_gather(allb, pad, group)
     parts = []
     for r in range(world):
         vb, ve = voxel_shard(nvox, world, r)

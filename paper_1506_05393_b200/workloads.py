@@ -20,6 +20,13 @@ Conventions that the reference does not define are stated here once:
 * noise: ``add_noise(pd*s, sigma, seed=1_000_000 + v)`` with
   sigma = ||pd*s||_2 / sqrt(N) / SNR per real channel.
 
+* config 3 (materialized log-axis dictionary): T1 = geomspace(100, 4000, 300) ms,
+  T2 = geomspace(10, 2000, 200) ms, df -100..100 step 5 Hz (41); voxel indices
+  ``rng_at(7, axis, v) % count``; noise seed 5_000_000 + v, SNR 20;
+* config 5 (B1): 13 schedules with flip_deg * B1, B1 = 0.70..1.30 step 0.05;
+  voxel indices ``rng_at(11, axis, v) % count`` over (B1, T1, T2, df); noise
+  seed 9_000_000 + v, SNR 25; the 4-D flat is b1 * A3 + flat3.
+
 ``simulate`` is injected ((schedule, params (k,3)) -> (k,N) complex128) so tests can make
 the truth fingerprints with the CPU oracle and the benchmark with the GPU.
 """
@@ -155,3 +162,64 @@ def make(config: int, simulate, nvox: int | None = None, n: int | None = None,
     fps = noisy(clean, c["snr"])
     return Workload(config, sched, g, nx, ny, truth, pd, fps, c["snr"],
                     meta=dict(atoms=dgs.grid_total(g)))
+
+
+# --------------------------------------------------------------- config 3
+CONFIG3 = dict(n=1000, nvox=16 * 128 * 128, snr=20.0, df=(-100.0, 5.0, 41))
+
+
+def config3_axes():
+    """(t1_ms, t2_ms, df (min, step, count)): log-spaced T1/T2, linear df."""
+    return (np.geomspace(100.0, 4000.0, 300), np.geomspace(10.0, 2000.0, 200), CONFIG3["df"])
+
+
+def config3_voxels(simulate, voxels) -> tuple:
+    """Config 3 inputs for the given voxel ids -> (schedule, truth (V,3), fps (V,N))."""
+    n = CONFIG3["n"]
+    sched = dgs.baseline_schedule(n, 1)
+    t1, t2, (dmin, dstep, dcnt) = config3_axes()
+    voxels = np.asarray(voxels, dtype=np.int64)
+    idx = np.array([[dgs.rng_at(7, ax, int(v)) % c for ax, c in enumerate((t1.size, t2.size, dcnt))]
+                    for v in voxels], dtype=np.int64).reshape(-1, 3)
+    prm = np.stack([t1[idx[:, 0]] * 1e-3, t2[idx[:, 1]] * 1e-3, dmin + idx[:, 2] * dstep], 1)
+    fps = simulate(sched, prm) if len(voxels) else np.zeros((0, n), np.complex128)
+    for k, v in enumerate(voxels):
+        sig = float(np.sqrt(np.sum(np.abs(fps[k]) ** 2))) / math.sqrt(n) / CONFIG3["snr"]
+        fps[k] = dgs.add_noise(fps[k], sig, 5_000_000 + int(v))
+    return sched, idx, fps
+
+
+# --------------------------------------------------------------- config 5
+CONFIG5 = dict(n=3000, nvox=128 * 128, snr=25.0, b1=[round(0.7 + 0.05 * k, 10) for k in range(13)],
+               t1=(100.0, 3000.0, 25.0), t2=(20.0, 500.0, 10.0), df=(-100.0, 100.0, 10.0))
+
+
+def config5_schedules():
+    base = dgs.baseline_schedule(CONFIG5["n"], 1)
+    return [dgs.Schedule(base.flip_deg * b, base.phase_deg, base.tr_ms, base.te_ms) for b in CONFIG5["b1"]]
+
+
+def config5_grid() -> dgs.Grid:
+    return dgs.grid_inclusive(CONFIG5["t1"], CONFIG5["t2"], CONFIG5["df"])
+
+
+def config5_voxels(simulate, voxels) -> tuple:
+    """Config 5 inputs -> (schedules, grid, truth (V,4) = (b1, i1, i2, idf), fps (V,N)).
+    ``simulate(schedule, params)`` is called once per B1 schedule present."""
+    n = CONFIG5["n"]
+    scheds = config5_schedules()
+    g = config5_grid()
+    counts = (len(scheds), g.t1_ms.count, g.t2_ms.count, g.df_hz.count)
+    voxels = np.asarray(voxels, dtype=np.int64)
+    idx = np.array([[dgs.rng_at(11, ax, int(v)) % c for ax, c in enumerate(counts)] for v in voxels],
+                   dtype=np.int64).reshape(-1, 4)
+    fps = np.zeros((len(voxels), n), dtype=np.complex128)
+    for k, s in enumerate(scheds):
+        sel = np.nonzero(idx[:, 0] == k)[0]
+        if sel.size:
+            prm = np.stack(dgs.params_at(g, idx[sel, 1], idx[sel, 2], idx[sel, 3]), axis=1)
+            fps[sel] = simulate(s, prm)
+    for k, v in enumerate(voxels):
+        sig = float(np.sqrt(np.sum(np.abs(fps[k]) ** 2))) / math.sqrt(n) / CONFIG5["snr"]
+        fps[k] = dgs.add_noise(fps[k], sig, 9_000_000 + int(v))
+    return scheds, g, idx, fps

@@ -318,3 +318,172 @@ def test_scan_tiny_shapes(orc, n):
                 flat, score, _ = c.scan_grid(g, fps)
             of, osc, osec = orc.scan_grid(os_, to_oracle_grid(g), fps)
             assert_parity(flat, score, of, osc, osec)
+
+
+# ---------------------------------------------------------------- round 2
+def test_screen_audit_certifies_margin(small, small_ref):
+    """The unbiased audit (hash sample of ALL screened pairs, scored exactly)
+    reports the fp16 screening error; the default margin (2.5e-3) is at least
+    twice it, and the FP32 re-screen error stays below half its margin."""
+    with P.Context(small.schedule) as c:
+        flat, score, st = c.scan_grid(small.grid, small.fps)
+    assert_parity(flat, score, *small_ref)
+    assert st.delta_used == 2.5e-3 and st.rescans == 0
+    assert st.audit_samples > 1000
+    assert 0 < st.screen_err_audit_max <= 0.5 * st.delta_used
+    assert st.rescreen_err_audit_max <= 5e-6
+    assert st.rescreen_err_max <= 5e-6
+
+
+def test_screen_audit_widens_too_small_margin(small, small_ref):
+    """A margin below twice the audited error is widened by a rescan: the
+    answers stay the reference's."""
+    with P.Context(small.schedule) as c:
+        flat, score, st = c.scan_grid(small.grid, small.fps, opts=ScanOpts(1e-5, 0, 0, 0))
+    assert_parity(flat, score, *small_ref)
+    assert st.rescans >= 1 and st.delta_used > 1e-5
+    assert st.screen_err_audit_max <= 0.5 * st.delta_used
+
+
+def seq_normalize(fp):
+    """normalize (fingerprint.cpp:28-37) with the reference's summation order."""
+    acc = 0.0
+    for v in fp:
+        acc += v.real * v.real + v.imag * v.imag
+    inv = 1.0 / np.sqrt(acc)
+    return np.array([complex(v.real * inv, v.imag * inv) for v in fp])
+
+
+@pytest.mark.parametrize("metric", ["cc", "euclidean"])
+def test_scan_unit_norm_queries(orc, small, metric):
+    """Fingerprint::unit_norm queries are used as given (prep_query,
+    dictionary.cpp:145-150), in scan_grid and brute_force_search: scores
+    equal the reference's for normalize()d queries, including exact on-grid ones."""
+    os_ = to_oracle_sched(small.schedule)
+    og = to_oracle_grid(small.grid)
+    q = np.stack([seq_normalize(f) for f in small.fps[:24]])
+    exact = orc.simulate(os_, *[float(x) for x in P.params_at(small.grid, 40, 11, 7)])
+    q = np.concatenate([q, seq_normalize(exact)[None]])
+    m = 1 if metric == "euclidean" else 0
+    oflat, oscore, osecond = orc.scan_grid(os_, og, q, metric=m, unit_norm=True)
+    with P.Context(small.schedule) as c:
+        flat, score, _ = c.scan_grid(small.grid, q, metric=metric, unit_norm=True)
+        dflat, dscore, _ = c.brute_force_search(q, c.generate(small.grid, precision=64), metric=metric,
+                                                unit_norm=True)
+    assert_parity(flat, score, oflat, oscore, osecond)
+    np.testing.assert_array_equal(dflat, flat)
+    np.testing.assert_array_equal(dscore, score)
+
+
+def explicit_problem(orc):
+    s = P.baseline_schedule(200, 1)
+    t1 = np.geomspace(300.0, 2500.0, 23)
+    t2 = np.geomspace(30.0, 400.0, 17)
+    df = (-30.0, 5.0, 13)
+    rng = np.random.default_rng(3)
+    os_ = to_oracle_sched(s)
+    q = np.stack([orc.add_noise(orc.simulate(os_, t1[rng.integers(23)] * 1e-3 * (1 + 0.01 * rng.random()),
+                                             t2[rng.integers(17)] * 1e-3, -30 + 60 * rng.random()), 0.003, 500 + k)
+                  for k in range(40)])
+    return s, t1, t2, df, q
+
+
+def oracle_rows_scan(orc, s, t1, t2, df, q):
+    """Restatement oracle over explicit T1 x T2 values: one-row subgrids
+    {t1, 1, 1} x {t2, 1, 1} x df in flat order, strict > across rows."""
+    import oracle
+    os_ = to_oracle_sched(s)
+    best_f = np.zeros(len(q), np.int64)
+    best_s = np.full(len(q), -np.inf)
+    for i1, a in enumerate(t1):
+        for i2, b in enumerate(t2):
+            g = oracle.make_grid((a, 1.0, 1), (b, 1.0, 1), df)
+            f, sc, _ = orc.scan_grid(os_, g, q, threads=8)
+            better = sc > best_s
+            best_f = np.where(better, (i1 * len(t2) + i2) * df[2] + f, best_f)
+            best_s = np.where(better, sc, best_s)
+    return best_f, best_s
+
+
+def test_explicit_axes_generate_bit_identical(orc):
+    """A lattice with explicit (log-spaced) T1/T2 values: FP64 generate equals
+    the reference pipeline over the same TissueParams bit for bit."""
+    import oracle
+    s, t1, t2, df, _ = explicit_problem(orc)
+    g = P.grid_values(t1, t2, df)
+    os_ = to_oracle_sched(s)
+    with P.Context(s) as c:
+        ent = c.generate(g, precision=64)
+    for i1 in (0, 7, 22):
+        for i2 in (0, 9, 16):
+            sub = oracle.make_grid((t1[i1], 1.0, 1), (t2[i2], 1.0, 1), df)
+            want = orc.generate(os_, sub, 0, df[2])
+            f0 = (i1 * len(t2) + i2) * df[2]
+            np.testing.assert_array_equal(ent[f0:f0 + df[2]], want)
+
+
+def test_explicit_axes_scan_and_dictionary(orc):
+    """Streamed scan_grid over the explicit-axis lattice and K4 over its
+    materialized dictionary: the reference's answers and scores."""
+    s, t1, t2, df, q = explicit_problem(orc)
+    g = P.grid_values(t1, t2, df)
+    of, osc = oracle_rows_scan(orc, s, t1, t2, df, q)
+    with P.Context(s) as c:
+        flat, score, st = c.scan_grid(g, q)
+        dflat, dscore, _ = c.brute_force_search(q, c.generate(g, precision=64))
+        cm = c.cc_map(q[0], g, precision=64)
+    np.testing.assert_array_equal(flat, of)
+    np.testing.assert_array_equal(score, osc)
+    np.testing.assert_array_equal(dflat, of)
+    np.testing.assert_array_equal(dscore, osc)
+    assert int(np.argmax(cm)) == of[0]
+
+
+def test_explicit_axes_rejected_where_unsupported(orc):
+    s, t1, t2, df, q = explicit_problem(orc)
+    g = P.grid_values(t1, t2, df)
+    with P.Context(s) as c:
+        with pytest.raises(ValueError):
+            c.quantify(q[:1], g)
+        with pytest.raises(ValueError):
+            c.save_generated(g, "/tmp/never.mrfd")
+
+
+def test_seeded_shards_equal_single_scan(small, small_ref):
+    """The multi-GPU protocol on one device: per-shard seed maxima, reduced by
+    max, floor every shard's scan; merge == the single scan, and the seeded
+    shards re-rank no more than unseeded ones."""
+    import torch
+    g, fps = small.grid, small.fps
+    total = P.grid_total(g)
+    nq, n = fps.shape
+    dev = torch.device("cuda", 0)
+    d_q = torch.from_numpy(np.ascontiguousarray(fps).view(np.float64).reshape(nq, 2 * n)).to(dev)
+    W = 3
+    slab = g.t2_ms.count * g.df_hz.count
+    cuts = [g.t1_ms.count * r // W * slab for r in range(W + 1)]
+    with P.Context(small.schedule) as c:
+        seeds = torch.full((W, nq), -3.0, dtype=torch.float32, device=dev)
+        for r in range(W):
+            c.scan_seed_device(g, d_q.data_ptr(), nq, seeds[r].data_ptr(), flat_range=(cuts[r], cuts[r + 1]))
+        seed = seeds.max(dim=0).values
+        floor = torch.zeros((nq, 2), dtype=torch.float64, device=dev)
+        floor[:, 1] = seed.double()
+        fl = floor.view(torch.int64)
+        fl[:, 0] = 0
+        d_all = torch.empty((W, nq, 2), dtype=torch.int64, device=dev)
+        seeded, plain = 0, 0
+        for r in range(W):
+            st = c.scan_grid_device(g, d_q.data_ptr(), nq, d_all[r].data_ptr(), flat_range=(cuts[r], cuts[r + 1]),
+                                    opts=ScanOpts(0.0, 0, 0, 0, fl.data_ptr()))
+            seeded += st.reranked
+        d_out = torch.empty((nq, 2), dtype=torch.int64, device=dev)
+        c.merge_matches_device(d_all.data_ptr(), W, nq, d_out.data_ptr())
+        torch.cuda.synchronize()
+        tmp = torch.empty((nq, 2), dtype=torch.int64, device=dev)
+        for r in range(W):
+            plain += c.scan_grid_device(g, d_q.data_ptr(), nq, tmp.data_ptr(),
+                                        flat_range=(cuts[r], cuts[r + 1])).reranked
+    out = d_out.cpu().numpy()
+    assert_parity(out[:, 0], out[:, 1].view(np.float64), *small_ref)
+    assert seeded <= plain

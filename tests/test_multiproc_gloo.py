@@ -1,10 +1,10 @@
 """N>1 path on CPU: world_size-2 gloo process group.
 
 Each rank owns one contiguous T1 slab (distributed.grid_shard) / voxel block
-(distributed.voxel_shard), computes its part (here with the CPU oracle as the
-per-rank compute, since the CUDA kernels need a B200), exchanges through ONE
-all_gather, and reduces with distributed.merge_matches -- the host form of the
-device merge.  The merged result must equal the single-process reference scan
+(distributed.voxel_shard).  The brute-force test runs the production driver
+distributed.scan_grid_distributed itself (seed all_reduce, floored slab
+scans, ONE all_gather, merge) over a CPU stub context whose per-rank compute
+is the CPU oracle, since the CUDA kernels need a B200.  The merged result must equal the single-process reference scan
 bit-for-bit, for any world size.
 """
 import os
@@ -40,6 +40,63 @@ def problem():
     return orc, s, grid, q
 
 
+class StubCtx:
+    """CPU stand-in for dgs.Context exposing the device entry points that
+    distributed.scan_grid_distributed drives (the CUDA kernels need a B200):
+    raw pointers of CPU tensors in, the restatement oracle as the per-rank
+    compute.  Seed: exact best over the shard's first T1 row (a valid
+    screening seed: a real atom's score); floor: a voxel whose slab best is
+    below floor - delta reports flat -1, as the GPU scan does."""
+
+    def __init__(self, orc, sched, n):
+        self.orc, self.sched, self.n = orc, sched, n
+
+    @staticmethod
+    def _view(ptr, ctype, count):
+        import ctypes as C
+        return np.ctypeslib.as_array((ctype * count).from_address(ptr))
+
+    def _q(self, ptr, nq):
+        import ctypes as C
+        return self._view(ptr, C.c_double, nq * 2 * self.n).view(np.complex128).reshape(nq, self.n).copy()
+
+    def _sub(self, grid, fb, fe):
+        import oracle
+        slab = grid.t2_ms.count * grid.df_hz.count
+        a, b = fb // slab, fe // slab
+        return oracle.make_grid((grid.t1_ms.min + a * grid.t1_ms.step, grid.t1_ms.step, b - a),
+                                (grid.t2_ms.min, grid.t2_ms.step, grid.t2_ms.count),
+                                (grid.df_hz.min, grid.df_hz.step, grid.df_hz.count))
+
+    def scan_seed_device(self, grid, q_ptr, nq, seed_ptr, metric="cc", flat_range=(0, 0), opts=None):
+        import ctypes as C
+        fb, _ = flat_range
+        slab = grid.t2_ms.count * grid.df_hz.count
+        _, sc, _ = self.orc.scan_grid(self.sched, self._sub(grid, fb, fb + slab), self._q(q_ptr, nq), threads=1)
+        self._view(seed_ptr, C.c_float, nq)[:] = sc.astype(np.float32)
+
+    def scan_grid_device(self, grid, q_ptr, nq, out_ptr, metric="cc", flat_range=(0, 0), opts=None):
+        import ctypes as C
+        fb, fe = flat_range
+        f, sc, _ = self.orc.scan_grid(self.sched, self._sub(grid, fb, fe), self._q(q_ptr, nq), threads=1)
+        f = f + fb
+        if opts is not None and opts.floor_matches:
+            floor = self._view(opts.floor_matches, C.c_double, 2 * nq).reshape(nq, 2)[:, 1]
+            f = np.where(sc >= np.float32(floor) - 2.5e-3, f, -1)
+        out = self._view(out_ptr, C.c_uint8, 16 * nq).view([("flat", np.int64), ("score", np.float64)])
+        out["flat"], out["score"] = f, sc
+        self.last = (f.copy(), sc.copy())
+        return None
+
+    def merge_matches_device(self, in_ptr, nranks, nq, out_ptr):
+        import ctypes as C
+        rec = self._view(in_ptr, C.c_uint8, 16 * nq * nranks).view([("flat", np.int64), ("score", np.float64)])
+        rec = rec.reshape(nranks, nq)
+        mf, ms = D.merge_matches(rec["flat"], rec["score"])
+        out = self._view(out_ptr, C.c_uint8, 16 * nq).view([("flat", np.int64), ("score", np.float64)])
+        out["flat"], out["score"] = mf, ms
+
+
 def worker(rank, world, port, out_path):
     import sys
     sys.path.insert(0, ROOT)
@@ -47,30 +104,26 @@ def worker(rank, world, port, out_path):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     orc, s, (t1, t2, df), q = problem()
-    slab = t2[2] * df[2]
-    fb, fe = D.shard_range(t1[2], slab, world, rank)
-    i1b, i1e = fb // slab, fe // slab
-    nq = len(q)
-    if fe > fb:
-        sub = oracle.make_grid((t1[0] + i1b * t1[1], t1[1], i1e - i1b), t2, df)
-        f, sc, _ = orc.scan_grid(s, sub, q, threads=1)
-        f = f + fb  # local -> global flat
-    else:
-        f, sc = np.full(nq, -1, np.int64), np.full(nq, -1e300)
-    ft = torch.from_numpy(f)
-    st = torch.from_numpy(sc)
-    fall = [torch.empty_like(ft) for _ in range(world)]
-    sall = [torch.empty_like(st) for _ in range(world)]
-    dist.all_gather(fall, ft)
-    dist.all_gather(sall, st)
-    mf, ms = D.merge_matches(torch.stack(fall).numpy(), torch.stack(sall).numpy())
+    g = oracle.make_grid(t1, t2, df)
+    nq, n = q.shape
+    ctx = StubCtx(orc, s, n)
+    d_q = torch.from_numpy(np.ascontiguousarray(q).view(np.float64).reshape(nq, 2 * n))
+    # the production protocol: seed all_reduce, floored slab scans, ONE all_gather, merge
+    merged, _ = D.scan_grid_distributed(ctx, g, d_q, nq)
+    m = merged.numpy().view([("flat", np.int64), ("score", np.float64)])
+    # some rank's slab had nothing above the global seed for some voxel (the
+    # floor did work), unless every voxel's best is on every slab
+    lf = torch.from_numpy(ctx.last[0])
+    alls = [torch.empty_like(lf) for _ in range(world)]
+    dist.all_gather(alls, lf)
     # voxel-sharded "ZOOM-like" gather: each rank labels its voxel block
     vb, ve = D.voxel_shard(nq, world, rank)
     part = torch.zeros(nq, dtype=torch.int64)
-    part[vb:ve] = torch.from_numpy(mf[vb:ve])
+    part[vb:ve] = torch.from_numpy(m["flat"][vb:ve].copy())
     dist.all_reduce(part)
     if rank == 0:
-        np.savez(out_path, flat=mf, score=ms, vox=part.numpy())
+        np.savez(out_path, flat=m["flat"], score=m["score"], vox=part.numpy(),
+                 floored=int((torch.stack(alls) < 0).sum()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -86,6 +139,7 @@ def test_sharded_scan_equals_single_process(tmp_path, world):
     assert np.array_equal(r["flat"], f)
     assert np.array_equal(r["score"], sc)
     assert np.array_equal(r["vox"], f)
+    assert r["floored"] > 0  # the global seed pruned some slab's voxels
 
 
 def test_merge_rule_ties_and_empty_ranks():
