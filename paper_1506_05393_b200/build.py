@@ -14,8 +14,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmrfg.so")
 SHIM = os.path.join(HERE, "libmrf_b200.so")  # the reference's C++ interface over LIB
-# zoom_k_var.cu (experimental K5 variants) is the slowest object: listed
-# first so its ptxas starts first
+# zoom_k_var.cu holds the experimental K5 variants (compiled only with
+# MRFG_BUILD_VARIANTS=1; then it is the slowest object, so it is listed first)
 SOURCES = ["zoom_k_var.cu", "zoom_k_main.cu", "zoom_k_rows.cu", "zoom.cu", "abi.cu", "bloch.cu",
            "match_sm100.cu", "rerank.cu", "synth.cpp"]
 HEADERS = ["mrfg_internal.cuh", "sim64.cuh"]
@@ -67,6 +67,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd[4:4] = ["-Xptxas", "-v"] if verbose else []
+            if src == "zoom_k_var.cu" and os.environ.get("MRFG_BUILD_VARIANTS") == "1":
+                cmd[4:4] = ["-DMRFG_ZOOM_VARIANTS"]
         else:
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-I", os.path.join(ROOT, "include"),
                    "-c", os.path.join(CSRC, src), "-o", obj]

@@ -1,8 +1,16 @@
 // zoom_k_var.cu -- K5 kernel variants: experimental block sizes / register budgets (MRFG_ZOOM_BS, _MINB, _ROWW) (see zoom_launch.h).
+//
+// These variants were measured in round 1 (K5) and none is a
+// default; they cost ~15 min of ptxas, so they are compiled only with
+// MRFG_BUILD_VARIANTS=1 (build.py then defines MRFG_ZOOM_VARIANTS).  Without
+// them, the env switches that select one fail with "kernel variant not built".
 #include "zoom_dev.cuh"
 
 namespace mrfg {
 
+#ifndef MRFG_ZOOM_VARIANTS
+bool zoom_tu_var(int, const void*, bool, unsigned, int, size_t, cudaStream_t, int*) { return false; }
+#else
 bool zoom_tu_var(int v, const void* P, bool launch, unsigned grid, int block, size_t smem, cudaStream_t s, int* occ) {
     switch (v) {
         case kZoom256x2:
@@ -31,5 +39,6 @@ bool zoom_tu_var(int v, const void* P, bool launch, unsigned grid, int block, si
     }
     return true;
 }
+#endif
 
 }  // namespace mrfg
