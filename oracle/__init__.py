@@ -53,6 +53,16 @@ class ZoomCfg(C.Structure):
                 ("prior_window_t2_ms", C.c_double), ("prior_window_df_hz", C.c_double)]
 
 
+class Stage(C.Structure):
+    """StageLog (zoom.hpp:54-59); stage codes in STAGE_NAMES order."""
+    _fields_ = [("stage", C.c_int32), ("pad", C.c_int32), ("evaluations", C.c_int64), ("best", C.c_double),
+                ("t1_ms", C.c_double), ("t2_ms", C.c_double), ("df_hz", C.c_double)]
+
+
+STAGE_NAMES = ("df.coarse", "df.refine", "df.translate", "df.rerefine", "df.plateau_stop", "df.finest",
+               "df.fallback", "t1t2.2d", "df.sweep", "t1.1d", "t2.1d", "t1t2.final")
+
+
 class Quant(C.Structure):
     _fields_ = [("i1", C.c_int64), ("i2", C.c_int64), ("idf", C.c_int64),
                 ("t1_ms", C.c_double), ("t2_ms", C.c_double), ("df_hz", C.c_double),
@@ -143,6 +153,9 @@ class Oracle:
                                        C.c_int, C.c_int, C.POINTER(i64), dp, dp]
         L.orc_quantify.argtypes = [C.POINTER(Sched), C.POINTER(Grid), C.POINTER(ZoomCfg), dp,
                                    C.POINTER(Quant)]
+        L.orc_quantify_ex.argtypes = [C.POINTER(Sched), C.POINTER(Grid), C.POINTER(ZoomCfg), dp,
+                                      C.POINTER(C.c_float), i64, C.POINTER(Stage), C.c_int,
+                                      C.POINTER(C.c_int), C.POINTER(Quant)]
         L.orc_quantify_slice.argtypes = [C.POINTER(Sched), C.POINTER(Grid),
                                          C.POINTER(ZoomCfg), dp, C.POINTER(C.c_uint8),
                                          C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(Quant)]
@@ -292,6 +305,28 @@ class Oracle:
         self._check(self.lib.orc_quantify(C.byref(cs), C.byref(g), C.byref(cfg),
                                           self._dp(fp.view(np.float64)), C.byref(out)))
         return out
+
+    def quantify_ex(self, s: Schedule, g: Grid, cfg: ZoomCfg, fp: np.ndarray, dict_payload=None):
+        """quantify with an explicit dictionary payload (float32 entries x 2N,
+        or None) -> (Quant, list of (stage name, evaluations, best, t1_ms, t2_ms, df_hz))."""
+        fp = np.ascontiguousarray(fp, dtype=np.complex128)
+        out = Quant()
+        cs = s.c()
+        cap = 256
+        tr = (Stage * cap)()
+        ntr = C.c_int(0)
+        d = None
+        nd = 0
+        if dict_payload is not None:
+            d = np.ascontiguousarray(dict_payload, dtype=np.float32).reshape(-1, 2 * s.n)
+            nd = d.shape[0]
+        self._check(self.lib.orc_quantify_ex(
+            C.byref(cs), C.byref(g), C.byref(cfg), self._dp(fp.view(np.float64)),
+            None if d is None else d.ctypes.data_as(C.POINTER(C.c_float)), nd, tr, cap, C.byref(ntr),
+            C.byref(out)))
+        trace = [(STAGE_NAMES[tr[k].stage], tr[k].evaluations, tr[k].best, tr[k].t1_ms, tr[k].t2_ms,
+                  tr[k].df_hz) for k in range(min(ntr.value, cap))]
+        return out, trace
 
     def quantify_slice(self, s: Schedule, g: Grid, cfg: ZoomCfg, fps: np.ndarray,
                        mask: np.ndarray, nx: int, ny: int, use_prior: bool, threads: int = 0):

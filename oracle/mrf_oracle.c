@@ -551,6 +551,7 @@ typedef struct {
     int dict_mode; /* 0 none, 1 df dictionary during stage 1, 2 full dictionary */
     int in_stage1;
     double* buf3;
+    const float* dict; /* caller's dictionary payload (NULL: the generated entries) */
 } Obj;
 
 static uint64_t key_of(int64_t i1, int64_t i2, int64_t idf) {
@@ -593,11 +594,21 @@ static double obj_eval(Obj* o, int64_t i1, int64_t i2, int64_t idf, int metric) 
                 axis_value(&o->g->df_hz, idf), o->buf);
         const double* e;
         if (o->dict_mode == 2 || (o->dict_mode == 1 && o->in_stage1)) {
-            /* dictionary entry (zoom.cpp:101-110): the generated float entry
-             * float(normalize(simulate)) (dictionary.cpp:44-51), then, with
+            /* dictionary entry (zoom.cpp:101-110): d->entry(flat) with flat the
+             * lattice flat (full dictionary) or idf (df slab), as given -- or,
+             * without a payload, the generated float entry
+             * float(normalize(simulate)) (dictionary.cpp:44-51); then, with
              * smoothing, normalize(smooth(entry)) */
-            normalize(o->buf, n, o->buf3);
-            for (int64_t j = 0; j < 2 * n; ++j) o->buf3[j] = (double)(float)o->buf3[j];
+            if (o->dict) {
+                const int64_t flat = o->dict_mode == 2
+                                         ? (i1 * o->g->t2_ms.count + i2) * o->g->df_hz.count + idf
+                                         : idf;
+                const float* raw = o->dict + flat * 2 * n;
+                for (int64_t j = 0; j < 2 * n; ++j) o->buf3[j] = (double)raw[j];
+            } else {
+                normalize(o->buf, n, o->buf3);
+                for (int64_t j = 0; j < 2 * n; ++j) o->buf3[j] = (double)(float)o->buf3[j];
+            }
             if (o->smooth_k) {
                 smooth(o->buf3, n, o->smooth_k, o->buf2);
                 normalize(o->buf2, n, o->buf3);
@@ -658,11 +669,36 @@ typedef struct {
     int allow_fallback;
 } DfParams; /* zoom.hpp:115-126 */
 
+/* StageLog recording (zoom.cpp:441-451 log_stage): evaluations added since
+ * the previous note, the stage's best value and its lattice point. */
+typedef struct {
+    orc_stage* out;
+    int cap, n;
+    int64_t last;
+} Trace;
+static void note(Trace* t, const Obj* o, int stage, int64_t i1, int64_t i2, int64_t idf, double best) {
+    if (!t || !t->out) return;
+    if (t->n < t->cap) {
+        orc_stage* r = &t->out[t->n];
+        r->stage = stage;
+        r->pad = 0;
+        r->evaluations = o->evals - t->last;
+        r->best = best;
+        r->t1_ms = axis_value(&o->g->t1_ms, i1);
+        r->t2_ms = axis_value(&o->g->t2_ms, i2);
+        r->df_hz = axis_value(&o->g->df_hz, idf);
+    }
+    t->n++;
+    t->last = o->evals;
+}
+
 typedef struct {
     Obj* o;
     int64_t i1, i2;
     int metric;
+    Trace* tr;
 } DfCtx;
+#define DF_NOTE(c, st, b) note((c)->tr, (c)->o, (st), (c)->i1, (c)->i2, (b).idx, (b).val)
 static double f_df(DfCtx* c, int64_t idf) { return obj_eval(c->o, c->i1, c->i2, idf, c->metric); }
 
 static int64_t clampl(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -693,12 +729,14 @@ static Best df_run(DfCtx* c, int64_t lo, int64_t hi, const DfParams* p, int64_t 
     int nm = 0;
     Best cur = {-1, -1e300};
     df_scan(c, lo, hi, lo, hi, coarse, &cur);
+    DF_NOTE(c, ORC_STAGE_DF_COARSE, cur);
     marks[nm++] = cur.val;
     {
         Best r = cur;
         df_scan(c, lo, hi, cur.idx - window_half, cur.idx + window_half, p->refine, &r);
         cur = r;
     }
+    DF_NOTE(c, ORC_STAGE_DF_REFINE, cur);
     marks[nm++] = cur.val;
     for (int round = 0; round < 8; ++round) {
         Best t = cur;
@@ -710,16 +748,25 @@ static Best df_run(DfCtx* c, int64_t lo, int64_t hi, const DfParams* p, int64_t 
             int64_t q = cur.idx - k * p->omega;
             offer(&t, q, f_df(c, q));
         }
+        DF_NOTE(c, ORC_STAGE_DF_TRANSLATE, t);
         if (t.idx == cur.idx) break;
         Best r = t;
         df_scan(c, lo, hi, t.idx - window_half, t.idx + window_half, p->refine, &r);
         cur = r;
+        DF_NOTE(c, ORC_STAGE_DF_REREFINE, cur);
         marks[nm++] = cur.val;
-        if (plateau(marks, nm, p->plateau_eps)) return cur;
+        if (plateau(marks, nm, p->plateau_eps)) {
+            DF_NOTE(c, ORC_STAGE_DF_PLATEAU_STOP, cur);
+            return cur;
+        }
     }
-    if (plateau(marks, nm, p->plateau_eps)) return cur;
+    if (plateau(marks, nm, p->plateau_eps)) {
+        DF_NOTE(c, ORC_STAGE_DF_PLATEAU_STOP, cur);
+        return cur;
+    }
     Best fin = cur;
     df_scan(c, lo, hi, cur.idx - p->omega / 2, cur.idx + p->omega / 2, p->finest, &fin);
+    DF_NOTE(c, ORC_STAGE_DF_FINEST, fin);
     return fin;
 }
 
@@ -728,6 +775,7 @@ static int64_t search_df(DfCtx* c, int64_t lo, int64_t hi, const DfParams* p) {
     Best mainb = df_run(c, lo, hi, p, p->coarse, p->window_half);
     if (p->allow_fallback && mainb.val < p->heavy_cc) {
         Best fb = df_run(c, lo, hi, p, p->fallback_coarse, p->fallback_window_half);
+        DF_NOTE(c, ORC_STAGE_DF_FALLBACK, fb);
         if (fb.val > mainb.val) return fb.idx;
     }
     return mainb.idx;
@@ -911,7 +959,7 @@ typedef struct {
 /* zoom.cpp:416-523 (quantify_impl) */
 static int quantify_impl(const Sim* sim, const orc_grid* g, const Bounds* b,
                          const orc_zoom_cfg* cfg, double init_t1, double init_t2,
-                         const double* fp, orc_quant* out) {
+                         const double* fp, const float* dict, Trace* tr, orc_quant* out) {
     int64_t n = sim->n;
     Obj o;
     memset(&o, 0, sizeof o);
@@ -924,6 +972,7 @@ static int quantify_impl(const Sim* sim, const orc_grid* g, const Bounds* b,
     o.buf2 = malloc(sizeof(double) * 2 * (size_t)n);
     o.buf3 = malloc(sizeof(double) * 2 * (size_t)n);
     o.dict_mode = cfg->dict_mode;
+    o.dict = dict;
     o.cap = 4096;
     o.tab = calloc((size_t)o.cap, sizeof(Slot));
     int rc = 0;
@@ -951,7 +1000,7 @@ static int quantify_impl(const Sim* sim, const orc_grid* g, const Bounds* b,
         prm.fallback_window_half = step_units(cfg->fallback_window_hz / 2, g->df_hz.step);
         prm.allow_fallback = 1;
         /* Stage 1 (zoom.cpp:465-469) */
-        DfCtx dc = {&o, i1, i2, metric};
+        DfCtx dc = {&o, i1, i2, metric, tr};
         o.in_stage1 = 1;
         int64_t idf = search_df(&dc, b->lodf, b->hidf, &prm);
         o.in_stage1 = 0;
@@ -962,7 +1011,7 @@ static int quantify_impl(const Sim* sim, const orc_grid* g, const Bounds* b,
             s2v[k] = step_units(cfg->t1t2_2d_steps_ms[k], g->t2_ms.step);
         }
         zoom_2d(&o, idf, metric, b->lo1, b->hi1, b->lo2, b->hi2, &i1, &i2, s1v, s2v, cfg->n2d);
-        obj_eval(&o, i1, i2, idf, metric);
+        note(tr, &o, ORC_STAGE_T1T2_2D, i1, i2, idf, obj_eval(&o, i1, i2, idf, metric));
         /* Stage 3 (zoom.cpp:482-489) */
         {
             Best bb = {-1, -1e300};
@@ -970,6 +1019,7 @@ static int quantify_impl(const Sim* sim, const orc_grid* g, const Bounds* b,
             int64_t z = clampl(idf + prm.omega / 2, b->lodf, b->hidf);
             for (int64_t k = a; k <= z; ++k) offer(&bb, k, obj_eval(&o, i1, i2, k, metric));
             idf = bb.idx;
+            note(tr, &o, ORC_STAGE_DF_SWEEP, i1, i2, idf, bb.val);
         }
         /* Stage 4 (zoom.cpp:492-501) */
         for (int k = 0; k < cfg->n1d; ++k) {
@@ -977,18 +1027,18 @@ static int quantify_impl(const Sim* sim, const orc_grid* g, const Bounds* b,
             int64_t u1 = step_units(s, g->t1_ms.step);
             LineCtx lc1 = {&o, 0, i1, i2, idf, metric};
             i1 = zoom_1d(&lc1, b->lo1, b->hi1, i1, &u1, 1);
-            obj_eval(&o, i1, i2, idf, metric);
+            note(tr, &o, ORC_STAGE_T1_1D, i1, i2, idf, obj_eval(&o, i1, i2, idf, metric));
             int64_t u2 = step_units(s, g->t2_ms.step);
             LineCtx lc2 = {&o, 1, i1, i2, idf, metric};
             i2 = zoom_1d(&lc2, b->lo2, b->hi2, i2, &u2, 1);
-            obj_eval(&o, i1, i2, idf, metric);
+            note(tr, &o, ORC_STAGE_T2_1D, i1, i2, idf, obj_eval(&o, i1, i2, idf, metric));
         }
         /* Stage 5 (zoom.cpp:505-512) */
         {
             int64_t f1 = step_units(cfg->final_2d_step_ms, g->t1_ms.step);
             int64_t f2 = step_units(cfg->final_2d_step_ms, g->t2_ms.step);
             zoom_2d(&o, idf, cfg->final_metric, b->lo1, b->hi1, b->lo2, b->hi2, &i1, &i2, &f1, &f2, 1);
-            obj_eval(&o, i1, i2, idf, cfg->final_metric);
+            note(tr, &o, ORC_STAGE_T1T2_FINAL, i1, i2, idf, obj_eval(&o, i1, i2, idf, cfg->final_metric));
         }
         /* zoom.cpp:514-519 */
         out->score = obj_eval(&o, i1, i2, idf, metric);
@@ -1032,7 +1082,30 @@ int orc_quantify(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg
     Sim sim;
     int rc = sim_init(&sim, s);
     Bounds b = full_bounds(lattice);
-    if (rc == 0) rc = quantify_impl(&sim, lattice, &b, cfg, cfg->init_t1_ms, cfg->init_t2_ms, fp, out);
+    if (rc == 0)
+        rc = quantify_impl(&sim, lattice, &b, cfg, cfg->init_t1_ms, cfg->init_t2_ms, fp, NULL, NULL, out);
+    sim_free(&sim);
+    return rc;
+}
+
+int orc_quantify_ex(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg* cfg,
+                    const double* fp, const float* dict, int64_t dict_entries, orc_stage* trace,
+                    int trace_cap, int* trace_len, orc_quant* out) {
+    if (check_lattice(lattice)) return -1;
+    if (dict) {
+        const int64_t need = cfg->dict_mode == 2
+                                 ? lattice->t1_ms.count * lattice->t2_ms.count * lattice->df_hz.count
+                                 : lattice->df_hz.count;
+        if (cfg->dict_mode == 0 || dict_entries != need)
+            return fail("objective: dictionary does not match the lattice");
+    }
+    Sim sim;
+    int rc = sim_init(&sim, s);
+    Bounds b = full_bounds(lattice);
+    Trace tr = {trace, trace_cap, 0, 0};
+    if (rc == 0)
+        rc = quantify_impl(&sim, lattice, &b, cfg, cfg->init_t1_ms, cfg->init_t2_ms, fp, dict, &tr, out);
+    if (trace_len) *trace_len = tr.n;
     sim_free(&sim);
     return rc;
 }
@@ -1077,7 +1150,7 @@ int orc_quantify_slice(const orc_sched* s, const orc_grid* g, const orc_zoom_cfg
                 b.lodf = b.lodf > pdf - wdf ? b.lodf : pdf - wdf;
                 b.hidf = b.hidf < pdf + wdf ? b.hidf : pdf + wdf;
             }
-            rc = quantify_impl(&sim, g, &b, cfg, it1, it2, fps + i * 2 * n, &out[i]);
+            rc = quantify_impl(&sim, g, &b, cfg, it1, it2, fps + i * 2 * n, NULL, NULL, &out[i]);
             prior = out[i];
             have = 1;
         }
@@ -1088,8 +1161,8 @@ int orc_quantify_slice(const orc_sched* s, const orc_grid* g, const orc_zoom_cfg
         for (int64_t i = 0; i < nvox; ++i) {
             if (!mask[i]) continue;
             Bounds b = full_bounds(g);
-            if (quantify_impl(&sim, g, &b, cfg, cfg->init_t1_ms, cfg->init_t2_ms, fps + i * 2 * n,
-                              &out[i]))
+            if (quantify_impl(&sim, g, &b, cfg, cfg->init_t1_ms, cfg->init_t2_ms, fps + i * 2 * n, NULL,
+                              NULL, &out[i]))
                 bad = 1;
         }
         if (bad) rc = -1;

@@ -98,6 +98,30 @@ int orc_quantify_slice(const orc_sched* s, const orc_grid* lattice, const orc_zo
                        const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
                        int threads, orc_quant* out);
 
+/* StageLog (zoom.hpp:54-59): one record per stage note of quantify_impl
+ * (zoom.cpp:441-451 log_stage; search_df's notes, zoom.cpp:179-249).  Stage
+ * names map to codes in this order (the same as mrfg.h's MRFG_STAGE_*). */
+enum {
+    ORC_STAGE_DF_COARSE, ORC_STAGE_DF_REFINE, ORC_STAGE_DF_TRANSLATE, ORC_STAGE_DF_REREFINE,
+    ORC_STAGE_DF_PLATEAU_STOP, ORC_STAGE_DF_FINEST, ORC_STAGE_DF_FALLBACK, ORC_STAGE_T1T2_2D,
+    ORC_STAGE_DF_SWEEP, ORC_STAGE_T1_1D, ORC_STAGE_T2_1D, ORC_STAGE_T1T2_FINAL
+};
+typedef struct {
+    int32_t stage, pad;
+    int64_t evaluations; /* unique evaluations this stage added */
+    double best;
+    double t1_ms, t2_ms, df_hz;
+} orc_stage;
+
+/* quantify (zoom.cpp:533-539) with an explicit dictionary payload and the
+ * stage trace.  dict: NULL (cfg->dict_mode 1/2 then use the dictionary
+ * generate() / make_df_dictionary() would build) or dict_entries x 2N float
+ * (re, im) entries: the df slab (dict_mode 1; entry idf) or the full lattice
+ * dictionary (dict_mode 2; flat order).  trace: trace_cap records or NULL. */
+int orc_quantify_ex(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg* cfg,
+                    const double* fp, const float* dict, int64_t dict_entries, orc_stage* trace,
+                    int trace_cap, int* trace_len, orc_quant* out);
+
 #ifdef __cplusplus
 }
 #endif

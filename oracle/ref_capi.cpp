@@ -292,6 +292,53 @@ int orc_quantify(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg
     });
 }
 
+int orc_quantify_ex(const orc_sched* s, const orc_grid* lattice, const orc_zoom_cfg* cfg,
+                    const double* fp, const float* dict, int64_t dict_entries, orc_stage* trace,
+                    int trace_cap, int* trace_len, orc_quant* out) {
+    return guard([&] {
+        mrf::SearchRanges r{to_range(lattice->t1_ms), to_range(lattice->t2_ms),
+                            to_range(lattice->df_hz)};
+        const mrf::Schedule sc = to_sched(s);
+        const mrf::ZoomConfig zc = to_cfg(cfg);
+        // the reference's own dictionaries (grid, digest, entry length), whose
+        // payload is then replaced by the caller's entries when given
+        mrf::Dictionary dict_obj;
+        const mrf::Dictionary *df = nullptr, *full = nullptr;
+        if (cfg->dict_mode == 1) {
+            dict_obj = mrf::make_df_dictionary(r, zc, sc, 1);
+            df = &dict_obj;
+        } else if (cfg->dict_mode == 2) {
+            dict_obj = mrf::generate(mrf::grid_from_ranges(r.t1_ms, r.t2_ms, r.df_hz), sc, 1);
+            full = &dict_obj;
+        }
+        if (dict) {
+            if (cfg->dict_mode == 0 ||
+                static_cast<std::size_t>(dict_entries) * dict_obj.entry_len * 2 != dict_obj.data.size())
+                throw std::invalid_argument("objective: dictionary does not match the lattice");
+            dict_obj.data.assign(dict, dict + dict_obj.data.size());
+        }
+        mrf::QuantResult q = mrf::quantify(to_fp(fp, s->n), r, zc, sc, df, full);
+        fill_quant(lattice, q.params.t1 * 1e3, q.params.t2 * 1e3, q.params.df, q.params.pd,
+                   q.score, q.evaluations, out);
+        static const char* kNames[] = {"df.coarse",  "df.refine", "df.translate", "df.rerefine",
+                                       "df.plateau_stop", "df.finest", "df.fallback", "t1t2.2d",
+                                       "df.sweep", "t1.1d", "t2.1d", "t1t2.final"};
+        int k = 0;
+        for (const mrf::StageLog& lg : q.trace) {
+            if (trace && k < trace_cap) {
+                int code = -1;
+                for (int c = 0; c < 12; ++c)
+                    if (lg.stage == kNames[c]) code = c;
+                if (code < 0) throw std::runtime_error("unknown stage name " + lg.stage);
+                trace[k] = orc_stage{code, 0, static_cast<int64_t>(lg.evaluations), lg.best, lg.t1_ms,
+                                     lg.t2_ms, lg.df_hz};
+            }
+            ++k;
+        }
+        if (trace_len) *trace_len = k;
+    });
+}
+
 int orc_quantify_slice(const orc_sched* s, const orc_grid* g, const orc_zoom_cfg* cfg,
                        const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
                        int threads, orc_quant* out) {

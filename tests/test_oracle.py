@@ -144,6 +144,64 @@ def test_quantify_smoothing_vs_reference(orc, ref, k, mode):
                (b.i1, b.i2, b.idf, b.score, b.pd, b.evaluations)
 
 
+def _perturbed_payload(orc, s, g, cfg, mode, seed):
+    """A dictionary payload that is NOT the recomputation: the generated
+    entries with seeded noise (a dictionary written on another machine, or
+    edited before save) -- quantify must score these bytes (zoom.cpp:101-113)."""
+    n = s.n
+    if mode == 2:
+        payload = orc.generate(s, g, 0, g.t1_ms.count * g.t2_ms.count * g.df_hz.count)
+    else:
+        i1 = min(max(int(round((cfg.init_t1_ms - g.t1_ms.min) / g.t1_ms.step)), 0), g.t1_ms.count - 1)
+        i2 = min(max(int(round((cfg.init_t2_ms - g.t2_ms.min) / g.t2_ms.step)), 0), g.t2_ms.count - 1)
+        first = (i1 * g.t2_ms.count + i2) * g.df_hz.count
+        payload = orc.generate(s, g, first, g.df_hz.count)
+    payload = payload.reshape(-1, 2 * n).astype(np.float32)
+    rng = np.random.default_rng(seed)
+    payload += (rng.standard_normal(payload.shape) * 2e-3).astype(np.float32)
+    return payload
+
+
+@pytest.mark.parametrize("mode,smooth,edge", [(0, 0, 0), (1, 0, 0), (2, 0, 0), (1, 3, 0), (2, 5, 0), (0, 0, 1),
+                                               (1, 0, 1)])
+def test_quantify_trace_and_payload_vs_reference(orc, ref, mode, smooth, edge):
+    """QuantResult::trace (zoom.cpp:441-451, test_zoom.cpp:334-336) and
+    dictionary payloads that differ from the recomputation: answers, scores,
+    PD, evaluation counts and every StageLog record equal the reference's.
+    `edge` reaches every stage name: the heavy-noise fallback rerun, the
+    omega-translate rerefinements and the plateau stop (zoom.cpp:189-249)."""
+    s = orc.baseline_schedule(200, 1)
+    if edge:
+        g = oracle.make_grid((300.0, 20.0, 50), (40.0, 5.0, 30), (-250.0, 2.0, 251))
+        cfg = oracle.zoom_cfg(smooth_k=smooth, df_coarse_hz=40, df_refine_hz=4, df_window_hz=30, omega_hz=82,
+                              t1t2_2d_steps_ms=[200, 40], t1t2_1d_steps_ms=[100, 20], final_2d_step_ms=20,
+                              heavy_noise_cc=0.6, plateau_eps=0.05)
+    else:
+        g = oracle.make_grid((300.0, 20.0, 50), (40.0, 5.0, 30), (-50.0, 1.0, 101))
+        cfg = oracle.zoom_cfg(smooth_k=smooth, df_coarse_hz=10, df_refine_hz=2, df_window_hz=10, omega_hz=82,
+                              t1t2_2d_steps_ms=[200, 40], t1t2_1d_steps_ms=[100, 20], final_2d_step_ms=20)
+    cfg.dict_mode = mode
+    payload = _perturbed_payload(orc, s, g, cfg, mode, 7) if mode else None
+    rng = np.random.default_rng(11)
+    dfr = 200.0 if edge else 40.0
+    seen = set()
+    for k in range(6 if edge else 4):
+        fp = orc.simulate(s, rng.uniform(0.4, 1.2), rng.uniform(0.06, 0.16), rng.uniform(-dfr, dfr))
+        snr = (20 if k % 2 else 0.5) if edge else (20 if k else 0.5)
+        fp = orc.add_noise(fp, float(np.linalg.norm(fp)) / np.sqrt(200) / snr, 500 + k)
+        a, ta = orc.quantify_ex(s, g, cfg, fp, payload)
+        b, tb = ref.quantify_ex(s, g, cfg, fp, payload)
+        assert (a.i1, a.i2, a.idf, a.score, a.pd, a.evaluations) == \
+               (b.i1, b.i2, b.idf, b.score, b.pd, b.evaluations)
+        assert ta == tb
+        assert sum(t[1] for t in ta) == a.evaluations
+        names = [t[0] for t in ta]
+        assert names[0] == "df.coarse" and names[-1] == "t1t2.final"
+        seen |= set(names)
+    if edge:
+        assert set(oracle.STAGE_NAMES) == seen
+
+
 def test_quantify_slice_prior_vs_reference(orc, ref):
     s = orc.build_schedule(60, 15)
     g = oracle.make_grid((600, 10, 40), (80, 5, 16), (-20, 2, 25))
