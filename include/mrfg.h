@@ -108,9 +108,11 @@ typedef struct {
  * during the off-resonance search (stage 1) are the dictionary's float
  * entries (quantify's df_dict, built by make_df_dictionary); 2 = full
  * dictionary: every entry is a float dictionary entry (quantify's full_dict).
- * The dictionary itself is not needed: its entries are float(normalize(
- * simulate)) of the lattice point (dictionary.cpp:37-53), reproduced
- * bit-exactly; the caller validates it against the schedule and lattice. */
+ * The payload is passed through mrfg_zoom_io (mrfg_quantify_ex) and read as
+ * given; the entry points without it score the entries generate() would
+ * produce, float(normalize(simulate)) (dictionary.cpp:37-53), reproduced
+ * bit-exactly.  The caller validates the dictionary against the schedule and
+ * lattice (zoom.cpp:50-69). */
 typedef struct {
     int32_t metric, final_metric, smooth_k, n2d, n1d, dict_mode;
     double omega_hz, df_coarse_hz, df_refine_hz, df_window_hz, plateau_eps, heavy_noise_cc,
@@ -127,6 +129,52 @@ typedef struct {
     double t1_ms, t2_ms, df_hz, pd, score;
     int64_t evaluations;
 } mrfg_quant;
+
+/* StageLog (zoom.hpp:54-59): one record per stage note of quantify_impl
+ * (log_stage, zoom.cpp:441-451, and search_df's notes, zoom.cpp:179-249):
+ * unique evaluations the stage added, its best objective value (exact, the
+ * reference's), and its lattice point.  Stage names map to these codes. */
+enum {
+    MRFG_STAGE_DF_COARSE = 0,    /* "df.coarse" */
+    MRFG_STAGE_DF_REFINE,        /* "df.refine" */
+    MRFG_STAGE_DF_TRANSLATE,     /* "df.translate" */
+    MRFG_STAGE_DF_REREFINE,      /* "df.rerefine" */
+    MRFG_STAGE_DF_PLATEAU_STOP,  /* "df.plateau_stop" */
+    MRFG_STAGE_DF_FINEST,        /* "df.finest" */
+    MRFG_STAGE_DF_FALLBACK,      /* "df.fallback" */
+    MRFG_STAGE_T1T2_2D,          /* "t1t2.2d" */
+    MRFG_STAGE_DF_SWEEP,         /* "df.sweep" */
+    MRFG_STAGE_T1_1D,            /* "t1.1d" */
+    MRFG_STAGE_T2_1D,            /* "t2.1d" */
+    MRFG_STAGE_T1T2_FINAL        /* "t1t2.final" */
+};
+/* Upper bound on the records of one voxel: 2 x 19 search_df notes + fallback
+ * + 2-D + sweep + 2 x 8 1-D + final = 58. */
+#define MRFG_TRACE_MAX 64
+typedef struct {
+    int32_t stage, pad;
+    int64_t evaluations;
+    double best, t1_ms, t2_ms, df_hz;
+} mrfg_stage;
+
+/* Optional inputs/outputs of mrfg_quantify_ex / mrfg_quantify_slice_ex.
+ * dict: the caller's dictionary payload, dict_entries x 2N float (re, im)
+ *   in the reference's entry layout -- the df slab of make_df_dictionary
+ *   (cfg->dict_mode 1: entry idf) or the full lattice dictionary (dict_mode 2:
+ *   flat (i1*n2 + i2)*ndf + idf).  K5 scores these bytes as given, exactly as
+ *   Objective::acquire reads d->entry(flat) (zoom.cpp:101-113); NULL with
+ *   dict_mode != 0 scores the entries generate() would produce
+ *   (float(normalize(simulate)), dictionary.cpp:44-51).  dict_on_device: the
+ *   pointer is device memory.
+ * trace / trace_len: nvox x MRFG_TRACE_MAX records and nvox counts (host
+ *   memory; device memory for the _dev form), or NULL. */
+typedef struct {
+    const float* dict;
+    int64_t dict_entries;
+    int32_t dict_on_device, pad;
+    mrfg_stage* trace;
+    int32_t* trace_len;
+} mrfg_zoom_io;
 
 /* ------------------------------------------------------------------ misc */
 const char* mrfg_last_error(void);
@@ -293,6 +341,16 @@ int mrfg_quantify(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_confi
 int mrfg_quantify_slice(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
                         const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
                         mrfg_quant* out, double* seconds);
+/* mrfg_quantify_bounded / mrfg_quantify_slice with dictionary payloads and
+ * the stage trace (mrfg_zoom_io, may be NULL).  In the slice form with
+ * use_prior = 1 the strict raster runs as ONE launch (the voxel chain on one
+ * SM, every warp of the block evaluating the running voxel's rounds). */
+int mrfg_quantify_ex(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                     const double* fps, int64_t nvox, const int64_t* bounds, const double* init_ms,
+                     const mrfg_zoom_io* io, mrfg_quant* out);
+int mrfg_quantify_slice_ex(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                           const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
+                           const mrfg_zoom_io* io, mrfg_quant* out, double* seconds);
 /* mrfg_quantify on device-resident fingerprints (nvox x 2N FP64) and results
  * (async on the ctx stream; t1_ms/t2_ms/df_hz of d_out are left 0 -- the
  * lattice indices are filled). */

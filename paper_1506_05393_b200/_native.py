@@ -70,6 +70,23 @@ class Quant(C.Structure):
                 ("pd", C.c_double), ("score", C.c_double), ("evaluations", C.c_int64)]
 
 
+class Stage(C.Structure):
+    """StageLog (reference zoom.hpp:54-59); stage codes in STAGE_NAMES order."""
+    _fields_ = [("stage", C.c_int32), ("pad", C.c_int32), ("evaluations", C.c_int64), ("best", C.c_double),
+                ("t1_ms", C.c_double), ("t2_ms", C.c_double), ("df_hz", C.c_double)]
+
+
+STAGE_NAMES = ("df.coarse", "df.refine", "df.translate", "df.rerefine", "df.plateau_stop", "df.finest",
+               "df.fallback", "t1t2.2d", "df.sweep", "t1.1d", "t2.1d", "t1t2.final")
+TRACE_MAX = 64  # MRFG_TRACE_MAX
+
+
+class ZoomIo(C.Structure):
+    """mrfg_zoom_io: dictionary payload and StageLog outputs."""
+    _fields_ = [("dict", C.c_void_p), ("dict_entries", C.c_int64), ("dict_on_device", C.c_int32),
+                ("pad", C.c_int32), ("trace", C.c_void_p), ("trace_len", C.c_void_p)]
+
+
 EXPORTS = [
     "mrfg_last_error", "mrfg_version", "mrfg_zoom_config_default", "mrfg_reference_schedule",
     "mrfg_baseline_schedule", "mrfg_add_noise", "mrfg_rng_at", "mrfg_rng_uniform01",
@@ -80,7 +97,7 @@ EXPORTS = [
     "mrfg_merge_matches_dev", "mrfg_screen_scores", "mrfg_cc_map", "mrfg_quantify", "mrfg_quantify_slice", "mrfg_quantify_bounded",
     "mrfg_quantify_dev", "mrfg_cc_map_ex", "mrfg_save_generated", "mrfg_cc_map_to_file",
     "mrfg_write_header", "mrfg_read_header", "mrfg_calibrate_noise", "mrfg_make_calibrated_noise",
-    "mrfg_smooth",
+    "mrfg_smooth", "mrfg_quantify_ex", "mrfg_quantify_slice_ex",
 ]
 
 _lib = None
@@ -152,6 +169,11 @@ def load() -> C.CDLL:
     L.mrfg_quantify_slice.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp,
                                       C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int,
                                       C.POINTER(Quant), dp]
+    L.mrfg_quantify_ex.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp, i64,
+                                   C.POINTER(i64), dp, C.POINTER(ZoomIo), C.POINTER(Quant)]
+    L.mrfg_quantify_slice_ex.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp,
+                                         C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int,
+                                         C.POINTER(ZoomIo), C.POINTER(Quant), dp]
     _lib = L
     return L
 

@@ -1206,9 +1206,64 @@ int mrfg_read_header(const char* path, const char* magic, mrfg_grid* grid, uint8
     });
 }
 
-int mrfg_quantify_bounded(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
-                          const double* fps, int64_t nvox, const int64_t* bounds,
-                          const double* init_ms, mrfg_quant* out) {
+namespace {
+// mrfg_zoom_io on the device: the dictionary payload (host payloads are
+// uploaded into a persistent buffer) and the trace outputs.
+struct ZoomDevIo {
+    const float* dict = nullptr;
+    int64_t entries = 0;
+    mrfg_stage* trace = nullptr;
+    int* trace_len = nullptr;
+};
+ZoomDevIo zoom_io_upload(Ctx& c, const mrfg_zoom_io* io, int64_t nvox) {
+    ZoomDevIo d;
+    if (!io) return d;
+    if (io->dict) {
+        MRFG_REQUIRE(io->dict_entries > 0, MRFG_E_INVALID, "objective: dictionary does not match the lattice");
+        if (io->dict_on_device) {
+            d.dict = io->dict;
+        } else {
+            const size_t b = sizeof(float) * 2 * c.n * io->dict_entries;
+            c.h_zdict.ensure(b);
+            MRFG_CUDA(cudaMemcpyAsync(c.h_zdict.p, io->dict, b, cudaMemcpyHostToDevice, c.stream));
+            d.dict = c.h_zdict.as<float>();
+        }
+        d.entries = io->dict_entries;
+    }
+    if (io->trace) {
+        MRFG_REQUIRE(io->trace_len, MRFG_E_INVALID, "quantify: trace without trace_len");
+        c.h_trace.ensure((sizeof(mrfg_stage) * MRFG_TRACE_MAX + sizeof(int)) * nvox);
+        d.trace = c.h_trace.as<mrfg_stage>();
+        d.trace_len = reinterpret_cast<int*>(d.trace + MRFG_TRACE_MAX * nvox);
+    }
+    return d;
+}
+// Device trace records of voxels [0, nvox) -> the caller's host records of
+// voxels dst[k] (identity when dst is null).
+void zoom_trace_download(Ctx& c, const mrfg_zoom_io* io, const ZoomDevIo& d, int64_t nvox, const int64_t* dst) {
+    if (!d.trace) return;
+    std::vector<mrfg_stage> rec(static_cast<size_t>(MRFG_TRACE_MAX * nvox));
+    std::vector<int> len(static_cast<size_t>(nvox));
+    MRFG_CUDA(cudaMemcpyAsync(rec.data(), d.trace, sizeof(mrfg_stage) * rec.size(), cudaMemcpyDeviceToHost, c.stream));
+    MRFG_CUDA(cudaMemcpyAsync(len.data(), d.trace_len, sizeof(int) * len.size(), cudaMemcpyDeviceToHost, c.stream));
+    MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    for (int64_t k = 0; k < nvox; ++k) {
+        const int64_t o = dst ? dst[k] : k;
+        std::memcpy(io->trace + o * MRFG_TRACE_MAX, rec.data() + k * MRFG_TRACE_MAX,
+                    sizeof(mrfg_stage) * MRFG_TRACE_MAX);
+        io->trace_len[o] = len[k];
+    }
+}
+void fill_axis_values(const mrfg_grid& g, mrfg_quant& q) {  // AxisSpec::value (dictionary.hpp:22)
+    q.t1_ms = g.t1_ms.min + static_cast<double>(q.i1) * g.t1_ms.step;
+    q.t2_ms = g.t2_ms.min + static_cast<double>(q.i2) * g.t2_ms.step;
+    q.df_hz = g.df_hz.min + static_cast<double>(q.idf) * g.df_hz.step;
+}
+}  // namespace
+
+int mrfg_quantify_ex(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg, const double* fps,
+                     int64_t nvox, const int64_t* bounds, const double* init_ms, const mrfg_zoom_io* io,
+                     mrfg_quant* out) {
     return guard([&] {
         Ctx& c = h->c;
         MRFG_CUDA(cudaSetDevice(c.device));
@@ -1223,15 +1278,20 @@ int mrfg_quantify_bounded(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom
         c.h_res.ensure(sizeof(mrfg_quant) * nvox);
         MRFG_CUDA(cudaMemcpyAsync(c.h_raw.p, fps, sizeof(double) * 2 * c.n * nvox, cudaMemcpyHostToDevice,
                                   c.stream));
-        run_quantify(c, *lattice, *cfg, c.h_raw.as<double>(), nvox, bounds, init_ms, c.h_res.as<mrfg_quant>());
+        const ZoomDevIo d = zoom_io_upload(c, io, nvox);
+        run_quantify(c, *lattice, *cfg, c.h_raw.as<double>(), nvox, bounds, init_ms, c.h_res.as<mrfg_quant>(), 0,
+                     nullptr, nullptr, d.dict, d.entries, d.trace, d.trace_len);
         MRFG_CUDA(cudaMemcpyAsync(out, c.h_res.p, sizeof(mrfg_quant) * nvox, cudaMemcpyDeviceToHost, c.stream));
         MRFG_CUDA(cudaStreamSynchronize(c.stream));
-        for (int64_t k = 0; k < nvox; ++k) {  // AxisSpec::value (dictionary.hpp:22)
-            out[k].t1_ms = lattice->t1_ms.min + static_cast<double>(out[k].i1) * lattice->t1_ms.step;
-            out[k].t2_ms = lattice->t2_ms.min + static_cast<double>(out[k].i2) * lattice->t2_ms.step;
-            out[k].df_hz = lattice->df_hz.min + static_cast<double>(out[k].idf) * lattice->df_hz.step;
-        }
+        zoom_trace_download(c, io, d, nvox, nullptr);
+        for (int64_t k = 0; k < nvox; ++k) fill_axis_values(*lattice, out[k]);
     });
+}
+
+int mrfg_quantify_bounded(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                          const double* fps, int64_t nvox, const int64_t* bounds,
+                          const double* init_ms, mrfg_quant* out) {
+    return mrfg_quantify_ex(h, lattice, cfg, fps, nvox, bounds, init_ms, nullptr, out);
 }
 
 int mrfg_quantify_dev(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
@@ -1285,9 +1345,9 @@ void full_bounds(const mrfg_grid& g, int64_t* b) {
 }
 }  // namespace
 
-int mrfg_quantify_slice(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
-                        const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
-                        mrfg_quant* out, double* seconds) {
+int mrfg_quantify_slice_ex(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                           const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
+                           const mrfg_zoom_io* io, mrfg_quant* out, double* seconds) {
     return guard([&] {
         Ctx& c = h->c;
         MRFG_CUDA(cudaSetDevice(c.device));
@@ -1297,59 +1357,90 @@ int mrfg_quantify_slice(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_c
         auto t0 = std::chrono::steady_clock::now();
         const int64_t nv = static_cast<int64_t>(nx) * ny, n2 = 2 * c.n;
         std::memset(out, 0, sizeof(mrfg_quant) * nv);
-        auto run = [&](const std::vector<int64_t>& vox, const std::vector<int64_t>* b,
-                       const std::vector<double>* init) {
-            std::vector<double> packed(n2 * vox.size());
-            for (size_t k = 0; k < vox.size(); ++k)
-                std::memcpy(&packed[n2 * k], fps + n2 * vox[k], sizeof(double) * n2);
-            std::vector<mrfg_quant> res(vox.size());
-            int rc = mrfg_quantify_bounded(h, lattice, cfg, packed.data(), static_cast<int64_t>(vox.size()),
-                                           b ? b->data() : nullptr, init ? init->data() : nullptr,
-                                           res.data());
-            if (rc) throw Error{rc, g_err};
-            for (size_t k = 0; k < vox.size(); ++k) out[vox[k]] = res[k];
-        };
-        if (use_prior == 0) {
-            std::vector<int64_t> idx;
-            for (int64_t i = 0; i < nv; ++i)
-                if (mask[i]) idx.push_back(i);
-            if (!idx.empty()) run(idx, nullptr, nullptr);
-        } else if (use_prior == 1) {
-            // strict raster order: one voxel in flight (zoom.cpp:589-615)
-            bool have = false;
-            int64_t prev = -1;
-            for (int64_t i = 0; i < nv; ++i) {
-                if (!mask[i]) continue;
-                std::vector<int64_t> b(6);
-                std::vector<double> init(2);
-                if (have) {
-                    prior_of(*lattice, *cfg, out[prev], b.data(), init.data());
-                } else {
-                    full_bounds(*lattice, b.data());
-                    init = {cfg->init_t1_ms, cfg->init_t2_ms};
+        if (io && io->trace) {
+            std::memset(io->trace, 0, sizeof(mrfg_stage) * MRFG_TRACE_MAX * nv);
+            std::memset(io->trace_len, 0, sizeof(int32_t) * nv);
+        }
+        // masked voxels in raster order (zoom.cpp:579-581)
+        std::vector<int64_t> masked;
+        for (int64_t i = 0; i < nv; ++i)
+            if (mask[i]) masked.push_back(i);
+        // the rows kernel stages the schedule in shared memory (72 B/TR)
+        const bool rows_fit = (sizeof(StepU) + sizeof(float2)) * c.n + 256 * 32 + 16 <= 200 * 1024;
+        if (use_prior == 0 || (use_prior == 1 && !rows_fit)) {
+            if (masked.empty()) return;
+            if (use_prior == 0) {  // independent voxels (zoom.cpp:616-624)
+                std::vector<double> packed(n2 * masked.size());
+                for (size_t k = 0; k < masked.size(); ++k)
+                    std::memcpy(&packed[n2 * k], fps + n2 * masked[k], sizeof(double) * n2);
+                const int64_t m = static_cast<int64_t>(masked.size());
+                c.h_raw.ensure(sizeof(double) * n2 * m);
+                c.h_res.ensure(sizeof(mrfg_quant) * m);
+                MRFG_CUDA(cudaMemcpyAsync(c.h_raw.p, packed.data(), sizeof(double) * n2 * m, cudaMemcpyHostToDevice,
+                                          c.stream));
+                const ZoomDevIo d = zoom_io_upload(c, io, m);
+                run_quantify(c, *lattice, *cfg, c.h_raw.as<double>(), m, nullptr, nullptr, c.h_res.as<mrfg_quant>(),
+                             0, nullptr, nullptr, d.dict, d.entries, d.trace, d.trace_len);
+                std::vector<mrfg_quant> res(masked.size());
+                MRFG_CUDA(cudaMemcpyAsync(res.data(), c.h_res.p, sizeof(mrfg_quant) * m, cudaMemcpyDeviceToHost,
+                                          c.stream));
+                MRFG_CUDA(cudaStreamSynchronize(c.stream));
+                zoom_trace_download(c, io, d, m, masked.data());
+                for (size_t k = 0; k < masked.size(); ++k) {
+                    out[masked[k]] = res[k];
+                    fill_axis_values(*lattice, out[masked[k]]);
                 }
-                run({i}, &b, &init);
-                prev = i;
-                have = true;
+            } else {
+                // strict raster with a schedule too long for the rows kernel:
+                // one voxel in flight, driven from the host (zoom.cpp:589-615)
+                bool have = false;
+                int64_t prev = -1;
+                for (int64_t i : masked) {
+                    int64_t b[6];
+                    double init[2];
+                    if (have) {
+                        prior_of(*lattice, *cfg, out[prev], b, init);
+                    } else {
+                        full_bounds(*lattice, b);
+                        init[0] = cfg->init_t1_ms;
+                        init[1] = cfg->init_t2_ms;
+                    }
+                    mrfg_zoom_io one{};
+                    if (io) {
+                        one = *io;
+                        if (io->trace) {
+                            one.trace = io->trace + i * MRFG_TRACE_MAX;
+                            one.trace_len = io->trace_len + i;
+                        }
+                    }
+                    const int rc = mrfg_quantify_ex(h, lattice, cfg, fps + n2 * i, 1, b, init, io ? &one : nullptr,
+                                                    &out[i]);
+                    if (rc) throw Error{rc, g_err};
+                    prev = i;
+                    have = true;
+                }
             }
         } else {
-            // row relaxation of the raster prior: rows of masked
-            // voxels; a row's first voxel is seeded by the first voxel of the
+            // ONE launch of the row kernel.  use_prior 1: the strict raster
+            // (zoom.cpp:589-615) as a single row -- each masked voxel seeded
+            // and windowed by the previous one, on one SM with all its warps
+            // evaluating the running voxel's rounds.  use_prior 2: the row
+            // relaxation SPEC.md:449 permits -- rows of masked voxels in
+            // parallel, a row's first voxel seeded by the first voxel of the
             // previous non-empty row, every other voxel by its left neighbour.
-            std::vector<std::vector<int64_t>> rows;
-            for (int y = 0; y < ny; ++y) {
-                std::vector<int64_t> r;
-                for (int x = 0; x < nx; ++x)
-                    if (mask[static_cast<int64_t>(y) * nx + x]) r.push_back(static_cast<int64_t>(y) * nx + x);
-                if (!r.empty()) rows.push_back(std::move(r));
-            }
-            // one launch: warp r walks row r, seeded on the device (k_zoom_rows)
-            const int64_t R = static_cast<int64_t>(rows.size());
             std::vector<int64_t> row_start(1, 0), vox;
-            for (const auto& r : rows) {
-                vox.insert(vox.end(), r.begin(), r.end());
-                row_start.push_back(static_cast<int64_t>(vox.size()));
+            if (use_prior == 1) {
+                vox = masked;
+                if (!vox.empty()) row_start.push_back(static_cast<int64_t>(vox.size()));
+            } else {
+                for (int y = 0; y < ny; ++y) {
+                    for (int x = 0; x < nx; ++x)
+                        if (mask[static_cast<int64_t>(y) * nx + x]) vox.push_back(static_cast<int64_t>(y) * nx + x);
+                    if (static_cast<int64_t>(vox.size()) > row_start.back())
+                        row_start.push_back(static_cast<int64_t>(vox.size()));
+                }
             }
+            const int64_t R = static_cast<int64_t>(row_start.size()) - 1;
             if (R > 0) {
                 DevBuf& d_fps = c.h_raw;
                 DevBuf& d_res = c.h_res;
@@ -1357,20 +1448,35 @@ int mrfg_quantify_slice(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_c
                 d_res.ensure(sizeof(mrfg_quant) * nv);
                 MRFG_CUDA(cudaMemcpyAsync(d_fps.p, fps, sizeof(double) * n2 * nv, cudaMemcpyHostToDevice, c.stream));
                 MRFG_CUDA(cudaMemsetAsync(d_res.p, 0, sizeof(mrfg_quant) * nv, c.stream));
+                const ZoomDevIo d = zoom_io_upload(c, io, nv);
+                if (d.trace) MRFG_CUDA(cudaMemsetAsync(d.trace_len, 0, sizeof(int) * nv, c.stream));
                 run_quantify(c, *lattice, *cfg, d_fps.as<double>(), nv, nullptr, nullptr, d_res.as<mrfg_quant>(), R,
-                             row_start.data(), vox.data());
+                             row_start.data(), vox.data(), d.dict, d.entries, d.trace, d.trace_len);
                 MRFG_CUDA(cudaMemcpyAsync(out, d_res.p, sizeof(mrfg_quant) * nv, cudaMemcpyDeviceToHost, c.stream));
                 MRFG_CUDA(cudaStreamSynchronize(c.stream));
-                for (int64_t v : vox) {  // AxisSpec::value (dictionary.hpp:22)
-                    out[v].t1_ms = lattice->t1_ms.min + static_cast<double>(out[v].i1) * lattice->t1_ms.step;
-                    out[v].t2_ms = lattice->t2_ms.min + static_cast<double>(out[v].i2) * lattice->t2_ms.step;
-                    out[v].df_hz = lattice->df_hz.min + static_cast<double>(out[v].idf) * lattice->df_hz.step;
+                if (d.trace) {
+                    std::vector<mrfg_stage> rec(static_cast<size_t>(MRFG_TRACE_MAX * nv));
+                    std::vector<int> len(static_cast<size_t>(nv));
+                    MRFG_CUDA(cudaMemcpy(rec.data(), d.trace, sizeof(mrfg_stage) * rec.size(), cudaMemcpyDeviceToHost));
+                    MRFG_CUDA(cudaMemcpy(len.data(), d.trace_len, sizeof(int) * nv, cudaMemcpyDeviceToHost));
+                    for (int64_t v : vox) {
+                        std::memcpy(io->trace + v * MRFG_TRACE_MAX, rec.data() + v * MRFG_TRACE_MAX,
+                                    sizeof(mrfg_stage) * MRFG_TRACE_MAX);
+                        io->trace_len[v] = len[v];
+                    }
                 }
+                for (int64_t v : vox) fill_axis_values(*lattice, out[v]);
             }
         }
         if (seconds)
             *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     });
+}
+
+int mrfg_quantify_slice(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                        const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
+                        mrfg_quant* out, double* seconds) {
+    return mrfg_quantify_slice_ex(h, lattice, cfg, fps, mask, nx, ny, use_prior, nullptr, out, seconds);
 }
 
 }  // extern "C"

@@ -151,11 +151,28 @@ QuantResult to_result(const ParameterGrid& lat, const mrfg_quant& q, double seco
     return r;
 }
 
-// df_dict validation of zoom.cpp:61-69 and :430-437.  A valid slab's entries
-// are float(normalize(simulate)) of the lattice points at the initial T1/T2
-// (generate, dictionary.cpp:37-53), which the GPU path reproduces bit-exactly,
-// so it only switches the objective to dictionary entries for stage-1
-// acquisitions (mrfg_zoom_config.dict_mode = 1) instead of reading the slab.
+// StageLog names (zoom.cpp:179-249, :441-512) by mrfg_stage code.
+const char* const kStageNames[] = {"df.coarse", "df.refine", "df.translate", "df.rerefine", "df.plateau_stop",
+                                   "df.finest", "df.fallback", "t1t2.2d", "df.sweep", "t1.1d", "t2.1d",
+                                   "t1t2.final"};
+std::vector<StageLog> to_trace(const mrfg_stage* rec, int count) {
+    std::vector<StageLog> out;
+    for (int k = 0; k < std::min(count, MRFG_TRACE_MAX); ++k) {
+        StageLog lg;
+        lg.stage = kStageNames[rec[k].stage];
+        lg.evaluations = static_cast<std::size_t>(rec[k].evaluations);
+        lg.best = rec[k].best;
+        lg.t1_ms = rec[k].t1_ms;
+        lg.t2_ms = rec[k].t2_ms;
+        lg.df_hz = rec[k].df_hz;
+        out.push_back(std::move(lg));
+    }
+    return out;
+}
+
+// df_dict validation of zoom.cpp:61-69 and :430-437.  The slab's payload is
+// passed to the GPU, which scores its entries as given for stage-1
+// acquisitions (mrfg_zoom_config.dict_mode = 1, zoom.cpp:101-113).
 void check_df_dict(const Dictionary* d, const ParameterGrid& lat, const ZoomConfig& cfg,
                    const Schedule& sched) {
     if (!d) return;
@@ -180,8 +197,8 @@ void check_df_dict(const Dictionary* d, const ParameterGrid& lat, const ZoomConf
         throw std::invalid_argument("lattice mismatch: df dictionary T2 vs initial value");
 }
 
-// full_dict validation (zoom.cpp:50-58); entries reproduced like df_dict's
-// (mrfg_zoom_config.dict_mode = 2).
+// full_dict validation (zoom.cpp:50-58); its payload is scored as given for
+// every acquisition (mrfg_zoom_config.dict_mode = 2).
 void check_full_dict(const Dictionary* d, const ParameterGrid& lat, const Schedule& sched) {
     if (!d) return;
     auto close = [](double a, double b) {
@@ -758,11 +775,23 @@ std::vector<QuantResult> quantify_batch(const std::vector<Fingerprint>& fps, con
     const mrfg_grid g = to_grid(lat);
     mrfg_zoom_config zc = to_cfg(cfg);
     zc.dict_mode = full_dict ? 2 : (df_dict ? 1 : 0);
+    const Dictionary* d = full_dict ? full_dict : df_dict;
     std::vector<mrfg_quant> q(fps.size());
+    std::vector<mrfg_stage> rec(MRFG_TRACE_MAX * fps.size());
+    std::vector<int32_t> len(fps.size());
+    mrfg_zoom_io io{};
+    io.dict = d ? d->data.data() : nullptr;
+    io.dict_entries = d ? static_cast<int64_t>(d->data.size() / (2 * n)) : 0;
+    io.trace = rec.data();
+    io.trace_len = len.data();
     const auto t0 = std::chrono::steady_clock::now();
-    check(mrfg_quantify(c.h, &g, &zc, flat.data(), static_cast<int64_t>(fps.size()), q.data()));
+    check(mrfg_quantify_ex(c.h, &g, &zc, flat.data(), static_cast<int64_t>(fps.size()), nullptr, nullptr, &io,
+                           q.data()));
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    for (const auto& r : q) out.push_back(to_result(lat, r, secs / static_cast<double>(fps.size())));
+    for (std::size_t k = 0; k < q.size(); ++k) {
+        out.push_back(to_result(lat, q[k], secs / static_cast<double>(fps.size())));
+        out.back().trace = to_trace(rec.data() + MRFG_TRACE_MAX * k, len[k]);
+    }
     return out;
 }
 
@@ -804,7 +833,41 @@ SliceResult quantify_slice(const std::vector<Fingerprint>& fps, const std::vecto
     zc.dict_mode = df_dict ? 1 : 0;
     std::vector<mrfg_quant> q(nv);
     double secs = 0;
-    check(mrfg_quantify_slice(c.h, &g, &zc, flat.data(), mask.data(), nx, ny, use_prior ? 1 : 0, q.data(), &secs));
+    mrfg_zoom_io io{};
+    io.dict = df_dict ? df_dict->data.data() : nullptr;
+    io.dict_entries = df_dict ? static_cast<int64_t>(df_dict->data.size() / (2 * n)) : 0;
+    check(mrfg_quantify_slice_ex(c.h, &g, &zc, flat.data(), mask.data(), nx, ny, use_prior ? 1 : 0, &io, q.data(),
+                                 &secs));
+    if (use_prior && df_dict) {
+        // quantify_impl's df_dict check (zoom.cpp:430-437) for every voxel
+        // after the first: its initial T1/T2 are the previous voxel's answer
+        // (zoom.cpp:593-597), clamped into its prior window; the reference
+        // throws at the first voxel whose start is not the slab's T1/T2.
+        auto close = [](double a, double b) {
+            return std::abs(a - b) <= 1e-9 * std::max({1.0, std::abs(a), std::abs(b)});
+        };
+        auto snap = [](double v, const AxisSpec& a) { return std::lround((v - a.min) / a.step); };
+        auto units = [](double st, double fine) { return std::max(1L, std::lround(st / fine)); };
+        long prev = -1;
+        for (std::size_t i = 0; i < nv; ++i) {
+            if (!mask[i]) continue;
+            if (prev >= 0) {
+                const double t1 = lat.t1_ms.value(static_cast<std::size_t>(q[prev].i1)) * 1e-3 * 1e3;
+                const double t2 = lat.t2_ms.value(static_cast<std::size_t>(q[prev].i2)) * 1e-3 * 1e3;
+                const long p1 = snap(t1, lat.t1_ms), p2 = snap(t2, lat.t2_ms);
+                const long w1 = units(cfg.prior_window_t1_ms, lat.t1_ms.step);
+                const long w2 = units(cfg.prior_window_t2_ms, lat.t2_ms.step);
+                const long lo1 = std::max(0L, p1 - w1), hi1 = std::min<long>(lat.t1_ms.count - 1, p1 + w1);
+                const long lo2 = std::max(0L, p2 - w2), hi2 = std::min<long>(lat.t2_ms.count - 1, p2 + w2);
+                const long i1 = std::clamp(p1, lo1, hi1), i2 = std::clamp(p2, lo2, hi2);
+                if (!close(df_dict->grid.t1_ms.value(0), lat.t1_ms.value(static_cast<std::size_t>(i1))))
+                    throw std::invalid_argument("lattice mismatch: df dictionary T1 vs initial value");
+                if (!close(df_dict->grid.t2_ms.value(0), lat.t2_ms.value(static_cast<std::size_t>(i2))))
+                    throw std::invalid_argument("lattice mismatch: df dictionary T2 vs initial value");
+            }
+            prev = static_cast<long>(i);
+        }
+    }
     SliceResult out;
     out.nx = nx;
     out.ny = ny;

@@ -117,7 +117,7 @@ struct Ctx {
     DevBuf q64, qprime, best, cand, cand_count, atoms_a, inv2, seed_a, seed_inv2, rerank,
         params, out64, misc, rerank_scratch, misc2, audit,
         // persistent buffers of the host-buffer entry points (no per-call cudaMalloc)
-        h_raw, h_res, h_dict;
+        h_raw, h_res, h_dict, h_zdict, h_trace;
     // producer stream + events for the K1/K2 overlap (created on first use)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev[8] = {};
@@ -245,6 +245,10 @@ void run_quantify(Ctx& c, const mrfg_grid& lattice, const mrfg_zoom_config& cfg,
                   // neighbour-seeded slice (d_fps/d_out: the raster): nrows rows of
                   // masked voxels, vox_list[row_start[r] .. row_start[r+1])
                   int64_t nrows = 0, const int64_t* h_row_start = nullptr,
-                  const int64_t* h_vox_list = nullptr);
+                  const int64_t* h_vox_list = nullptr,
+                  // the caller's dictionary payload (device, or null) and the
+                  // StageLog outputs (device, nvox x MRFG_TRACE_MAX / nvox, or null)
+                  const float* d_dict = nullptr, int64_t dict_entries = 0, mrfg_stage* d_trace = nullptr,
+                  int* d_trace_len = nullptr);
 
 }  // namespace mrfg

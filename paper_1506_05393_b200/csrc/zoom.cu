@@ -7,7 +7,8 @@ namespace mrfg {
 
 void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, const double* d_fps,
                   int64_t nvox, const int64_t* h_bounds, const double* h_init, mrfg_quant* d_out,
-                  int64_t nrows, const int64_t* h_row_start, const int64_t* h_vox_list) {
+                  int64_t nrows, const int64_t* h_row_start, const int64_t* h_vox_list, const float* d_dict,
+                  int64_t dict_entries, mrfg_stage* d_trace, int* d_trace_len) {
     for (const mrfg_axis* ax : {&lat.t1_ms, &lat.t2_ms, &lat.df_hz})
         MRFG_REQUIRE(ax->count > 0 && ax->count < (int64_t(1) << 21), MRFG_E_INVALID,
                      "objective: lattice axis empty or too fine");  // zoom.cpp:46-48
@@ -41,6 +42,14 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     P.df_step = lat.df_hz.step;
     MRFG_REQUIRE(cfg.dict_mode >= 0 && cfg.dict_mode <= 2, MRFG_E_INVALID, "quantify: bad dictionary mode");
     P.dict_mode = cfg.dict_mode;
+    if (d_dict) {  // zoom.cpp:101-113: the df slab (entry idf) or the full lattice dictionary
+        MRFG_REQUIRE(cfg.dict_mode != 0, MRFG_E_INVALID, "quantify: dictionary payload without a dictionary mode");
+        const int64_t need = cfg.dict_mode == 2 ? grid_total(lat) : lat.df_hz.count;
+        MRFG_REQUIRE(dict_entries == need, MRFG_E_INVALID, "objective: dictionary does not match the lattice");
+    }
+    P.dict = reinterpret_cast<const float2*>(d_dict);
+    P.trace = d_trace;
+    P.trace_len = d_trace_len;
     P.smooth_k = cfg.smooth_k;
     if (cfg.smooth_k) {  // fingerprint.cpp:125-129, host libm
         const double sigma = cfg.smooth_k == 3 ? 0.85 : 1.0;

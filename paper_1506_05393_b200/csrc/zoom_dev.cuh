@@ -111,6 +111,13 @@ struct ZParams {
     long long pw1, pw2, pwdf;
     int smem_stage;            // StepU rows + per-warp q32 staged in dynamic shared memory
     int dict_mode;             // 0 none, 1 df dictionary (stage-1 acquisitions), 2 full dictionary
+    // the caller's dictionary payload (zoom.cpp:101-113: entry idf of the df
+    // slab, or the lattice flat of the full dictionary), scored as given;
+    // null: the generated entries float(normalize(simulate)) are reproduced
+    const float2* dict;
+    // StageLog records (zoom.cpp:441-451), nvox x MRFG_TRACE_MAX, or null
+    mrfg_stage* trace;
+    int* trace_len;
     // smoothing (fingerprint.cpp:122-145): k = 0 (off), 3 or 5 taps, host-libm weights
     int smooth_k;
     double sw[5];
@@ -156,6 +163,9 @@ struct Z {
     int* ctl;
     int lane;
     long long evals;
+    int64_t vox;             // voxel being quantified (trace records)
+    int ntrace;              // trace records of this pass
+    long long tr_last;       // evaluation count at the previous record
     long long cyc32, cyc64;  // stats: cycles in screening / exact rounds
     long long r64;           // stats: exact rounds
     long long lo1, hi1, lo2, hi2, lodf, hidf;
@@ -261,17 +271,33 @@ __device__ double zsmooth64(const ZParams& P, double2* v, int st, int n) {
 __device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, bool dict, ZSlot& s) {
     const ZParams& P = *z.p;
     const int n = P.n;
-    // pass 1: the recursion, |s|^2 in the reference's order (fingerprint.cpp:14-18);
-    // the entries are kept (lane-interleaved scratch) for pass 2
     double2* fx = z.fpx + z.lane;
-    double acc = 0.0;
-    sim64_walk(P.rf, P.e1d, P.e2d, P.phd, P.inv0, n, P.L, i1, i2, idf, [&](int j, double x, double y) {
-        acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
-        fx[32 * j] = make_double2(x, y);
-    });
-    double inv = 1.0 / sqrt(acc);  // fingerprint.cpp:30-32
+    double acc = 0.0, inv;
     bool cast = dict;
-    if (P.smooth_k) {
+    if (dict && P.dict) {
+        // the caller's entry d->entry(flat), as given (zoom.cpp:101-110):
+        // scored without normalization unless smoothed; nrm2 < -1 marks "no
+        // simulation norm" (estimate_pd then re-simulates, zoom.cpp:518)
+        const int64_t flat = P.dict_mode == 2 ? (static_cast<int64_t>(i1) * P.L.n2 + i2) * P.L.ndf + idf : idf;
+        const float2* e = P.dict + flat * n;
+        for (int j = 0; j < n; ++j) {
+            const float2 v = e[j];
+            fx[32 * j] = make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
+        }
+        acc = -2.0;
+        inv = 1.0;
+        cast = false;
+        if (P.smooth_k) inv = 1.0 / sqrt(zsmooth64(P, fx, 32, n));
+    } else {
+        // pass 1: the recursion, |s|^2 in the reference's order (fingerprint.cpp:14-18);
+        // the entries are kept (lane-interleaved scratch) for pass 2
+        sim64_walk(P.rf, P.e1d, P.e2d, P.phd, P.inv0, n, P.L, i1, i2, idf, [&](int j, double x, double y) {
+            acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
+            fx[32 * j] = make_double2(x, y);
+        });
+        inv = 1.0 / sqrt(acc);  // fingerprint.cpp:30-32
+    }
+    if (P.smooth_k && !(dict && P.dict)) {
         // entry = normalize(smooth(e)), e the raw simulation (zoom.cpp:116-118)
         // or the float dictionary entry (zoom.cpp:106-110)
         if (dict)
@@ -1026,7 +1052,10 @@ __device__ V zf(Z& z, long long i1, long long i2, long long idf, int metric) {
         }
         zsync();
         ++z.evals;
-        if (P.eps < 0) zexact(z, 1, [&](int) { return s; });  // all-FP64 mode: entry type may differ
+        // all-FP64 mode (the entry type may differ), and payload dictionary
+        // entries: their screening value approximates the simulation, not
+        // the caller's bytes, so they are scored exactly on acquisition
+        if (P.eps < 0 || (P.dict && zentry_type(z) == 1)) zexact(z, 1, [&](int) { return s; });
     }
     return zread(z, s, metric);
 }
@@ -1112,6 +1141,48 @@ __device__ __forceinline__ void offer(Z& z, Best& b, long long i, V v, int metri
     }
 }
 
+// ------------------------------------------------------------- StageLog
+// One trace record (log_stage, zoom.cpp:441-451): evaluations added since
+// the previous record, the stage's best value and lattice point.  A value
+// that is still a screening value keeps its memo slot in `pad` and is made
+// exact when the voxel finishes (ztrace_finish).
+__device__ void znote(Z& z, int stage, long long i1, long long i2, long long idf, const V& v) {
+    const ZParams& P = *z.p;
+    if (!P.trace) return;
+    if (z.lane == 0 && z.ntrace < MRFG_TRACE_MAX) {
+        mrfg_stage* r = P.trace + z.vox * MRFG_TRACE_MAX + z.ntrace;
+        r->stage = stage;
+        r->pad = v.exact ? -1 : v.slot;
+        r->evaluations = z.evals - z.tr_last;
+        r->best = v.v;
+        r->t1_ms = __dadd_rn(P.t1_min, __dmul_rn(static_cast<double>(i1), P.t1_step));  // AxisSpec::value
+        r->t2_ms = __dadd_rn(P.t2_min, __dmul_rn(static_cast<double>(i2), P.t2_step));
+        r->df_hz = __dadd_rn(P.df_min, __dmul_rn(static_cast<double>(idf), P.df_step));
+    }
+    ++z.ntrace;
+    z.tr_last = z.evals;
+}
+// Exact values for the final pass's records (their slots' entry types are
+// the reference's), then the count.
+__device__ void ztrace_finish(Z& z) {
+    const ZParams& P = *z.p;
+    if (!P.trace) return;
+    mrfg_stage* rec = P.trace + z.vox * MRFG_TRACE_MAX;
+    const int nt = z.ntrace < MRFG_TRACE_MAX ? z.ntrace : MRFG_TRACE_MAX;
+    zsync();
+    zexact(z, nt, [&](int k) { return static_cast<int>(*reinterpret_cast<volatile int*>(&rec[k].pad)); });
+    if (z.lane == 0) {
+        for (int k = 0; k < nt; ++k) {
+            const int s = rec[k].pad;
+            if (s >= 0)
+                rec[k].best = zread(z, s, rec[k].stage == MRFG_STAGE_T1T2_FINAL ? P.final_metric : P.metric).v;
+            rec[k].pad = 0;
+        }
+        P.trace_len[z.vox] = z.ntrace;
+    }
+    zsync();
+}
+
 // Offer the points pt(0..count-1) to bst in order: the reference's
 // per-point eval + offer (zoom.cpp:125-138, 182-187) with the memo reads done
 // 32 points at a time -- each lane looks up one point and takes its
@@ -1146,7 +1217,8 @@ __device__ void offer_batch(Z& z, Best& bst, long long count, PT pt, int metric)
         }
         z.evals += __popc(__ballot_sync(0xffffffffu, newly));
         zsync();
-        if (P.eps < 0) zexact(z, 32, [&](int) { return s; });  // all-FP64 mode: entry type may differ
+        if (P.eps < 0 || (P.dict && zentry_type(z) == 1))  // as in zf
+            zexact(z, 32, [&](int) { return s; });
         V v{-1e300, -1, 1};
         if (s >= 0) v = zread(z, s, metric);
         const int nv = count - base < 32 ? static_cast<int>(count - base) : 32;
@@ -1220,12 +1292,14 @@ __device__ Best df_run(Z& z, long long i1, long long i2, long long coarse, long 
     int nm = 0;
     Best cur = best_init();
     df_scan(z, i1, i2, z.lodf, z.hidf, coarse, cur);
+    znote(z, MRFG_STAGE_DF_COARSE, i1, i2, cur.idx, cur.val);
     marks[nm++] = cur.val;
     {
         Best r = cur;
         df_scan(z, i1, i2, cur.idx - wh, cur.idx + wh, P.df_refine, r);
         cur = r;
     }
+    znote(z, MRFG_STAGE_DF_REFINE, i1, i2, cur.idx, cur.val);
     marks[nm++] = cur.val;
     for (int round = 0; round < 8; ++round) {
         Best t = cur;
@@ -1239,16 +1313,25 @@ __device__ Best df_run(Z& z, long long i1, long long i2, long long coarse, long 
         };
         zensure(z, nf + nb, hop);
         offer_batch(z, t, nf + nb, hop, P.metric);  // forward hops, then backward (zoom.cpp:213-220)
+        znote(z, MRFG_STAGE_DF_TRANSLATE, i1, i2, t.idx, t.val);
         if (t.idx == cur.idx) break;
         Best r = t;
         df_scan(z, i1, i2, t.idx - wh, t.idx + wh, P.df_refine, r);
         cur = r;
+        znote(z, MRFG_STAGE_DF_REREFINE, i1, i2, cur.idx, cur.val);
         marks[nm++] = cur.val;
-        if (plateau(z, marks, nm, P.plateau_eps)) return cur;
+        if (plateau(z, marks, nm, P.plateau_eps)) {
+            znote(z, MRFG_STAGE_DF_PLATEAU_STOP, i1, i2, cur.idx, cur.val);
+            return cur;
+        }
     }
-    if (plateau(z, marks, nm, P.plateau_eps)) return cur;
+    if (plateau(z, marks, nm, P.plateau_eps)) {
+        znote(z, MRFG_STAGE_DF_PLATEAU_STOP, i1, i2, cur.idx, cur.val);
+        return cur;
+    }
     Best fin = cur;
     df_scan(z, i1, i2, cur.idx - P.omega / 2, cur.idx + P.omega / 2, 1, fin);
+    znote(z, MRFG_STAGE_DF_FINEST, i1, i2, fin.idx, fin.val);
     return fin;
 }
 
@@ -1258,6 +1341,7 @@ __device__ long long search_df(Z& z, long long i1, long long i2) {
     Best mainb = df_run(z, i1, i2, P.df_coarse, P.df_window_half);
     if (lt_const(z, mainb.val, P.heavy_cc, P.metric)) {
         Best fb = df_run(z, i1, i2, P.fb_coarse, P.fb_window_half);
+        znote(z, MRFG_STAGE_DF_FALLBACK, i1, i2, fb.idx, fb.val);
         if (gt(z, fb.val, mainb.val, P.metric)) return fb.idx;
     }
     return mainb.idx;
@@ -1459,6 +1543,7 @@ __device__ void zoom_2d(Z& z, long long idf, int metric, long long& x, long long
 __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v, const long long* b6, long long s1,
                            long long s2) {
     z.evals = 0;
+    z.vox = v;
     z.cyc32 = z.cyc64 = z.r64 = 0;
     const long long tstart = clock64();
     const int n = P.n;
@@ -1529,6 +1614,8 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v, const long long* b
         }
         if (pass >= kEagerAfter) z.eager = 1;
         z.evals = 0;
+        z.ntrace = 0;
+        z.tr_last = 0;
         i1 = clampll(s1, z.lo1, z.hi1);  // zoom.cpp:428-429
         i2 = clampll(s2, z.lo2, z.hi2);
         // Stage 1 (zoom.cpp:465-469)
@@ -1537,7 +1624,7 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v, const long long* b
         z.stage1 = 0;
         // Stage 2 (zoom.cpp:472-479)
         zoom_2d(z, idf, P.metric, i1, i2, P.s2d1, P.s2d2, P.n2d);
-        zf(z, i1, i2, idf, P.metric);
+        znote(z, MRFG_STAGE_T1T2_2D, i1, i2, idf, zf(z, i1, i2, idf, P.metric));
         // Stage 3 (zoom.cpp:482-489)
         {
             Best b = best_init();
@@ -1552,17 +1639,18 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v, const long long* b
             zensure_df(z, c1, c2, a, e - a + 1);
             offer_batch(z, b, e - a + 1, pt, P.metric);
             idf = b.idx;
+            znote(z, MRFG_STAGE_DF_SWEEP, i1, i2, idf, b.val);
         }
         // Stage 4 (zoom.cpp:492-501)
         for (int k = 0; k < P.n1d; ++k) {
             i1 = zoom_1d(z, 0, i1, i2, idf, z.lo1, z.hi1, i1, P.s1d1[k], P.metric);
-            zf(z, i1, i2, idf, P.metric);
+            znote(z, MRFG_STAGE_T1_1D, i1, i2, idf, zf(z, i1, i2, idf, P.metric));
             i2 = zoom_1d(z, 1, i1, i2, idf, z.lo2, z.hi2, i2, P.s1d2[k], P.metric);
-            zf(z, i1, i2, idf, P.metric);
+            znote(z, MRFG_STAGE_T2_1D, i1, i2, idf, zf(z, i1, i2, idf, P.metric));
         }
         // Stage 5 (zoom.cpp:505-512)
         zoom_2d(z, idf, P.final_metric, i1, i2, &P.f2d1, &P.f2d2, 1);
-        zf(z, i1, i2, idf, P.final_metric);
+        znote(z, MRFG_STAGE_T1T2_FINAL, i1, i2, idf, zf(z, i1, i2, idf, P.final_metric));
         if (z.lane == 0) zstat(z, 9, 1);
         if (z.npend == 0) break;  // every decision of this pass was certified
         zflush(z);
@@ -1571,6 +1659,16 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v, const long long* b
     V score = zf(z, i1, i2, idf, P.metric);
     zmake_exact(z, score, P.metric);
     const int s = score.slot;
+    ztrace_finish(z);
+    // estimate_pd (fingerprint.cpp:147-152) divides by the SIMULATED entry's
+    // norm (Objective::ideal_at, zoom.cpp:152-156): a payload dictionary
+    // entry has none, so simulate it once
+    double nrm2 = z.tab[s].nrm2;
+    if (nrm2 < -1.0) {
+        ZSlot t;
+        zsim(z, static_cast<int>(i1), static_cast<int>(i2), static_cast<int>(idf), false, t);
+        nrm2 = __shfl_sync(0xffffffffu, t.nrm2, 0);
+    }
     if (z.lane == 0) {
         mrfg_quant r;
         r.i1 = i1;
@@ -1580,7 +1678,7 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v, const long long* b
         r.t2_ms = 0;
         r.df_hz = 0;
         // estimate_pd (fingerprint.cpp:147-152): |fp| / |ideal|, ideal unnormalized
-        r.pd = nq / sqrt(z.tab[s].nrm2);
+        r.pd = nq / sqrt(nrm2);
         r.score = score.v;
         r.evaluations = z.evals;
         P.out[v] = r;

@@ -32,7 +32,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from ._native import Axis, Grid, Match, Quant, ScanOpts, ScanStats, ZoomConfig, check
+from ._native import (STAGE_NAMES, TRACE_MAX, Axis, Grid, Match, Quant, ScanOpts, ScanStats, Stage, ZoomConfig,
+                      ZoomIo, check)
 
 METRIC = {"cc": 0, "euclidean": 1}
 
@@ -466,14 +467,55 @@ class Context:
                                            str(path).encode(), chunk_entries, precision))
 
     # -- K5
-    def quantify(self, fps, lattice: Grid, cfg: ZoomConfig = None) -> "np.ndarray":
-        """quantify (zoom.cpp:533-539) for a batch of fingerprints -> Quant records."""
+    def _zoom_io(self, nvox: int, dictionary, trace: bool):
+        """mrfg_zoom_io for a dictionary payload (float32 (entries, 2N) or
+        complex64 (entries, N), or None) and/or the StageLog outputs."""
+        if dictionary is None and not trace:
+            return None, None
+        io = ZoomIo()
+        keep = []
+        if dictionary is not None:
+            d = np.ascontiguousarray(dictionary)
+            d = d.view(np.float32) if d.dtype == np.complex64 else np.ascontiguousarray(d, dtype=np.float32)
+            d = d.reshape(-1, 2 * self.n)
+            keep.append(d)
+            io.dict = d.ctypes.data
+            io.dict_entries = d.shape[0]
+        bufs = None
+        if trace:
+            rec = (Stage * (TRACE_MAX * nvox))()
+            ln = np.zeros(nvox, dtype=np.int32)
+            io.trace = C.addressof(rec)
+            io.trace_len = ln.ctypes.data
+            bufs = (rec, ln)
+        return io, (keep, bufs)
+
+    @staticmethod
+    def _traces(bufs, idx):
+        rec, ln = bufs
+        out = []
+        for v in idx:
+            k0 = int(v) * TRACE_MAX
+            out.append([(STAGE_NAMES[rec[k0 + k].stage], rec[k0 + k].evaluations, rec[k0 + k].best,
+                         rec[k0 + k].t1_ms, rec[k0 + k].t2_ms, rec[k0 + k].df_hz)
+                        for k in range(min(int(ln[v]), TRACE_MAX))])
+        return out
+
+    def quantify(self, fps, lattice: Grid, cfg: ZoomConfig = None, dictionary=None, trace: bool = False):
+        """quantify (zoom.cpp:533-539) for a batch of fingerprints -> Quant records.
+
+        dictionary: the df slab (cfg.dict_mode 1) or full lattice dictionary
+        (dict_mode 2) payload, scored as given (zoom.cpp:101-113).  trace=True
+        also returns each voxel's StageLog list (zoom.cpp:441-451) as
+        (stage, evaluations, best, t1_ms, t2_ms, df_hz) tuples."""
         q = np.ascontiguousarray(np.atleast_2d(fps), dtype=np.complex128)
         cfg = cfg or zoom_config()
         out = (Quant * q.shape[0])()
-        check(self.lib.mrfg_quantify(self.h, C.byref(lattice), C.byref(cfg),
-                                     _dp(q.view(np.float64)), q.shape[0], out))
-        return quant_array(out)
+        io, keep = self._zoom_io(q.shape[0], dictionary, trace)
+        check(self.lib.mrfg_quantify_ex(self.h, C.byref(lattice), C.byref(cfg), _dp(q.view(np.float64)),
+                                        q.shape[0], None, None, None if io is None else C.byref(io), out))
+        res = quant_array(out)
+        return (res, self._traces(keep[1], range(q.shape[0]))) if trace else res
 
     def quantify_device(self, d_fps_ptr: int, nvox: int, lattice: Grid, cfg: ZoomConfig,
                         d_out_ptr: int) -> None:
@@ -482,33 +524,41 @@ class Context:
                                          C.c_void_p(d_fps_ptr), nvox, C.c_void_p(d_out_ptr)))
 
     def quantify_bounded(self, fps, lattice: Grid, cfg: ZoomConfig = None, bounds=None,
-                         init_ms=None) -> "np.ndarray":
+                         init_ms=None, dictionary=None, trace: bool = False):
         """quantify_impl with per-voxel index bounds (V,6) and initial T1/T2 ms (V,2)."""
         q = np.ascontiguousarray(np.atleast_2d(fps), dtype=np.complex128)
         cfg = cfg or zoom_config()
         out = (Quant * q.shape[0])()
         b = None if bounds is None else np.ascontiguousarray(bounds, dtype=np.int64)
         i = None if init_ms is None else np.ascontiguousarray(init_ms, dtype=np.float64)
-        check(self.lib.mrfg_quantify_bounded(
+        io, keep = self._zoom_io(q.shape[0], dictionary, trace)
+        check(self.lib.mrfg_quantify_ex(
             self.h, C.byref(lattice), C.byref(cfg), _dp(q.view(np.float64)), q.shape[0],
             None if b is None else b.ctypes.data_as(C.POINTER(C.c_int64)),
-            None if i is None else _dp(i), out))
-        return quant_array(out)
+            None if i is None else _dp(i), None if io is None else C.byref(io), out))
+        res = quant_array(out)
+        return (res, self._traces(keep[1], range(q.shape[0]))) if trace else res
 
     def quantify_slice(self, fps, mask, nx: int, ny: int, lattice: Grid,
-                       cfg: ZoomConfig = None, use_prior: int = 0):
+                       cfg: ZoomConfig = None, use_prior: int = 0, dictionary=None, trace: bool = False):
         """quantify_slice (zoom.cpp:555-629).  use_prior: 0/False none, 1/True the
-        reference's raster order, 2 the row-wavefront relaxation."""
+        reference's raster order, 2 the row-wavefront relaxation.
+        Returns (Quant records, seconds) [+ per-voxel StageLog lists with trace]."""
         q = np.ascontiguousarray(fps, dtype=np.complex128)
         m = np.ascontiguousarray(mask, dtype=np.uint8)
         cfg = cfg or zoom_config()
         out = (Quant * (nx * ny))()
         secs = C.c_double()
-        check(self.lib.mrfg_quantify_slice(self.h, C.byref(lattice), C.byref(cfg),
-                                           _dp(q.view(np.float64)),
-                                           m.ctypes.data_as(C.POINTER(C.c_uint8)), nx, ny,
-                                           int(use_prior), out, C.byref(secs)))
-        return quant_array(out), secs.value
+        io, keep = self._zoom_io(nx * ny, dictionary, trace)
+        check(self.lib.mrfg_quantify_slice_ex(self.h, C.byref(lattice), C.byref(cfg),
+                                              _dp(q.view(np.float64)),
+                                              m.ctypes.data_as(C.POINTER(C.c_uint8)), nx, ny,
+                                              int(use_prior), None if io is None else C.byref(io), out,
+                                              C.byref(secs)))
+        res = quant_array(out)
+        if trace:
+            return res, secs.value, self._traces(keep[1], range(nx * ny))
+        return res, secs.value
 
 
 QUANT_DTYPE = np.dtype([("i1", np.int64), ("i2", np.int64), ("idf", np.int64),

@@ -50,6 +50,10 @@ int main() {
         EXPECT(z.params.t1 == t.t1 && z.params.df == t.df);
         EXPECT(std::abs(z.params.pd - 1.7) < 1e-9);
         EXPECT(z.evaluations > 0 && z.evaluations < grid.total());
+        std::size_t traced = 0;  // test_zoom.cpp:334-336
+        for (const auto& st : z.trace) traced += st.evaluations;
+        EXPECT(traced == z.evaluations);
+        EXPECT(!z.trace.empty() && z.trace.front().stage == "df.coarse" && z.trace.back().stage == "t1t2.final");
     }
     ScanOutcome sc = scan_grid(grid, s, q, Metric::cc, 1, 7);
     for (std::size_t k = 0; k < q.size(); ++k) {

@@ -296,3 +296,93 @@ def test_zoom_tiny_shapes(orc, n):
         cfg = P.zoom_config(df_coarse_hz=5.0)
         with P.Context(s) as c:
             check_same(c.quantify(fps, g, cfg), orc, s, g, cfg, fps)
+
+
+def _payload(orc, s, g, cfg, mode, seed):
+    """A dictionary payload that is NOT the recomputation (generated entries
+    plus seeded noise): K5 must score these bytes (zoom.cpp:101-113)."""
+    os_, og = to_oracle_sched(s), to_oracle_grid(g)
+    if mode == 2:
+        payload = orc.generate(os_, og, 0, P.grid_total(g))
+    else:
+        i1 = min(max(_lround((cfg.init_t1_ms - g.t1_ms.min) / g.t1_ms.step), 0), g.t1_ms.count - 1)
+        i2 = min(max(_lround((cfg.init_t2_ms - g.t2_ms.min) / g.t2_ms.step), 0), g.t2_ms.count - 1)
+        payload = orc.generate(os_, og, (i1 * g.t2_ms.count + i2) * g.df_hz.count, g.df_hz.count)
+    payload = payload.reshape(-1, 2 * s.n).astype(np.float32)
+    rng = np.random.default_rng(seed)
+    return payload + (rng.standard_normal(payload.shape) * 2e-3).astype(np.float32)
+
+
+@pytest.mark.parametrize("mode,smooth,edge", [(0, 0, 0), (1, 0, 0), (2, 0, 0), (1, 3, 0), (2, 5, 0), (0, 0, 1),
+                                               (1, 0, 1)])
+def test_zoom_trace_and_payload(orc, mode, smooth, edge):
+    """QuantResult::trace (zoom.cpp:441-451; test_zoom.cpp:334-336: the stage
+    counts sum to evaluations) and dictionary payloads that differ from the
+    recomputation, against the oracle (itself pinned to the reference on the
+    same cases, tests/test_oracle.py): answer, score, PD, evaluations and
+    every StageLog record (stage, evaluations, exact best, lattice point)."""
+    s = P.baseline_schedule(200, 1)
+    if edge:  # every stage name: fallback rerun, rerefinements, plateau stop
+        g = P.grid((300.0, 20.0, 50), (40.0, 5.0, 30), (-250.0, 2.0, 251))
+        cfg = P.zoom_config(smooth_k=smooth, dict_mode=mode, df_coarse_hz=40, df_refine_hz=4, df_window_hz=30,
+                            omega_hz=82, t1t2_2d_steps_ms=[200, 40], t1t2_1d_steps_ms=[100, 20],
+                            final_2d_step_ms=20, heavy_noise_cc=0.6, plateau_eps=0.05)
+    else:
+        g = P.grid((300.0, 20.0, 50), (40.0, 5.0, 30), (-50.0, 1.0, 101))
+        cfg = P.zoom_config(smooth_k=smooth, dict_mode=mode, df_coarse_hz=10, df_refine_hz=2, df_window_hz=10,
+                            omega_hz=82, t1t2_2d_steps_ms=[200, 40], t1t2_1d_steps_ms=[100, 20],
+                            final_2d_step_ms=20)
+    payload = _payload(orc, s, g, cfg, mode, 7) if mode else None
+    os_, og, oc = to_oracle_sched(s), to_oracle_grid(g), ocfg(cfg)
+    rng = np.random.default_rng(11)
+    dfr = 200.0 if edge else 40.0
+    fps = []
+    for k in range(6 if edge else 4):
+        fp = orc.simulate(os_, rng.uniform(0.4, 1.2), rng.uniform(0.06, 0.16), rng.uniform(-dfr, dfr))
+        snr = (20 if k % 2 else 0.5) if edge else (20 if k else 0.5)
+        fps.append(orc.add_noise(fp, float(np.linalg.norm(fp)) / np.sqrt(200) / snr, 500 + k))
+    fps = np.stack(fps)
+    seen = set()
+    with P.Context(s) as c:
+        got, traces = c.quantify(fps, g, cfg, dictionary=payload, trace=True)
+    for v, fp in enumerate(fps):
+        w, tw = orc.quantify_ex(os_, og, oc, fp, payload)
+        assert (got["i1"][v], got["i2"][v], got["idf"][v]) == (w.i1, w.i2, w.idf), v
+        assert (got["score"][v], got["pd"][v], got["evaluations"][v]) == (w.score, w.pd, w.evaluations), v
+        assert traces[v] == tw, v
+        assert sum(t[1] for t in traces[v]) == got["evaluations"][v]
+        seen |= {t[0] for t in traces[v]}
+    if edge:
+        assert seen == set(oracle.STAGE_NAMES)
+
+
+@pytest.mark.parametrize("prior", [0, 1, 2])
+def test_zoom_slice_traces(orc, prior):
+    """quantify_slice traces: per voxel the stage counts sum to evaluations;
+    without priors each voxel's trace equals quantify's; with the strict
+    raster (one launch) the maps, evaluations and traces equal the same
+    chain driven voxel by voxel from the host through quantify_bounded."""
+    s, g, cfg, nx, ny, mask, fps = _slice_problem(orc)
+    with P.Context(s) as c:
+        res, _, tr = c.quantify_slice(fps, mask, nx, ny, g, cfg, use_prior=prior, trace=True)
+        m = np.nonzero(mask)[0]
+        for v in m:
+            assert sum(t[1] for t in tr[v]) == res["evaluations"][v], v
+        for v in np.nonzero(mask == 0)[0]:
+            assert tr[v] == []
+        if prior == 0:
+            q, tq = c.quantify(fps[m], g, cfg, trace=True)
+            for k, v in enumerate(m):
+                assert tr[v] == tq[k]
+        if prior == 1:
+            prev = None
+            for v in m:
+                if prev is None:
+                    h, th = c.quantify_bounded(fps[v:v + 1], g, cfg, trace=True)
+                else:
+                    b, init = _prior_of(g, cfg, res[prev])
+                    h, th = c.quantify_bounded(fps[v:v + 1], g, cfg, bounds=[b], init_ms=[init], trace=True)
+                for k in ("i1", "i2", "idf", "score", "pd", "evaluations"):
+                    assert res[k][v] == h[k][0], (v, k)
+                assert tr[v] == th[0]
+                prev = v
