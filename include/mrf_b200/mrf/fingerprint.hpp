@@ -1,0 +1,5 @@
+// mrf/fingerprint.hpp -- include shim: code written against the reference's
+// proj/include/mrf/fingerprint.hpp compiles unchanged with -I include/mrf_b200
+// (all declarations live in the single drop-in header).
+#pragma once
+#include "../mrf.hpp"

@@ -121,6 +121,12 @@ def build(quiet: bool = True) -> None:
     """Compile the oracles (restatement always; reference when its sources exist)."""
     subprocess.run(["make", "-C", HERE], check=True,
                    stdout=subprocess.DEVNULL if quiet else None)
+    # the CLI parity harness needs the drop-in libraries (built by the
+    # package's build.py); skipped until they exist
+    pkg = os.path.join(os.path.dirname(HERE), "paper_1506_05393_b200")
+    if os.path.exists(os.path.join(pkg, "libmrf_b200.so")):
+        subprocess.run(["make", "-C", HERE, "cli"], check=True,
+                       stdout=subprocess.DEVNULL if quiet else None)
 
 
 def available(which: str) -> bool:

@@ -15,10 +15,10 @@ def pytest_configure(config):
 @pytest.fixture(scope="session", autouse=True)
 def _built():
     """Build the oracle (test infrastructure) and the product extension."""
-    import oracle
-    oracle.build()
     from paper_1506_05393_b200 import build as B
     B.build()
+    import oracle
+    oracle.build()
 
 
 @pytest.fixture(scope="session")

@@ -1,0 +1,86 @@
+"""End-to-end parity harness: the
+reference's OWN command functions (proj/src/cli.cpp: cmd_eval, cmd_slice,
+cmd_ccmap, cmd_noise, cmd_gen_dict), compiled from the reference sources by
+oracle/Makefile (`make -C oracle cli`) around oracle/cli_main.cpp and linked
+twice -- against the reference library (oracle/_ref/cli_ref) and against the
+drop-in (oracle/_ref/cli_b200: include/mrf_b200 shims + libmrf_b200.so +
+libmrfg.so).  Every CSV the commands write must agree field for field, except
+the wall-clock columns; binary files (.mrfd, .mrfc) byte for byte.
+
+The binaries are built here (where /root/reference exists) and travel to the
+GPU box in oracle/_ref/ like the reference library itself.
+"""
+import csv
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "oracle", "_ref", "cli_ref")
+OURS = os.path.join(ROOT, "oracle", "_ref", "cli_b200")
+TIMING = {"ms_elapsed", "mean_ms", "speedup_vs_brute"}
+SMALL = ["t1_range=500:900:20", "t2_range=40:200:10", "df_range=-20:20:2", "n=300"]
+CASES = {
+    "eval": ("eval", ["targets=12", "modes=brute,zoom,zoom-euclid,zoom-dfdict"]),
+    "eval_fulldict": ("eval", ["targets=6", "modes=brute,zoom,zoom-fulldict", "df_coarse=4", "omega=82",
+                               "t1t2_2d_steps=80,40", "t1t2_1d_steps=40,20", "final_2d_step=20"] + SMALL),
+    "slice": ("slice", []),
+    "ccmap": ("ccmap", ["write_binary_map=true"]),
+    "noise": ("noise", []),
+    "gen_dict": ("gen-dict", SMALL),
+}
+
+
+def _have_binaries():
+    return os.path.exists(REF) and os.path.exists(OURS)
+
+
+def test_cli_harness_built():
+    """The recipe builds both binaries wherever the reference sources exist."""
+    if not os.path.isdir("/root/reference/proj/src"):
+        pytest.skip("reference sources absent (GPU box): binaries come prebuilt")
+    subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "cli"], check=True, stdout=subprocess.DEVNULL)
+    assert _have_binaries()
+
+
+def _rows(path):
+    with open(path, newline="") as f:
+        return list(csv.reader(f))
+
+
+def compare_outputs(a, b):
+    fa, fb = sorted(os.listdir(a)), sorted(os.listdir(b))
+    assert fa == fb
+    for name in fa:
+        pa, pb = os.path.join(a, name), os.path.join(b, name)
+        if not name.endswith(".csv"):
+            with open(pa, "rb") as x, open(pb, "rb") as y:
+                assert x.read() == y.read(), name
+            continue
+        ra, rb = _rows(pa), _rows(pb)
+        assert len(ra) == len(rb), name
+        head = ra[0]
+        skip = {i for i, h in enumerate(head) if h in TIMING}
+        for k, (x, y) in enumerate(zip(ra, rb)):
+            assert len(x) == len(y), (name, k)
+            for i, (u, v) in enumerate(zip(x, y)):
+                if i not in skip:
+                    assert u == v, (name, k, head[i] if i < len(head) else i, u, v)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_cli_outputs_identical(tmp_path, case):
+    if not _have_binaries():
+        pytest.fail("oracle/_ref/cli_{ref,b200} missing: run `make -C oracle cli` where /root/reference exists")
+    cmd, args = CASES[case]
+    workers = f"workers={os.cpu_count() or 1}"
+    outs = {}
+    for tag, exe in (("ref", REF), ("b200", OURS)):
+        out = str(tmp_path / tag)
+        extra = [f"dict_out={out}/dictionary.mrfd"] if cmd == "gen-dict" else []
+        r = subprocess.run([exe, cmd, out, workers] + args + extra, capture_output=True, text=True, timeout=1200)
+        assert r.returncode == 0, (tag, r.stdout[-2000:], r.stderr[-2000:])
+        outs[tag] = out
+    compare_outputs(outs["ref"], outs["b200"])
