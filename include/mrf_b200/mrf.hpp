@@ -19,6 +19,7 @@
 #include <functional>
 #include <span>
 #include <string>
+#include <unordered_map>
 #include <utility>
 #include <vector>
 
@@ -69,13 +70,41 @@ Fingerprint smooth(const Fingerprint& fp, int k);                       // :63-6
 void save_csv(const Fingerprint& fp, const std::filesystem::path& path);  // :73-74
 Fingerprint load_fingerprint_csv(const std::filesystem::path& path);
 
+// ------------------------------------------------------------- bloch.hpp:12-74
+// Host primitives of the Bloch model (FP64, the reference's operand order:
+// bit-identical results).  They are the per-TR building blocks the GPU
+// kernels run fused; here for code that composes them directly.
+struct Magnetization {
+    double x = 0, y = 0, z = 1;
+};
+struct Matrix3 {  // row-major (bloch.hpp:22-41)
+    double m[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    static Matrix3 identity() { return {}; }
+    Matrix3 operator*(const Matrix3& o) const;
+    Magnetization operator*(const Magnetization& v) const;
+};
+enum class Axis { X, Y, Z };
+struct RfPulse {  // bloch.hpp:48-53: flip, phase (rad), duration (s), off-resonance (rad/s)
+    double alpha = 0, phi = 0, tau = 0, delta_omega = 0;
+};
+Matrix3 rot(Axis axis, double theta);                                    // bloch.hpp:56
+Magnetization relax_step(const Magnetization& m, double dt, double t1, double t2);  // bloch.hpp:60
+// Simplified Rz(phi) Rx(-alpha) Rz(-phi), or the full off-resonant-axis form
+// (bloch.hpp:62-69); std::invalid_argument for the full form's undefined cases.
+Matrix3 rf_matrix(const RfPulse& pulse, bool simplified = true);
+std::pair<std::complex<double>, Magnetization> evolve_tr(const Magnetization& m, const RfPulse& pulse,
+                                                         double tr, double te,
+                                                         const TissueParams& p);  // bloch.hpp:71-74
+
 // ------------------------------------------------------------- bloch.hpp:79-102
+// Holds one GPU context (the schedule's RF rotations composed once, as the
+// reference's constructor does); copies create their own context.
 class BlochSimulator {
   public:
     explicit BlochSimulator(const Schedule& sched);
     ~BlochSimulator();
-    BlochSimulator(const BlochSimulator&) = delete;
-    BlochSimulator& operator=(const BlochSimulator&) = delete;
+    BlochSimulator(const BlochSimulator& o);
+    BlochSimulator& operator=(const BlochSimulator& o);
     void simulate(const TissueParams& p, std::complex<double>* out) const;
     Fingerprint simulate(const TissueParams& p) const;
     // Batched form (GPU-native): params.size() fingerprints, row-major.
@@ -86,6 +115,7 @@ class BlochSimulator {
   private:
     mrfg_ctx* ctx_ = nullptr;
     std::size_t n_ = 0;
+    Schedule sched_;
 };
 Fingerprint simulate_fingerprint(const TissueParams& p, const Schedule& sched);  // bloch.hpp:102
 
@@ -189,7 +219,7 @@ struct QuantResult {
     double score = 0;
     std::size_t evaluations = 0;
     double seconds = 0;
-    std::vector<StageLog> trace;  // not recorded by the GPU kernel (empty)
+    std::vector<StageLog> trace;  // recorded by K5 (exact bests, the reference's stages)
 };
 struct DfSearchParams {
     long coarse = 60, refine = 3, finest = 1, window_half = 75, omega = 70;
@@ -205,6 +235,39 @@ long zoom_1d(const std::function<double(long)>& f, long lo, long hi, long init,
 std::pair<long, long> zoom_2d(const std::function<double(long, long)>& f, long lo1, long hi1,
                               long lo2, long hi2, long init1, long init2,
                               std::span<const std::pair<long, long>> steps);
+// Memoizing objective over a search lattice (zoom.hpp:72-110): each unique
+// point costs one FP64 simulation on the GPU (bit-identical to the
+// reference's) or one dictionary lookup; repeats and metric switches are
+// free.  The K5 kernel runs the same objective fused on the device; this
+// class serves callers that drive search_df / zoom_1d / zoom_2d themselves.
+class Objective {
+  public:
+    struct Options {
+        int smooth_k = 0;
+        const Dictionary* full_dict = nullptr;  // every point is a lookup
+        const Dictionary* df_dict = nullptr;    // first-stage lookups only
+    };
+    Objective(const Fingerprint& query, const ParameterGrid& lattice, const Schedule& sched,
+              const Options& opt);
+    ~Objective();
+    double eval(long i1, long i2, long idf, Metric metric);
+    double eval_df_stage(long i1, long i2, long idf, Metric metric);
+    std::size_t evaluations() const { return evals_; }
+    const ParameterGrid& lattice() const { return lattice_; }
+    Fingerprint ideal_at(long i1, long i2, long idf) const;
+
+  private:
+    double score_from_entry(const std::vector<std::complex<double>>& entry, Metric metric) const;
+    const std::vector<std::complex<double>>& acquire(long i1, long i2, long idf, bool df_stage);
+    ParameterGrid lattice_;
+    BlochSimulator sim_;
+    Options opt_;
+    std::vector<std::complex<double>> query_;
+    std::size_t evals_ = 0;
+    std::unordered_map<std::uint64_t, std::vector<std::complex<double>>> entries_;
+    std::unordered_map<std::uint64_t, double> memo_cc_, memo_euc_;
+};
+
 QuantResult quantify(const Fingerprint& fp, const SearchRanges& ranges, const ZoomConfig& cfg,
                      const Schedule& sched, const Dictionary* df_dict = nullptr,
                      const Dictionary* full_dict = nullptr);            // zoom.hpp:148-151

@@ -17,7 +17,9 @@
 #include <cstring>
 #include <fstream>
 #include <sstream>
+#include <exception>
 #include <stdexcept>
+#include <thread>
 
 #include "mrf_b200/mrf.hpp"
 #include "mrfg.h"
@@ -28,6 +30,51 @@ namespace {
 int device() {
     const char* e = std::getenv("MRFG_DEVICE");
     return e ? std::atoi(e) : 0;
+}
+
+// Devices the drop-in spreads its work over: MRFG_DEVICES="0,1,...,7" (one
+// context per listed device; a device may repeat), else the single
+// MRFG_DEVICE.  The reference's `workers` selects host threads and never
+// changes results (parallel.hpp:12-15); the device list likewise never
+// changes results: atom shards are merged by (max score, lowest flat), voxel
+// shards are independent.
+std::vector<int> devices() {
+    std::vector<int> out;
+    if (const char* e = std::getenv("MRFG_DEVICES")) {
+        std::string v(e);
+        std::size_t pos = 0;
+        while (pos < v.size()) {
+            const std::size_t c = v.find(',', pos);
+            const std::string tok = v.substr(pos, c == std::string::npos ? std::string::npos : c - pos);
+            if (!tok.empty()) out.push_back(std::atoi(tok.c_str()));
+            if (c == std::string::npos) break;
+            pos = c + 1;
+        }
+    }
+    if (out.empty()) out.push_back(device());
+    return out;
+}
+
+// fn(k) on one host thread per shard; the first exception is rethrown.
+template <class F>
+void on_shards(std::size_t count, F&& fn) {
+    if (count == 1) {
+        fn(std::size_t{0});
+        return;
+    }
+    std::vector<std::thread> th;
+    std::vector<std::exception_ptr> err(count);
+    for (std::size_t k = 0; k < count; ++k)
+        th.emplace_back([&, k] {
+            try {
+                fn(k);
+            } catch (...) {
+                err[k] = std::current_exception();
+            }
+        });
+    for (auto& t : th) t.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
 }
 
 [[noreturn]] void raise(int rc) {
@@ -47,7 +94,7 @@ struct CtxGuard {
     }
 };
 
-mrfg_ctx* create(const Schedule& s) {
+mrfg_ctx* create(const Schedule& s, int dev = device()) {
     const std::size_t n = s.size();
     std::vector<double> f(n), p(n), tr(n), te(n);
     for (std::size_t i = 0; i < n; ++i) {
@@ -57,7 +104,7 @@ mrfg_ctx* create(const Schedule& s) {
         te[i] = s.entries[i].te_ms;
     }
     mrfg_ctx* h = nullptr;
-    check(mrfg_create(f.data(), p.data(), tr.data(), te.data(), static_cast<int64_t>(n), device(), &h));
+    check(mrfg_create(f.data(), p.data(), tr.data(), te.data(), static_cast<int64_t>(n), dev, &h));
     return h;
 }
 
@@ -381,7 +428,91 @@ double estimate_pd(const Fingerprint& acquired, const Fingerprint& matched_ideal
 }
 
 // --------------------------------------------------------------------- bloch
-BlochSimulator::BlochSimulator(const Schedule& sched) : ctx_(create(sched)), n_(sched.size()) {}
+// Host primitives (bloch.cpp:11-93), FP64 in the reference's operand order
+// (this file is compiled without FMA contraction, like the reference).
+Matrix3 Matrix3::operator*(const Matrix3& o) const {  // bloch.hpp:26-33
+    Matrix3 r;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            r.m[3 * i + j] = m[3 * i] * o.m[j] + m[3 * i + 1] * o.m[3 + j] + m[3 * i + 2] * o.m[6 + j];
+    return r;
+}
+
+Magnetization Matrix3::operator*(const Magnetization& v) const {  // bloch.hpp:35-38
+    return {m[0] * v.x + m[1] * v.y + m[2] * v.z, m[3] * v.x + m[4] * v.y + m[5] * v.z,
+            m[6] * v.x + m[7] * v.y + m[8] * v.z};
+}
+
+Matrix3 rot(Axis axis, double theta) {  // bloch.cpp:31-53: counterclockwise about a lab axis
+    const double c = std::cos(theta), s = std::sin(theta);
+    Matrix3 r;
+    int a = 0, b = 1;  // the rotated coordinate pair
+    if (axis == Axis::X) a = 1, b = 2;
+    if (axis == Axis::Y) a = 2, b = 0;  // about y: (z, x) -> r[x][z] = s, r[z][x] = -s
+    r.m[4 * a] = c;
+    r.m[4 * b] = c;
+    r.m[3 * b + a] = s;
+    r.m[3 * a + b] = -s;
+    return r;
+}
+
+Magnetization relax_step(const Magnetization& m, double dt, double t1, double t2) {  // bloch.cpp:55-61
+    if (dt < 0 || t1 <= 0 || t2 <= 0)
+        throw std::invalid_argument("relax_step: dt must be >= 0 and T1, T2 > 0");
+    const double e2 = std::exp(-dt / t2), e1 = std::exp(-dt / t1);
+    return {m.x * e2, m.y * e2, 1.0 + (m.z - 1.0) * e1};
+}
+
+Matrix3 rf_matrix(const RfPulse& pulse, bool simplified) {  // bloch.cpp:63-78
+    if (simplified) return rot(Axis::Z, pulse.phi) * rot(Axis::X, -pulse.alpha) * rot(Axis::Z, -pulse.phi);
+    if (pulse.alpha == 0)
+        throw std::invalid_argument("rf_matrix: full rotation model is undefined for a zero flip angle");
+    if (pulse.tau <= 0) throw std::invalid_argument("rf_matrix: full rotation model needs tau > 0");
+    const double beta = std::atan(pulse.tau * pulse.delta_omega / pulse.alpha);
+    const double rate = pulse.alpha / pulse.tau;
+    const double alpha_eff = -pulse.tau * std::sqrt(pulse.delta_omega * pulse.delta_omega + rate * rate);
+    return rot(Axis::Z, pulse.phi) * rot(Axis::Y, beta) * rot(Axis::X, alpha_eff) * rot(Axis::Y, -beta) *
+           rot(Axis::Z, -pulse.phi);
+}
+
+namespace {
+// relax_precess (bloch.cpp:15-27): rotate by 2 pi df dt, scale by E2; recover z.
+void relax_precess_host(Magnetization& m, double dt, double inv_t1, double inv_t2, double df) {
+    const double e2 = std::exp(-dt * inv_t2), e1 = std::exp(-dt * inv_t1);
+    const double a = 6.283185307179586476925286766559 * df * dt;
+    const double c = std::cos(a), s = std::sin(a);
+    const double x = (m.x * c - m.y * s) * e2, y = (m.x * s + m.y * c) * e2;
+    m.x = x;
+    m.y = y;
+    m.z = 1.0 + (m.z - 1.0) * e1;
+}
+}  // namespace
+
+std::pair<std::complex<double>, Magnetization> evolve_tr(const Magnetization& m, const RfPulse& pulse, double tr,
+                                                         double te, const TissueParams& p) {  // bloch.cpp:80-93
+    if (te < 0 || te > tr) throw std::invalid_argument("evolve_tr: need 0 <= te <= tr");
+    if (p.t1 <= 0 || p.t2 <= 0) throw std::invalid_argument("evolve_tr: T1 and T2 must be positive");
+    Magnetization cur = rf_matrix(pulse) * m;
+    relax_precess_host(cur, te, 1.0 / p.t1, 1.0 / p.t2, p.df);
+    const std::complex<double> echo(cur.x, cur.y);
+    relax_precess_host(cur, tr - te, 1.0 / p.t1, 1.0 / p.t2, p.df);
+    return {echo, cur};
+}
+
+BlochSimulator::BlochSimulator(const Schedule& sched) : ctx_(create(sched)), n_(sched.size()), sched_(sched) {}
+
+BlochSimulator::BlochSimulator(const BlochSimulator& o) : ctx_(create(o.sched_)), n_(o.n_), sched_(o.sched_) {}
+
+BlochSimulator& BlochSimulator::operator=(const BlochSimulator& o) {
+    if (this != &o) {
+        mrfg_ctx* c = create(o.sched_);
+        if (ctx_) mrfg_destroy(ctx_);
+        ctx_ = c;
+        n_ = o.n_;
+        sched_ = o.sched_;
+    }
+    return *this;
+}
 
 BlochSimulator::~BlochSimulator() {
     if (ctx_) mrfg_destroy(ctx_);
@@ -522,7 +653,6 @@ ScanOutcome scan_grid(const ParameterGrid& grid, const Schedule& sched,
     for (const auto& q : queries)
         if (q.size() != sched.size())
             throw std::invalid_argument("query length does not match dictionary entries");
-    CtxGuard c{create(sched)};
     const std::size_t n = sched.size(), nq = queries.size();
     std::vector<double> flat(2 * n * nq);
     std::vector<uint8_t> unit(nq);  // prep_query: unit_norm queries are used as given
@@ -530,13 +660,37 @@ ScanOutcome scan_grid(const ParameterGrid& grid, const Schedule& sched,
         std::memcpy(&flat[2 * n * k], interleaved(queries[k]), 16 * n);
         unit[k] = queries[k].unit_norm ? 1 : 0;
     }
-    std::vector<mrfg_match> m(nq);
-    mrfg_scan_stats st{};
-    mrfg_scan_opts o{};
-    o.unit_queries = unit.data();
     const mrfg_grid g = to_grid(grid);
-    check(mrfg_scan_grid(c.h, &g, 0, 0, flat.data(), static_cast<int64_t>(nq),
-                         metric == Metric::cc ? MRFG_METRIC_CC : MRFG_METRIC_EUCLIDEAN, &o, m.data(), &st));
+    // atom shards: contiguous T1 slabs, one per listed device
+    const std::vector<int> devs = devices();
+    const std::size_t row = grid.t2_ms.count * grid.df_hz.count;
+    const std::size_t rows_per = (grid.t1_ms.count + devs.size() - 1) / devs.size();
+    std::vector<std::vector<mrfg_match>> part(devs.size(), std::vector<mrfg_match>(nq, mrfg_match{-1, 0.0}));
+    std::vector<mrfg_scan_stats> sts(devs.size());
+    on_shards(devs.size(), [&](std::size_t k) {
+        const std::size_t fb = std::min(grid.total(), k * rows_per * row);
+        const std::size_t fe = std::min(grid.total(), (k + 1) * rows_per * row);
+        if (fe <= fb) return;
+        CtxGuard c{create(sched, devs[k])};
+        mrfg_scan_opts o{};
+        o.unit_queries = unit.data();
+        check(mrfg_scan_grid(c.h, &g, static_cast<int64_t>(fb), static_cast<int64_t>(fe), flat.data(),
+                             static_cast<int64_t>(nq), metric == Metric::cc ? MRFG_METRIC_CC : MRFG_METRIC_EUCLIDEAN,
+                             &o, part[k].data(), &sts[k]));
+    });
+    // merge: highest score, lowest flat on ties (dictionary.cpp:291-294)
+    std::vector<mrfg_match> m(nq, mrfg_match{-1, 0.0});
+    for (const auto& pm : part)
+        for (std::size_t q = 0; q < nq; ++q)
+            if (pm[q].flat >= 0 && (m[q].flat < 0 || pm[q].score > m[q].score ||
+                                    (pm[q].score == m[q].score && pm[q].flat < m[q].flat)))
+                m[q] = pm[q];
+    mrfg_scan_stats st{};
+    for (const auto& x : sts) {  // the shards run concurrently: the slowest one's times
+        st.gemm_ms = std::max(st.gemm_ms, x.gemm_ms);
+        st.rerank_ms = std::max(st.rerank_ms, x.rerank_ms);
+        st.bloch_ms = std::max(st.bloch_ms, x.bloch_ms);
+    }
     ScanOutcome out;
     for (std::size_t k = 0; k < nq; ++k) {
         const auto u = grid.unflatten(static_cast<std::size_t>(m[k].flat));
@@ -757,6 +911,125 @@ std::pair<long, long> zoom_2d(const std::function<double(long, long)>& f, long l
     return {x, y};
 }
 
+// ------------------------------------------------------------------ Objective
+// zoom.cpp:41-156: lattice-key memo; acquisitions simulate on the GPU in FP64
+// (bit-identical entries) or read the caller's dictionary entry.
+namespace {
+constexpr long kMaxAxis = 1L << 21;
+std::uint64_t key_of(long i1, long i2, long idf) {  // zoom.cpp:14-19
+    return (static_cast<std::uint64_t>(i1) << 42) | (static_cast<std::uint64_t>(i2) << 21) |
+           static_cast<std::uint64_t>(idf);
+}
+void check_close_axis(const AxisSpec& a, const AxisSpec& b, const char* what) {  // zoom.cpp:27-37
+    auto close = [](double x, double y) {
+        return std::abs(x - y) <= 1e-9 * std::max({1.0, std::abs(x), std::abs(y)});
+    };
+    if (!close(a.min, b.min) || !close(a.step, b.step) || a.count != b.count)
+        throw std::invalid_argument(std::string("lattice mismatch: ") + what);
+}
+}  // namespace
+
+Objective::Objective(const Fingerprint& query, const ParameterGrid& lattice, const Schedule& sched,
+                     const Options& opt)
+    : lattice_(lattice), sim_(sched), opt_(opt) {
+    if (query.size() != sched.size())
+        throw std::invalid_argument("objective: query length does not match schedule");
+    for (const AxisSpec* ax : {&lattice.t1_ms, &lattice.t2_ms, &lattice.df_hz})
+        if (ax->count == 0 || ax->count >= static_cast<std::size_t>(kMaxAxis))
+            throw std::invalid_argument("objective: lattice axis empty or too fine");
+    query_ = normalize(opt_.smooth_k ? smooth(query, opt_.smooth_k) : query).s;
+    if (opt_.full_dict) {
+        if (opt_.full_dict->digest != schedule_digest(sched))
+            throw std::invalid_argument("objective: dictionary built from another schedule");
+        check_close_axis(opt_.full_dict->grid.t1_ms, lattice.t1_ms, "t1 axis");
+        check_close_axis(opt_.full_dict->grid.t2_ms, lattice.t2_ms, "t2 axis");
+        check_close_axis(opt_.full_dict->grid.df_hz, lattice.df_hz, "df axis");
+        if (opt_.full_dict->entry_len != sched.size())
+            throw std::invalid_argument("objective: dictionary entry length mismatch");
+    }
+    if (opt_.df_dict) {
+        if (opt_.df_dict->digest != schedule_digest(sched))
+            throw std::invalid_argument("objective: df dictionary from another schedule");
+        if (opt_.df_dict->grid.t1_ms.count != 1 || opt_.df_dict->grid.t2_ms.count != 1)
+            throw std::invalid_argument("objective: df dictionary must fix T1 and T2");
+        check_close_axis(opt_.df_dict->grid.df_hz, lattice.df_hz, "df axis");
+        if (opt_.df_dict->entry_len != sched.size())
+            throw std::invalid_argument("objective: df dictionary entry length mismatch");
+    }
+}
+
+Objective::~Objective() = default;
+
+double Objective::score_from_entry(const std::vector<std::complex<double>>& e, Metric metric) const {
+    if (metric == Metric::cc) {  // zoom.cpp:74-84
+        double re = 0, im = 0;
+        for (std::size_t j = 0; j < query_.size(); ++j) {
+            re += query_[j].real() * e[j].real() + query_[j].imag() * e[j].imag();
+            im += query_[j].imag() * e[j].real() - query_[j].real() * e[j].imag();
+        }
+        const double v = std::sqrt(re * re + im * im);
+        return v < 1.0 ? v : 1.0;
+    }
+    double acc = 0;  // zoom.cpp:85-91
+    for (std::size_t j = 0; j < query_.size(); ++j) {
+        const double dr = query_[j].real() - e[j].real(), di = query_[j].imag() - e[j].imag();
+        acc += dr * dr + di * di;
+    }
+    return -std::sqrt(acc);
+}
+
+const std::vector<std::complex<double>>& Objective::acquire(long i1, long i2, long idf, bool df_stage) {
+    const std::uint64_t k = key_of(i1, i2, idf);  // zoom.cpp:94-123
+    if (auto it = entries_.find(k); it != entries_.end()) return it->second;
+    std::vector<std::complex<double>> entry;
+    if (opt_.full_dict || (df_stage && opt_.df_dict)) {
+        const Dictionary* d = opt_.full_dict ? opt_.full_dict : opt_.df_dict;
+        const std::size_t flat = opt_.full_dict ? d->grid.flatten(static_cast<std::size_t>(i1),
+                                                                  static_cast<std::size_t>(i2),
+                                                                  static_cast<std::size_t>(idf))
+                                                : static_cast<std::size_t>(idf);
+        auto raw = d->entry(flat);
+        Fingerprint f;
+        f.s.reserve(d->entry_len);
+        for (std::size_t j = 0; j < d->entry_len; ++j) f.s.emplace_back(raw[2 * j], raw[2 * j + 1]);
+        entry = opt_.smooth_k ? normalize(smooth(f, opt_.smooth_k)).s : std::move(f.s);
+    } else {
+        Fingerprint f = sim_.simulate(lattice_.params_at(static_cast<std::size_t>(i1), static_cast<std::size_t>(i2),
+                                                          static_cast<std::size_t>(idf)));
+        entry = normalize(opt_.smooth_k ? smooth(f, opt_.smooth_k) : f).s;
+    }
+    ++evals_;
+    return entries_.emplace(k, std::move(entry)).first->second;
+}
+
+double Objective::eval(long i1, long i2, long idf, Metric metric) {  // zoom.cpp:125-138
+    if (i1 < 0 || i2 < 0 || idf < 0 || i1 >= static_cast<long>(lattice_.t1_ms.count) ||
+        i2 >= static_cast<long>(lattice_.t2_ms.count) || idf >= static_cast<long>(lattice_.df_hz.count))
+        throw std::out_of_range("objective: lattice index out of range");
+    auto& memo = metric == Metric::cc ? memo_cc_ : memo_euc_;
+    const std::uint64_t k = key_of(i1, i2, idf);
+    if (auto it = memo.find(k); it != memo.end()) return it->second;
+    const double s = score_from_entry(acquire(i1, i2, idf, false), metric);
+    memo.emplace(k, s);
+    return s;
+}
+
+double Objective::eval_df_stage(long i1, long i2, long idf, Metric metric) {  // zoom.cpp:140-150
+    if (idf < 0 || idf >= static_cast<long>(lattice_.df_hz.count))
+        throw std::out_of_range("objective: lattice index out of range");
+    auto& memo = metric == Metric::cc ? memo_cc_ : memo_euc_;
+    const std::uint64_t k = key_of(i1, i2, idf);
+    if (auto it = memo.find(k); it != memo.end()) return it->second;
+    const double s = score_from_entry(acquire(i1, i2, idf, true), metric);
+    memo.emplace(k, s);
+    return s;
+}
+
+Fingerprint Objective::ideal_at(long i1, long i2, long idf) const {  // zoom.cpp:152-156
+    return sim_.simulate(lattice_.params_at(static_cast<std::size_t>(i1), static_cast<std::size_t>(i2),
+                                            static_cast<std::size_t>(idf)));
+}
+
 std::vector<QuantResult> quantify_batch(const std::vector<Fingerprint>& fps, const SearchRanges& ranges,
                                         const ZoomConfig& cfg, const Schedule& sched, const Dictionary* df_dict,
                                         const Dictionary* full_dict) {
@@ -768,7 +1041,6 @@ std::vector<QuantResult> quantify_batch(const std::vector<Fingerprint>& fps, con
             throw std::invalid_argument("objective: query length does not match schedule");
     std::vector<QuantResult> out;
     if (fps.empty()) return out;
-    CtxGuard c{create(sched)};
     const std::size_t n = sched.size();
     std::vector<double> flat(2 * n * fps.size());
     for (std::size_t k = 0; k < fps.size(); ++k) std::memcpy(&flat[2 * n * k], interleaved(fps[k]), 16 * n);
@@ -779,14 +1051,22 @@ std::vector<QuantResult> quantify_batch(const std::vector<Fingerprint>& fps, con
     std::vector<mrfg_quant> q(fps.size());
     std::vector<mrfg_stage> rec(MRFG_TRACE_MAX * fps.size());
     std::vector<int32_t> len(fps.size());
-    mrfg_zoom_io io{};
-    io.dict = d ? d->data.data() : nullptr;
-    io.dict_entries = d ? static_cast<int64_t>(d->data.size() / (2 * n)) : 0;
-    io.trace = rec.data();
-    io.trace_len = len.data();
     const auto t0 = std::chrono::steady_clock::now();
-    check(mrfg_quantify_ex(c.h, &g, &zc, flat.data(), static_cast<int64_t>(fps.size()), nullptr, nullptr, &io,
-                           q.data()));
+    // voxel shards: contiguous blocks, one per listed device
+    const std::vector<int> devs = devices();
+    const std::size_t per = (fps.size() + devs.size() - 1) / devs.size();
+    on_shards(devs.size(), [&](std::size_t k) {
+        const std::size_t vb = std::min(fps.size(), k * per), ve = std::min(fps.size(), (k + 1) * per);
+        if (ve <= vb) return;
+        CtxGuard c{create(sched, devs[k])};
+        mrfg_zoom_io io{};
+        io.dict = d ? d->data.data() : nullptr;
+        io.dict_entries = d ? static_cast<int64_t>(d->data.size() / (2 * n)) : 0;
+        io.trace = rec.data() + MRFG_TRACE_MAX * vb;
+        io.trace_len = len.data() + vb;
+        check(mrfg_quantify_ex(c.h, &g, &zc, flat.data() + 2 * n * vb, static_cast<int64_t>(ve - vb), nullptr,
+                               nullptr, &io, q.data() + vb));
+    });
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     for (std::size_t k = 0; k < q.size(); ++k) {
         out.push_back(to_result(lat, q[k], secs / static_cast<double>(fps.size())));
@@ -820,6 +1100,35 @@ SliceResult quantify_slice(const std::vector<Fingerprint>& fps, const std::vecto
         throw std::invalid_argument("quantify_slice: inconsistent raster dimensions");
     const ParameterGrid lat = grid_from_ranges(ranges.t1_ms, ranges.t2_ms, ranges.df_hz);
     check_df_dict(df_dict, lat, cfg, sched);
+    if (!use_prior && devices().size() > 1) {
+        // independent voxels (zoom.cpp:616-624): voxel shards over the devices
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<Fingerprint> sel;
+        std::vector<std::size_t> idx;
+        for (std::size_t i = 0; i < nv; ++i)
+            if (mask[i]) {
+                sel.push_back(fps[i]);
+                idx.push_back(i);
+            }
+        const std::vector<QuantResult> r = quantify_batch(sel, ranges, cfg, sched, df_dict, nullptr);
+        SliceResult out;
+        out.nx = nx;
+        out.ny = ny;
+        for (auto* v : {&out.t1_ms, &out.t2_ms, &out.df_hz, &out.pd, &out.score}) v->assign(nv, 0);
+        out.evaluations.assign(nv, 0);
+        for (std::size_t k = 0; k < idx.size(); ++k) {
+            const std::size_t i = idx[k];
+            out.t1_ms[i] = r[k].params.t1 * 1e3;  // zoom.cpp:581-586
+            out.t2_ms[i] = r[k].params.t2 * 1e3;
+            out.df_hz[i] = r[k].params.df;
+            out.pd[i] = r[k].params.pd;
+            out.score[i] = r[k].score;
+            out.evaluations[i] = r[k].evaluations;
+            out.total_evaluations += r[k].evaluations;
+        }
+        out.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return out;
+    }
     CtxGuard c{create(sched)};
     const std::size_t n = sched.size();
     std::vector<double> flat(2 * n * nv, 0.0);

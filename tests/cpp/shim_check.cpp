@@ -61,6 +61,37 @@ int main() {
         EXPECT(sc.matches[k].params.t1 == b.params.t1 && sc.matches[k].score == b.score);
         EXPECT(sc.matches[k].evaluations == grid.total());
     }
+    // Objective (zoom.hpp:72-110): the memo the search runs on; its value at
+    // quantify's answer is quantify's score, repeats are free, metric
+    // switches reuse the entry, range errors are out_of_range
+    {
+        Fingerprint fp = q[1];
+        QuantResult z = quantify(fp, ranges, cfg, s);
+        Objective obj(fp, grid, s, Objective::Options{});
+        const long i1 = std::lround((z.params.t1 * 1e3 - grid.t1_ms.min) / grid.t1_ms.step);
+        const long i2 = std::lround((z.params.t2 * 1e3 - grid.t2_ms.min) / grid.t2_ms.step);
+        const long idf = std::lround((z.params.df - grid.df_hz.min) / grid.df_hz.step);
+        EXPECT(obj.eval(i1, i2, idf, Metric::cc) == z.score);
+        EXPECT(obj.evaluations() == 1);
+        obj.eval(i1, i2, idf, Metric::euclidean);
+        obj.eval_df_stage(i1, i2, idf, Metric::cc);
+        EXPECT(obj.evaluations() == 1);
+        Fingerprint ideal = obj.ideal_at(i1, i2, idf);
+        EXPECT(std::abs(estimate_pd(fp, ideal) - z.params.pd) < 1e-15);
+        bool oor = false;
+        try {
+            obj.eval(-1, 0, 0, Metric::cc);
+        } catch (const std::out_of_range&) {
+            oor = true;
+        }
+        EXPECT(oor);
+        // a full dictionary: the objective scores the stored float entries
+        Objective::Options o;
+        o.full_dict = &dict;
+        Objective od(fp, grid, s, o);
+        const double vd = od.eval(i1, i2, idf, Metric::cc);
+        EXPECT(std::abs(vd - z.score) < 1e-6 && od.evaluations() == 1);
+    }
     // cc_map streams every score in order
     std::size_t got = 0;
     cc_map(q[0], grid, s, [&](std::size_t first, std::span<const float> v) {

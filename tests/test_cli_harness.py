@@ -29,7 +29,11 @@ CASES = {
     "ccmap": ("ccmap", ["write_binary_map=true"]),
     "noise": ("noise", []),
     "gen_dict": ("gen-dict", SMALL),
+    # the drop-in over three device contexts (atom shards for brute force,
+    # voxel shards for ZOOM): outputs still identical to the reference's
+    "eval_3dev": ("eval", ["targets=8", "modes=brute,zoom"]),
 }
+DEVICES = {"eval_3dev": "0,0,0"}
 
 
 def _have_binaries():
@@ -77,10 +81,14 @@ def test_cli_outputs_identical(tmp_path, case):
     cmd, args = CASES[case]
     workers = f"workers={os.cpu_count() or 1}"
     outs = {}
+    env = dict(os.environ)
+    if case in DEVICES:
+        env["MRFG_DEVICES"] = DEVICES[case]
     for tag, exe in (("ref", REF), ("b200", OURS)):
         out = str(tmp_path / tag)
         extra = [f"dict_out={out}/dictionary.mrfd"] if cmd == "gen-dict" else []
-        r = subprocess.run([exe, cmd, out, workers] + args + extra, capture_output=True, text=True, timeout=1200)
+        r = subprocess.run([exe, cmd, out, workers] + args + extra, capture_output=True, text=True, timeout=1200,
+                           env=env)
         assert r.returncode == 0, (tag, r.stdout[-2000:], r.stderr[-2000:])
         outs[tag] = out
     compare_outputs(outs["ref"], outs["b200"])
