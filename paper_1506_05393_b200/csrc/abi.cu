@@ -607,6 +607,14 @@ int mrfg_create(const double* flip_deg, const double* phase_deg, const double* t
             rf32[12 * i + 9] = static_cast<float>(c.te_s[i]);  // per-step intervals (s) in the pad
             rf32[12 * i + 10] = static_cast<float>(c.rest_s[i]);
         }
+        // x-axis pulses: the x row and column are (1, 0, 0) up to FP64 dust
+        // (rot(Z, pi) carries sin(pi) = 1.2e-16), far below FP32 resolution
+        c.rf_xaxis = n > 0;
+        for (int64_t i = 0; i < n && c.rf_xaxis; ++i) {
+            const double* r = &c.rf64[9 * i];
+            c.rf_xaxis = std::fabs(r[0] - 1.0) <= 1e-12 && std::fabs(r[1]) <= 1e-12 && std::fabs(r[2]) <= 1e-12 &&
+                         std::fabs(r[3]) <= 1e-12 && std::fabs(r[6]) <= 1e-12;
+        }
         double inv[9];
         host_rf_matrix(3.14159265358979323846, 0, inv);  // bloch.cpp:113
         // kInvert * (0,0,1) = third column

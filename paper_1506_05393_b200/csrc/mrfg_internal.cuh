@@ -110,6 +110,7 @@ struct Ctx {
     std::vector<double> rf64;       // n x 9 (bloch.cpp:101)
     std::vector<double> te_s, rest_s;
     double inv64[9];                // kInvert (bloch.cpp:113)
+    bool rf_xaxis = false;          // every RF rotation is about x (phases 0/180 deg): K1 specialization
     DevBuf rf64_d, rf32_d;          // n x 9 doubles; n x 12 floats (9 RF, te, rest, pad)
     GridTables tab;                 // cache for the last grid
     // scratch
