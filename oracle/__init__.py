@@ -159,6 +159,9 @@ class Oracle:
                                        C.c_int, C.c_int, C.POINTER(i64), dp, dp]
         L.orc_quantify.argtypes = [C.POINTER(Sched), C.POINTER(Grid), C.POINTER(ZoomCfg), dp,
                                    C.POINTER(Quant)]
+        L.orc_quantify_b1.argtypes = [C.POINTER(Sched), C.c_int, C.POINTER(Grid), C.POINTER(ZoomCfg),
+                                      C.POINTER(C.c_int64), C.c_int, C.c_int64, dp, C.POINTER(Quant),
+                                      C.POINTER(C.c_int64)]
         L.orc_quantify_ex.argtypes = [C.POINTER(Sched), C.POINTER(Grid), C.POINTER(ZoomCfg), dp,
                                       C.POINTER(C.c_float), i64, C.POINTER(Stage), C.c_int,
                                       C.POINTER(C.c_int), C.POINTER(Quant)]
@@ -333,6 +336,18 @@ class Oracle:
         trace = [(STAGE_NAMES[tr[k].stage], tr[k].evaluations, tr[k].best, tr[k].t1_ms, tr[k].t2_ms,
                   tr[k].df_hz) for k in range(min(ntr.value, cap))]
         return out, trace
+
+    def quantify_b1(self, scheds, g: Grid, cfg: ZoomCfg, fp: np.ndarray, steps, init_ib: int):
+        """Four-parameter ZOOM (oracle_api.h orc_quantify_b1) -> (Quant, ib)."""
+        fp = np.ascontiguousarray(fp, dtype=np.complex128)
+        cs = (Sched * len(scheds))(*[x.c() for x in scheds])
+        st = np.ascontiguousarray(steps, dtype=np.int64)
+        out = Quant()
+        ib = C.c_int64(-1)
+        self._check(self.lib.orc_quantify_b1(cs, len(scheds), C.byref(g), C.byref(cfg),
+                                             st.ctypes.data_as(C.POINTER(C.c_int64)), len(st), init_ib,
+                                             self._dp(fp.view(np.float64)), C.byref(out), C.byref(ib)))
+        return out, ib.value
 
     def quantify_slice(self, s: Schedule, g: Grid, cfg: ZoomCfg, fps: np.ndarray,
                        mask: np.ndarray, nx: int, ny: int, use_prior: bool, threads: int = 0):

@@ -1170,3 +1170,58 @@ int orc_quantify_slice(const orc_sched* s, const orc_grid* g, const orc_zoom_cfg
     sim_free(&sim);
     return rc;
 }
+
+/* Four-parameter ZOOM (oracle_api.h): outer zoom_1d over the B1 index with
+ * the memoized objective g(ib) = quantify(fp, scheds[ib]).score; the inner
+ * search is quantify_impl above (zoom.cpp:416-523), the outer walk zoom_1d's
+ * probe order (zoom.cpp:252-282: left flank first, strict improvement,
+ * clamped, ties keep the centre). */
+int orc_quantify_b1(const orc_sched* scheds, int nb, const orc_grid* lattice, const orc_zoom_cfg* cfg,
+                    const int64_t* steps, int nsteps, int64_t init_ib, const double* fp, orc_quant* out,
+                    int64_t* ib_out) {
+    if (nb <= 0) return fail("quantify_b1: no B1 values");
+    if (check_lattice(lattice)) return -1;
+    for (int k = 0; k < nsteps; ++k)
+        if (steps[k] <= 0) return fail("zoom_1d: step must be positive");
+    orc_quant* res = calloc((size_t)nb, sizeof(orc_quant));
+    int* have = calloc((size_t)nb, sizeof(int));
+    int64_t evals = 0;
+    int rc = 0;
+#define G(ib) (have[ib] ? 0 : (rc = rc ? rc : orc_quantify(&scheds[ib], lattice, cfg, fp, &res[ib]), \
+                                 have[ib] = 1, evals += res[ib].evaluations, 0), res[ib].score)
+    int64_t x = clampl(init_ib, 0, nb - 1);
+    double fx = G(x);
+    for (int si = 0; si < nsteps && rc == 0; ++si) {
+        const int64_t st = steps[si];
+        for (;;) {
+            const int64_t xl = clampl(x - st, 0, nb - 1);
+            if (xl != x) {
+                const double fl = G(xl);
+                if (fl > fx) {
+                    x = xl;
+                    fx = fl;
+                    continue;
+                }
+            }
+            const int64_t xr = clampl(x + st, 0, nb - 1);
+            if (xr != x) {
+                const double fr = G(xr);
+                if (fr > fx) {
+                    x = xr;
+                    fx = fr;
+                    continue;
+                }
+            }
+            break;
+        }
+    }
+#undef G
+    if (rc == 0) {
+        *out = res[x];
+        out->evaluations = evals;
+        *ib_out = x;
+    }
+    free(res);
+    free(have);
+    return rc;
+}

@@ -122,6 +122,20 @@ int orc_quantify_ex(const orc_sched* s, const orc_grid* lattice, const orc_zoom_
                     const double* fp, const float* dict, int64_t dict_entries, orc_stage* trace,
                     int trace_cap, int* trace_len, orc_quant* out);
 
+/* Four-parameter MRF-ZOOM (BASELINE configs[4]; no reference counterpart --
+ * the reference has no B1 axis, fingerprint.hpp:12-17).  B1 scales every
+ * excitation flip (scheds[ib] = the schedule with flip_deg * b1[ib]; the
+ * inversion stays ideal).  Parameter-separable extension of the reference's
+ * search: an OUTER zoom_1d (zoom.cpp:252-282) over the B1 index, whose
+ * objective g(ib) is the score of the reference's own three-parameter
+ * quantify (zoom.cpp:533-539) under scheds[ib], memoized per ib; steps are
+ * B1-index units (coarse to fine), init_ib the starting index.  The answer
+ * is quantify's result at the chosen ib; evaluations = the inner unique
+ * evaluations summed over the B1 values acquired. */
+int orc_quantify_b1(const orc_sched* scheds, int nb, const orc_grid* lattice, const orc_zoom_cfg* cfg,
+                    const int64_t* steps, int nsteps, int64_t init_ib, const double* fp, orc_quant* out,
+                    int64_t* ib_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -339,6 +339,35 @@ int orc_quantify_ex(const orc_sched* s, const orc_grid* lattice, const orc_zoom_
     });
 }
 
+int orc_quantify_b1(const orc_sched* scheds, int nb, const orc_grid* lattice, const orc_zoom_cfg* cfg,
+                    const int64_t* steps, int nsteps, int64_t init_ib, const double* fp, orc_quant* out,
+                    int64_t* ib_out) {
+    // the reference's own zoom_1d (zoom.cpp:252-282) over the B1 index, its
+    // objective the reference's own quantify under each B1 schedule, memoized
+    return guard([&] {
+        if (nb <= 0) throw std::invalid_argument("quantify_b1: no B1 values");
+        mrf::SearchRanges r{to_range(lattice->t1_ms), to_range(lattice->t2_ms), to_range(lattice->df_hz)};
+        const mrf::ZoomConfig zc = to_cfg(cfg);
+        const mrf::Fingerprint q = to_fp(fp, scheds[0].n);
+        std::vector<mrf::QuantResult> res(static_cast<std::size_t>(nb));
+        std::vector<bool> have(static_cast<std::size_t>(nb), false);
+        std::size_t evals = 0;
+        auto g = [&](long ib) {
+            if (!have[ib]) {
+                res[ib] = mrf::quantify(q, r, zc, to_sched(&scheds[ib]));
+                have[ib] = true;
+                evals += res[ib].evaluations;
+            }
+            return res[ib].score;
+        };
+        std::vector<long> st(steps, steps + nsteps);
+        const long ib = mrf::zoom_1d(g, 0, nb - 1, static_cast<long>(init_ib), st);
+        const mrf::QuantResult& b = res[ib];
+        fill_quant(lattice, b.params.t1 * 1e3, b.params.t2 * 1e3, b.params.df, b.params.pd, b.score, evals, out);
+        *ib_out = ib;
+    });
+}
+
 int orc_quantify_slice(const orc_sched* s, const orc_grid* g, const orc_zoom_cfg* cfg,
                        const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
                        int threads, orc_quant* out) {

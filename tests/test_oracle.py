@@ -259,3 +259,30 @@ def test_golden_exp3_slice(orc):
         assert float(f"{res[v].t1_ms:.9g}") == pytest.approx(d["t1_map"][v], abs=1e-9)
         assert float(f"{res[v].t2_ms:.9g}") == pytest.approx(d["t2_map"][v], abs=1e-9)
         assert float(f"{res[v].df_hz:.9g}") == pytest.approx(d["df_map"][v], abs=1e-9)
+
+
+def test_quantify_b1_vs_reference(orc, ref):
+    """Four-parameter ZOOM (BASELINE configs[4]): the restatement's outer B1
+    zoom_1d over memoized three-parameter quantify equals the composition of
+    the reference's OWN zoom_1d and quantify (oracle/ref_capi.cpp), answer,
+    B1 index, score, PD and summed evaluations."""
+    base = orc.baseline_schedule(200, 1)
+    b1 = [0.7 + 0.1 * k for k in range(7)]
+    scheds = [oracle.Schedule(base.flip_deg * b, base.phase_deg, base.tr_ms, base.te_ms) for b in b1]
+    g = oracle.make_grid((300.0, 25.0, 40), (20.0, 10.0, 30), (-50.0, 5.0, 21))
+    cfg = oracle.zoom_cfg(df_coarse_hz=5, df_refine_hz=5, df_window_hz=20, omega_hz=82,
+                          t1t2_2d_steps_ms=[200, 100], t1t2_1d_steps_ms=[50, 25], final_2d_step_ms=10,
+                          init_t2_ms=100)
+    rng = np.random.default_rng(21)
+    hits = 0
+    for k in range(6):
+        kb = int(rng.integers(0, len(b1)))
+        fp = orc.simulate(scheds[kb], rng.uniform(0.4, 1.2), rng.uniform(0.03, 0.25), rng.uniform(-40, 40))
+        fp = orc.add_noise(fp, float(np.linalg.norm(fp)) / np.sqrt(200) / 25, 700 + k)
+        a, ia = orc.quantify_b1(scheds, g, cfg, fp, [2, 1], 3)
+        b, ib = ref.quantify_b1(scheds, g, cfg, fp, [2, 1], 3)
+        assert (ia, a.i1, a.i2, a.idf, a.score, a.pd, a.evaluations) == \
+               (ib, b.i1, b.i2, b.idf, b.score, b.pd, b.evaluations)
+        per_b1 = [orc.quantify(x, g, cfg, fp).score for x in scheds]
+        hits += a.score == max(per_b1)
+    assert hits >= 5  # the outer walk reaches the best B1 of the inner searches
