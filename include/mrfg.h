@@ -351,6 +351,21 @@ int mrfg_quantify_ex(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_co
 int mrfg_quantify_slice_ex(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
                            const double* fps, const uint8_t* mask, int nx, int ny, int use_prior,
                            const mrfg_zoom_io* io, mrfg_quant* out, double* seconds);
+/* Four-parameter MRF-ZOOM (BASELINE configs[4]; the reference has no B1
+ * axis, fingerprint.hpp:12-17).  ctxs[ib] is a context of the schedule whose
+ * excitation flips are scaled by the ib-th B1 value (same device, same
+ * length).  Per voxel: an outer zoom_1d (zoom.cpp:252-282) over the B1
+ * index -- steps in index units, coarse to fine, from init_ib -- whose
+ * objective is the score of the three-parameter quantify (K5) under
+ * ctxs[ib], memoized per voxel and B1 value.  Rounds of the outer walks run
+ * as one K5 launch per requested B1 value, concurrently (one host thread per
+ * context); the flanks a walk may probe next are evaluated speculatively and
+ * only the probes the walk takes count.  out: quantify's result at the
+ * chosen B1 with evaluations summed over the B1 values the walk acquired;
+ * ib_out: the chosen index.  The oracle is oracle_api.h orc_quantify_b1. */
+int mrfg_quantify_b1(mrfg_ctx* const* ctxs, int nb, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                     const int64_t* steps, int nsteps, int64_t init_ib, const double* fps, int64_t nvox,
+                     mrfg_quant* out, int64_t* ib_out);
 /* mrfg_quantify on device-resident fingerprints (nvox x 2N FP64) and results
  * (async on the ctx stream; t1_ms/t2_ms/df_hz of d_out are left 0 -- the
  * lattice indices are filled). */

@@ -9,10 +9,10 @@ from ._native import LIB_PATH, load  # noqa: F401
 from .dgs import (Context, Schedule, add_noise, baseline_schedule, grid, grid_from_ranges,  # noqa: F401
                   grid_inclusive, grid_total, params_at, reference_schedule, unflatten,
                   zoom_config, calibrate_noise, make_calibrated_noise, smooth, read_header,
-                  save_dictionary, load_dictionary, load_cc_map, grid_values, axis_values)
+                  save_dictionary, load_dictionary, load_cc_map, grid_values, axis_values, quantify_b1)
 
 __all__ = ["Context", "Schedule", "add_noise", "baseline_schedule", "grid", "grid_from_ranges",
            "grid_inclusive", "grid_total", "params_at", "reference_schedule", "unflatten",
            "zoom_config", "load", "LIB_PATH", "dgs", "calibrate_noise", "make_calibrated_noise",
            "smooth", "read_header", "save_dictionary", "load_dictionary", "load_cc_map",
-           "grid_values", "axis_values"]
+           "grid_values", "axis_values", "quantify_b1"]

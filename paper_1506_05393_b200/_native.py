@@ -97,7 +97,7 @@ EXPORTS = [
     "mrfg_merge_matches_dev", "mrfg_screen_scores", "mrfg_cc_map", "mrfg_quantify", "mrfg_quantify_slice", "mrfg_quantify_bounded",
     "mrfg_quantify_dev", "mrfg_cc_map_ex", "mrfg_save_generated", "mrfg_cc_map_to_file",
     "mrfg_write_header", "mrfg_read_header", "mrfg_calibrate_noise", "mrfg_make_calibrated_noise",
-    "mrfg_smooth", "mrfg_quantify_ex", "mrfg_quantify_slice_ex",
+    "mrfg_smooth", "mrfg_quantify_ex", "mrfg_quantify_slice_ex", "mrfg_quantify_b1",
 ]
 
 _lib = None
@@ -169,6 +169,8 @@ def load() -> C.CDLL:
     L.mrfg_quantify_slice.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp,
                                       C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int,
                                       C.POINTER(Quant), dp]
+    L.mrfg_quantify_b1.argtypes = [C.POINTER(vp), C.c_int, C.POINTER(Grid), C.POINTER(ZoomConfig),
+                                   C.POINTER(i64), C.c_int, i64, dp, i64, C.POINTER(Quant), C.POINTER(i64)]
     L.mrfg_quantify_ex.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp, i64,
                                    C.POINTER(i64), dp, C.POINTER(ZoomIo), C.POINTER(Quant)]
     L.mrfg_quantify_slice_ex.argtypes = [vp, C.POINTER(Grid), C.POINTER(ZoomConfig), dp,

@@ -1296,6 +1296,152 @@ int mrfg_quantify_ex(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_conf
     });
 }
 
+int mrfg_quantify_b1(mrfg_ctx* const* ctxs, int nb, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
+                     const int64_t* steps, int nsteps, int64_t init_ib, const double* fps, int64_t nvox,
+                     mrfg_quant* out, int64_t* ib_out) {
+    return guard([&] {
+        MRFG_REQUIRE(nb > 0 && ctxs, MRFG_E_INVALID, "quantify_b1: no B1 values");
+        MRFG_REQUIRE(nvox >= 0, MRFG_E_INVALID, "quantify: negative voxel count");
+        for (int k = 0; k < nsteps; ++k)
+            MRFG_REQUIRE(steps[k] > 0, MRFG_E_INVALID, "zoom_1d: step must be positive");  // zoom.cpp:258
+        const int64_t n = ctxs[0]->c.n;
+        for (int k = 0; k < nb; ++k)
+            MRFG_REQUIRE(ctxs[k] && ctxs[k]->c.n == n && ctxs[k]->c.device == ctxs[0]->c.device, MRFG_E_INVALID,
+                         "quantify_b1: contexts differ in length or device");
+        if (nvox == 0) return;
+        const int64_t n2 = 2 * n;
+        auto clampi = [&](int64_t v) { return v < 0 ? int64_t(0) : (v >= nb ? int64_t(nb - 1) : v); };
+        // per-voxel memo of the inner searches and the outer walk's state
+        std::vector<mrfg_quant> res(static_cast<size_t>(nvox * nb));
+        std::vector<uint8_t> have(static_cast<size_t>(nvox * nb), 0), acq(static_cast<size_t>(nvox * nb), 0);
+        struct Walk {
+            int64_t x = 0;
+            double fx = 0;
+            int si = 0, phase = 0;  // 0 start, 1 left flank, 2 right flank, 3 done
+            int64_t evals = 0;
+        };
+        std::vector<Walk> w(static_cast<size_t>(nvox));
+        for (auto& v : w) v.x = clampi(init_ib);
+        // g(ib) in the walk's order: the first read acquires (counts) the value
+        auto read = [&](int64_t v, int64_t ib) {
+            const size_t k = static_cast<size_t>(v * nb + ib);
+            if (!acq[k]) {
+                acq[k] = 1;
+                w[v].evals += res[k].evaluations;
+            }
+            return res[k].score;
+        };
+        // advance voxel v's walk (zoom.cpp:252-282) as far as the memo allows;
+        // returns the B1 indices it needs next (first: the one it waits on)
+        auto advance = [&](int64_t v, std::vector<int64_t>& need) {
+            Walk& s = w[v];
+            auto ready = [&](int64_t ib) { return have[static_cast<size_t>(v * nb + ib)] != 0; };
+            for (;;) {
+                if (s.phase == 0) {
+                    if (!ready(s.x)) {
+                        need.push_back(s.x);
+                        if (nsteps) {  // speculative: the first step's flanks
+                            need.push_back(clampi(s.x - steps[0]));
+                            need.push_back(clampi(s.x + steps[0]));
+                        }
+                        return;
+                    }
+                    s.fx = read(v, s.x);
+                    s.phase = 1;
+                }
+                if (s.si >= nsteps) {
+                    s.phase = 3;
+                    return;
+                }
+                const int64_t st = steps[s.si];
+                if (s.phase == 1) {
+                    const int64_t xl = clampi(s.x - st);
+                    if (xl != s.x) {
+                        if (!ready(xl)) {
+                            need.push_back(xl);
+                            need.push_back(clampi(s.x + st));  // speculative: the right flank
+                            return;
+                        }
+                        const double fl = read(v, xl);
+                        if (fl > s.fx) {
+                            s.x = xl;
+                            s.fx = fl;
+                            continue;
+                        }
+                    }
+                    s.phase = 2;
+                }
+                const int64_t xr = clampi(s.x + st);
+                if (xr != s.x) {
+                    if (!ready(xr)) {
+                        need.push_back(xr);
+                        return;
+                    }
+                    const double fr = read(v, xr);
+                    if (fr > s.fx) {
+                        s.x = xr;
+                        s.fx = fr;
+                        s.phase = 1;
+                        continue;
+                    }
+                }
+                s.phase = 1;
+                ++s.si;
+            }
+        };
+        std::vector<std::vector<int64_t>> group(static_cast<size_t>(nb));
+        for (;;) {
+            for (auto& g : group) g.clear();
+            bool any = false;
+            std::vector<int64_t> need;
+            for (int64_t v = 0; v < nvox; ++v) {
+                if (w[v].phase == 3) continue;
+                need.clear();
+                advance(v, need);
+                for (int64_t ib : need)
+                    if (!have[static_cast<size_t>(v * nb + ib)] &&
+                        (group[ib].empty() || group[ib].back() != v)) {
+                        group[ib].push_back(v);
+                        any = true;
+                    }
+            }
+            if (!any) break;
+            // one K5 launch per requested B1 value, concurrently
+            std::vector<std::thread> th;
+            std::vector<int> rc(static_cast<size_t>(nb), 0);
+            std::vector<std::string> msg(static_cast<size_t>(nb));
+            for (int ib = 0; ib < nb; ++ib) {
+                if (group[ib].empty()) continue;
+                th.emplace_back([&, ib] {
+                    const auto& vs = group[ib];
+                    std::vector<double> packed(static_cast<size_t>(n2) * vs.size());
+                    for (size_t k = 0; k < vs.size(); ++k)
+                        std::memcpy(&packed[n2 * k], fps + n2 * vs[k], sizeof(double) * n2);
+                    std::vector<mrfg_quant> r(vs.size());
+                    rc[ib] = mrfg_quantify_ex(ctxs[ib], lattice, cfg, packed.data(), static_cast<int64_t>(vs.size()),
+                                              nullptr, nullptr, nullptr, r.data());
+                    if (rc[ib]) {
+                        msg[ib] = g_err;
+                        return;
+                    }
+                    for (size_t k = 0; k < vs.size(); ++k) {
+                        res[static_cast<size_t>(vs[k] * nb + ib)] = r[k];
+                        have[static_cast<size_t>(vs[k] * nb + ib)] = 1;
+                    }
+                });
+            }
+            for (auto& t : th) t.join();
+            for (int ib = 0; ib < nb; ++ib)
+                if (rc[ib]) throw Error{rc[ib], msg[ib]};
+        }
+        for (int64_t v = 0; v < nvox; ++v) {
+            out[v] = res[static_cast<size_t>(v * nb + w[v].x)];
+            out[v].evaluations = w[v].evals;
+            ib_out[v] = w[v].x;
+        }
+    });
+}
+
 int mrfg_quantify_bounded(mrfg_ctx* h, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,
                           const double* fps, int64_t nvox, const int64_t* bounds,
                           const double* init_ms, mrfg_quant* out) {

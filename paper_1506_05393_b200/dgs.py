@@ -561,6 +561,24 @@ class Context:
         return res, secs.value
 
 
+def quantify_b1(contexts, fps, lattice: Grid, cfg: ZoomConfig = None, steps=(4, 1), init_ib: int = 0):
+    """Four-parameter MRF-ZOOM (BASELINE configs[4]): contexts[ib] holds the
+    schedule with flips scaled by the ib-th B1 value; an outer zoom_1d over
+    the B1 index (steps in index units) of the three-parameter quantify
+    (mrfg_quantify_b1).  Returns (Quant records, chosen B1 indices)."""
+    q = np.ascontiguousarray(np.atleast_2d(fps), dtype=np.complex128)
+    cfg = cfg or zoom_config()
+    hs = (C.c_void_p * len(contexts))(*[c.h for c in contexts])
+    st = np.ascontiguousarray(steps, dtype=np.int64)
+    out = (Quant * q.shape[0])()
+    ib = np.zeros(q.shape[0], dtype=np.int64)
+    check(N.load().mrfg_quantify_b1(hs, len(contexts), C.byref(lattice), C.byref(cfg),
+                                    st.ctypes.data_as(C.POINTER(C.c_int64)), len(st), int(init_ib),
+                                    _dp(q.view(np.float64)), q.shape[0], out,
+                                    ib.ctypes.data_as(C.POINTER(C.c_int64))))
+    return quant_array(out), ib
+
+
 QUANT_DTYPE = np.dtype([("i1", np.int64), ("i2", np.int64), ("idf", np.int64),
                         ("t1_ms", np.float64), ("t2_ms", np.float64), ("df_hz", np.float64),
                         ("pd", np.float64), ("score", np.float64), ("evaluations", np.int64)])

@@ -194,6 +194,18 @@ CONFIG5 = dict(n=3000, nvox=128 * 128, snr=25.0, b1=[round(0.7 + 0.05 * k, 10) f
                t1=(100.0, 3000.0, 25.0), t2=(20.0, 500.0, 10.0), df=(-100.0, 100.0, 10.0))
 
 
+# Four-parameter ZOOM on the config-5 lattice (T1 25 ms, T2 10 ms, df 10 Hz,
+# B1 0.05): the three-parameter stages in lattice units (df coarse 1, omega
+# 8; 2-D steps 8/4 x 20/10; 1-D 2/1 x 5/3; final 1 x 1), T2 started at
+# 100 ms (the axis ends at 500 ms), and the outer B1 walk from B1 = 1.0
+# (index 6) in steps of 0.2 then 0.05 (4, 1 index units).
+CONFIG5_ZOOM = dict(df_coarse_hz=10.0, df_refine_hz=10.0, df_window_hz=20.0, omega_hz=82.0,
+                    t1t2_2d_steps_ms=[200.0, 100.0], t1t2_1d_steps_ms=[50.0, 25.0], final_2d_step_ms=10.0,
+                    init_t2_ms=100.0)
+CONFIG5_B1_STEPS = (4, 1)
+CONFIG5_B1_INIT = 6
+
+
 def config5_schedules():
     base = dgs.baseline_schedule(CONFIG5["n"], 1)
     return [dgs.Schedule(base.flip_deg * b, base.phase_deg, base.tr_ms, base.te_ms) for b in CONFIG5["b1"]]

@@ -21,8 +21,10 @@ REFERENCE LIBRARY's own:
   the CONFIG4_ZOOM settings, without and with priors (strict raster).
 * c5: BASELINE configs[4], 13 B1 schedules x 117 x 49 x 21, N = 3000; 128 of
   the 16,384 voxels; per-B1 argmax then max over B1 (ties: lower B1).
+* c5z: the same 128 voxels through four-parameter ZOOM (CONFIG5_ZOOM; the
+  reference's zoom_1d over B1 of the reference's quantify).
 
-Usage: python tests/golden/make_scale_fixtures.py {c2,c3,c4,c5} [threads]
+Usage: python tests/golden/make_scale_fixtures.py {c2,c3,c4,c5,c5z} [threads]
 """
 import json
 import os
@@ -124,11 +126,35 @@ def run_c5(ref, threads):
     return dict(voxels=vox, flat=best_f, score=best_s, seconds=time.time() - t0)
 
 
+def run_c5z(ref, threads):
+    """Four-parameter ZOOM on the config-5 lattice: the reference's own zoom_1d
+    over the B1 index of its own quantify (oracle/ref_capi.cpp
+    orc_quantify_b1), 128 voxels, voxel-parallel."""
+    import concurrent.futures as cf
+    vox = np.linspace(0, workloads.CONFIG5["nvox"] - 1, 128).astype(np.int64)
+    scheds, g, idx, fps = workloads.config5_voxels(sim, vox)
+    og = oracle.make_grid((g.t1_ms.min, g.t1_ms.step, g.t1_ms.count), (g.t2_ms.min, g.t2_ms.step, g.t2_ms.count),
+                          (g.df_hz.min, g.df_hz.step, g.df_hz.count))
+    cfg = oracle.zoom_cfg(**workloads.CONFIG5_ZOOM)
+    os_ = [osched(x) for x in scheds]
+    t0 = time.time()
+
+    def one(k):
+        return ref.quantify_b1(os_, og, cfg, fps[k], list(workloads.CONFIG5_B1_STEPS), workloads.CONFIG5_B1_INIT)
+    with cf.ThreadPoolExecutor(threads) as ex:
+        r = list(ex.map(one, range(len(vox))))
+    return dict(voxels=vox, ib=np.array([b for _, b in r], dtype=np.int64),
+                ijk=np.array([[q.i1, q.i2, q.idf] for q, _ in r], dtype=np.int64),
+                score=np.array([q.score for q, _ in r]), pd=np.array([q.pd for q, _ in r]),
+                evals=np.array([q.evaluations for q, _ in r], dtype=np.int64), truth=idx,
+                seconds=time.time() - t0)
+
+
 def main():
     which = sys.argv[1]
     threads = int(sys.argv[2]) if len(sys.argv) > 2 else (os.cpu_count() or 1)
     ref = oracle.Oracle("reference")
-    out = {"c2": run_c2, "c3": run_c3, "c4": run_c4, "c5": run_c5}[which](ref, threads)
+    out = {"c2": run_c2, "c3": run_c3, "c4": run_c4, "c5": run_c5, "c5z": run_c5z}[which](ref, threads)
     out["threads"] = threads
     np.savez_compressed(os.path.join(HERE, f"scale_{which}.npz"), **out)
     print(json.dumps({k: (v if np.isscalar(v) else f"array{np.shape(v)}") for k, v in out.items()}))

@@ -144,3 +144,25 @@ def test_exp3_golden_slice_on_gpu(orc, prior):
     for key, mp in (("t1_ms", d["t1_map"]), ("t2_ms", d["t2_map"]), ("df_hz", d["df_map"])):
         got = np.array([float(f"{x:.9g}") for x in q[key][m]])
         np.testing.assert_allclose(got, mp[m], rtol=0, atol=1e-9)
+
+
+def test_config5_four_parameter_zoom_vs_reference(orc):
+    """BASELINE configs[4] ZOOM: four-parameter MRF-ZOOM (outer zoom_1d over
+    the 13 B1 values of K5's three-parameter quantify, N = 3000) on 128 voxels
+    against the composition of the reference's own zoom_1d and quantify
+    (tests/golden/scale_c5z.npz): B1 index, lattice point, score, PD and
+    summed evaluations."""
+    d = load("scale_c5z.npz")
+    scheds, g, idx, fps = workloads.config5_voxels(oracle_sim(orc), d["voxels"])
+    cfg = P.zoom_config(**workloads.CONFIG5_ZOOM)
+    ctxs = [P.Context(s) for s in scheds]
+    try:
+        q, ib = P.quantify_b1(ctxs, fps, g, cfg, workloads.CONFIG5_B1_STEPS, workloads.CONFIG5_B1_INIT)
+    finally:
+        for c in ctxs:
+            c.close()
+    np.testing.assert_array_equal(ib, d["ib"])
+    np.testing.assert_array_equal(np.stack([q["i1"], q["i2"], q["idf"]], 1), d["ijk"])
+    np.testing.assert_array_equal(q["score"], d["score"])
+    np.testing.assert_array_equal(q["pd"], d["pd"])
+    np.testing.assert_array_equal(q["evaluations"], d["evals"])

@@ -386,3 +386,43 @@ def test_zoom_slice_traces(orc, prior):
                     assert res[k][v] == h[k][0], (v, k)
                 assert tr[v] == th[0]
                 prev = v
+
+
+def test_zoom_four_parameter_b1(orc):
+    """Four-parameter ZOOM (mrfg_quantify_b1): the outer B1 walk over K5's
+    three-parameter quantify equals the oracle restatement (itself pinned to
+    the reference's zoom_1d + quantify): B1 index, point, score, PD,
+    evaluations; with one B1 value it is plain quantify."""
+    base = P.baseline_schedule(200, 1)
+    b1 = [0.7 + 0.1 * k for k in range(7)]
+    scheds = [P.Schedule(base.flip_deg * b, base.phase_deg, base.tr_ms, base.te_ms) for b in b1]
+    g = P.grid((300.0, 25.0, 40), (20.0, 10.0, 30), (-50.0, 5.0, 21))
+    kw = dict(df_coarse_hz=5, df_refine_hz=5, df_window_hz=20, omega_hz=82, t1t2_2d_steps_ms=[200, 100],
+              t1t2_1d_steps_ms=[50, 25], final_2d_step_ms=10, init_t2_ms=100)
+    cfg = P.zoom_config(**kw)
+    rng = np.random.default_rng(21)
+    fps = []
+    for k in range(12):
+        kb = int(rng.integers(0, len(b1)))
+        fp = orc.simulate(to_oracle_sched(scheds[kb]), rng.uniform(0.4, 1.2), rng.uniform(0.03, 0.25),
+                          rng.uniform(-40, 40))
+        fps.append(orc.add_noise(fp, float(np.linalg.norm(fp)) / np.sqrt(200) / 25, 700 + k))
+    fps = np.stack(fps)
+    ctxs = [P.Context(s) for s in scheds]
+    try:
+        q, ib = P.quantify_b1(ctxs, fps, g, cfg, (2, 1), 3)
+        q1, ib1 = P.quantify_b1(ctxs[2:3], fps, g, cfg, (2, 1), 0)
+        plain = ctxs[2].quantify(fps, g, cfg)
+    finally:
+        for c in ctxs:
+            c.close()
+    os_ = [to_oracle_sched(s) for s in scheds]
+    ocf = ocfg(cfg)
+    og = to_oracle_grid(g)
+    for v, fp in enumerate(fps):
+        w, wb = orc.quantify_b1(os_, og, ocf, fp, [2, 1], 3)
+        assert (ib[v], q["i1"][v], q["i2"][v], q["idf"][v]) == (wb, w.i1, w.i2, w.idf), v
+        assert (q["score"][v], q["pd"][v], q["evaluations"][v]) == (w.score, w.pd, w.evaluations), v
+    assert (ib1 == 0).all()
+    for k in ("i1", "i2", "idf", "score", "pd", "evaluations"):
+        np.testing.assert_array_equal(q1[k], plain[k])
