@@ -165,6 +165,18 @@ const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
     up(t.e2f, e2f.data(), e2f.size() * 4);
     up(t.phf, phf.data(), phf.size() * 4);
     up(t.stepu, su.data(), su.size() * sizeof(StepU));
+    // x-axis schedules: the K5 screening step rows, 2 x float4 per step:
+    // (r4, r5, r7, r8) -- the RF entries that are not 0 or 1 -- and the
+    // one-df-step phasors (wtc, wts, wrc, wrs)
+    if (c.rf_xaxis) {
+        std::vector<float> sx(8 * n);
+        for (int64_t j = 0; j < n; ++j) {
+            const StepU& u = su[j];
+            const float v[8] = {u.r[4], u.r[5], u.r[7], u.r[8], u.wtc, u.wts, u.wrc, u.wrs};
+            std::memcpy(&sx[8 * j], v, sizeof v);
+        }
+        up(t.stepx, sx.data(), sx.size() * 4);
+    }
     // K1 row producers: log2(e)/T per lattice index (ex2 arguments), FP64 -> FP32
     std::vector<float> kt(n1 + n2);
     for (int64_t i = 0; i < n1; ++i) kt[i] = static_cast<float>(1.4426950408889634 / (axis_value(g.t1_ms, i) * 1e-3));

@@ -90,6 +90,7 @@ struct GridTables {
     std::vector<double> v1, v2;  // explicit T1/T2 values of the cached grid (empty: evenly spaced)
     DevBuf kt;  // float log2(e)/T1 [n1] then log2(e)/T2 [n2], 1/s (K1 row producers)
     DevBuf stepu;  // n x StepU
+    DevBuf stepx;  // x-axis schedules: n x 2 float4 (r4, r5, r7, r8), (wtc, wts, wrc, wrs) (K5 screening)
     bool valid = false;
     // Parameter-major (lattice index i, step j):
     // FP32: e1[i*n+j] = (E1te, 1-E1te, E1rest, 1-E1rest); e2[i*n+j] = (E2te, E2rest);

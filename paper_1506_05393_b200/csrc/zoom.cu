@@ -26,6 +26,17 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     P.e2d = t.e2d.as<double>();
     P.phd = t.phd.as<double>();
     P.su = t.stepu.as<float4>();
+    // x-axis screening rows (FP32 screening only: the exact FP64 walk keeps
+    // the full matrices, the MUFU and smoothing screens the StepU rows);
+    // MRFG_ZOOM_XR=0 forces the general rows
+    {
+        const char* xe = std::getenv("MRFG_ZOOM_XR");
+        const char* sm = std::getenv("MRFG_ZOOM_SCREEN");
+        P.xr = c.rf_xaxis && t.stepx.p && cfg.smooth_k == 0 && !(sm && std::string(sm) == "mufu") &&
+               !(xe && std::atoi(xe) == 0);
+        P.sut = P.xr ? t.stepx.as<float4>() : P.su;
+        P.sus = P.xr ? 2 : 4;
+    }
     P.e1f = t.e1f.as<float4>();
     P.e2f = t.e2f.as<float2>();
     P.phf = t.phf.as<float4>();
@@ -98,6 +109,8 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
         P.spec2d_cta = c2 ? std::max(1, std::atoi(c2)) : (e2 ? P.spec2d : 2);
         const char* sm = std::getenv("MRFG_ZOOM_SCREEN");
         const std::string smode = sm ? sm : "";
+        // (a third variant -- E1/E2 by MUFU.EX2, phasor rows streamed --
+        // measured 83 vs 65 ms on config 4 with 8x the screening error: dropped)
         P.screen_mode = smode == "mufu" ? 1 : 0;
         const char* ee = std::getenv("MRFG_ZOOM_EPS");
         P.eps = ee ? std::atof(ee) : 1e-5;
@@ -142,8 +155,9 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     };
     const int bsk = rows ? 32 * row_w : bs;
     // shared staging: StepU rows (64 B/step) + one FP32 query per warp (8 B/step)
-    size_t smem = rows ? sizeof(StepU) * c.n + sizeof(float2) * c.n + sizeof(ZItem) * kQCap + 16
-                       : (sizeof(StepU) + sizeof(float2) * (bsk / 32)) * c.n;
+    const size_t row_bytes = sizeof(float4) * P.sus;  // staged screening step row
+    size_t smem = rows ? row_bytes * c.n + sizeof(float2) * c.n + sizeof(ZItem) * kQCap + 16
+                       : (row_bytes + sizeof(float2) * (bsk / 32)) * c.n;
     const char* st_env = std::getenv("MRFG_ZOOM_SMEM");
     P.smem_stage = smem <= 200 * 1024 && !(st_env && std::atoi(st_env) == 0) ? 1 : 0;
     // rows mode keeps its shared layout (the helper-warp queue follows the

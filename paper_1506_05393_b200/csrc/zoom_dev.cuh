@@ -75,6 +75,11 @@ struct ZParams {
     // tables
     const double *rf, *e1d, *e2d, *phd;
     const float4 *su, *e1f, *phf;  // su: StepU rows (RF rotation, te, rest, one-df-step phasor)
+    // screening step rows (staged in shared memory): su (sus = 4 float4 per
+    // step), or for x-axis schedules (xr) the compact rows (r4, r5, r7, r8),
+    // (wtc, wts, wrc, wrs) (sus = 2)
+    const float4* sut;
+    int sus, xr;
     const float2* e2f;
     double inv0[3];
     int n;
@@ -398,6 +403,20 @@ __device__ __forceinline__ void zstep32(const float4 ra, const float4 rb, const 
     zz = fmaf(zz, e1.z, e1.w);
 }
 
+// x-axis pulses: RF = [[1,0,0],[0,r4,r5],[0,r7,r8]] (rx = (r4, r5, r7, r8)):
+// 4 FFMA instead of 9; the rest as zstep32.
+__device__ __forceinline__ void zstep32x(const float4 rx, const float2 qq, const float4 e1, const float2 e2,
+                                         const float4 ph, float& x, float& y, float& zz, zf2& pq, zf2& pn) {
+    const float ny = fmaf(rx.x, y, rx.y * zz);
+    const float nz = fmaf(rx.z, y, rx.w * zz);
+    const zf2 v = zmul2(zcmul(zpk(x, ny), ph.x, ph.y), zpk(e2.x, e2.x));
+    zz = fmaf(nz, e1.x, e1.y);
+    pq = zcmac(v, qq.x, -qq.y, pq);
+    pn = zfma2(v, v, pn);
+    zup(zmul2(zcmul(v, ph.z, ph.w), zpk(e2.y, e2.y)), x, y);
+    zz = fmaf(zz, e1.z, e1.w);
+}
+
 // Parameter-major tables: the walk streams n consecutive entries per lane
 // (rows warp-uniform where the lanes share T1, T2 or df).  The per-step
 // uniform operands (StepU rows, query) come from shared memory (SMEM) or
@@ -406,9 +425,10 @@ __device__ __forceinline__ void zstep32(const float4 ra, const float4 rb, const 
 // runs whole 8-step pairs without guards (per-block pointers, immediate
 // offsets; the tables carry tail padding for the last look-ahead), a guarded
 // loop finishes n % 8 steps.
-template <bool SMEM>
+template <bool SMEM, bool XR>
 __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
     constexpr int kB = 4;
+    constexpr int S = XR ? 2 : 4;  // float4 per step row
     const ZParams& P = *z.p;
     const int n = P.n;
     const float4* __restrict__ e1p = P.e1f + static_cast<int64_t>(i1) * n;
@@ -416,7 +436,7 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
     const float4* __restrict__ php = P.phf + static_cast<int64_t>(idf) * n;
     extern __shared__ float4 zsm[];
     const float4* rfp = SMEM ? zsm : z.rfs;
-    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + 4 * n) +
+    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + S * n) +
                                  (z.cta_w ? 0 : static_cast<int>(threadIdx.x / 32)) * n
                            : z.q32;
     float x = static_cast<float>(P.inv0[0]), y = static_cast<float>(P.inv0[1]),
@@ -449,8 +469,12 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
     auto run = [&](const float4* E1, const float2* E2, const float4* PH, const float4* r, const float2* qb) {
         zf2 pq = zpk(0.f, 0.f), pn = zpk(0.f, 0.f);
 #pragma unroll
-        for (int m = 0; m < kB; ++m)
-            zstep32(r[4 * m], r[4 * m + 1], r[4 * m + 2], qb[m], E1[m], E2[m], PH[m], x, y, zz, pq, pn);
+        for (int m = 0; m < kB; ++m) {
+            if (XR)
+                zstep32x(r[S * m], qb[m], E1[m], E2[m], PH[m], x, y, zz, pq, pn);
+            else
+                zstep32(r[S * m], r[S * m + 1], r[S * m + 2], qb[m], E1[m], E2[m], PH[m], x, y, zz, pq, pn);
+        }
         fold(pq, pn);
     };
     const int nmain = n & ~(2 * kB - 1);
@@ -464,15 +488,19 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
             prefetch_l1(e2p + jb + 32);
         }
         load(B1, B2, BP, e1p + jb + kB, e2p + jb + kB, php + jb + kB);
-        run(A1, A2, AP, rfp + 4 * jb, q + jb);
+        run(A1, A2, AP, rfp + S * jb, q + jb);
         load(A1, A2, AP, e1p + jb + 2 * kB, e2p + jb + 2 * kB, php + jb + 2 * kB);
-        run(B1, B2, BP, rfp + 4 * (jb + kB), q + jb + kB);
+        run(B1, B2, BP, rfp + S * (jb + kB), q + jb + kB);
     }
     {  // tail: n % 8 steps
         zf2 pq = zpk(0.f, 0.f), pn = zpk(0.f, 0.f);
-        for (int j = nmain; j < n; ++j)
-            zstep32(rfp[4 * j], rfp[4 * j + 1], rfp[4 * j + 2], q[j], __ldg(e1p + j), __ldg(e2p + j),
-                    __ldg(php + j), x, y, zz, pq, pn);
+        for (int j = nmain; j < n; ++j) {
+            if (XR)
+                zstep32x(rfp[S * j], q[j], __ldg(e1p + j), __ldg(e2p + j), __ldg(php + j), x, y, zz, pq, pn);
+            else
+                zstep32(rfp[S * j], rfp[S * j + 1], rfp[S * j + 2], q[j], __ldg(e1p + j), __ldg(e2p + j),
+                        __ldg(php + j), x, y, zz, pq, pn);
+        }
         fold(pq, pn);
     }
     const double inv = rsqrt(nn);
@@ -489,9 +517,10 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
 struct Apx2 {
     Apx a, b;
 };
-template <bool SMEM>
+template <bool SMEM, bool XR>
 __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
     constexpr int kB = 2;
+    constexpr int S = XR ? 2 : 4;  // float4 per step row
     const ZParams& P = *z.p;
     const int n = P.n;
     const float4* __restrict__ e1p = P.e1f + static_cast<int64_t>(i1) * n;
@@ -499,7 +528,7 @@ __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
     const float4* __restrict__ php = P.phf + static_cast<int64_t>(idf) * n;
     extern __shared__ float4 zsm[];
     const float4* rfp = SMEM ? zsm : z.rfs;
-    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + 4 * n) +
+    const float2* q = SMEM ? reinterpret_cast<const float2*>(zsm + S * n) +
                                  (z.cta_w ? 0 : static_cast<int>(threadIdx.x / 32)) * n
                            : z.q32;
     const float x0 = static_cast<float>(P.inv0[0]), y0 = static_cast<float>(P.inv0[1]),
@@ -525,8 +554,18 @@ __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
     // one step of both points; w = (wtc, wts) for te, (wrc, wrs) for rest: rc.w, rd.x, rd.y, rd.z
     auto step2 = [&](const float4* r, const float2 qq, const float4 e1, const float2 e2, const float4 pa, zf2& pra,
                      zf2& pna, zf2& prb, zf2& pnb) {
-        const float4 ra = r[0], rb = r[1], rc = r[2], rd = r[3];
         float4 pb;
+        if (XR) {  // r[0] = (r4, r5, r7, r8), r[1] = (wtc, wts, wrc, wrs)
+            const float4 rx = r[0], w = r[1];
+            pb.x = fmaf(pa.x, w.x, -pa.y * w.y);
+            pb.y = fmaf(pa.y, w.x, pa.x * w.y);
+            pb.z = fmaf(pa.z, w.z, -pa.w * w.w);
+            pb.w = fmaf(pa.w, w.z, pa.z * w.w);
+            zstep32x(rx, qq, e1, e2, pa, xa, ya, za, pra, pna);
+            zstep32x(rx, qq, e1, e2, pb, xb, yb, zb, prb, pnb);
+            return;
+        }
+        const float4 ra = r[0], rb = r[1], rc = r[2], rd = r[3];
         pb.x = fmaf(pa.x, rc.w, -pa.y * rd.x);
         pb.y = fmaf(pa.y, rc.w, pa.x * rd.x);
         pb.z = fmaf(pa.z, rd.y, -pa.w * rd.z);
@@ -550,7 +589,7 @@ __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
     auto run = [&](const float4* E1, const float2* E2, const float4* PH, const float4* r, const float2* qb) {
         zf2 pra = zpk(0.f, 0.f), pna = pra, prb = pra, pnb = pra;
 #pragma unroll
-        for (int m = 0; m < kB; ++m) step2(r + 4 * m, qb[m], E1[m], E2[m], PH[m], pra, pna, prb, pnb);
+        for (int m = 0; m < kB; ++m) step2(r + S * m, qb[m], E1[m], E2[m], PH[m], pra, pna, prb, pnb);
         fold(pra, pna, prb, pnb);
     };
     const int nmain = n & ~(2 * kB - 1);
@@ -562,14 +601,14 @@ __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
             if ((jb & 15) == 0) prefetch_l1(e2p + jb + 32);
         }
         load(B1, B2, BP, e1p + jb + kB, e2p + jb + kB, php + jb + kB);
-        run(A1, A2, AP, rfp + 4 * jb, q + jb);
+        run(A1, A2, AP, rfp + S * jb, q + jb);
         load(A1, A2, AP, e1p + jb + 2 * kB, e2p + jb + 2 * kB, php + jb + 2 * kB);
-        run(B1, B2, BP, rfp + 4 * (jb + kB), q + jb + kB);
+        run(B1, B2, BP, rfp + S * (jb + kB), q + jb + kB);
     }
     {  // tail: n % 4 steps
         zf2 pra = zpk(0.f, 0.f), pna = pra, prb = pra, pnb = pra;
         for (int j = nmain; j < n; ++j)
-            step2(rfp + 4 * j, q[j], __ldg(e1p + j), __ldg(e2p + j), __ldg(php + j), pra, pna, prb, pnb);
+            step2(rfp + S * j, q[j], __ldg(e1p + j), __ldg(e2p + j), __ldg(php + j), pra, pna, prb, pnb);
         fold(pra, pna, prb, pnb);
     }
     Apx2 r;
@@ -722,7 +761,8 @@ __device__ __forceinline__ Apx zsim32(const Z& z, int i1, int i2, int idf) {
     const int m = z.p->screen_mode;
     if (z.p->smooth_k) return zsim32_smooth(z, i1, i2, idf);
     if (m == 1) return zsim32_mufu(z, i1, i2, idf);
-    return z.p->smem_stage ? zsim32_tab<true>(z, i1, i2, idf) : zsim32_tab<false>(z, i1, i2, idf);
+    if (z.p->xr) return z.p->smem_stage ? zsim32_tab<true, true>(z, i1, i2, idf) : zsim32_tab<false, true>(z, i1, i2, idf);
+    return z.p->smem_stage ? zsim32_tab<true, false>(z, i1, i2, idf) : zsim32_tab<false, false>(z, i1, i2, idf);
 }
 
 // ---------------------------------------------------------- helper warps
@@ -929,7 +969,8 @@ __device__ void zdo_pair(Z& z, int s0, int s1, int i1, int i2, int idf0) {
     const ZParams& P = *z.p;
     // only row idf0 is read (the second point's phasor comes from the ladder)
     const int c0 = static_cast<int>(clampll(idf0, 0, P.L.ndf - 1));
-    const Apx2 v = P.smem_stage ? zsim32_df2<true>(z, i1, i2, c0) : zsim32_df2<false>(z, i1, i2, c0);
+    const Apx2 v = P.xr ? (P.smem_stage ? zsim32_df2<true, true>(z, i1, i2, c0) : zsim32_df2<false, true>(z, i1, i2, c0))
+                        : (P.smem_stage ? zsim32_df2<true, false>(z, i1, i2, c0) : zsim32_df2<false, false>(z, i1, i2, c0));
     const int sl[2] = {s0, s1};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -1717,12 +1758,12 @@ __device__ void zwarp_setup(Z& z, const ZParams& P, int64_t w) {
     z.ctl = nullptr;
     extern __shared__ float4 zsm[];
     if (P.smem_stage) {
-        for (int i = threadIdx.x; i < 4 * P.n; i += blockDim.x) zsm[i] = P.su[i];
+        for (int i = threadIdx.x; i < P.sus * P.n; i += blockDim.x) zsm[i] = P.sut[i];
         __syncthreads();
         z.rfs = zsm;
-        z.q32 = reinterpret_cast<float2*>(zsm + 4 * P.n) + z.qw * P.n;
+        z.q32 = reinterpret_cast<float2*>(zsm + P.sus * P.n) + z.qw * P.n;
     } else {
-        z.rfs = P.su;
+        z.rfs = P.sut;
         z.q32 = P.q32 + w * P.n;
     }
 }
@@ -1787,12 +1828,12 @@ __global__ void __launch_bounds__(BS, 1) k_zoom_rows(const ZParams P) {
     extern __shared__ float4 zsm[];
     z.qw = 0;
     if (P.smem_stage)
-        z.q32 = reinterpret_cast<float2*>(zsm + 4 * P.n);
+        z.q32 = reinterpret_cast<float2*>(zsm + P.sus * P.n);
     else
         z.q32 = P.q32 + ctrl * P.n;
     if (W > 1) {
         z.cta_w = W;
-        z.queue = reinterpret_cast<ZItem*>(reinterpret_cast<float2*>(zsm + 4 * P.n) + P.n);
+        z.queue = reinterpret_cast<ZItem*>(reinterpret_cast<float2*>(zsm + P.sus * P.n) + P.n);
         z.ctl = reinterpret_cast<int*>(z.queue + kQCap);
     }
     if (r >= P.nrows) return;  // whole block
