@@ -193,6 +193,14 @@ const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
     return t;
 }
 
+// dst[k] = src[idx[k]] for rows of `row` doubles (K5 voxel groups)
+__global__ void k_gather_rows(const double* __restrict__ src, const int64_t* __restrict__ idx, int64_t row,
+                              double* __restrict__ dst) {
+    const double* s = src + idx[blockIdx.x] * row;
+    double* d = dst + static_cast<int64_t>(blockIdx.x) * row;
+    for (int64_t t = threadIdx.x; t < row; t += blockDim.x) d[t] = s[t];
+}
+
 __global__ void k_fill(float* p, int64_t n, float v) {
     int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i < n) p[i] = v;
@@ -1322,6 +1330,12 @@ int mrfg_quantify_b1(mrfg_ctx* const* ctxs, int nb, const mrfg_grid* lattice, co
                          "quantify_b1: contexts differ in length or device");
         if (nvox == 0) return;
         const int64_t n2 = 2 * n;
+        // the fingerprints go to the device once; each round gathers its
+        // voxel groups there (k_gather_rows) instead of re-uploading them
+        MRFG_CUDA(cudaSetDevice(ctxs[0]->c.device));
+        DevBuf d_all;
+        d_all.ensure(sizeof(double) * n2 * nvox);
+        MRFG_CUDA(cudaMemcpy(d_all.p, fps, sizeof(double) * n2 * nvox, cudaMemcpyHostToDevice));
         auto clampi = [&](int64_t v) { return v < 0 ? int64_t(0) : (v >= nb ? int64_t(nb - 1) : v); };
         // per-voxel memo of the inner searches and the outer walk's state
         std::vector<mrfg_quant> res(static_cast<size_t>(nvox * nb));
@@ -1426,12 +1440,25 @@ int mrfg_quantify_b1(mrfg_ctx* const* ctxs, int nb, const mrfg_grid* lattice, co
                 if (group[ib].empty()) continue;
                 th.emplace_back([&, ib] {
                     const auto& vs = group[ib];
-                    std::vector<double> packed(static_cast<size_t>(n2) * vs.size());
-                    for (size_t k = 0; k < vs.size(); ++k)
-                        std::memcpy(&packed[n2 * k], fps + n2 * vs[k], sizeof(double) * n2);
+                    const int64_t m = static_cast<int64_t>(vs.size());
                     std::vector<mrfg_quant> r(vs.size());
-                    rc[ib] = mrfg_quantify_ex(ctxs[ib], lattice, cfg, packed.data(), static_cast<int64_t>(vs.size()),
-                                              nullptr, nullptr, nullptr, r.data());
+                    rc[ib] = guard([&] {
+                        Ctx& c = ctxs[ib]->c;
+                        MRFG_CUDA(cudaSetDevice(c.device));
+                        c.zidx.ensure(sizeof(int64_t) * m);
+                        c.h_raw.ensure(sizeof(double) * n2 * m);
+                        c.h_res.ensure(sizeof(mrfg_quant) * m);
+                        MRFG_CUDA(cudaMemcpyAsync(c.zidx.p, vs.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice,
+                                                  c.stream));
+                        k_gather_rows<<<static_cast<unsigned>(m), 256, 0, c.stream>>>(
+                            d_all.as<double>(), c.zidx.as<int64_t>(), n2, c.h_raw.as<double>());
+                        MRFG_CUDA(cudaGetLastError());
+                        run_quantify(c, *lattice, *cfg, c.h_raw.as<double>(), m, nullptr, nullptr,
+                                     c.h_res.as<mrfg_quant>());
+                        MRFG_CUDA(cudaMemcpyAsync(r.data(), c.h_res.p, sizeof(mrfg_quant) * m, cudaMemcpyDeviceToHost,
+                                                  c.stream));
+                        MRFG_CUDA(cudaStreamSynchronize(c.stream));
+                    });
                     if (rc[ib]) {
                         msg[ib] = g_err;
                         return;

@@ -119,7 +119,7 @@ struct Ctx {
     DevBuf q64, qprime, best, cand, cand_count, atoms_a, inv2, seed_a, seed_inv2, rerank,
         params, out64, misc, rerank_scratch, misc2, audit,
         // persistent buffers of the host-buffer entry points (no per-call cudaMalloc)
-        h_raw, h_res, h_dict, h_zdict, h_trace;
+        h_raw, h_res, h_dict, h_zdict, h_trace, zidx;
     // producer stream + events for the K1/K2 overlap (created on first use)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev[8] = {};
