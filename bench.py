@@ -401,6 +401,33 @@ def run_ours(args, world, rank, local):
                                      "zoom steps " + str(workloads.CONFIG4_ZOOM)}
         zoom["config4"]["roofline"] = zoom_roofline(zoom["config4"]["voxels_per_s"],
                                                     zoom["config4"]["evals_per_voxel_mean"])
+        if world == 1:
+            # the reference's strict raster prior (zoom.cpp:589-615) on the same
+            # slice: one launch, the voxel chain on one SM (host API, wall time)
+            with P.Context(wl4.schedule, local) as ctx4:
+                mask = np.ones(nq4, np.uint8)
+                ctx4.quantify_slice(wl4.fps[:64], mask[:64], 64, 1, g4, z4cfg, use_prior=1)  # tables, warm
+                rp, secs = ctx4.quantify_slice(wl4.fps, mask, wl4.nx, wl4.ny, g4, z4cfg, use_prior=1)
+            zoom["config4"]["raster_prior"] = {"seconds": secs, "voxels_per_s": nq4 / secs,
+                                               "evals_per_voxel_mean": float(rp["evaluations"].mean())}
+            # BASELINE configs[4]: four-parameter ZOOM (outer B1 zoom_1d of K5,
+            # mrfg_quantify_b1) on the whole 128x128 slice, N = 3000 (host API, wall time)
+            sc5, g5, _, fps5 = workloads.config5_voxels(gpu_sim, np.arange(workloads.CONFIG5["nvox"]))
+            c5cfg = P.zoom_config(**workloads.CONFIG5_ZOOM)
+            ctx5 = [P.Context(s5, local) for s5 in sc5]
+            try:
+                P.quantify_b1(ctx5, fps5[:256], g5, c5cfg, workloads.CONFIG5_B1_STEPS, workloads.CONFIG5_B1_INIT)
+                t5 = time.perf_counter()
+                q5, _ = P.quantify_b1(ctx5, fps5, g5, c5cfg, workloads.CONFIG5_B1_STEPS, workloads.CONFIG5_B1_INIT)
+                s5 = time.perf_counter() - t5
+            finally:
+                for c5 in ctx5:
+                    c5.close()
+            zoom["config5_b1"] = {"voxels_per_s": len(fps5) / s5, "seconds": s5,
+                                  "evals_per_voxel_mean": float(q5["evaluations"].mean()),
+                                  "config": "BASELINE configs[4] 128x128, B1 x T1 x T2 x df = 13 x 117 x 49 x 21, "
+                                            "N=3000; outer B1 zoom_1d (steps 4, 1) of three-parameter ZOOM "
+                                            + str(workloads.CONFIG5_ZOOM)}
 
     # ---- roofline of the dominant kernel (K2) from the in-ABI CUDA events
     pk, pk_kind = peaks()
