@@ -6,6 +6,7 @@ O=gpurun_out/prof
 mkdir -p $O
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err; echo "ref rc=$?"
+timeout 600 python tools/bench_config5_zoom.py > $O/config5_zoom.json 2> $O/config5_zoom.err; echo "c5zoom rc=$?"
 B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-zoom --atoms 4194304"
 timeout 600 $B > $O/short.json 2>&1; echo "short rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file $O/launches.csv \
@@ -27,6 +28,6 @@ for spec in "k2:regex:k_match_sm100_2cta:4" "k1:regex:k_bloch_rows2:4" "k3:regex
 done
 timeout 600 python tools/zoom4_quick.py 4096 1e-5 > $O/zoom4.json 2>&1; echo "zoom4 rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_zoom -s 1 -c 1 \
-    -o $O/ncu_k5 python tools/zoom4_quick.py 4096 1e-5 > $O/ncu_k5.log 2>&1; echo "ncu k5 rc=$?"
+    -o $O/ncu_k5 python tools/zoom4_once.py > $O/ncu_k5.log 2>&1; echo "ncu k5 rc=$?"
 export_rep ncu_k5
 du -sh $O
