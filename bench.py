@@ -49,9 +49,9 @@ def peaks():
 
 def k2_traffic(args, n, nq):
     """DRAM bytes (read + write) of one K2 launch from the committed ncu --set
-    full capture (profiles/r01_k2_traffic.json), when it was taken on this
+    full capture (profiles/r02_k2_traffic.json), when it was taken on this
     workload shape; else None."""
-    p = os.path.join(ROOT, "profiles", "r01_k2_traffic.json")
+    p = os.path.join(ROOT, "profiles", "r02_k2_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
