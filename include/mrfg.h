@@ -357,10 +357,11 @@ int mrfg_quantify_slice_ex(mrfg_ctx* ctx, const mrfg_grid* lattice, const mrfg_z
  * length).  Per voxel: an outer zoom_1d (zoom.cpp:252-282) over the B1
  * index -- steps in index units, coarse to fine, from init_ib -- whose
  * objective is the score of the three-parameter quantify (K5) under
- * ctxs[ib], memoized per voxel and B1 value.  Rounds of the outer walks run
- * as one K5 launch per requested B1 value, concurrently (one host thread per
- * context); the flanks a walk may probe next are evaluated speculatively and
- * only the probes the walk takes count.  out: quantify's result at the
+ * ctxs[ib], memoized per voxel and B1 value.  Each round of the outer walks
+ * is ONE K5 launch over every (voxel, B1) pair the walks need, each voxel with
+ * its B1 schedule's RF rows (the E1/E2/phasor tables do not depend on B1);
+ * the flanks a walk may probe next are evaluated speculatively and only the
+ * probes the walk takes count.  At most 16 B1 values.  out: quantify's result at the
  * chosen B1 with evaluations summed over the B1 values the walk acquired;
  * ib_out: the chosen index.  The oracle is oracle_api.h orc_quantify_b1. */
 int mrfg_quantify_b1(mrfg_ctx* const* ctxs, int nb, const mrfg_grid* lattice, const mrfg_zoom_config* cfg,

@@ -1415,63 +1415,54 @@ int mrfg_quantify_b1(mrfg_ctx* const* ctxs, int nb, const mrfg_grid* lattice, co
                 ++s.si;
             }
         };
-        std::vector<std::vector<int64_t>> group(static_cast<size_t>(nb));
+        // each round: the (voxel, B1) pairs the walks need, in ONE K5 launch
+        // (voxel k of the launch uses schedule ib[k]: rf_b / sut_b per B1)
+        MRFG_REQUIRE(nb <= 16, MRFG_E_INVALID, "quantify_b1: at most 16 B1 values");
+        Ctx& c0 = ctxs[0]->c;
+        std::vector<Ctx*> sched(static_cast<size_t>(nb));
+        for (int k = 0; k < nb; ++k) sched[k] = &ctxs[k]->c;
+        std::vector<int64_t> iv;
+        std::vector<int> ibv;
+        std::vector<uint8_t> pend(static_cast<size_t>(nvox * nb), 0);
         for (;;) {
-            for (auto& g : group) g.clear();
-            bool any = false;
+            iv.clear();
+            ibv.clear();
             std::vector<int64_t> need;
             for (int64_t v = 0; v < nvox; ++v) {
                 if (w[v].phase == 3) continue;
                 need.clear();
                 advance(v, need);
-                for (int64_t ib : need)
-                    if (!have[static_cast<size_t>(v * nb + ib)] &&
-                        (group[ib].empty() || group[ib].back() != v)) {
-                        group[ib].push_back(v);
-                        any = true;
+                for (int64_t ib : need) {
+                    const size_t key = static_cast<size_t>(v * nb + ib);
+                    if (!have[key] && !pend[key]) {
+                        pend[key] = 1;
+                        iv.push_back(v);
+                        ibv.push_back(static_cast<int>(ib));
                     }
+                }
             }
-            if (!any) break;
-            // one K5 launch per requested B1 value, concurrently
-            std::vector<std::thread> th;
-            std::vector<int> rc(static_cast<size_t>(nb), 0);
-            std::vector<std::string> msg(static_cast<size_t>(nb));
-            for (int ib = 0; ib < nb; ++ib) {
-                if (group[ib].empty()) continue;
-                th.emplace_back([&, ib] {
-                    const auto& vs = group[ib];
-                    const int64_t m = static_cast<int64_t>(vs.size());
-                    std::vector<mrfg_quant> r(vs.size());
-                    rc[ib] = guard([&] {
-                        Ctx& c = ctxs[ib]->c;
-                        MRFG_CUDA(cudaSetDevice(c.device));
-                        c.zidx.ensure(sizeof(int64_t) * m);
-                        c.h_raw.ensure(sizeof(double) * n2 * m);
-                        c.h_res.ensure(sizeof(mrfg_quant) * m);
-                        MRFG_CUDA(cudaMemcpyAsync(c.zidx.p, vs.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice,
-                                                  c.stream));
-                        k_gather_rows<<<static_cast<unsigned>(m), 256, 0, c.stream>>>(
-                            d_all.as<double>(), c.zidx.as<int64_t>(), n2, c.h_raw.as<double>());
-                        MRFG_CUDA(cudaGetLastError());
-                        run_quantify(c, *lattice, *cfg, c.h_raw.as<double>(), m, nullptr, nullptr,
-                                     c.h_res.as<mrfg_quant>());
-                        MRFG_CUDA(cudaMemcpyAsync(r.data(), c.h_res.p, sizeof(mrfg_quant) * m, cudaMemcpyDeviceToHost,
-                                                  c.stream));
-                        MRFG_CUDA(cudaStreamSynchronize(c.stream));
-                    });
-                    if (rc[ib]) {
-                        msg[ib] = g_err;
-                        return;
-                    }
-                    for (size_t k = 0; k < vs.size(); ++k) {
-                        res[static_cast<size_t>(vs[k] * nb + ib)] = r[k];
-                        have[static_cast<size_t>(vs[k] * nb + ib)] = 1;
-                    }
-                });
+            if (iv.empty()) break;
+            const int64_t m = static_cast<int64_t>(iv.size());
+            std::vector<mrfg_quant> r(iv.size());
+            MRFG_CUDA(cudaSetDevice(c0.device));
+            c0.zidx.ensure(sizeof(int64_t) * m);
+            c0.zib.ensure(sizeof(int) * m);
+            c0.h_raw.ensure(sizeof(double) * n2 * m);
+            c0.h_res.ensure(sizeof(mrfg_quant) * m);
+            MRFG_CUDA(cudaMemcpyAsync(c0.zidx.p, iv.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice, c0.stream));
+            MRFG_CUDA(cudaMemcpyAsync(c0.zib.p, ibv.data(), sizeof(int) * m, cudaMemcpyHostToDevice, c0.stream));
+            k_gather_rows<<<static_cast<unsigned>(m), 256, 0, c0.stream>>>(d_all.as<double>(), c0.zidx.as<int64_t>(),
+                                                                           n2, c0.h_raw.as<double>());
+            MRFG_CUDA(cudaGetLastError());
+            run_quantify(c0, *lattice, *cfg, c0.h_raw.as<double>(), m, nullptr, nullptr, c0.h_res.as<mrfg_quant>(), 0,
+                         nullptr, nullptr, nullptr, 0, nullptr, nullptr, c0.zib.as<int>(), sched.data(), nb);
+            MRFG_CUDA(cudaMemcpyAsync(r.data(), c0.h_res.p, sizeof(mrfg_quant) * m, cudaMemcpyDeviceToHost, c0.stream));
+            MRFG_CUDA(cudaStreamSynchronize(c0.stream));
+            for (int64_t k = 0; k < m; ++k) {
+                const size_t key = static_cast<size_t>(iv[k] * nb + ibv[k]);
+                res[key] = r[k];
+                have[key] = 1;
             }
-            for (auto& t : th) t.join();
-            for (int ib = 0; ib < nb; ++ib)
-                if (rc[ib]) throw Error{rc[ib], msg[ib]};
         }
         for (int64_t v = 0; v < nvox; ++v) {
             out[v] = res[static_cast<size_t>(v * nb + w[v].x)];

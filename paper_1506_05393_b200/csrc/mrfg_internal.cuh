@@ -119,7 +119,7 @@ struct Ctx {
     DevBuf q64, qprime, best, cand, cand_count, atoms_a, inv2, seed_a, seed_inv2, rerank,
         params, out64, misc, rerank_scratch, misc2, audit,
         // persistent buffers of the host-buffer entry points (no per-call cudaMalloc)
-        h_raw, h_res, h_dict, h_zdict, h_trace, zidx;
+        h_raw, h_res, h_dict, h_zdict, h_trace, zidx, zib;
     // producer stream + events for the K1/K2 overlap (created on first use)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev[8] = {};
@@ -251,6 +251,9 @@ void run_quantify(Ctx& c, const mrfg_grid& lattice, const mrfg_zoom_config& cfg,
                   // the caller's dictionary payload (device, or null) and the
                   // StageLog outputs (device, nvox x MRFG_TRACE_MAX / nvox, or null)
                   const float* d_dict = nullptr, int64_t dict_entries = 0, mrfg_stage* d_trace = nullptr,
-                  int* d_trace_len = nullptr);
+                  int* d_trace_len = nullptr,
+                  // several schedules in one launch: voxel v of schedule d_vox_ib[v]
+                  // (device), contexts sched[0 .. nsched) of the same length
+                  const int* d_vox_ib = nullptr, Ctx* const* sched = nullptr, int nsched = 0);
 
 }  // namespace mrfg

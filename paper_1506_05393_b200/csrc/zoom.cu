@@ -8,7 +8,8 @@ namespace mrfg {
 void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, const double* d_fps,
                   int64_t nvox, const int64_t* h_bounds, const double* h_init, mrfg_quant* d_out,
                   int64_t nrows, const int64_t* h_row_start, const int64_t* h_vox_list, const float* d_dict,
-                  int64_t dict_entries, mrfg_stage* d_trace, int* d_trace_len) {
+                  int64_t dict_entries, mrfg_stage* d_trace, int* d_trace_len, const int* d_vox_ib,
+                  Ctx* const* sched, int nsched) {
     for (const mrfg_axis* ax : {&lat.t1_ms, &lat.t2_ms, &lat.df_hz})
         MRFG_REQUIRE(ax->count > 0 && ax->count < (int64_t(1) << 21), MRFG_E_INVALID,
                      "objective: lattice axis empty or too fine");  // zoom.cpp:46-48
@@ -159,7 +160,20 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     size_t smem = rows ? row_bytes * c.n + sizeof(float2) * c.n + sizeof(ZItem) * kQCap + 16
                        : (row_bytes + sizeof(float2) * (bsk / 32)) * c.n;
     const char* st_env = std::getenv("MRFG_ZOOM_SMEM");
-    P.smem_stage = smem <= 200 * 1024 && !(st_env && std::atoi(st_env) == 0) ? 1 : 0;
+    P.smem_stage = smem <= 200 * 1024 && !(st_env && std::atoi(st_env) == 0) && !d_vox_ib ? 1 : 0;
+    P.vox_ib = d_vox_ib;
+    if (d_vox_ib) {
+        MRFG_REQUIRE(!rows && nsched > 0 && nsched <= 16, MRFG_E_INVALID, "quantify: 1 to 16 schedules per launch");
+        for (int k = 0; k < nsched; ++k) {
+            Ctx& s = *sched[k];
+            MRFG_REQUIRE(s.n == c.n && s.device == c.device && s.rf_xaxis == c.rf_xaxis, MRFG_E_INVALID,
+                         "quantify: schedules differ in length, device or RF axis");
+            const GridTables& tk = ensure_tables(s, lat, true);
+            if (&s != &c) MRFG_CUDA(cudaStreamSynchronize(s.stream));  // its table uploads
+            P.rf_b[k] = s.rf64_d.as<double>();
+            P.sut_b[k] = P.xr ? tk.stepx.as<float4>() : tk.stepu.as<float4>();
+        }
+    }
     // rows mode keeps its shared layout (the helper-warp queue follows the
     // staged rows) whether or not the kernel reads the staged copies
     MRFG_REQUIRE(!rows || smem <= 200 * 1024, MRFG_E_INVALID,

@@ -115,6 +115,13 @@ struct ZParams {
     int* done;
     long long pw1, pw2, pwdf;
     int smem_stage;            // StepU rows + per-warp q32 staged in dynamic shared memory
+    // several schedules in one launch (four-parameter ZOOM: one per B1
+    // value): voxel v uses schedule vox_ib[v] -- its FP64 RF rows rf_b[] and
+    // screening rows sut_b[] (the E1/E2/phasor tables do not depend on B1);
+    // null: every voxel uses rf / sut
+    const int* vox_ib;
+    const double* rf_b[16];
+    const float4* sut_b[16];
     int dict_mode;             // 0 none, 1 df dictionary (stage-1 acquisitions), 2 full dictionary
     // the caller's dictionary payload (zoom.cpp:101-113: entry idf of the df
     // slab, or the lattice flat of the full dictionary), scored as given;
@@ -153,6 +160,7 @@ struct ZItem {
 
 struct Z {
     const ZParams* p;
+    const double* rf;   // FP64 RF rows of this voxel's schedule
     ZSlot* tab;
     const double* q;
     const float2* q32;  // shared memory when staged
@@ -296,7 +304,7 @@ __device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, bool dict
     } else {
         // pass 1: the recursion, |s|^2 in the reference's order (fingerprint.cpp:14-18);
         // the entries are kept (lane-interleaved scratch) for pass 2
-        sim64_walk(P.rf, P.e1d, P.e2d, P.phd, P.inv0, n, P.L, i1, i2, idf, [&](int j, double x, double y) {
+        sim64_walk(z.rf, P.e1d, P.e2d, P.phd, P.inv0, n, P.L, i1, i2, idf, [&](int j, double x, double y) {
             acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
             fx[32 * j] = make_double2(x, y);
         });
@@ -1585,6 +1593,11 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v, const long long* b
                            long long s2) {
     z.evals = 0;
     z.vox = v;
+    if (P.vox_ib) {  // this voxel's schedule (the staged rows are off in this mode)
+        const int ib = P.vox_ib[v];
+        z.rf = P.rf_b[ib];
+        z.rfs = P.sut_b[ib];
+    }
     z.cyc32 = z.cyc64 = z.r64 = 0;
     const long long tstart = clock64();
     const int n = P.n;
@@ -1746,6 +1759,7 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v, const long long* b
 // thread of the block takes part).
 __device__ void zwarp_setup(Z& z, const ZParams& P, int64_t w) {
     z.p = &P;
+    z.rf = P.rf;
     z.lane = threadIdx.x % 32;
     z.tab = P.tab + w * (static_cast<int64_t>(P.cap_mask) + 1);
     z.q = P.q + w * 2 * P.n;
