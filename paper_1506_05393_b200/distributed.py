@@ -47,14 +47,34 @@ def merge_matches(flats: np.ndarray, scores: np.ndarray):
     return best_f, best_s
 
 
-def _all_gather(out, inp, group):
-    """all_gather_into_tensor (NCCL) or its list form (gloo, CPU tensors)."""
+def _gloo(group) -> bool:
     import torch.distributed as dist
-    if inp.device.type == "cuda":
+    return dist.get_backend(group) == "gloo"
+
+
+def _all_gather(out, inp, group):
+    """all_gather_into_tensor (NCCL, device tensors) or, under gloo, its list
+    form on host copies (CPU tests; ranks sharing one GPU)."""
+    import torch.distributed as dist
+    if inp.device.type == "cuda" and not _gloo(group):
         dist.all_gather_into_tensor(out, inp, group=group)
+        return
+    world = out.numel() // inp.numel()
+    o = out.cpu() if out.device.type == "cuda" else out
+    dist.all_gather(list(o.view(world, -1).unbind(0)), inp.cpu().view(-1), group=group)
+    if o is not out:
+        out.copy_(o)
+
+
+def _all_reduce_max(t, group):
+    """all_reduce(MAX) (NCCL), or on a host copy under gloo."""
+    import torch.distributed as dist
+    if t.device.type == "cuda" and _gloo(group):
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+        t.copy_(h)
     else:
-        world = out.numel() // inp.numel()
-        dist.all_gather(list(out.view(world, -1).unbind(0)), inp.view(-1), group=group)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
 
 
 def scan_grid_distributed(ctx, grid, d_queries, nq: int, group=None, opts=None, metric="cc",
@@ -92,7 +112,7 @@ def scan_grid_distributed(ctx, grid, d_queries, nq: int, group=None, opts=None, 
         if fe > fb:
             ctx.scan_seed_device(grid, d_queries.data_ptr(), nq, seed.data_ptr(), metric=metric,
                                  flat_range=(fb, fe), opts=opts)
-        dist.all_reduce(seed, op=dist.ReduceOp.MAX, group=group)
+        _all_reduce_max(seed, group)
         floor = torch.zeros((nq, 2), dtype=torch.float64, device=dev)
         floor[:, 1] = seed.double()
         floor_rec = floor.view(torch.int64)
