@@ -161,6 +161,13 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
                        : (row_bytes + sizeof(float2) * (bsk / 32)) * c.n;
     const char* st_env = std::getenv("MRFG_ZOOM_SMEM");
     P.smem_stage = smem <= 200 * 1024 && !(st_env && std::atoi(st_env) == 0) && !d_vox_ib ? 1 : 0;
+    // CTA mode (the slice kernels): small rounds screened parallel in time,
+    // one point per warp (x-axis rows; not with smoothing, MUFU screening or
+    // the all-FP64 mode); MRFG_ZOOM_PIT=0 disables it
+    {
+        const char* pe = std::getenv("MRFG_ZOOM_PIT");
+        P.pit = P.xr && P.eps >= 0 && P.screen_mode == 0 && !P.smooth_k && !(pe && std::atoi(pe) == 0) ? 1 : 0;
+    }
     P.vox_ib = d_vox_ib;
     if (d_vox_ib) {
         MRFG_REQUIRE(!rows && nsched > 0 && nsched <= 16, MRFG_E_INVALID, "quantify: 1 to 16 schedules per launch");

@@ -115,6 +115,7 @@ struct ZParams {
     int* done;
     long long pw1, pw2, pwdf;
     int smem_stage;            // StepU rows + per-warp q32 staged in dynamic shared memory
+    int pit;                   // CTA mode: parallel-in-time screening of small rounds (x-axis rows)
     // several schedules in one launch (four-parameter ZOOM: one per B1
     // value): voxel v uses schedule vox_ib[v] -- its FP64 RF rows rf_b[] and
     // screening rows sut_b[] (the E1/E2/phasor tables do not depend on B1);
@@ -819,9 +820,20 @@ __device__ void zdo_screen(Z& z, int slot, int a, int b, int c) {
 
 __device__ void zdo_pair(Z& z, int s0, int s1, int i1, int i2, int idf0);
 __device__ void zdo_exact(Z& z, int s);
+__device__ void zpit_point(Z& z, int slot, int i1, int i2, int idf);
 
-// Evaluate queued items k = warp*32 + lane, stride 32 * cta_w.
+// Evaluate queued items k = warp*32 + lane, stride 32 * cta_w (kind 3: one
+// point per warp, screened parallel-in-time by all its lanes).
 __device__ void zwork(Z& z, int m) {
+    if (m > 0 && z.queue[0].kind == 3) {
+        const int w = static_cast<int>(threadIdx.x / 32);
+        if (w < m) {
+            const ZItem it = z.queue[w];
+            zpit_point(z, it.s0, it.a, it.b, it.c);
+        }
+        __threadfence_block();
+        return;
+    }
     for (int k = static_cast<int>(threadIdx.x / 32) * 32 + z.lane; k < m; k += 32 * z.cta_w) {
         const ZItem it = z.queue[k];
         if (it.kind == 0)
@@ -895,6 +907,18 @@ __device__ void zensure(Z& z, long long count, PT pt) {
             }
         }
         __syncwarp();
+        if (z.cta_w && z.p->pit && qn == 0) {
+            // a small round (<= one point per warp): each warp screens one
+            // point with all its lanes, parallel in time (zpit_point)
+            const unsigned int mm = __ballot_sync(0xffffffffu, mine);
+            if (mm && __popc(mm) <= z.cta_w) {
+                if (mine) z.queue[__popc(mm & ((1u << z.lane) - 1u))] =
+                    ZItem{3, slot, -1, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c)};
+                __syncwarp();
+                zdispatch(z, __popc(mm));
+                continue;
+            }
+        }
         if (z.cta_w) {
             zenqueue(z, qn, mine, ZItem{0, slot, -1, static_cast<int>(a), static_cast<int>(b), static_cast<int>(c)});
             continue;
@@ -1018,6 +1042,104 @@ __device__ void zdo_exact(Z& z, int s) {
     z.tab[s].queued = 0;
     __threadfence_block();
     z.tab[s].xtype = ty;
+}
+
+// Parallel-in-time screening of ONE point by all 32 lanes of a warp (CTA
+// mode, small rounds): lane k takes steps [kL, (k+1)L), L = ceil(n / 32):
+//   1. the segment's affine map m -> G m + t (zstep32x's linear part: x-axis
+//      RF rows, relax and precess over te and rest) is composed in FP32;
+//   2. the start states are chained through the warp by shuffles (lane 0
+//      starts from the inversion);
+//   3. each lane re-walks its segment from its start state with zstep32x,
+//      the CC partial sums reduced over the warp in FP64.
+// Lane 0 writes the slot like zdo_screen.  Same tables and rounding order
+// per step as the sequential walk; the composition adds FP32 rounding of the
+// same order (audited in stats mode).
+__device__ void zpit_point(Z& z, int slot, int i1, int i2, int idf) {
+    const ZParams& P = *z.p;
+    const int n = P.n;
+    const int k = z.lane;
+    const int L = (n + 31) / 32;
+    const int j0 = min(n, k * L), j1 = min(n, j0 + L);
+    const float4* __restrict__ e1p = P.e1f + static_cast<int64_t>(i1) * n;
+    const float2* __restrict__ e2p = P.e2f + static_cast<int64_t>(i2) * n;
+    const float4* __restrict__ php = P.phf + static_cast<int64_t>(idf) * n;
+    extern __shared__ float4 zsm[];
+    const float4* rfp = P.smem_stage ? zsm : z.rfs;  // x-axis rows: 2 float4 per step
+    const float2* q = P.smem_stage ? reinterpret_cast<const float2*>(zsm + 2 * n) + z.qw * n : z.q32;
+    // 1. compose: columns x0, y0, z0 and the constant column
+    float gx[4] = {1.f, 0.f, 0.f, 0.f}, gy[4] = {0.f, 1.f, 0.f, 0.f}, gz[4] = {0.f, 0.f, 1.f, 0.f};
+    for (int j = j0; j < j1; ++j) {
+        const float4 rx = rfp[2 * j], e1 = __ldg(e1p + j), ph = __ldg(php + j);
+        const float2 e2 = __ldg(e2p + j);
+        const float tc = ph.x * e2.x, ts = ph.y * e2.x, rc = ph.z * e2.y, rs = ph.w * e2.y;
+#pragma unroll
+        for (int col = 0; col < 4; ++col) {
+            const float X = gx[col], Y = gy[col], Zc = gz[col];
+            const float ny = fmaf(rx.x, Y, rx.y * Zc), nz = fmaf(rx.z, Y, rx.w * Zc);
+            const float x1 = fmaf(X, tc, -ny * ts), y1 = fmaf(X, ts, ny * tc);
+            const float z1 = col == 3 ? fmaf(nz, e1.x, e1.y) : nz * e1.x;
+            gx[col] = fmaf(x1, rc, -y1 * rs);
+            gy[col] = fmaf(x1, rs, y1 * rc);
+            gz[col] = col == 3 ? fmaf(z1, e1.z, e1.w) : z1 * e1.z;
+        }
+    }
+    // 2. chain the start states
+    float sx = static_cast<float>(P.inv0[0]), sy = static_cast<float>(P.inv0[1]), sz = static_cast<float>(P.inv0[2]);
+    for (int it = 1; it < 32; ++it) {
+        const float nx = fmaf(gx[0], sx, fmaf(gx[1], sy, fmaf(gx[2], sz, gx[3])));
+        const float ny = fmaf(gy[0], sx, fmaf(gy[1], sy, fmaf(gy[2], sz, gy[3])));
+        const float nz = fmaf(gz[0], sx, fmaf(gz[1], sy, fmaf(gz[2], sz, gz[3])));
+        const float ux = __shfl_up_sync(0xffffffffu, nx, 1), uy = __shfl_up_sync(0xffffffffu, ny, 1),
+                    uz = __shfl_up_sync(0xffffffffu, nz, 1);
+        if (k == it) {
+            sx = ux;
+            sy = uy;
+            sz = uz;
+        }
+    }
+    // 3. re-walk the segment
+    double re = 0.0, im = 0.0, nn = 0.0;
+    {
+        float x = sx, y = sy, zz = sz;
+        zf2 pq = zpk(0.f, 0.f), pn = zpk(0.f, 0.f);
+        for (int j = j0; j < j1; ++j) {
+            zstep32x(rfp[2 * j], q[j], __ldg(e1p + j), __ldg(e2p + j), __ldg(php + j), x, y, zz, pq, pn);
+            if (((j - j0) & 15) == 15 || j + 1 == j1) {
+                float pr, pi, na, nb;
+                zup(pq, pr, pi);
+                zup(pn, na, nb);
+                re += pr;
+                im += pi;
+                nn += na + nb;
+                pq = zpk(0.f, 0.f);
+                pn = zpk(0.f, 0.f);
+            }
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, off);
+        im += __shfl_xor_sync(0xffffffffu, im, off);
+        nn += __shfl_xor_sync(0xffffffffu, nn, off);
+    }
+    if (k == 0) {
+        const double inv = rsqrt(nn);
+        ZSlot& t = z.tab[slot];
+        t.acc = static_cast<float>(fmin(sqrt(re * re + im * im) * inv, 1.0));
+        t.are = static_cast<float>(re * inv);
+        t.nrm2 = -1.0;
+        t.xtype = 0xFFu;
+        t.atype = 0;
+        t.queued = 0;
+        if (P.stats && (zhash(zkey(i1, i2, idf) * 0x9E3779B97F4A7C15ull) & 63) == 0) {
+            ZSlot r;  // audit (stats mode only), as in zdo_screen
+            zsim(z, i1, i2, idf, false, r);
+            const double e = fabs(static_cast<double>(t.acc) - r.cc);
+            atomicMax(P.stats + 10, static_cast<unsigned long long>(__double_as_longlong(e)));
+            atomicAdd(P.stats + 11, 1ull);
+        }
+    }
+    __syncwarp();
 }
 
 // Exact (FP64) evaluation of the memo slots named by slot_of(0..count-1)
