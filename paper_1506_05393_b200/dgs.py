@@ -334,6 +334,10 @@ class Context:
                                      out.ctypes.data_as(C.POINTER(C.c_float))))
         return out
 
+    def generate_device(self, g: Grid, first: int, count: int, d_out_ptr: int, precision: int = 64) -> None:
+        """generate into device memory: (count, 2N) float32 at d_out_ptr."""
+        check(self.lib.mrfg_generate_dev(self.h, C.byref(g), first, count, precision, C.c_void_p(d_out_ptr)))
+
     # -- K2/K3
     @staticmethod
     def _unit_opts(opts, unit_norm, nq):

@@ -6,9 +6,11 @@
 in HBM, matched with K4 (`mrfg_scan_dict_dev`: fp16 screening GEMM on tcgen05,
 exact FP64 re-rank against the stored entries, dictionary.cpp:117-143).
 
-Log axes are not a ParameterGrid, so the dictionary is built from explicit
-TissueParams (FP64 simulate + normalize on the GPU, cast to float32) -- an
-index-space dictionary, as SURVEY 8(d) prescribes for the oracle.  Voxel
+Log axes are not a ParameterGrid: the dictionary is generated on the GPU
+over an explicit-axis lattice (grid_values: host-libm tables from the axis
+values, FP64 recursion), so every stored entry equals the reference's
+generate() over the same TissueParams bit for bit (pinned on 256 voxels by
+tests/test_gpu_scale.py::test_config3_log_axes_vs_reference).  Voxel
 parameters: per-axis indices rng_at(7, axis, voxel) % count; SNR 20 noise
 (sigma = |s|/sqrt(N)/SNR per real channel, add_noise stream).
 
@@ -52,20 +54,13 @@ def main():
         t0 = time.perf_counter()
         d_dict = torch.empty((A, 2 * n), dtype=torch.float32, device=dev)
         chunk = 1 << 17
-        d_tmp = torch.empty((chunk, 2 * n), dtype=torch.float64, device=dev)
+        g = P.grid_values(t1, t2, (-100.0, 5.0, 41))
         for f0 in range(0, A, chunk):
             f1 = min(A, f0 + chunk)
-            fl = torch.arange(f0, f1, device=dev, dtype=torch.int64)
-            idf, rest = fl % df.size, fl // df.size
-            i2, i1 = rest % t2.size, rest // t2.size
-            prm = torch.stack([torch.as_tensor(t1 * 1e-3, device=dev)[i1], torch.as_tensor(t2 * 1e-3, device=dev)[i2],
-                               torch.as_tensor(df, device=dev)[idf]], 1).contiguous()
-            c.simulate_device(prm.data_ptr(), f1 - f0, d_tmp.data_ptr(), 64, True)
-            d_dict[f0:f1] = d_tmp[: f1 - f0].float()
+            c.generate_device(g, f0, f1 - f0, d_dict[f0:f1].data_ptr(), precision=64)
         torch.cuda.synchronize()
         out["dictionary_build_s"] = time.perf_counter() - t0
         out["dictionary_gb"] = d_dict.numel() * 4 / 1e9
-        del d_tmp
         # ---- voxels
         t0 = time.perf_counter()
         idx = np.array([[P.dgs.rng_at(7, ax, v) % cnt for ax, cnt in enumerate((t1.size, t2.size, df.size))]
@@ -80,12 +75,12 @@ def main():
         d_m = torch.empty(nvox * 16, dtype=torch.uint8, device=dev)
         # ---- timed K4 scan (warm-up on a slice of the voxels)
         c.scan_dict_device(d_dict.data_ptr(), A, d_q.data_ptr(), min(nvox, 4096), d_m.data_ptr(),
-                           opts=ScanOpts(1e-3, 524288, max(1 << 25, 1024 * nvox), 16384))
+                           opts=ScanOpts(0.0, 524288, max(1 << 25, 1024 * nvox), 16384))
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         # candidate buffer sized for ~1,000 survivors per voxel (16 B each)
-        opts = ScanOpts(1e-3, 524288, max(1 << 25, 1024 * nvox), 16384)
+        opts = ScanOpts(0.0, 524288, max(1 << 25, 1024 * nvox), 16384)  # delta: the certified default
         st = c.scan_dict_device(d_dict.data_ptr(), A, d_q.data_ptr(), nvox, d_m.data_ptr(), opts=opts)
         e1.record(stream)
         torch.cuda.synchronize()
