@@ -635,6 +635,11 @@ int mrfg_create(const double* flip_deg, const double* phase_deg, const double* t
             c.rf_xaxis = std::fabs(r[0] - 1.0) <= 1e-12 && std::fabs(r[1]) <= 1e-12 && std::fabs(r[2]) <= 1e-12 &&
                          std::fabs(r[3]) <= 1e-12 && std::fabs(r[6]) <= 1e-12;
         }
+        // symmetric echo: the te and rest intervals are equal in FP64 (TE = TR/2:
+        // tr*1e-3 - (tr/2)*1e-3 == (tr/2)*1e-3 exactly), so every table value
+        // and StepU field of the two stages is identical
+        c.te_sym = n > 0;
+        for (int64_t i = 0; i < n && c.te_sym; ++i) c.te_sym = c.te_s[i] == c.rest_s[i];
         double inv[9];
         host_rf_matrix(3.14159265358979323846, 0, inv);  // bloch.cpp:113
         // kInvert * (0,0,1) = third column

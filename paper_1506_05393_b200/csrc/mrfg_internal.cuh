@@ -112,6 +112,7 @@ struct Ctx {
     std::vector<double> te_s, rest_s;
     double inv64[9];                // kInvert (bloch.cpp:113)
     bool rf_xaxis = false;          // every RF rotation is about x (phases 0/180 deg): K1 specialization
+    bool te_sym = false;            // te == rest at every TR (TE = TR/2): K1 symmetric-echo specialization
     DevBuf rf64_d, rf32_d;          // n x 9 doubles; n x 12 floats (9 RF, te, rest, pad)
     GridTables tab;                 // cache for the last grid
     // scratch

@@ -61,12 +61,17 @@ def test_screen_close_to_exact_cc2(orc, small):
 
 
 @pytest.mark.parametrize("k1,apt", [("fold", "2"), ("fold", "4"), ("fold", "8"), ("rows", "4"), ("rows", "8"),
-                                    ("rows2", "4"), ("rows2", "8")])
+                                    ("rows2", "4"), ("rows2", "8"), ("pairs", "4"), ("pairs", "8"),
+                                    ("pairs_nost", "4"), ("pairs_nost_hb4", "4"), ("pairs_hb4", "8"),
+                                    ("pairs_minb3", "4")])
 def test_screen_production_producer(orc, small, monkeypatch, k1, apt):
     """The GEMM operand of the production K1 (scan_grid's producer) screens
     within fp16 rounding of the exact CC; ranges start and end mid-row and
     cut T2 pencils."""
-    monkeypatch.setenv("MRFG_K1", k1)
+    monkeypatch.setenv("MRFG_K1", k1.split("_")[0])
+    monkeypatch.setenv("MRFG_K1_HB", "4" if "_hb4" in k1 else "8")
+    monkeypatch.setenv("MRFG_K1_ST", "0" if "_nost" in k1 else "1")
+    monkeypatch.setenv("MRFG_K1_MINB", "3" if "_minb3" in k1 else "2")
     monkeypatch.setenv("MRFG_K1_APT", apt)
     first, count = 4999, 1777
     with P.Context(small.schedule) as c:
@@ -79,6 +84,34 @@ def test_screen_production_producer(orc, small, monkeypatch, k1, apt):
     assert np.isfinite(a).all()
     assert np.abs(np.sqrt(a) - cc).max() < 1e-3
     assert np.abs(a - b).max() < 1e-3
+
+
+@pytest.mark.parametrize("apt", ["4", "8"])
+@pytest.mark.parametrize("xr", ["1", "0"])
+def test_k1_symmetric_echo_identical(orc, monkeypatch, apt, xr):
+    """BASELINE schedules have TE = TR/2, so te == rest at every TR and the
+    packed K1 takes its symmetric-echo path (one E1/E2/phasor per step):
+    the GEMM operand screens bit-identically to the two-stage path
+    (MRFG_K1_SYM=0), and the fused FP32 cc_map is identical too.  (The
+    default producer for such schedules, the atom-pair kernel, is checked
+    against the exact scores in test_screen_production_producer and
+    test_cc_map_fp32_close.)"""
+    monkeypatch.setenv("MRFG_K1", "rows2")
+    monkeypatch.setenv("MRFG_K1_APT", apt)
+    monkeypatch.setenv("MRFG_K1_XR", xr)
+    s = P.baseline_schedule(1000, 3)
+    assert np.array_equal(s.te_ms, s.tr_ms / 2)
+    g = P.grid((100, 20, 50), (20, 10, 40), (-250, 1, 501))
+    fp = orc.add_noise(orc.simulate(to_oracle_sched(s), 0.9, 0.06, -3.0), 0.002, 5)
+    q = np.stack([fp, fp * 1j, np.conj(fp)])
+    out = {}
+    with P.Context(s) as c:
+        for sym in ("1", "0"):
+            monkeypatch.setenv("MRFG_K1_SYM", sym)
+            out[sym] = (c.screen_scores(g, q, 12345, 9 * 512 + 77, producer="rows"),
+                        c.cc_map(fp, g, first=777, count=3333, precision=32))
+    np.testing.assert_array_equal(out["1"][0], out["0"][0])
+    np.testing.assert_array_equal(out["1"][1], out["0"][1])
 
 
 @pytest.mark.parametrize("pair", ["1", "0"])
