@@ -47,7 +47,7 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
-def k2_traffic(args, n, nq):
+def k2_traffic(chunk_atoms, n, nq):
     """DRAM bytes (read + write) of one K2 launch from the committed ncu --set
     full capture (profiles/r02_k2_traffic.json), when it was taken on this
     workload shape; else None."""
@@ -57,7 +57,7 @@ def k2_traffic(args, n, nq):
             d = json.load(f)
     except (OSError, ValueError):
         return None
-    if (d.get("chunk_atoms"), d.get("voxels"), d.get("timepoints")) != (args.chunk, nq, n):
+    if (d.get("chunk_atoms"), d.get("voxels"), d.get("timepoints")) != (chunk_atoms, nq, n):
         return None
     return d.get("dram_bytes_per_launch")
 
@@ -213,7 +213,8 @@ def arm_config(args, world, nx, ny, n, nq, total):
     """The workload description both arms print (config of the JSON line)."""
     return {"workload": f"BASELINE configs[{args.config - 1}]: {nx}x{ny} slice, N={n}, "
                         f"{total} atoms, brute-force streamed DGS",
-            "voxels": nq, "atoms": total, "timepoints": n, "chunk_atoms": args.chunk,
+            "voxels": nq, "atoms": total, "timepoints": n,
+            "chunk_atoms": args.chunk or "library default (one K1 wave of whole lattice rows)",
             "delta": args.delta or 2.5e-3, "parallelism": f"atom-shard x{world}",
             "l2": "256 MB flush per step; each step streams >100 GB of fp16 atoms"}
 
@@ -435,6 +436,7 @@ def run_ours(args, world, rank, local):
     launches = sum(s.gemm_launches for s in stats)
     flops_alg = 8.0 * n * nq * (fe - fb) * len(stats)
     gemm_tflops = flops_alg / (gemm_ms * 1e-3) / 1e12
+    chunk_atoms = int(stats[-1].chunk_atoms)  # atoms per K2 launch (the library's choice when --chunk 0)
     peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     bloch_ms = sum(s.bloch_ms for s in stats)
     bloch_rate = (fe - fb) * n * len(stats) / (bloch_ms * 1e-3)
@@ -463,10 +465,10 @@ def run_ours(args, world, rank, local):
                          "rule": "hash sample of ALL screened (voxel, atom) pairs, scored exactly; "
                                  "certificate needs err_max <= delta/2"},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
-                     "frac": gemm_tflops / peak_t, "traffic": k2_traffic(args, n, nq),
+                     "frac": gemm_tflops / peak_t, "traffic": k2_traffic(chunk_atoms, n, nq),
                      "kernel": "k_match_sm100_2cta (K2)", "peak_kind": f"{pk_kind} bf16 dense sustained",
                      "avg_launch_ms": gemm_ms / max(launches, 1),
-                     "flop_per_launch": 8.0 * n * nq * args.chunk},
+                     "flop_per_launch": 8.0 * n * nq * chunk_atoms, "atoms_per_launch": chunk_atoms},
         "e2e": {"value": nq * total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nq * n * 16,
                 "d2h_bytes_per_step": nq * 16, "seconds_per_step": e2e_s},
         # our kernels per scan: per chunk K1 + K2 (+ k_zero_rows for the chunk's
@@ -497,7 +499,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--nvox", type=int, default=None)
     ap.add_argument("--atoms", type=int, default=0, help="limit atoms (debug only)")
-    ap.add_argument("--chunk", type=int, default=524288)
+    ap.add_argument("--chunk", type=int, default=0, help="atoms per streamed chunk (0: the library default)")
     ap.add_argument("--delta", type=float, default=0.0, help="screening margin (0: library default 2.5e-3)")
     ap.add_argument("--ref-voxels", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -66,7 +66,9 @@ typedef struct { int64_t flat; double score; } mrfg_match;
 typedef struct {
     double delta;          /* screening margin in CC units (default 2.5e-3: twice the analytic
                               bound on the fp16 screening error) */
-    int64_t chunk_atoms;   /* atoms simulated per streamed chunk (default 524288) */
+    int64_t chunk_atoms;   /* atoms simulated per streamed chunk (default: lattice scans one full
+                              wave of the K1 producer in whole rows, ~300 K atoms on 148 SMs;
+                              stored dictionaries 524288) */
     int64_t cand_capacity; /* candidate buffer entries (default 1<<25) */
     int64_t seed_atoms;    /* strided pre-pass atoms that seed the running max (default 16384) */
     /* Optional (device, *_dev calls, metric cc): nq matches of an earlier scan
@@ -100,6 +102,7 @@ typedef struct {
     double screen_err_audit_max, rescreen_err_audit_max, delta_used;
     int64_t audit_samples, rescans;
     double rescreen_err_max;   /* max |FP32 re-screen - exact| over the FP64 survivors */
+    int64_t chunk_atoms;       /* atoms per streamed chunk (whole lattice rows) */
 } mrfg_scan_stats;
 
 /* ZoomConfig (zoom.hpp:23-52) as a POD; the step lists hold up to 8 values.

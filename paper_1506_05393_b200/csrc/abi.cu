@@ -258,10 +258,17 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
     if (fb == 0 && fe == 0) fe = total;
     MRFG_REQUIRE(0 <= fb && fb < fe && fe <= total, MRFG_E_INVALID, "scan_grid: bad flat range");
     const GridTables* tp = grid ? &ensure_tables(c, *grid, true) : nullptr;
-    int64_t chunk = (o && o->chunk_atoms > 0) ? o->chunk_atoms : 524288;
     // K1 tiles whole lattice rows (ndf atoms): a chunk is crows rows.  A stored
     // dictionary is chunked in flat order directly (ndf = 1).
     const int64_t ndf = grid ? grid->df_hz.count : 1;
+    // Default lattice chunk: ONE full wave of the K1 producer (2 resident
+    // blocks of 256 threads per SM, 4 atoms per thread, whole rows) -- the
+    // 524,288-atom chunk ran K1 as 1.73 waves (config 2: 128 vs 118 ms per step)
+    int64_t chunk = (o && o->chunk_atoms > 0) ? o->chunk_atoms : 524288;
+    if (grid && !(o && o->chunk_atoms > 0)) {
+        const int64_t threads_per_row = (ndf + 3) / 4;
+        chunk = std::max<int64_t>(1, int64_t(c.num_sms) * 2 * 256 / threads_per_row) * ndf;
+    }
     const int64_t crows = std::max<int64_t>(1, chunk / ndf);
     int64_t cap = (o && o->cand_capacity > 0) ? o->cand_capacity : (int64_t(1) << 25);
     const int64_t seed_atoms = (o && o->seed_atoms > 0) ? o->seed_atoms : 16384;
@@ -519,6 +526,7 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
         st->audit_samples = nsamp;
         st->delta_used = delta;
         st->rescreen_err_max = err32;
+        st->chunk_atoms = crows * ndf;
         st->rerank_ms += tm.ms(ra0, ra1);
     }
     return true;
