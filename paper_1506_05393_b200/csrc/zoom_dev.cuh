@@ -356,6 +356,10 @@ __device__ __noinline__ void zsim(const Z& z, int i1, int i2, int idf, bool dict
 struct Apx {
     float cc, re;
 };
+#ifndef MRFG_ZPF
+#define MRFG_ZPF 24
+#endif
+constexpr int kZPf = MRFG_ZPF;  // L1 prefetch distance of the table streams, in steps (whole 128-byte lines)
 // Packed f32x2 helpers: sm_100a executes fma/mul.rn.f32x2 as FFMA2/FMUL2 and
 // folds a scalar broadcast, a half swap and a one-half negation into the
 // operand selectors, so a complex product v*(c + i s) is 2 instructions.
@@ -451,12 +455,12 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
     float x = static_cast<float>(P.inv0[0]), y = static_cast<float>(P.inv0[1]),
           zz = static_cast<float>(P.inv0[2]);
     double re = 0.0, im = 0.0, nn = 0.0;
-    for (int j = 0; j < 24; j += 8) {
+    for (int j = 0; j < kZPf; j += 8) {
         prefetch_l1(e1p + j);
         prefetch_l1(php + j);
     }
     prefetch_l1(e2p);
-    prefetch_l1(e2p + 16);
+    if (kZPf > 8) prefetch_l1(e2p + 16);
     float4 A1[kB], AP[kB], B1[kB], BP[kB];
     float2 A2[kB], B2[kB];
     auto load = [&](float4* E1, float2* E2, float4* PH, const float4* p1, const float2* p2, const float4* pp) {
@@ -490,11 +494,11 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
     load(A1, A2, AP, e1p, e2p, php);
     for (int jb = 0; jb < nmain; jb += 2 * kB) {
         if ((jb & 15) == 0) {  // one L1 prefetch per 128-byte line, 3 lines ahead
-            prefetch_l1(e1p + jb + 24);
-            prefetch_l1(e1p + jb + 32);
-            prefetch_l1(php + jb + 24);
-            prefetch_l1(php + jb + 32);
-            prefetch_l1(e2p + jb + 32);
+            prefetch_l1(e1p + jb + kZPf);
+            prefetch_l1(e1p + jb + kZPf + 8);
+            prefetch_l1(php + jb + kZPf);
+            prefetch_l1(php + jb + kZPf + 8);
+            prefetch_l1(e2p + jb + kZPf + 8);
         }
         load(B1, B2, BP, e1p + jb + kB, e2p + jb + kB, php + jb + kB);
         run(A1, A2, AP, rfp + S * jb, q + jb);
@@ -520,12 +524,21 @@ __device__ __noinline__ Apx zsim32_tab(const Z& z, int i1, int i2, int idf) {
 }
 
 // Two adjacent off-resonance points (idf, idf + 1) of one (T1, T2) in one
-// lane: the second phasor is the first times the one-df-step phasor w of the
-// StepU row (complex multiply), so the pair costs one table stream and the
-// uniform operands are read once.  Same arithmetic otherwise as zsim32_tab.
+// lane.  Every f32x2 register holds the SAME component of the two points
+// (X = (x_a, x_b), ...), as in the K1 atom-pair producer: each operation of the
+// recursion is one FFMA2/FMUL2 for both points with the step's scalars as
+// broadcast operands, and no (x, y) packing is needed.  The second point's
+// E2-scaled phasors are the first's times the one-df-step phasor w of the step
+// row (scalar complex multiply), so the pair costs one table stream.  Per
+// pair-step: 12 scalar FMA-pipe instructions (phasors) + 20 FFMA2/FMUL2
+// (x-axis rows; 25 with a general RF matrix) against 38 + 6 register moves of
+// the (x, y)-packed form it replaces; the FP32 partial sums are folded into
+// FP64 every 16 steps.
 struct Apx2 {
     Apx a, b;
 };
+__device__ __forceinline__ zf2 zneg2(zf2 v) { return v ^ 0x8000000080000000ull; }
+__device__ __forceinline__ zf2 zbc(float s) { return zpk(s, s); }
 template <bool SMEM, bool XR>
 __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
     constexpr int kB = 2;
@@ -542,14 +555,15 @@ __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
                            : z.q32;
     const float x0 = static_cast<float>(P.inv0[0]), y0 = static_cast<float>(P.inv0[1]),
                 z0 = static_cast<float>(P.inv0[2]);
-    float xa = x0, ya = y0, za = z0, xb = x0, yb = y0, zb = z0;
+    zf2 X = zpk(x0, x0), Y = zpk(y0, y0), Zc = zpk(z0, z0);
+    zf2 DR = zpk(0.f, 0.f), DI = DR, NN = DR;  // sum conj(q) s (re, im) and |s|^2, both points
     double rea = 0.0, ima = 0.0, nna = 0.0, reb = 0.0, imb = 0.0, nnb = 0.0;
-    for (int j = 0; j < 24; j += 8) {
+    for (int j = 0; j < kZPf; j += 8) {
         prefetch_l1(e1p + j);
         prefetch_l1(php + j);
     }
     prefetch_l1(e2p);
-    prefetch_l1(e2p + 16);
+    if (kZPf > 8) prefetch_l1(e2p + 16);
     float4 A1[kB], AP[kB], B1[kB], BP[kB];
     float2 A2[kB], B2[kB];
     auto load = [&](float4* E1, float2* E2, float4* PH, const float4* p1, const float2* p2, const float4* pp) {
@@ -560,66 +574,75 @@ __device__ __noinline__ Apx2 zsim32_df2(const Z& z, int i1, int i2, int idf) {
             E2[m] = __ldg(p2 + m);
         }
     };
-    // one step of both points; w = (wtc, wts) for te, (wrc, wrs) for rest: rc.w, rd.x, rd.y, rd.z
-    auto step2 = [&](const float4* r, const float2 qq, const float4 e1, const float2 e2, const float4 pa, zf2& pra,
-                     zf2& pna, zf2& prb, zf2& pnb) {
-        float4 pb;
-        if (XR) {  // r[0] = (r4, r5, r7, r8), r[1] = (wtc, wts, wrc, wrs)
-            const float4 rx = r[0], w = r[1];
-            pb.x = fmaf(pa.x, w.x, -pa.y * w.y);
-            pb.y = fmaf(pa.y, w.x, pa.x * w.y);
-            pb.z = fmaf(pa.z, w.z, -pa.w * w.w);
-            pb.w = fmaf(pa.w, w.z, pa.z * w.w);
-            zstep32x(rx, qq, e1, e2, pa, xa, ya, za, pra, pna);
-            zstep32x(rx, qq, e1, e2, pb, xb, yb, zb, prb, pnb);
-            return;
+    // one step of both points (bloch.hpp:34-38, bloch.cpp:22-26)
+    auto step2 = [&](const float4* r, const float2 qq, const float4 e1, const float2 e2, const float4 pa) {
+        float4 w;  // one-df-step phasors: (wtc, wts) over te, (wrc, wrs) over the rest of TR
+        zf2 nX, nY, nZ;
+        if (XR) {  // r[0] = (r4, r5, r7, r8), r[1] = w
+            const float4 rx = r[0];
+            w = r[1];
+            nX = X;
+            nY = zfma2(Y, zbc(rx.x), zmul2(Zc, zbc(rx.y)));
+            nZ = zfma2(Y, zbc(rx.z), zmul2(Zc, zbc(rx.w)));
+        } else {
+            const float4 ra = r[0], rb = r[1], rc = r[2], rd = r[3];
+            w = make_float4(rc.w, rd.x, rd.y, rd.z);
+            nX = zfma2(X, zbc(ra.x), zfma2(Y, zbc(ra.y), zmul2(Zc, zbc(ra.z))));
+            nY = zfma2(X, zbc(ra.w), zfma2(Y, zbc(rb.x), zmul2(Zc, zbc(rb.y))));
+            nZ = zfma2(X, zbc(rb.z), zfma2(Y, zbc(rb.w), zmul2(Zc, zbc(rc.x))));
         }
-        const float4 ra = r[0], rb = r[1], rc = r[2], rd = r[3];
-        pb.x = fmaf(pa.x, rc.w, -pa.y * rd.x);
-        pb.y = fmaf(pa.y, rc.w, pa.x * rd.x);
-        pb.z = fmaf(pa.z, rd.y, -pa.w * rd.z);
-        pb.w = fmaf(pa.w, rd.y, pa.z * rd.z);
-        zstep32(ra, rb, rc, qq, e1, e2, pa, xa, ya, za, pra, pna);
-        zstep32(ra, rb, rc, qq, e1, e2, pb, xb, yb, zb, prb, pnb);
+        // E2-scaled phasors: point a from the table row, point b = a * w
+        const float cta = pa.x * e2.x, sta = pa.y * e2.x, cra = pa.z * e2.y, sra = pa.w * e2.y;
+        const zf2 Ct = zpk(cta, fmaf(cta, w.x, -sta * w.y)), St = zpk(sta, fmaf(sta, w.x, cta * w.y));
+        const zf2 Cr = zpk(cra, fmaf(cra, w.z, -sra * w.w)), Sr = zpk(sra, fmaf(sra, w.z, cra * w.w));
+        // relax/precess over te: the echo sample; z' = z E1 + (1 - E1)
+        const zf2 Xt = zfma2(zneg2(nY), St, zmul2(nX, Ct));
+        const zf2 Yt = zfma2(nX, St, zmul2(nY, Ct));
+        const zf2 Zt = zfma2(nZ, zbc(e1.x), zbc(e1.y));
+        DR = zfma2(Xt, zbc(qq.x), zfma2(Yt, zbc(qq.y), DR));
+        DI = zfma2(Yt, zbc(qq.x), zfma2(zneg2(Xt), zbc(qq.y), DI));
+        NN = zfma2(Yt, Yt, zfma2(Xt, Xt, NN));
+        // over the rest of TR
+        X = zfma2(zneg2(Yt), Sr, zmul2(Xt, Cr));
+        Y = zfma2(Xt, Sr, zmul2(Yt, Cr));
+        Zc = zfma2(Zt, zbc(e1.z), zbc(e1.w));
     };
-    auto fold = [&](zf2 pra, zf2 pna, zf2 prb, zf2 pnb) {
-        float r0, i0, n0, n1;
-        zup(pra, r0, i0);
-        zup(pna, n0, n1);
-        rea += r0;
-        ima += i0;
-        nna += n0 + n1;
-        zup(prb, r0, i0);
-        zup(pnb, n0, n1);
-        reb += r0;
-        imb += i0;
-        nnb += n0 + n1;
+    auto fold = [&]() {  // FP32 partial sums into FP64
+        float a, b;
+        zup(DR, a, b);
+        rea += a;
+        reb += b;
+        zup(DI, a, b);
+        ima += a;
+        imb += b;
+        zup(NN, a, b);
+        nna += a;
+        nnb += b;
+        DR = DI = NN = zpk(0.f, 0.f);
     };
     auto run = [&](const float4* E1, const float2* E2, const float4* PH, const float4* r, const float2* qb) {
-        zf2 pra = zpk(0.f, 0.f), pna = pra, prb = pra, pnb = pra;
 #pragma unroll
-        for (int m = 0; m < kB; ++m) step2(r + S * m, qb[m], E1[m], E2[m], PH[m], pra, pna, prb, pnb);
-        fold(pra, pna, prb, pnb);
+        for (int m = 0; m < kB; ++m) step2(r + S * m, qb[m], E1[m], E2[m], PH[m]);
     };
     const int nmain = n & ~(2 * kB - 1);
     load(A1, A2, AP, e1p, e2p, php);
     for (int jb = 0; jb < nmain; jb += 2 * kB) {
         if ((jb & 7) == 0) {  // one L1 prefetch per 128-byte line, 3 lines ahead
-            prefetch_l1(e1p + jb + 24);
-            prefetch_l1(php + jb + 24);
-            if ((jb & 15) == 0) prefetch_l1(e2p + jb + 32);
+            prefetch_l1(e1p + jb + kZPf);
+            prefetch_l1(php + jb + kZPf);
+            if ((jb & 15) == 0) {
+                prefetch_l1(e2p + jb + kZPf + 8);
+                fold();
+            }
         }
         load(B1, B2, BP, e1p + jb + kB, e2p + jb + kB, php + jb + kB);
         run(A1, A2, AP, rfp + S * jb, q + jb);
         load(A1, A2, AP, e1p + jb + 2 * kB, e2p + jb + 2 * kB, php + jb + 2 * kB);
         run(B1, B2, BP, rfp + S * (jb + kB), q + jb + kB);
     }
-    {  // tail: n % 4 steps
-        zf2 pra = zpk(0.f, 0.f), pna = pra, prb = pra, pnb = pra;
-        for (int j = nmain; j < n; ++j)
-            step2(rfp + S * j, q[j], __ldg(e1p + j), __ldg(e2p + j), __ldg(php + j), pra, pna, prb, pnb);
-        fold(pra, pna, prb, pnb);
-    }
+    for (int j = nmain; j < n; ++j)  // tail: n % 4 steps
+        step2(rfp + S * j, q[j], __ldg(e1p + j), __ldg(e2p + j), __ldg(php + j));
+    fold();
     Apx2 r;
     double inv = rsqrt(nna);
     r.a.cc = static_cast<float>(fmin(sqrt(rea * rea + ima * ima) * inv, 1.0));
