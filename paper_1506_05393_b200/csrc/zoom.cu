@@ -198,12 +198,13 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     const size_t fbytes = sizeof(double2) * 32 * c.n * nwarps;
     const size_t tbytes = sizeof(ZSlot) * cap * nwarps;
     const size_t pbytes = sizeof(int) * kPendCap * nwarps;
+    const size_t dbytes = sizeof(ZDec) * kDecCap * nwarps;
     const size_t bbytes = h_bounds ? sizeof(long long) * 6 * nvox : 0;
     const size_t rbytes = rows ? sizeof(int64_t) * (nrows + 1 + h_row_start[nrows]) + sizeof(int) * nvox : 0;
     const size_t ibytes = h_init ? sizeof(long long) * 2 * nvox : 0;
     const size_t vbytes = want_stats ? sizeof(long long) * 4 * nvox : 0;
     DevBuf& scratch = c.zoom;
-    scratch.ensure(fbytes + qbytes + tbytes + pbytes + bbytes + ibytes + rbytes + 256 + vbytes);
+    scratch.ensure(fbytes + qbytes + tbytes + dbytes + pbytes + bbytes + ibytes + rbytes + 256 + vbytes);
     char* base = scratch.as<char>();
     P.fpx = reinterpret_cast<double2*>(base);
     base += fbytes;
@@ -212,6 +213,8 @@ void run_quantify(Ctx& c, const mrfg_grid& lat, const mrfg_zoom_config& cfg, con
     base += qbytes;
     P.tab = reinterpret_cast<ZSlot*>(base);
     base += tbytes;
+    P.dec = reinterpret_cast<ZDec*>(base);
+    base += dbytes;
     P.pend = reinterpret_cast<int*>(base);
     base += pbytes;
     P.bounds = h_bounds ? reinterpret_cast<long long*>(base) : nullptr;

@@ -48,6 +48,19 @@ constexpr unsigned long long kEmpty = ~0ull;
 constexpr unsigned long long kAcq = 1ull << 63;  // "acquired" flag in the key word
 constexpr int kPendCap = 256;                    // deferred exact evaluations per warp
 constexpr int kEagerAfter = 6;                   // passes before certifying eagerly
+constexpr int kDecCap = 256;                     // uncertified decisions recorded per pass
+
+// An uncertified decision of the current pass (taken on screening values
+// closer than the margin): what was compared and how it came out.  After the
+// deferred points are exact the decisions are re-taken on exact values
+// (zflipped); when none flips, the replay would walk the identical path -- the
+// pass stands and the confirming replay is skipped.
+struct ZDec {
+    int kind;     // 0: a > b, 1: a < c, 2: spread(a, b, c) < eps
+    int metric, outcome, sa, sb, sc;  // memo slots (-1: the constant kept in v*)
+    double va, vb, vc;                // values at decision time; kind 1: vb = c, kind 2: eps in `eps`
+    double eps;
+};
 
 // Memo slot.  `acc`/`are` are the single-pass FP32 screening values (CC
 // magnitude and normalized real part); cc/euc/nrm2 are the reference's FP64
@@ -105,6 +118,7 @@ struct ZParams {
     float2* q32;        // nwarps x N normalized query, FP32
     double2* fpx;       // nwarps x N x 32 exact-evaluation fingerprints
     int* pend;          // nwarps x kPendCap deferred exact evaluations
+    ZDec* dec;          // nwarps x kDecCap uncertified decisions of the current pass
     ZSlot* tab;         // nwarps x cap memo tables
     unsigned long long* next;  // voxel work counter
     // neighbour-seeded slice (row wavefront): rows of masked
@@ -169,6 +183,9 @@ struct Z {
     double2* fpx;       // exact-evaluation scratch: n x 32 lanes
     int* pend;          // deferred exact evaluations (memo slots), kPendCap
     int npend;          // warp-uniform
+    ZDec* dec;          // uncertified decisions of this pass (kDecCap)
+    int ndec;           // warp-uniform; > kDecCap: overflow
+    int must_replay;    // the pass flushed mid-way or overflowed the record: replay it
     int eager;          // 1: certify each close decision immediately
     int stage1;         // inside search_df (df-dictionary acquisitions)
     int qw;             // shared-memory query slot (the voxel's warp in the block)
@@ -1286,7 +1303,58 @@ __device__ void zdefer(Z& z, const V& a) {
         z.pend[z.npend] = a.slot;
     }
     zsync();
-    if (++z.npend == kPendCap) zflush(z);
+    if (++z.npend == kPendCap) {
+        zflush(z);
+        z.must_replay = 1;  // later decisions of this pass saw exact values the earlier ones did not
+    }
+}
+
+__device__ void zrecord(Z& z, int kind, int metric, bool outcome, const V& a, const V* b, const V* c, double cval,
+                        double eps) {
+    if (z.ndec < kDecCap) {
+        if (z.lane == 0) {
+            ZDec d;
+            d.kind = kind;
+            d.metric = metric;
+            d.outcome = outcome ? 1 : 0;
+            d.sa = a.slot;
+            d.va = a.v;
+            d.sb = b ? b->slot : -1;
+            d.vb = b ? b->v : cval;
+            d.sc = c ? c->slot : -1;
+            d.vc = c ? c->v : 0.0;
+            d.eps = eps;
+            z.dec[z.ndec] = d;
+        }
+    } else {
+        z.must_replay = 1;
+    }
+    ++z.ndec;
+}
+
+// Re-take the pass's uncertified decisions on the (now exact) values; true
+// when any comes out differently.
+__device__ bool zflipped(Z& z) {
+    zsync();
+    bool flip = false;
+    const int nd = z.ndec < kDecCap ? z.ndec : kDecCap;
+    for (int k = z.lane; k < nd; k += 32) {
+        const ZDec d = z.dec[k];
+        const double a = d.sa >= 0 ? zread(z, d.sa, d.metric).v : d.va;
+        const double b = d.sb >= 0 ? zread(z, d.sb, d.metric).v : d.vb;
+        bool r;
+        if (d.kind == 0) {
+            r = a > b;
+        } else if (d.kind == 1) {
+            r = a < d.vb;
+        } else {
+            const double c = d.sc >= 0 ? zread(z, d.sc, d.metric).v : d.vc;
+            const double mn = fmin(a, fmin(b, c)), mx = fmax(a, fmax(b, c));
+            r = (mx - mn) < d.eps;
+        }
+        flip |= r != (d.outcome != 0);
+    }
+    return __any_sync(0xffffffffu, flip);
 }
 
 // The reference's `a > b` on objective values.  Screening values decide when
@@ -1300,6 +1368,7 @@ __device__ bool gt(Z& z, V& a, V& b, int metric) {
     if (!(a.exact && b.exact) && fabs(a.v - b.v) <= zmargin(z, metric)) {
         if (z.lane == 0) zstat(z, 3, 1);
         if (!z.eager) {
+            zrecord(z, 0, metric, a.v > b.v, a, &b, nullptr, 0.0, 0.0);
             zdefer(z, a);
             zdefer(z, b);
             return a.v > b.v;
@@ -1315,6 +1384,7 @@ __device__ bool gt(Z& z, V& a, V& b, int metric) {
 __device__ bool lt_const(Z& z, V& a, double c, int metric) {
     if (!a.exact && fabs(a.v - c) <= zmargin(z, metric)) {
         if (!z.eager) {
+            zrecord(z, 1, metric, a.v < c, a, nullptr, nullptr, c, 0.0);
             zdefer(z, a);
             return a.v < c;
         }
@@ -1465,6 +1535,7 @@ __device__ bool plateau(Z& z, V* marks, int nm, double eps) {
     const bool all_exact = marks[nm - 3].exact && marks[nm - 2].exact && marks[nm - 1].exact;
     if (!all_exact && fabs(s - eps) <= 2.0 * zmargin(z, metric)) {
         if (!z.eager) {
+            zrecord(z, 2, metric, s < eps, marks[nm - 3], &marks[nm - 2], &marks[nm - 1], 0.0, eps);
             for (int j = nm - 3; j < nm; ++j) zdefer(z, marks[j]);
             return s < eps;
         }
@@ -1812,6 +1883,8 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v, const long long* b
             zsync();
         }
         if (pass >= kEagerAfter) z.eager = 1;
+        z.ndec = 0;
+        z.must_replay = 0;
         z.evals = 0;
         z.ntrace = 0;
         z.tr_last = 0;
@@ -1853,6 +1926,10 @@ __device__ void zoom_voxel(Z& z, const ZParams& P, int64_t v, const long long* b
         if (z.lane == 0) zstat(z, 9, 1);
         if (z.npend == 0) break;  // every decision of this pass was certified
         zflush(z);
+        // the uncertified decisions re-taken on exact values: when none flips,
+        // the replay would repeat this pass step for step (same acquisitions,
+        // same trace), so the pass stands
+        if (!z.must_replay && !zflipped(z)) break;
     }
     // result (zoom.cpp:514-519): the exact score of the answer
     V score = zf(z, i1, i2, idf, P.metric);
@@ -1910,6 +1987,7 @@ __device__ void zwarp_setup(Z& z, const ZParams& P, int64_t w) {
     z.q = P.q + w * 2 * P.n;
     z.fpx = P.fpx + w * P.n * 32;
     z.pend = P.pend + w * kPendCap;
+    z.dec = P.dec + w * kDecCap;
     z.stage1 = 0;
     z.qw = static_cast<int>(threadIdx.x / 32);
     z.cta_w = 0;
@@ -1984,6 +2062,7 @@ __global__ void __launch_bounds__(BS, 1) k_zoom_rows(const ZParams P) {
     z.tab = P.tab + ctrl * (static_cast<int64_t>(P.cap_mask) + 1);
     z.q = P.q + ctrl * 2 * P.n;
     z.pend = P.pend + ctrl * kPendCap;
+    z.dec = P.dec + ctrl * kDecCap;
     extern __shared__ float4 zsm[];
     z.qw = 0;
     if (P.smem_stage)
