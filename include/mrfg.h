@@ -103,6 +103,13 @@ typedef struct {
     int64_t audit_samples, rescans;
     double rescreen_err_max;   /* max |FP32 re-screen - exact| over the FP64 survivors */
     int64_t chunk_atoms;       /* atoms per streamed chunk (whole lattice rows) */
+    /* Per-off-resonance subspace screening (opt-in, MRFG_SUBSPACE=r): complex
+     * rank used (0: off), time of the projection kernels, and the largest
+     * relative residual |a - P a| / |a| the projection measured (fp16 noise
+     * included). */
+    double project_ms;
+    int64_t subspace_rank;
+    double subspace_residual_max;
 } mrfg_scan_stats;
 
 /* ZoomConfig (zoom.hpp:23-52) as a POD; the step lists hold up to 8 values.

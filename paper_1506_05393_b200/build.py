@@ -17,7 +17,7 @@ SHIM = os.path.join(HERE, "libmrf_b200.so")  # the reference's C++ interface ove
 # zoom_k_var.cu holds the experimental K5 variants (compiled only with
 # MRFG_BUILD_VARIANTS=1; then it is the slowest object, so it is listed first)
 SOURCES = ["zoom_k_var.cu", "zoom_k_main.cu", "zoom_k_rows.cu", "zoom.cu", "abi.cu", "bloch.cu",
-           "match_sm100.cu", "rerank.cu", "synth.cpp"]
+           "match_sm100.cu", "rerank.cu", "subspace.cu", "synth.cpp"]
 HEADERS = ["mrfg_internal.cuh", "sim64.cuh"]
 # per-source extra dependencies
 EXTRA_DEPS = {s: ["zoom_dev.cuh", "zoom_launch.h"] for s in

@@ -91,6 +91,7 @@ static void check_grid(const mrfg_grid& g) {
 const GridTables& ensure_tables(Ctx& c, const mrfg_grid& g, bool /*need64*/) {
     if (c.tab.valid && same_grid(g, c.tab)) return c.tab;
     check_grid(g);
+    c.tab.sub_r = 0;  // the subspace bases belong to the grid
     const int64_t n = c.n, n1 = g.t1_ms.count, n2 = g.t2_ms.count, nd = g.df_hz.count;
     std::vector<double> e1(n * n1 * 2), e2(n * n2 * 2), ph(n * nd * 4);
     std::vector<float> e1f(n * n1 * 4), e2f(n * n2 * 2), phf(n * nd * 4);
@@ -270,6 +271,16 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
         chunk = std::max<int64_t>(1, int64_t(c.num_sms) * 2 * 256 / threads_per_row) * ndf;
     }
     const int64_t crows = std::max<int64_t>(1, chunk / ndf);
+    // Per-off-resonance subspace screening (subspace.cu; opt-in, whole-lattice
+    // CC scans with the atom-pair producer): MRFG_SUBSPACE = complex rank
+    int sub_r = 0;
+    if (const char* e = std::getenv("MRFG_SUBSPACE")) sub_r = std::atoi(e);
+    if (sub_r > 0) sub_r = sub_r <= 8 ? 8 : 16;
+    if (!(grid && metric == MRFG_METRIC_CC && fb == 0 && fe == total && bloch_dfquad_ok(c) && !seed_out &&
+          grid->t1_ms.count * grid->t2_ms.count >= 64))
+        sub_r = 0;
+    const int sub_nw = sub_r ? subspace_cols(sub_r) : 0;
+    const __half* sub_w = sub_r ? ensure_subspace(c, *tp, sub_r) : nullptr;  // cached per grid
     int64_t cap = (o && o->cand_capacity > 0) ? o->cand_capacity : (int64_t(1) << 25);
     const int64_t seed_atoms = (o && o->seed_atoms > 0) ? o->seed_atoms : 16384;
     const int64_t n = c.n, kp = k_pad_of(n), qrows = round_up(2 * nq, 256);
@@ -321,7 +332,7 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
     mp.delta = static_cast<float>(delta);
     mp.metric = metric;
 
-    double gemm_ms = 0, bloch_ms = 0;
+    double gemm_ms = 0, bloch_ms = 0, project_ms = 0, sub_rho2 = 0;
     int64_t gemm_launches = 0, chunks = 0;
     // Voxel batch: query rows of <= ~40 MB (L2 is 126 MB).  Measured on config 3
     // (stored dictionary): the GEMM runs at 1,255 / 1,039 / 890 TFLOP/s with
@@ -409,11 +420,79 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
         }();
         const cudaStream_t S = c.stream, A = overlap ? c.aux : c.stream;
         EventTimer ta(A);
-        std::vector<int> pm, gm;
+        std::vector<int> pm, gm, pj;
         MRFG_CUDA(cudaEventRecord(c.ev[0], S));
         MRFG_CUDA(cudaStreamWaitEvent(A, c.ev[0], 0));
         int64_t i = 0;
-        for (int64_t r0 = fb / ndf; r0 * ndf < fe; r0 += crows, ++i) {
+        if (sub_r) {
+            // df-major: K1 produces the four off-resonance slabs of a quad (all
+            // lattice rows each), every slab is projected onto its basis and
+            // screened by K2 in 2r dimensions against that df's query coefficients
+            const int64_t nrows = grid->t1_ms.count * grid->t2_ms.count, pitch = round_up(nrows, 256);
+            c.atoms_a.ensure(sizeof(__half) * 4 * pitch * kp);
+            c.inv2.ensure(sizeof(float) * 4 * pitch);
+            c.sub_c.ensure(sizeof(__half) * 4 * pitch * 64);
+            c.sub_q.ensure(sizeof(__half) * ndf * qrows * 64);
+            c.sub_rho.ensure(64);
+            __half* abuf = c.atoms_a.as<__half>();
+            float* ibuf = c.inv2.as<float>();
+            __half* cbuf = c.sub_c.as<__half>();
+            __half* qbuf = c.sub_q.as<__half>();
+            auto* rho = c.sub_rho.as<unsigned int>();
+            MRFG_CUDA(cudaMemsetAsync(abuf, 0, sizeof(__half) * 4 * pitch * kp, S));
+            MRFG_CUDA(cudaMemsetAsync(ibuf, 0, sizeof(float) * 4 * pitch, S));
+            MRFG_CUDA(cudaMemsetAsync(cbuf, 0, sizeof(__half) * 4 * pitch * 64, S));
+            MRFG_CUDA(cudaMemsetAsync(qbuf, 0, sizeof(__half) * ndf * qrows * 64, S));
+            MRFG_CUDA(cudaMemsetAsync(rho, 0, sizeof(unsigned int), S));
+            pm.push_back(tm.mark());
+            for (int64_t d = 0; d < ndf; ++d)
+                launch_project(c, c.qprime.as<__half>(), qrows, kp, sub_w + d * sub_nw * kp, sub_nw,
+                               qbuf + d * qrows * 64, nullptr, 0, nullptr);
+            pm.push_back(tm.mark());
+            for (int64_t q0 = 0; q0 < ndf; q0 += 4, ++i) {
+                pm.push_back(tm.mark());
+                launch_bloch_dfquad(c, *tp, static_cast<int>(q0), pitch, metric, abuf, ibuf);
+                pm.push_back(tm.mark());
+                for (int64_t m = 0; m < 4 && q0 + m < ndf; ++m) {
+                    const int64_t d = q0 + m;
+                    pj.push_back(tm.mark());
+                    launch_project(c, abuf + m * pitch * kp, pitch, kp, sub_w + d * sub_nw * kp, sub_nw,
+                                   cbuf + m * pitch * 64, ibuf + m * pitch, nrows, rho);
+                    pj.push_back(tm.mark());
+                    mp.a = cbuf + m * pitch * 64;
+                    mp.inv2 = ibuf + m * pitch;
+                    mp.atoms = pitch;
+                    mp.k_pad = 64;
+                    mp.k_valid = sub_nw;
+                    mp.valid_begin = 0;
+                    mp.valid_atoms = nrows;
+                    mp.flat_base = d;
+                    mp.flat_stride = ndf;
+                    mp.b = qbuf + d * qrows * 64;
+                    mp.q_rows = qrows;
+                    mp.nvox = nq;
+                    mp.best = best;
+                    mp.vox_base = 0;
+                    gm.push_back(tm.mark());
+                    launch_match(c, mp);
+                    gm.push_back(tm.mark());
+                }
+                ++chunks;
+            }
+            mp.k_pad = kp;
+            mp.k_valid = 0;
+            unsigned int rbits = 0;
+            MRFG_CUDA(cudaMemcpyAsync(&rbits, rho, sizeof rbits, cudaMemcpyDeviceToHost, S));
+            MRFG_CUDA(cudaStreamSynchronize(S));
+            float r2;
+            std::memcpy(&r2, &rbits, sizeof r2);
+            sub_rho2 = r2;
+            for (size_t k = 0; k + 1 < pj.size(); k += 2) project_ms += tm.ms(pj[k], pj[k + 1]);
+            // pm holds tm marks here (one stream)
+            for (size_t k = 0; k + 1 < pm.size(); k += 2) bloch_ms += tm.ms(pm[k], pm[k + 1]);
+            pm.clear();
+        }
+        for (int64_t r0 = fb / ndf; !sub_r && r0 * ndf < fe; r0 += crows, ++i) {
             const int64_t vb = std::max(fb, r0 * ndf), ve = std::min(fe, (r0 + crows) * ndf);
             const int64_t base = r0 * ndf;
             const int64_t rows = round_up(ve - base, 256);
@@ -526,7 +605,10 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
         st->audit_samples = nsamp;
         st->delta_used = delta;
         st->rescreen_err_max = err32;
-        st->chunk_atoms = crows * ndf;
+        st->chunk_atoms = sub_r ? grid->t1_ms.count * grid->t2_ms.count : crows * ndf;
+        st->project_ms = project_ms;
+        st->subspace_rank = sub_r;
+        st->subspace_residual_max = sub_rho2 > 0 ? std::sqrt(sub_rho2) : 0.0;
         st->rerank_ms += tm.ms(ra0, ra1);
     }
     return true;

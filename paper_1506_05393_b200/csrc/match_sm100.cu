@@ -773,7 +773,7 @@ void launch_match(Ctx& c, const MatchParams& p) {
                                    static_cast<int>(SMEM_BYTES)));
     MRFG_CUDA(cudaFuncSetAttribute(k_match_sm100_2cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(SMEM2_BYTES)));
-    Dev d = dev_of(p, 2 * c.n);
+    Dev d = dev_of(p, p.k_valid > 0 ? p.k_valid : 2 * c.n);
     if (use_pair_kernel() && p.atoms % 256 == 0) {
         CUtensorMap ma = make_map(c, p.a, p.atoms, p.k_pad, 128);
         CUtensorMap mb = make_map(c, p.b, p.q_rows, p.k_pad, BN / 2);
@@ -794,7 +794,7 @@ void launch_match(Ctx& c, const MatchParams& p) {
 }
 
 void launch_match_simt(Ctx& c, const MatchParams& p) {
-    Dev d = dev_of(p, 2 * c.n);
+    Dev d = dev_of(p, p.k_valid > 0 ? p.k_valid : 2 * c.n);
     dim3 grid(static_cast<unsigned>((p.atoms + 127) / 128), static_cast<unsigned>(p.nvox));
     k_match_simt<<<grid, 128, 0, c.stream>>>(p.a, p.b, p.k_pad, d, p.atoms, p.debug_scores);
     MRFG_CUDA(cudaGetLastError());

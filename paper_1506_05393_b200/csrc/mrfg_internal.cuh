@@ -99,6 +99,9 @@ struct GridTables {
     // FP64, same index order: e1d[(i*n+j)*2 + {0,1}] = (E1te, E1rest); e2d likewise;
     // phd[(i*n+j)*4 + {0..3}] = (cos te, sin te, cos rest, sin rest)
     DevBuf e1d, e2d, phd;
+    // subspace screening (MRFG_SUBSPACE=r): per-df bases W[df][cols][k_pad] (fp16), built on first use
+    DevBuf subw;
+    int sub_r = 0;
 };
 
 struct Ctx {
@@ -120,7 +123,8 @@ struct Ctx {
     DevBuf q64, qprime, best, cand, cand_count, atoms_a, inv2, seed_a, seed_inv2, rerank,
         params, out64, misc, rerank_scratch, misc2, audit,
         // persistent buffers of the host-buffer entry points (no per-call cudaMalloc)
-        h_raw, h_res, h_dict, h_zdict, h_trace, zidx, zib;
+        h_raw, h_res, h_dict, h_zdict, h_trace, zidx, zib,
+        sub_c, sub_q, sub_rho;  // subspace screening: atom / query coefficients, max residual
     // producer stream + events for the K1/K2 overlap (created on first use)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev[8] = {};
@@ -168,6 +172,14 @@ int64_t launch_bloch_rows(Ctx& c, const GridTables& t, int64_t vb, int64_t ve, i
                           int64_t rows, __half* d_a, float* d_outf, float* d_inv2,
                           const float2* d_q32 = nullptr);
 void launch_bloch_norms(Ctx& c, const GridTables& t, int64_t first, int64_t count, float* d_norm2);
+// subspace screening (subspace.cu)
+int subspace_cols(int r);
+const __half* ensure_subspace(Ctx& c, const GridTables& t, int r);
+void launch_project(Ctx& c, const __half* A, int64_t rows, int64_t kpad, const __half* W, int nw, __half* out,
+                    const float* inv2, int64_t valid, unsigned int* rho2max);
+bool bloch_dfquad_ok(const Ctx& c);
+void launch_bloch_dfquad(Ctx& c, const GridTables& t, int idf0, int64_t pitch, int metric, __half* d_a,
+                         float* d_inv2);
 
 // K2 (match_sm100.cu)
 struct CandRec {
@@ -182,6 +194,7 @@ struct MatchParams {
     int64_t atoms;      // multiple of 128
     int64_t q_rows;     // multiple of 256
     int64_t k_pad;      // multiple of 64
+    int64_t k_valid = 0;  // valid K elements (0: 2 * timepoints); subspace operands: 2 * rank
     int64_t valid_atoms;  // local atoms in [valid_begin, valid_atoms) are real
     int64_t valid_begin;
     int64_t nvox;

@@ -520,3 +520,19 @@ def test_seeded_shards_equal_single_scan(small, small_ref):
     out = d_out.cpu().numpy()
     assert_parity(out[:, 0], out[:, 1].view(np.float64), *small_ref)
     assert seeded <= plain
+
+
+def test_subspace_screening_same_answers(small, monkeypatch):
+    """Experimental per-off-resonance subspace screening (MRFG_SUBSPACE, csrc/subspace.cu):
+    the K1 off-resonance-major slabs, the projection and K2 on one K block only
+    change WHICH atoms survive the screen; the audit-driven margin and the exact
+    FP64 re-rank keep best atoms and scores identical to the default path
+    (dictionary.cpp:257-308)."""
+    with P.Context(small.schedule) as c:
+        monkeypatch.delenv("MRFG_SUBSPACE", raising=False)
+        f0, s0, st0 = c.scan_grid(small.grid, small.fps)
+        monkeypatch.setenv("MRFG_SUBSPACE", "16")
+        f1, s1, st1 = c.scan_grid(small.grid, small.fps)
+    assert st0.subspace_rank == 0 and st1.subspace_rank == 16 and st1.project_ms > 0
+    np.testing.assert_array_equal(f0, f1)
+    np.testing.assert_array_equal(s0, s1)
