@@ -275,11 +275,11 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
     // CC scans with the atom-pair producer): MRFG_SUBSPACE = complex rank
     int sub_r = 0;
     if (const char* e = std::getenv("MRFG_SUBSPACE")) sub_r = std::atoi(e);
-    if (sub_r > 0) sub_r = sub_r <= 8 ? 8 : 16;
+    if (sub_r > 0) sub_r = subspace_rank(sub_r);
     if (!(grid && metric == MRFG_METRIC_CC && fb == 0 && fe == total && bloch_dfquad_ok(c) && !seed_out &&
           grid->t1_ms.count * grid->t2_ms.count >= 64))
         sub_r = 0;
-    const int sub_nw = sub_r ? subspace_cols(sub_r) : 0;
+    const int sub_nw = sub_r ? subspace_cols(sub_r) : 0, sub_kc = sub_r ? subspace_pitch(sub_r) : 0;
     const __half* sub_w = sub_r ? ensure_subspace(c, *tp, sub_r) : nullptr;  // cached per grid
     int64_t cap = (o && o->cand_capacity > 0) ? o->cand_capacity : (int64_t(1) << 25);
     const int64_t seed_atoms = (o && o->seed_atoms > 0) ? o->seed_atoms : 16384;
@@ -431,8 +431,8 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
             const int64_t nrows = grid->t1_ms.count * grid->t2_ms.count, pitch = round_up(nrows, 256);
             c.atoms_a.ensure(sizeof(__half) * 4 * pitch * kp);
             c.inv2.ensure(sizeof(float) * 4 * pitch);
-            c.sub_c.ensure(sizeof(__half) * 4 * pitch * 64);
-            c.sub_q.ensure(sizeof(__half) * ndf * qrows * 64);
+            c.sub_c.ensure(sizeof(__half) * 4 * pitch * sub_kc);
+            c.sub_q.ensure(sizeof(__half) * ndf * qrows * sub_kc);
             c.sub_rho.ensure(64);
             __half* abuf = c.atoms_a.as<__half>();
             float* ibuf = c.inv2.as<float>();
@@ -441,14 +441,14 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
             auto* rho = c.sub_rho.as<unsigned int>();
             MRFG_CUDA(cudaMemsetAsync(abuf, 0, sizeof(__half) * 4 * pitch * kp, S));
             MRFG_CUDA(cudaMemsetAsync(ibuf, 0, sizeof(float) * 4 * pitch, S));
-            MRFG_CUDA(cudaMemsetAsync(cbuf, 0, sizeof(__half) * 4 * pitch * 64, S));
-            MRFG_CUDA(cudaMemsetAsync(qbuf, 0, sizeof(__half) * ndf * qrows * 64, S));
+            MRFG_CUDA(cudaMemsetAsync(cbuf, 0, sizeof(__half) * 4 * pitch * sub_kc, S));
+            MRFG_CUDA(cudaMemsetAsync(qbuf, 0, sizeof(__half) * ndf * qrows * sub_kc, S));
             MRFG_CUDA(cudaMemsetAsync(rho, 0, sizeof(unsigned int), S));
-            pm.push_back(tm.mark());
+            pj.push_back(tm.mark());
             for (int64_t d = 0; d < ndf; ++d)
                 launch_project(c, c.qprime.as<__half>(), qrows, kp, sub_w + d * sub_nw * kp, sub_nw,
-                               qbuf + d * qrows * 64, nullptr, 0, nullptr);
-            pm.push_back(tm.mark());
+                               qbuf + d * qrows * sub_kc, sub_kc, nullptr, 0, nullptr);
+            pj.push_back(tm.mark());
             for (int64_t q0 = 0; q0 < ndf; q0 += 4, ++i) {
                 pm.push_back(tm.mark());
                 launch_bloch_dfquad(c, *tp, static_cast<int>(q0), pitch, metric, abuf, ibuf);
@@ -457,18 +457,18 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
                     const int64_t d = q0 + m;
                     pj.push_back(tm.mark());
                     launch_project(c, abuf + m * pitch * kp, pitch, kp, sub_w + d * sub_nw * kp, sub_nw,
-                                   cbuf + m * pitch * 64, ibuf + m * pitch, nrows, rho);
+                                   cbuf + m * pitch * sub_kc, sub_kc, ibuf + m * pitch, nrows, rho);
                     pj.push_back(tm.mark());
-                    mp.a = cbuf + m * pitch * 64;
+                    mp.a = cbuf + m * pitch * sub_kc;
                     mp.inv2 = ibuf + m * pitch;
                     mp.atoms = pitch;
-                    mp.k_pad = 64;
+                    mp.k_pad = sub_kc;
                     mp.k_valid = sub_nw;
                     mp.valid_begin = 0;
                     mp.valid_atoms = nrows;
                     mp.flat_base = d;
                     mp.flat_stride = ndf;
-                    mp.b = qbuf + d * qrows * 64;
+                    mp.b = qbuf + d * qrows * sub_kc;
                     mp.q_rows = qrows;
                     mp.nvox = nq;
                     mp.best = best;

@@ -173,10 +173,12 @@ int64_t launch_bloch_rows(Ctx& c, const GridTables& t, int64_t vb, int64_t ve, i
                           const float2* d_q32 = nullptr);
 void launch_bloch_norms(Ctx& c, const GridTables& t, int64_t first, int64_t count, float* d_norm2);
 // subspace screening (subspace.cu)
-int subspace_cols(int r);
+int subspace_rank(int r);   // supported complex ranks: 8, 16, 32, 48, 64
+int subspace_cols(int r);   // real basis rows, 2 r
+int subspace_pitch(int r);  // coefficient row pitch (multiple of 64: K2's K blocks)
 const __half* ensure_subspace(Ctx& c, const GridTables& t, int r);
 void launch_project(Ctx& c, const __half* A, int64_t rows, int64_t kpad, const __half* W, int nw, __half* out,
-                    const float* inv2, int64_t valid, unsigned int* rho2max);
+                    int opitch, const float* inv2, int64_t valid, unsigned int* rho2max);
 bool bloch_dfquad_ok(const Ctx& c);
 void launch_bloch_dfquad(Ctx& c, const GridTables& t, int idf0, int64_t pitch, int metric, __half* d_a,
                          float* d_inv2);

@@ -20,12 +20,16 @@
 //           rescans when the sampled error exceeds delta/2) and the exact FP64
 //           re-rank are unchanged, so the answers are the default path's.
 //
-// Status: the pipeline (K1 off-resonance-major slabs, projection, K2 on one K
-// block, audit, re-rank) runs end to end with identical answers, but this
-// kernel holds the whole basis in shared memory, which caps the rank at 16 --
-// at that rank the residual reaches 0.17 on config 2, the audit widens the
-// margin to ~0.1 and the scan is no faster than the default.  Rank 48-64 needs
-// the basis tiled through shared memory.
+// Status: the pipeline (K1 off-resonance-major slabs, projection, K2 on one or
+// two K blocks, audit, re-rank) runs end to end with identical answers at
+// complex ranks 8 .. 64, but it is not profitable yet (config 2, one B200):
+// the bases from pivoted Gram-Schmidt over 4r sampled atoms leave the worst
+// atoms of a slab at a residual of 0.07 whatever the rank (the SVD of 2,500
+// samples reaches 3e-4 at rank 64), so the audit widens the margin to ~0.05
+// (1.2e8 candidates, K3 0.5 s); this mma.sync projection runs at 0.6 TB/s
+// (0.7 s per scan) and K2 takes 0.93 s: 2.45 s against 2.77 s.  Missing: a
+// better basis (SVD / more samples), a projection kernel at the HBM roofline
+// (~0.06 s), an accurate per-atom residual for the analytic certificate.
 //
 // k_project: out[row][0..63] = sum_k A[row][k] W[n][k] (fp16 in, fp32
 // accumulate, fp16 out; columns >= NW stay zero), mma.sync m16n8k16 with a
@@ -34,7 +38,6 @@
 
 #include <algorithm>
 #include <cmath>
-#include <complex>
 #include <cstring>
 #include <vector>
 
@@ -54,21 +57,18 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// A: rows x kpad (fp16, K-major, rows a multiple of 128); W: NW x kpad; out: rows x 64.
-// inv2 (1/|a|^2 per row, or null): when given, rho2max <- max over rows < valid of
-// 1 - |P a|^2 / |a|^2 (as float bits; values are clamped at 0).
+// A: rows x kpad (fp16, K-major, rows a multiple of 128); W: NW x kpad; out: rows x opitch.
+// The basis goes through shared memory KT columns at a time (KT = kpad when
+// the whole basis fits).  inv2 (1/|a|^2 per row, or null): when given,
+// rho2max <- max over rows < valid of 1 - |P a|^2 / |a|^2 (float bits, >= 0;
+// the fp16 rounding of W and A puts a floor of ~1e-4 under it).
 template <int NW>
-__global__ void __launch_bounds__(256) k_project(const __half* __restrict__ A, int64_t kpad,
+__global__ void __launch_bounds__(256) k_project(const __half* __restrict__ A, int64_t kpad, int kt,
                                                  const __half* __restrict__ W, __half* __restrict__ out,
-                                                 const float* __restrict__ inv2, int64_t valid,
+                                                 int opitch, const float* __restrict__ inv2, int64_t valid,
                                                  unsigned int* __restrict__ rho2max) {
-    extern __shared__ __align__(16) __half wsm[];  // NW x (kpad + kWPad)
-    const int64_t wp = kpad + kWPad;
-    for (int64_t i = threadIdx.x; i < NW * (kpad / 8); i += blockDim.x) {
-        const int64_t n = i / (kpad / 8), k8 = i % (kpad / 8);
-        *reinterpret_cast<uint4*>(wsm + n * wp + 8 * k8) = *reinterpret_cast<const uint4*>(W + n * kpad + 8 * k8);
-    }
-    __syncthreads();
+    extern __shared__ __align__(16) __half wsm[];  // NW x (kt + kWPad)
+    const int wp = kt + kWPad;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int64_t r0 = blockIdx.x * static_cast<int64_t>(kProjRows) + warp * 16;
     const __half* a_lo = A + (r0 + g) * kpad + 8 * t;
@@ -81,20 +81,29 @@ __global__ void __launch_bounds__(256) k_project(const __half* __restrict__ A, i
     // 32 K elements per step (thread t holds k0 + 8t .. 8t+7 of rows g, g+8);
     // two steps are in flight
     uint4 lo = *reinterpret_cast<const uint4*>(a_lo), hi = *reinterpret_cast<const uint4*>(a_hi);
-    for (int64_t k0 = 0; k0 < kpad; k0 += 32) {
-        uint4 nlo = lo, nhi = hi;
-        if (k0 + 32 < kpad) {
-            nlo = *reinterpret_cast<const uint4*>(a_lo + k0 + 32);
-            nhi = *reinterpret_cast<const uint4*>(a_hi + k0 + 32);
+    for (int64_t kt0 = 0; kt0 < kpad; kt0 += kt) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < NW * (kt / 8); i += blockDim.x) {
+            const int n = i / (kt / 8), k8 = i % (kt / 8);
+            *reinterpret_cast<uint4*>(wsm + n * wp + 8 * k8) =
+                *reinterpret_cast<const uint4*>(W + static_cast<int64_t>(n) * kpad + kt0 + 8 * k8);
         }
+        __syncthreads();
+        for (int k0 = 0; k0 < kt; k0 += 32) {
+            uint4 nlo = lo, nhi = hi;
+            if (kt0 + k0 + 32 < kpad) {
+                nlo = *reinterpret_cast<const uint4*>(a_lo + kt0 + k0 + 32);
+                nhi = *reinterpret_cast<const uint4*>(a_hi + kt0 + k0 + 32);
+            }
 #pragma unroll
-        for (int j = 0; j < NW / 8; ++j) {
-            const uint4 b = *reinterpret_cast<const uint4*>(wsm + (8 * j + g) * wp + k0 + 8 * t);
-            mma16816(acc[j], lo.x, hi.x, lo.y, hi.y, b.x, b.y);
-            mma16816(acc[j], lo.z, hi.z, lo.w, hi.w, b.z, b.w);
+            for (int j = 0; j < NW / 8; ++j) {
+                const uint4 b = *reinterpret_cast<const uint4*>(wsm + (8 * j + g) * wp + k0 + 8 * t);
+                mma16816(acc[j], lo.x, hi.x, lo.y, hi.y, b.x, b.y);
+                mma16816(acc[j], lo.z, hi.z, lo.w, hi.w, b.z, b.w);
+            }
+            lo = nlo;
+            hi = nhi;
         }
-        lo = nlo;
-        hi = nhi;
     }
     // rows g (acc[..][0,1]) and g + 8 (acc[..][2,3]); columns 8 j + 2 t, + 1
     float s_lo = 0.f, s_hi = 0.f;
@@ -102,8 +111,8 @@ __global__ void __launch_bounds__(256) k_project(const __half* __restrict__ A, i
     for (int j = 0; j < NW / 8; ++j) {
         s_lo = fmaf(acc[j][0], acc[j][0], fmaf(acc[j][1], acc[j][1], s_lo));
         s_hi = fmaf(acc[j][2], acc[j][2], fmaf(acc[j][3], acc[j][3], s_hi));
-        *reinterpret_cast<__half2*>(out + (r0 + g) * 64 + 8 * j + 2 * t) = __floats2half2_rn(acc[j][0], acc[j][1]);
-        *reinterpret_cast<__half2*>(out + (r0 + g + 8) * 64 + 8 * j + 2 * t) =
+        *reinterpret_cast<__half2*>(out + (r0 + g) * opitch + 8 * j + 2 * t) = __floats2half2_rn(acc[j][0], acc[j][1]);
+        *reinterpret_cast<__half2*>(out + (r0 + g + 8) * opitch + 8 * j + 2 * t) =
             __floats2half2_rn(acc[j][2], acc[j][3]);
     }
     if (inv2) {
@@ -120,24 +129,37 @@ __global__ void __launch_bounds__(256) k_project(const __half* __restrict__ A, i
     }
 }
 
+template <int NW>
+void project_variant(Ctx& c, const __half* A, int64_t rows, int64_t kpad, const __half* W, __half* out, int opitch,
+                     const float* inv2, int64_t valid, unsigned int* rho2max) {
+    // the largest K tile (a divisor of kpad, multiple of 32) whose basis tile fits ~128 KB
+    int kt = static_cast<int>(kpad);
+    while (static_cast<int64_t>(sizeof(__half)) * NW * (kt + kWPad) > 132 * 1024 && kt % 64 == 0) kt /= 2;
+    const int smem = static_cast<int>(sizeof(__half) * NW * (kt + kWPad));
+    MRFG_CUDA(cudaFuncSetAttribute(k_project<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_project<NW><<<static_cast<unsigned>(rows / kProjRows), 256, smem, c.stream>>>(A, kpad, kt, W, out, opitch, inv2,
+                                                                                   valid, rho2max);
+    MRFG_CUDA(cudaGetLastError());
+}
+
 }  // namespace
 
-int subspace_cols(int r) { return r <= 8 ? 16 : 32; }
+// complex rank -> real basis rows (2r) and the operand width K2 sees (a multiple of 64)
+int subspace_rank(int r) { return r <= 8 ? 8 : (r <= 16 ? 16 : (r <= 32 ? 32 : (r <= 48 ? 48 : 64))); }
+int subspace_cols(int r) { return 2 * subspace_rank(r); }
+int subspace_pitch(int r) { return (subspace_cols(r) + 63) / 64 * 64; }
 
 void launch_project(Ctx& c, const __half* A, int64_t rows, int64_t kpad, const __half* W, int nw, __half* out,
-                    const float* inv2, int64_t valid, unsigned int* rho2max) {
-    MRFG_REQUIRE(rows % kProjRows == 0 && kpad % 32 == 0 && (nw == 16 || nw == 32), MRFG_E_INVALID,
-                 "project: bad operand shape");
-    const int smem = static_cast<int>(sizeof(__half) * nw * (kpad + kWPad));
-    const unsigned grid = static_cast<unsigned>(rows / kProjRows);
-    if (nw == 16) {
-        MRFG_CUDA(cudaFuncSetAttribute(k_project<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        k_project<16><<<grid, 256, smem, c.stream>>>(A, kpad, W, out, inv2, valid, rho2max);
-    } else {
-        MRFG_CUDA(cudaFuncSetAttribute(k_project<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        k_project<32><<<grid, 256, smem, c.stream>>>(A, kpad, W, out, inv2, valid, rho2max);
+                    int opitch, const float* inv2, int64_t valid, unsigned int* rho2max) {
+    MRFG_REQUIRE(rows % kProjRows == 0 && kpad % 64 == 0, MRFG_E_INVALID, "project: bad operand shape");
+    switch (nw) {
+        case 16: project_variant<16>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max); break;
+        case 32: project_variant<32>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max); break;
+        case 64: project_variant<64>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max); break;
+        case 96: project_variant<96>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max); break;
+        case 128: project_variant<128>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max); break;
+        default: throw Error{MRFG_E_INVALID, "project: unsupported basis width"};
     }
-    MRFG_CUDA(cudaGetLastError());
 }
 
 // The bases of every off-resonance slab of the cached grid: W[df][nw][kpad]
@@ -149,52 +171,70 @@ const __half* ensure_subspace(Ctx& c, const GridTables& tc, int r) {
     GridTables& t = const_cast<GridTables&>(tc);
     const int nw = subspace_cols(r);
     const int64_t n = c.n, kp = k_pad_of(n);
-    const int64_t ndf = t.grid.df_hz.count, nrows = t.grid.t1_ms.count * t.grid.t2_ms.count;
+    const int64_t ndf = t.grid.df_hz.count, n1 = t.grid.t1_ms.count, n2 = t.grid.t2_ms.count;
     if (t.sub_r == r && t.subw.p) return t.subw.as<__half>();
-    constexpr int kSamples = 64;
-    const int64_t step = std::max<int64_t>(1, (nrows - 1) / (kSamples - 1));
-    const int64_t ns = std::min<int64_t>(kSamples, (nrows + step - 1) / step);
+    // sample atoms of a slab: an s1 x s2 grid over (T1, T2) that includes both
+    // ends of each axis (the slab's extreme atoms sit on its edges)
+    const int64_t want = std::max<int64_t>(64, 4 * r);
+    int64_t s2 = std::min<int64_t>(n2, 16), s1 = std::min<int64_t>(n1, (want + s2 - 1) / s2);
+    const int64_t st2 = s2 > 1 ? (n2 - 1) / (s2 - 1) : 1;
+    const int64_t ns = s1 * s2;
     MRFG_REQUIRE(ns >= r, MRFG_E_INVALID, "subspace: fewer lattice rows than the rank");
-    const int64_t srows = 256;  // operand producer granularity
     DevBuf samp, sinv;
-    samp.ensure(sizeof(__half) * srows * kp * ndf);
-    sinv.ensure(sizeof(float) * srows);
+    samp.ensure(sizeof(__half) * ns * kp * ndf);
+    sinv.ensure(sizeof(float) * 256);
     for (int64_t d = 0; d < ndf; ++d)
-        launch_bloch_operand(c, t, d, step * ndf, nrows * ndf, srows, MRFG_METRIC_CC,
-                             samp.as<__half>() + d * srows * kp, sinv.as<float>());
-    std::vector<__half> hs(static_cast<size_t>(srows) * kp * ndf);
+        for (int64_t a = 0; a < s1; ++a) {
+            const int64_t i1 = s1 > 1 ? a * (n1 - 1) / (s1 - 1) : 0;
+            launch_bloch_operand(c, t, (i1 * n2) * ndf + d, st2 * ndf, (i1 * n2 + n2) * ndf, s2, MRFG_METRIC_CC,
+                                 samp.as<__half>() + (d * ns + a * s2) * kp, sinv.as<float>());
+        }
+    std::vector<__half> hs(static_cast<size_t>(ns) * kp * ndf);
     MRFG_CUDA(cudaMemcpyAsync(hs.data(), samp.p, sizeof(__half) * hs.size(), cudaMemcpyDeviceToHost, c.stream));
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
+    const int64_t srows = ns;
     std::vector<__half> hw(static_cast<size_t>(ndf) * nw * kp, __float2half(0.f));
-#pragma omp parallel for schedule(dynamic, 4)
+#pragma omp parallel for schedule(dynamic, 2)
     for (int64_t d = 0; d < ndf; ++d) {
-        std::vector<std::complex<double>> v(static_cast<size_t>(ns) * n), b(static_cast<size_t>(r) * n);
-        std::vector<double> res(ns);
+        // sample residuals (re, im planes) and the current basis vector
+        std::vector<double> vr(static_cast<size_t>(ns) * n), vi(static_cast<size_t>(ns) * n), br(n), bi(n), res(ns);
         for (int64_t k = 0; k < ns; ++k) {
             const __half* row = hs.data() + (d * srows + k) * kp;
             double nn = 0;
             for (int64_t j = 0; j < n; ++j) {
-                const std::complex<double> z(__half2float(row[2 * j]), __half2float(row[2 * j + 1]));
-                v[k * n + j] = z;
-                nn += std::norm(z);
+                const double x = __half2float(row[2 * j]), y = __half2float(row[2 * j + 1]);
+                vr[k * n + j] = x;
+                vi[k * n + j] = y;
+                nn += x * x + y * y;
             }
             const double inv = nn > 0 ? 1.0 / std::sqrt(nn) : 0.0;
-            for (int64_t j = 0; j < n; ++j) v[k * n + j] *= inv;
+            for (int64_t j = 0; j < n; ++j) {
+                vr[k * n + j] *= inv;
+                vi[k * n + j] *= inv;
+            }
             res[k] = nn > 0 ? 1.0 : 0.0;
         }
         for (int m = 0; m < r; ++m) {
             const int64_t piv = std::max_element(res.begin(), res.end()) - res.begin();
             if (res[piv] < 1e-20) break;  // the samples are exhausted: the remaining rows stay zero
             const double inv = 1.0 / std::sqrt(res[piv]);
-            std::complex<double>* bm = &b[static_cast<size_t>(m) * n];
-            for (int64_t j = 0; j < n; ++j) bm[j] = v[piv * n + j] * inv;
+            for (int64_t j = 0; j < n; ++j) {
+                br[j] = vr[piv * n + j] * inv;
+                bi[j] = vi[piv * n + j] * inv;
+            }
             for (int64_t k = 0; k < ns; ++k) {
-                std::complex<double> dot = 0;
-                for (int64_t j = 0; j < n; ++j) dot += std::conj(bm[j]) * v[k * n + j];
+                double* xr = &vr[k * n];
+                double* xi = &vi[k * n];
+                double dr = 0, di = 0;  // <b, v_k> = sum conj(b) v
+                for (int64_t j = 0; j < n; ++j) {
+                    dr += br[j] * xr[j] + bi[j] * xi[j];
+                    di += br[j] * xi[j] - bi[j] * xr[j];
+                }
                 double nn = 0;
                 for (int64_t j = 0; j < n; ++j) {
-                    v[k * n + j] -= dot * bm[j];
-                    nn += std::norm(v[k * n + j]);
+                    xr[j] -= dr * br[j] - di * bi[j];
+                    xi[j] -= dr * bi[j] + di * br[j];
+                    nn += xr[j] * xr[j] + xi[j] * xi[j];
                 }
                 res[k] = nn;
             }
@@ -203,10 +243,10 @@ const __half* ensure_subspace(Ctx& c, const GridTables& tc, int r) {
             __half* u = hw.data() + (d * nw + 2 * m) * kp;
             __half* ju = u + kp;
             for (int64_t j = 0; j < n; ++j) {
-                u[2 * j] = __float2half(static_cast<float>(bm[j].real()));
-                u[2 * j + 1] = __float2half(static_cast<float>(bm[j].imag()));
-                ju[2 * j] = __float2half(static_cast<float>(-bm[j].imag()));
-                ju[2 * j + 1] = __float2half(static_cast<float>(bm[j].real()));
+                u[2 * j] = __float2half(static_cast<float>(br[j]));
+                u[2 * j + 1] = __float2half(static_cast<float>(bi[j]));
+                ju[2 * j] = __float2half(static_cast<float>(-bi[j]));
+                ju[2 * j + 1] = __float2half(static_cast<float>(br[j]));
             }
         }
     }
