@@ -271,14 +271,19 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
         chunk = std::max<int64_t>(1, int64_t(c.num_sms) * 2 * 256 / threads_per_row) * ndf;
     }
     const int64_t crows = std::max<int64_t>(1, chunk / ndf);
-    // Per-off-resonance subspace screening (subspace.cu; opt-in, whole-lattice
-    // CC scans with the atom-pair producer): MRFG_SUBSPACE = complex rank
+    // Per-off-resonance subspace screening (subspace.cu): CC scans of whole
+    // lattice rows with the atom-pair producer.  Default: complex rank 32 when
+    // the range is large enough to pay for the projections (>= 2e7 atoms,
+    // >= 4,096 lattice rows); MRFG_SUBSPACE=0 turns it off, =r forces rank r.
     int sub_r = 0;
-    if (const char* e = std::getenv("MRFG_SUBSPACE")) sub_r = std::atoi(e);
+    const bool sub_ok = grid && metric == MRFG_METRIC_CC && fb % ndf == 0 && fe % ndf == 0 && bloch_dfquad_ok(c) &&
+                        !seed_out && (fe - fb) / ndf >= 256 && grid->t1_ms.count * grid->t2_ms.count >= 640;
+    if (const char* e = std::getenv("MRFG_SUBSPACE"))
+        sub_r = std::atoi(e);
+    else if (sub_ok && fe - fb >= 20000000 && (fe - fb) / ndf >= 4096)
+        sub_r = 32;
     if (sub_r > 0) sub_r = subspace_rank(sub_r);
-    if (!(grid && metric == MRFG_METRIC_CC && fb == 0 && fe == total && bloch_dfquad_ok(c) && !seed_out &&
-          grid->t1_ms.count * grid->t2_ms.count >= 64))
-        sub_r = 0;
+    if (!sub_ok) sub_r = 0;
     const int sub_nw = sub_r ? subspace_cols(sub_r) : 0, sub_kc = sub_r ? subspace_pitch(sub_r) : 0;
     const __half* sub_w = sub_r ? ensure_subspace(c, *tp, sub_r) : nullptr;  // cached per grid
     int64_t cap = (o && o->cand_capacity > 0) ? o->cand_capacity : (int64_t(1) << 25);
@@ -428,7 +433,7 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
             // df-major: K1 produces the four off-resonance slabs of a quad (all
             // lattice rows each), every slab is projected onto its basis and
             // screened by K2 in 2r dimensions against that df's query coefficients
-            const int64_t nrows = grid->t1_ms.count * grid->t2_ms.count, pitch = round_up(nrows, 256);
+            const int64_t row_lo = fb / ndf, nrows = (fe - fb) / ndf, pitch = round_up(nrows, 256);
             c.atoms_a.ensure(sizeof(__half) * 4 * pitch * kp);
             c.inv2.ensure(sizeof(float) * 4 * pitch);
             c.sub_c.ensure(sizeof(__half) * 4 * pitch * sub_kc);
@@ -451,7 +456,7 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
             pj.push_back(tm.mark());
             for (int64_t q0 = 0; q0 < ndf; q0 += 4, ++i) {
                 pm.push_back(tm.mark());
-                launch_bloch_dfquad(c, *tp, static_cast<int>(q0), pitch, metric, abuf, ibuf);
+                launch_bloch_dfquad(c, *tp, static_cast<int>(q0), row_lo, nrows, pitch, metric, abuf, ibuf);
                 pm.push_back(tm.mark());
                 for (int64_t m = 0; m < 4 && q0 + m < ndf; ++m) {
                     const int64_t d = q0 + m;
@@ -466,7 +471,7 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
                     mp.k_valid = sub_nw;
                     mp.valid_begin = 0;
                     mp.valid_atoms = nrows;
-                    mp.flat_base = d;
+                    mp.flat_base = row_lo * ndf + d;
                     mp.flat_stride = ndf;
                     mp.b = qbuf + d * qrows * sub_kc;
                     mp.q_rows = qrows;
@@ -605,7 +610,7 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
         st->audit_samples = nsamp;
         st->delta_used = delta;
         st->rescreen_err_max = err32;
-        st->chunk_atoms = sub_r ? grid->t1_ms.count * grid->t2_ms.count : crows * ndf;
+        st->chunk_atoms = sub_r ? (fe - fb) / ndf : crows * ndf;
         st->project_ms = project_ms;
         st->subspace_rank = sub_r;
         st->subspace_residual_max = sub_rho2 > 0 ? std::sqrt(sub_rho2) : 0.0;

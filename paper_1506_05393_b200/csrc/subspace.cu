@@ -163,43 +163,67 @@ void launch_project(Ctx& c, const __half* A, int64_t rows, int64_t kpad, const _
 }
 
 // The bases of every off-resonance slab of the cached grid: W[df][nw][kpad]
-// (fp16).  Per df, kSamples atoms spread over the (T1, T2) rows are produced
-// by the FP32 operand producer (fp16 rows, as screened), copied to the host,
-// and orthonormalized by pivoted Gram-Schmidt in double precision: the
-// largest remaining residual becomes the next basis vector until r are found.
+// (fp16).  About 5 r sample rows (T1, T2) are produced at ALL their
+// off-resonance values by the FP32 operand producer (fp16 rows, as screened),
+// copied to the host, and per df orthonormalized by pivoted Gram-Schmidt in
+// double precision: the largest remaining residual becomes the next basis
+// vector until r are found.
 const __half* ensure_subspace(Ctx& c, const GridTables& tc, int r) {
     GridTables& t = const_cast<GridTables&>(tc);
     const int nw = subspace_cols(r);
     const int64_t n = c.n, kp = k_pad_of(n);
     const int64_t ndf = t.grid.df_hz.count, n1 = t.grid.t1_ms.count, n2 = t.grid.t2_ms.count;
     if (t.sub_r == r && t.subw.p) return t.subw.as<__half>();
-    // sample atoms of a slab: an s1 x s2 grid over (T1, T2) that includes both
-    // ends of each axis (the slab's extreme atoms sit on its edges)
-    const int64_t want = std::max<int64_t>(64, 4 * r);
-    int64_t s2 = std::min<int64_t>(n2, 16), s1 = std::min<int64_t>(n1, (want + s2 - 1) / s2);
-    const int64_t st2 = s2 > 1 ? (n2 - 1) / (s2 - 1) : 1;
-    const int64_t ns = s1 * s2;
-    MRFG_REQUIRE(ns >= r, MRFG_E_INVALID, "subspace: fewer lattice rows than the rank");
-    DevBuf samp, sinv;
-    samp.ensure(sizeof(__half) * ns * kp * ndf);
-    sinv.ensure(sizeof(float) * 256);
-    for (int64_t d = 0; d < ndf; ++d)
-        for (int64_t a = 0; a < s1; ++a) {
-            const int64_t i1 = s1 > 1 ? a * (n1 - 1) / (s1 - 1) : 0;
-            launch_bloch_operand(c, t, (i1 * n2) * ndf + d, st2 * ndf, (i1 * n2 + n2) * ndf, s2, MRFG_METRIC_CC,
-                                 samp.as<__half>() + (d * ns + a * s2) * kp, sinv.as<float>());
+    // sample atoms of a slab: an s1 x s2 grid over (T1, T2) whose axis VALUES are
+    // geometrically spaced, both ends included -- the fingerprints change
+    // fastest at short T2 / T1 (an evenly spaced 16-point T2 grid left atoms
+    // between its first two points at a residual of 0.07 whatever the rank)
+    auto geo = [](const mrfg_axis& ax, int64_t cnt) {
+        const int64_t nn = ax.count;
+        std::vector<int64_t> idx;
+        const double lo = axis_value(ax, 0), hi = axis_value(ax, nn - 1);
+        for (int64_t k = 0; k < cnt; ++k) {
+            const double v = cnt > 1 && lo > 0 && hi > lo ? lo * std::pow(hi / lo, static_cast<double>(k) / (cnt - 1))
+                                                           : lo + (hi - lo) * (cnt > 1 ? double(k) / (cnt - 1) : 0.0);
+            int64_t a = 0, b = nn - 1;  // nearest index on the (monotonic) axis
+            while (b - a > 1) {
+                const int64_t m = (a + b) / 2;
+                (axis_value(ax, m) <= v ? a : b) = m;
+            }
+            const int64_t i = std::fabs(axis_value(ax, b) - v) < std::fabs(axis_value(ax, a) - v) ? b : a;
+            if (idx.empty() || idx.back() != i) idx.push_back(i);
         }
-    std::vector<__half> hs(static_cast<size_t>(ns) * kp * ndf);
+        return idx;
+    };
+    const int64_t want2 = r > 48 ? 28 : 24;
+    const std::vector<int64_t> I2 = geo(t.grid.t2_ms, std::min<int64_t>(n2, want2));
+    const std::vector<int64_t> I1 = geo(t.grid.t1_ms, std::min<int64_t>(n1, std::max<int64_t>(6, (5 * r + want2 - 1) / want2)));
+    const int64_t ns = static_cast<int64_t>(I1.size() * I2.size());
+    MRFG_REQUIRE(ns >= r, MRFG_E_INVALID, "subspace: fewer lattice rows than the rank");
+    // one launch per sample row: all its off-resonance values (flat stride 1)
+    DevBuf samp, sinv;
+    samp.ensure(sizeof(__half) * ns * ndf * kp);
+    sinv.ensure(sizeof(float) * ndf);
+    {
+        int64_t k = 0;
+        for (int64_t i1 : I1)
+            for (int64_t i2 : I2) {
+                const int64_t row = i1 * n2 + i2;
+                launch_bloch_operand(c, t, row * ndf, 1, (row + 1) * ndf, ndf, MRFG_METRIC_CC,
+                                     samp.as<__half>() + k * ndf * kp, sinv.as<float>());
+                ++k;
+            }
+    }
+    std::vector<__half> hs(static_cast<size_t>(ns) * ndf * kp);
     MRFG_CUDA(cudaMemcpyAsync(hs.data(), samp.p, sizeof(__half) * hs.size(), cudaMemcpyDeviceToHost, c.stream));
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
-    const int64_t srows = ns;
     std::vector<__half> hw(static_cast<size_t>(ndf) * nw * kp, __float2half(0.f));
 #pragma omp parallel for schedule(dynamic, 2)
     for (int64_t d = 0; d < ndf; ++d) {
         // sample residuals (re, im planes) and the current basis vector
         std::vector<double> vr(static_cast<size_t>(ns) * n), vi(static_cast<size_t>(ns) * n), br(n), bi(n), res(ns);
         for (int64_t k = 0; k < ns; ++k) {
-            const __half* row = hs.data() + (d * srows + k) * kp;
+            const __half* row = hs.data() + (k * ndf + d) * kp;  // sample k at off-resonance d
             double nn = 0;
             for (int64_t j = 0; j < n; ++j) {
                 const double x = __half2float(row[2 * j]), y = __half2float(row[2 * j + 1]);
