@@ -215,7 +215,7 @@ def arm_config(args, world, nx, ny, n, nq, total):
                         f"{total} atoms, brute-force streamed DGS",
             "voxels": nq, "atoms": total, "timepoints": n,
             "chunk_atoms": args.chunk or "library default (one K1 wave of whole lattice rows)",
-            "delta": args.delta or 2.5e-3, "parallelism": f"atom-shard x{world}",
+            "delta": args.delta or "library default (2.5e-3; + twice the held-out residual with subspace screening)", "parallelism": f"atom-shard x{world}",
             "l2": "256 MB flush per step; each step streams >100 GB of fp16 atoms"}
 
 
@@ -343,6 +343,26 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     e2e_s = allmax((time.perf_counter() - t0) / e2e_steps, world)
 
+    # ---- the same step with full-length (2N-dimensional) screening, one scan:
+    # the regime the K2 tensor roofline describes
+    full = None
+    if world == 1 and not args.no_full and os.environ.get("MRFG_SUBSPACE") is None:
+        os.environ["MRFG_SUBSPACE"] = "0"
+        try:
+            ctx.scan_grid_device(g, d_q.data_ptr(), nq, d_out.data_ptr(), opts=opts, flat_range=(fb, fe))  # warm
+            sf = ctx.scan_grid_device(g, d_q.data_ptr(), nq, d_out.data_ptr(), opts=opts, flat_range=(fb, fe))
+            torch.cuda.synchronize()
+        finally:
+            del os.environ["MRFG_SUBSPACE"]
+        ftf = 8.0 * n * nq * (fe - fb) / (sf.gemm_ms * 1e-3) / 1e12
+        pkf, _ = peaks()
+        full = {"ms_per_step": sf.total_ms, "value": nq * (fe - fb) / (sf.total_ms * 1e-3), "unit": UNIT,
+                "breakdown_ms": {"bloch": sf.bloch_ms, "gemm": sf.gemm_ms, "rerank": sf.rerank_ms},
+                "k2_tflops": ftf, "k2_frac_of_tensor_peak": ftf / pkf.get("bf16_tflops_sustained", pkf["bf16_tflops"]),
+                "screen_err_audit_max": sf.screen_err_audit_max, "delta": sf.delta_used,
+                "candidates": sf.candidates, "atoms_per_launch": int(sf.chunk_atoms),
+                "how": "MRFG_SUBSPACE=0, one scan after a warm-up scan, device-resident queries, the ABI's CUDA events"}
+
     # ---- MRF-ZOOM on the same slice (K5), voxel-sharded, device-resident
     zoom = None
     if not args.no_zoom:
@@ -434,8 +454,14 @@ def run_ours(args, world, rank, local):
     pk, pk_kind = peaks()
     gemm_ms = sum(s.gemm_ms for s in stats)
     launches = sum(s.gemm_launches for s in stats)
-    flops_alg = 8.0 * n * nq * (fe - fb) * len(stats)
+    # K2 flops: 8 flop per voxel-atom pair and complex dimension it multiplies
+    # over -- N timepoints with full-length screening, r with per-off-resonance
+    # subspace screening (the library's default on this lattice)
+    sub_r = int(stats[-1].subspace_rank)
+    kdim = sub_r if sub_r else n
+    flops_alg = 8.0 * kdim * nq * (fe - fb) * len(stats)
     gemm_tflops = flops_alg / (gemm_ms * 1e-3) / 1e12
+    project_ms = sum(s.project_ms for s in stats)
     chunk_atoms = int(stats[-1].chunk_atoms)  # atoms per K2 launch (the library's choice when --chunk 0)
     peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     bloch_ms = sum(s.bloch_ms for s in stats)
@@ -454,7 +480,8 @@ def run_ours(args, world, rank, local):
         "bloch_fp32_tflops": bloch_rate * BLOCH_FLOP_PER_STEP / 1e12,
         "bloch_frac_of_fp32_peak_nominal": bloch_rate * BLOCH_FLOP_PER_STEP / 1e12 / FP32_PEAK_TFLOPS_NOMINAL,
         "candidates_per_step": cand, "reranked_per_step": rer,
-        "breakdown_ms_per_step": {"bloch": bloch_ms / len(stats), "gemm": gemm_ms / len(stats),
+        "breakdown_ms_per_step": {"bloch": bloch_ms / len(stats), "project": project_ms / len(stats),
+                                  "gemm": gemm_ms / len(stats),
                                   "rerank": sum(s.rerank_ms for s in stats) / len(stats),
                                   "scan_total": sum(s.total_ms for s in stats) / len(stats)},
         "screen_err_max": max(s.screen_err_max for s in stats),
@@ -466,9 +493,27 @@ def run_ours(args, world, rank, local):
                                  "certificate needs err_max <= delta/2"},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
                      "frac": gemm_tflops / peak_t, "traffic": k2_traffic(chunk_atoms, n, nq),
-                     "kernel": "k_match_sm100_2cta (K2)", "peak_kind": f"{pk_kind} bf16 dense sustained",
+                     "kernel": "k_match_sm100_2cta (K2)" + (f" on {2 * sub_r} subspace dimensions" if sub_r else ""),
+                     "peak_kind": f"{pk_kind} bf16 dense sustained",
                      "avg_launch_ms": gemm_ms / max(launches, 1),
-                     "flop_per_launch": 8.0 * n * nq * chunk_atoms, "atoms_per_launch": chunk_atoms},
+                     "flop_per_launch": 8.0 * kdim * nq * chunk_atoms, "atoms_per_launch": chunk_atoms,
+                     "k_dims": 2 * kdim,
+                     "pairs_per_s": nq * (fe - fb) * len(stats) / (gemm_ms * 1e-3),
+                     "note": ("executed tensor flops (8 r per voxel-atom pair); with 2r-dimensional operands K2 "
+                              "is bound by its epilogue (TMEM loads, score, threshold per pair), see "
+                              "full_length_screening for the 2N-dimensional regime") if sub_r else
+                             "algorithmic flops 8 N per voxel-atom pair"},
+        # the projection kernel of subspace screening: HBM-bound (reads the fp16
+        # atom operand once, writes 2r coefficients per atom)
+        "roofline_project": None if not sub_r else {
+            "bound": "hbm", "unit": "GB/s", "peak": pk["hbm_gbs"], "kernel": "k_project (mma.sync m16n8k16)",
+            "achieved": (fe - fb) * len(stats) * 2.0 * (2 * n + 2 * sub_r) / (project_ms * 1e-3) / 1e9,
+            "frac": (fe - fb) * len(stats) * 2.0 * (2 * n + 2 * sub_r) / (project_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+            "bytes_per_atom": 2.0 * (2 * n + 2 * sub_r), "traffic": None},
+        "screening": {"subspace_rank": sub_r, "residual_held_out_max": stats[-1].subspace_residual_max,
+                      "residual_device_estimate_max": stats[-1].subspace_residual_device,
+                      "note": "per-off-resonance subspace screening (csrc/subspace.cu); MRFG_SUBSPACE=0 = full length"},
+        "full_length_screening": full,
         "e2e": {"value": nq * total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nq * n * 16,
                 "d2h_bytes_per_step": nq * 16, "seconds_per_step": e2e_s},
         # our kernels per scan: per chunk K1 + K2 (+ k_zero_rows for the chunk's
@@ -476,7 +521,10 @@ def run_ours(args, world, rank, local):
         # re-rank: filter, keys, FP32 re-screen, flag, FP64 re-rank, select,
         # FP32 error check, write (CUB sort/select kernels not counted); the
         # screening audit; + seed pass and k_merge when N > 1
-        "gpu_launches": int(sum(3 * s.chunks + 13 for s in stats) + (3 * args.steps if world > 1 else 0)),
+        # subspace screening: per scan one K1 launch per off-resonance quad (chunks),
+        # per off-resonance value a slab projection, a K2 launch and a query projection
+        "gpu_launches": int(sum((s.chunks + 3 * g.df_hz.count + 13) if s.subspace_rank else (3 * s.chunks + 13)
+                                for s in stats) + (3 * args.steps if world > 1 else 0)),
         "clocks": clk.summary(),
         "zoom": zoom,
     }
@@ -499,6 +547,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--nvox", type=int, default=None)
     ap.add_argument("--atoms", type=int, default=0, help="limit atoms (debug only)")
+    ap.add_argument("--no-full", action="store_true", help="skip the full-length-screening comparison scan")
     ap.add_argument("--chunk", type=int, default=0, help="atoms per streamed chunk (0: the library default)")
     ap.add_argument("--delta", type=float, default=0.0, help="screening margin (0: library default 2.5e-3)")
     ap.add_argument("--ref-voxels", type=int, default=64)

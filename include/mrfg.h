@@ -103,13 +103,17 @@ typedef struct {
     int64_t audit_samples, rescans;
     double rescreen_err_max;   /* max |FP32 re-screen - exact| over the FP64 survivors */
     int64_t chunk_atoms;       /* atoms per streamed chunk (whole lattice rows) */
-    /* Per-off-resonance subspace screening (opt-in, MRFG_SUBSPACE=r): complex
-     * rank used (0: off), time of the projection kernels, and the largest
-     * relative residual |a - P a| / |a| the projection measured (fp16 noise
-     * included). */
+    /* Per-off-resonance subspace screening (csrc/subspace.cu; default for large
+     * lattice scans, MRFG_SUBSPACE=0 off): complex rank used (0: full-length
+     * screening), time of the projection kernels, the largest relative
+     * residual |a - P a| / |a| over the held-out rows of the basis
+     * construction (the default margin grows by twice it), and the device
+     * estimate 1 - |P a|^2 / |a|^2 over every screened atom (its fp16 noise
+     * floor is ~0.02). */
     double project_ms;
     int64_t subspace_rank;
     double subspace_residual_max;
+    double subspace_residual_device;
 } mrfg_scan_stats;
 
 /* ZoomConfig (zoom.hpp:23-52) as a POD; the step lists hold up to 8 values.

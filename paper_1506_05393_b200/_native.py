@@ -45,7 +45,7 @@ class ScanStats(C.Structure):
                 ("delta_used", C.c_double), ("audit_samples", C.c_int64), ("rescans", C.c_int64),
                 ("rescreen_err_max", C.c_double), ("chunk_atoms", C.c_int64),
                 ("project_ms", C.c_double), ("subspace_rank", C.c_int64),
-                ("subspace_residual_max", C.c_double)]
+                ("subspace_residual_max", C.c_double), ("subspace_residual_device", C.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

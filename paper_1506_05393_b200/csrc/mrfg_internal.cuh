@@ -102,6 +102,7 @@ struct GridTables {
     // subspace screening (MRFG_SUBSPACE=r): per-df bases W[df][cols][k_pad] (fp16), built on first use
     DevBuf subw;
     int sub_r = 0;
+    double sub_rho_held = 0;  // largest relative residual |a - P a| / |a| over the held-out rows, all df
 };
 
 struct Ctx {

@@ -200,9 +200,21 @@ const __half* ensure_subspace(Ctx& c, const GridTables& tc, int r) {
     const std::vector<int64_t> I1 = geo(t.grid.t1_ms, std::min<int64_t>(n1, std::max<int64_t>(6, (5 * r + want2 - 1) / want2)));
     const int64_t ns = static_cast<int64_t>(I1.size() * I2.size());
     MRFG_REQUIRE(ns >= r, MRFG_E_INVALID, "subspace: fewer lattice rows than the rank");
+    // held-out rows: the index midpoints between neighbouring samples (where an
+    // interpolating basis is worst); their residual is the truncation error the
+    // scan adds to its screening margin
+    auto mids = [](const std::vector<int64_t>& v) {
+        std::vector<int64_t> m;
+        for (size_t k = 0; k + 1 < v.size(); ++k)
+            if (v[k + 1] - v[k] > 1) m.push_back((v[k] + v[k + 1]) / 2);
+        if (m.empty()) m.push_back(v[0]);
+        return m;
+    };
+    const std::vector<int64_t> H1 = mids(I1), H2 = mids(I2);
+    const int64_t nh = static_cast<int64_t>(H1.size() * H2.size());
     // one launch per sample row: all its off-resonance values (flat stride 1)
     DevBuf samp, sinv;
-    samp.ensure(sizeof(__half) * ns * ndf * kp);
+    samp.ensure(sizeof(__half) * (ns + nh) * ndf * kp);
     sinv.ensure(sizeof(float) * ndf);
     {
         int64_t k = 0;
@@ -213,13 +225,22 @@ const __half* ensure_subspace(Ctx& c, const GridTables& tc, int r) {
                                      samp.as<__half>() + k * ndf * kp, sinv.as<float>());
                 ++k;
             }
+        for (int64_t i1 : H1)
+            for (int64_t i2 : H2) {
+                const int64_t row = i1 * n2 + i2;
+                launch_bloch_operand(c, t, row * ndf, 1, (row + 1) * ndf, ndf, MRFG_METRIC_CC,
+                                     samp.as<__half>() + k * ndf * kp, sinv.as<float>());
+                ++k;
+            }
     }
-    std::vector<__half> hs(static_cast<size_t>(ns) * ndf * kp);
+    std::vector<__half> hs(static_cast<size_t>(ns + nh) * ndf * kp);
     MRFG_CUDA(cudaMemcpyAsync(hs.data(), samp.p, sizeof(__half) * hs.size(), cudaMemcpyDeviceToHost, c.stream));
     MRFG_CUDA(cudaStreamSynchronize(c.stream));
     std::vector<__half> hw(static_cast<size_t>(ndf) * nw * kp, __float2half(0.f));
-#pragma omp parallel for schedule(dynamic, 2)
+    double rho2_held = 0;
+#pragma omp parallel for schedule(dynamic, 2) reduction(max : rho2_held)
     for (int64_t d = 0; d < ndf; ++d) {
+        std::vector<double> Br(static_cast<size_t>(r) * n, 0.0), Bi(static_cast<size_t>(r) * n, 0.0);  // the basis
         // sample residuals (re, im planes) and the current basis vector
         std::vector<double> vr(static_cast<size_t>(ns) * n), vi(static_cast<size_t>(ns) * n), br(n), bi(n), res(ns);
         for (int64_t k = 0; k < ns; ++k) {
@@ -263,6 +284,8 @@ const __half* ensure_subspace(Ctx& c, const GridTables& tc, int r) {
                 res[k] = nn;
             }
             res[piv] = 0;
+            std::copy(br.begin(), br.end(), Br.begin() + static_cast<size_t>(m) * n);
+            std::copy(bi.begin(), bi.end(), Bi.begin() + static_cast<size_t>(m) * n);
             // real embedding: u = (re, im, ...), J u = (-im, re, ...)
             __half* u = hw.data() + (d * nw + 2 * m) * kp;
             __half* ju = u + kp;
@@ -273,7 +296,28 @@ const __half* ensure_subspace(Ctx& c, const GridTables& tc, int r) {
                 ju[2 * j + 1] = __float2half(static_cast<float>(br[j]));
             }
         }
+        // residual of the held-out rows: 1 - |B^H a|^2 / |a|^2
+        for (int64_t k = 0; k < nh; ++k) {
+            const __half* row = hs.data() + ((ns + k) * ndf + d) * kp;
+            double nn = 0;
+            for (int64_t j = 0; j < 2 * n; ++j) nn += double(__half2float(row[j])) * double(__half2float(row[j]));
+            if (!(nn > 0)) continue;
+            double pp = 0;
+            for (int m = 0; m < r; ++m) {
+                const double* xr = &Br[static_cast<size_t>(m) * n];
+                const double* xi = &Bi[static_cast<size_t>(m) * n];
+                double dr = 0, di = 0;
+                for (int64_t j = 0; j < n; ++j) {
+                    const double ar = __half2float(row[2 * j]), ai = __half2float(row[2 * j + 1]);
+                    dr += xr[j] * ar + xi[j] * ai;
+                    di += xr[j] * ai - xi[j] * ar;
+                }
+                pp += dr * dr + di * di;
+            }
+            rho2_held = std::max(rho2_held, 1.0 - pp / nn);
+        }
     }
+    t.sub_rho_held = std::sqrt(std::max(0.0, rho2_held));
     t.subw.ensure(sizeof(__half) * hw.size());
     MRFG_CUDA(cudaMemcpyAsync(t.subw.p, hw.data(), sizeof(__half) * hw.size(), cudaMemcpyHostToDevice, c.stream));
     MRFG_CUDA(cudaStreamSynchronize(c.stream));

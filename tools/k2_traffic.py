@@ -24,7 +24,7 @@ def main():
     b = json.loads(line)
     atoms = b["roofline"]["atoms_per_launch"]
     nq, n = b["config"]["voxels"], b["config"]["timepoints"]
-    kpad = (2 * n + 63) // 64 * 64
+    kpad = (b["roofline"].get("k_dims", 2 * n) + 63) // 64 * 64  # operand width K2 sees
     arows = (atoms + 255) // 256 * 256
     qrows = (2 * nq + 255) // 256 * 256
     alg = (arows + qrows) * kpad * 2
