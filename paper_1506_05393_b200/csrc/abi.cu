@@ -273,14 +273,14 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
     const int64_t crows = std::max<int64_t>(1, chunk / ndf);
     // Per-off-resonance subspace screening (subspace.cu): CC scans of whole
     // lattice rows with the atom-pair producer.  Default: complex rank 48 when
-    // the range is large enough to pay for the projections (>= 2e7 atoms,
-    // >= 4,096 lattice rows); MRFG_SUBSPACE=0 turns it off, =r forces rank r.
+    // the range is large enough to pay for the projections (>= 4e6 atoms and
+    // >= 4,096 lattice rows: also the atom shards of an 8-GPU config-2 scan); MRFG_SUBSPACE=0 turns it off, =r forces rank r.
     int sub_r = 0;
     const bool sub_ok = grid && metric == MRFG_METRIC_CC && fb % ndf == 0 && fe % ndf == 0 && bloch_dfquad_ok(c) &&
                         !seed_out && (fe - fb) / ndf >= 256 && grid->t1_ms.count * grid->t2_ms.count >= 640;
     if (const char* e = std::getenv("MRFG_SUBSPACE"))
         sub_r = std::atoi(e);
-    else if (sub_ok && fe - fb >= 20000000 && (fe - fb) / ndf >= 4096)
+    else if (sub_ok && fe - fb >= 4000000 && (fe - fb) / ndf >= 4096)
         sub_r = 48;  // held-out residual 5e-4 on config 2 (rank 32: 3e-3, a margin of 8.6e-3 and an overflow pass)
     if (sub_r > 0) sub_r = subspace_rank(sub_r);
     if (!sub_ok) sub_r = 0;

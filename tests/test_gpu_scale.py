@@ -53,6 +53,44 @@ def test_config2_full_lattice_vs_reference(orc):
     np.testing.assert_array_equal(flat[v], d["flat"])
     np.testing.assert_array_equal(score[v], d["score"])
     assert st.rescans == 0 and st.screen_err_audit_max <= 0.5 * st.delta_used
+    assert st.subspace_rank == 48  # the default on this lattice (csrc/subspace.cu)
+
+
+def test_config2_full_length_screening_vs_reference(orc, monkeypatch):
+    """The same scan with full-length (2N-dimensional) screening, MRFG_SUBSPACE=0."""
+    d = load("scale_c2.npz")
+    monkeypatch.setenv("MRFG_SUBSPACE", "0")
+    wl = workloads.make(2, oracle_sim(orc))
+    with P.Context(wl.schedule) as c:
+        flat, score, st = c.scan_grid(wl.grid, wl.fps)
+    assert st.subspace_rank == 0 and st.rescans == 0
+    v = d["voxels"]
+    np.testing.assert_array_equal(flat[v], d["flat"])
+    np.testing.assert_array_equal(score[v], d["score"])
+
+
+def test_config2_atom_shards_subspace_vs_reference(orc):
+    """The 8-GPU partition of the config-2 scan on one device: every T1 slab
+    (12.2 M atoms, scanned with per-off-resonance subspace screening like the
+    whole lattice) and the host form of the merge; 256 voxels against the
+    reference, all 4,096 against the one-scan result."""
+    from paper_1506_05393_b200 import distributed as D
+    d = load("scale_c2.npz")
+    wl = workloads.make(2, oracle_sim(orc))
+    with P.Context(wl.schedule) as c:
+        flat, score, st = c.scan_grid(wl.grid, wl.fps)
+        assert st.subspace_rank > 0 and st.rescans == 0
+        fs, ss = [], []
+        for r in range(8):
+            f, s, sr = c.scan_grid(wl.grid, wl.fps, flat_range=D.grid_shard(wl.grid, 8, r))
+            assert sr.subspace_rank == st.subspace_rank
+            fs.append(f)
+            ss.append(s)
+    mf, ms = D.merge_matches(np.stack(fs), np.stack(ss))
+    np.testing.assert_array_equal(mf, flat)
+    np.testing.assert_array_equal(ms, score)
+    np.testing.assert_array_equal(mf[d["voxels"]], d["flat"])
+    np.testing.assert_array_equal(ms[d["voxels"]], d["score"])
 
 
 def test_config3_log_axes_vs_reference(orc):
