@@ -3,8 +3,12 @@
 
 One step = one full brute-force dictionary generating-and-searching pass of
 the 4,096-voxel slice over the whole T1 x T2 x df grid: FP32 Bloch producer
-(K1) -> fp16 tcgen05 screening GEMM with fused candidate epilogue (K2) ->
-exact FP64 re-rank (K3), streamed in chunks so the dictionary never exists.
+(K1) -> [projection of each off-resonance slab onto its subspace basis] ->
+fp16 tcgen05 screening GEMM with fused candidate epilogue (K2) -> exact FP64
+re-rank (K3), streamed in chunks so the dictionary never exists.  The
+library screens this lattice in per-off-resonance subspaces by default
+(csrc/subspace.cu); `full_length_screening` in the JSON line is one scan of the
+same step with the 2N-dimensional screening (MRFG_SUBSPACE=0).
 With N GPUs the atom range is sharded (contiguous T1-major slabs) and the
 per-voxel (flat, score) pairs are merged after one NCCL all_gather (C1):
 total work is fixed, so scaling is "strong".
