@@ -30,7 +30,7 @@ def main():
     alg = (arows + qrows) * kpad * 2
     out = {"kernel": "k_match_sm100_2cta (K2)",
            "source": "ncu --set full --clock-control none, one k_match_sm100_2cta launch of python bench.py "
-                     "--steps 1 --warmup 1 --no-cpu-baseline --no-zoom --atoms 4194304 (-s 4 -c 1), "
+                     "--steps 1 --warmup 1 --no-cpu-baseline --no-zoom --no-full (-s 4 -c 1), "
                      "profiles/r02_ncu/ncu_k2_raw.csv.gz",
            "chunk_atoms": atoms, "voxels": nq, "timepoints": n,
            "dram_bytes_read": rd, "dram_bytes_write": wr,
