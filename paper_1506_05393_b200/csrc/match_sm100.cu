@@ -66,6 +66,12 @@ struct Dev {
     unsigned long long* audit_count;
     int64_t audit_cap;
     uint32_t audit_thr;
+    // two-level audit sample (same expected fraction audit_thr / 2^32 of all
+    // pairs, still independent of the scores): atoms whose hash has its top
+    // audit_shift bits clear, then pairs whose mixed hash is below
+    // audit_thr << audit_shift -- the per-pair hash is computed for 1/2^shift
+    // of the atom rows only (it was half of the epilogue's per-pair work)
+    uint32_t audit_shift, audit_thr_pairs;
 };
 
 // Tile t -> (atom tile, query tile).  ga = 1: atom-major (the query operand
@@ -376,6 +382,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const bool avalid = atom >= p.valid_begin && atom < p.valid_atoms;
             const float inv = __ldg(p.inv2 + atom);
             const uint32_t ha = audit_hash_flat(static_cast<uint64_t>(p.flat_base + atom * p.flat_stride));
+            const bool asamp = p.audit_thr != 0u && avalid && (p.audit_shift == 0u || (ha >> (32u - p.audit_shift)) == 0u);
             const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
@@ -399,11 +406,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         if ((hits >> i) & 1u)
                             store_hit(p, s.bst[acc][q * 32 + i], vt * 128 + q * 32 + i, atom, sc[i], slot++);
                 }
-                if (p.audit_thr != 0u && avalid) {
+                if (asamp) {
                     uint32_t samp = 0;
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
-                        samp |= (audit_mix(ha, s.hv[acc][q * 32 + i]) < p.audit_thr ? 1u : 0u) << i;
+                        samp |= (audit_mix(ha, s.hv[acc][q * 32 + i]) < p.audit_thr_pairs ? 1u : 0u) << i;
                     if (samp) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
@@ -612,6 +619,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             const bool avalid = atom >= p.valid_begin && atom < p.valid_atoms;
             const float inv = __ldg(p.inv2 + atom);
             const uint32_t ha = audit_hash_flat(static_cast<uint64_t>(p.flat_base + atom * p.flat_stride));
+            const bool asamp = p.audit_thr != 0u && avalid && (p.audit_shift == 0u || (ha >> (32u - p.audit_shift)) == 0u);
             const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
@@ -635,11 +643,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                         if ((hits >> i) & 1u)
                             store_hit(p, s.bst[acc][q * 32 + i], vt * 128 + q * 32 + i, atom, sc[i], slot++);
                 }
-                if (p.audit_thr != 0u && avalid) {
+                if (asamp) {
                     uint32_t samp = 0;
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
-                        samp |= (audit_mix(ha, s.hv[acc][q * 32 + i]) < p.audit_thr ? 1u : 0u) << i;
+                        samp |= (audit_mix(ha, s.hv[acc][q * 32 + i]) < p.audit_thr_pairs ? 1u : 0u) << i;
                     if (samp) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
@@ -744,6 +752,11 @@ Dev dev_of(const MatchParams& p, int64_t k_valid) {
     d.audit_count = p.audit_count;
     d.audit_cap = p.audit_cap;
     d.audit_thr = (p.audit != nullptr && p.audit_count != nullptr) ? p.audit_thr : 0u;
+    d.audit_shift = 0;
+    while (d.audit_shift < 8 && (static_cast<uint64_t>(d.audit_thr) << (d.audit_shift + 1)) <= 0xffffffffull &&
+           d.audit_thr != 0u)
+        ++d.audit_shift;
+    d.audit_thr_pairs = d.audit_thr << d.audit_shift;
     return d;
 }
 
