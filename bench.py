@@ -526,8 +526,8 @@ def run_ours(args, world, rank, local):
         # FP32 error check, write (CUB sort/select kernels not counted); the
         # screening audit; + seed pass and k_merge when N > 1
         # subspace screening: per scan one K1 launch per off-resonance quad (chunks),
-        # per off-resonance value a slab projection, a K2 launch and a query projection
-        "gpu_launches": int(sum((s.chunks + 3 * g.df_hz.count + 13) if s.subspace_rank else (3 * s.chunks + 13)
+        # per off-resonance value a slab projection and a K2 launch, one query projection
+        "gpu_launches": int(sum((s.chunks + 2 * g.df_hz.count + 14) if s.subspace_rank else (3 * s.chunks + 13)
                                 for s in stats) + (3 * args.steps if world > 1 else 0)),
         "clocks": clk.summary(),
         "zoom": zoom,

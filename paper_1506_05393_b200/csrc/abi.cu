@@ -453,9 +453,9 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
             MRFG_CUDA(cudaMemsetAsync(qbuf, 0, sizeof(__half) * ndf * qrows * sub_kc, S));
             MRFG_CUDA(cudaMemsetAsync(rho, 0, sizeof(unsigned int), S));
             pj.push_back(tm.mark());
-            for (int64_t d = 0; d < ndf; ++d)
-                launch_project(c, c.qprime.as<__half>(), qrows, kp, sub_w + d * sub_nw * kp, sub_nw,
-                               qbuf + d * qrows * sub_kc, sub_kc, nullptr, 0, nullptr);
+            // the query coefficients of every df in one launch (grid.y = df)
+            launch_project(c, c.qprime.as<__half>(), qrows, kp, sub_w, sub_nw, qbuf, sub_kc, nullptr, 0, nullptr,
+                           static_cast<int>(ndf), sub_nw * kp, qrows * sub_kc);
             pj.push_back(tm.mark());
             for (int64_t q0 = 0; q0 < ndf; q0 += 4, ++i) {
                 pm.push_back(tm.mark());

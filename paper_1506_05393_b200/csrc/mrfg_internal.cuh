@@ -179,7 +179,8 @@ int subspace_cols(int r);   // real basis rows, 2 r
 int subspace_pitch(int r);  // coefficient row pitch (multiple of 64: K2's K blocks)
 const __half* ensure_subspace(Ctx& c, const GridTables& t, int r);
 void launch_project(Ctx& c, const __half* A, int64_t rows, int64_t kpad, const __half* W, int nw, __half* out,
-                    int opitch, const float* inv2, int64_t valid, unsigned int* rho2max);
+                    int opitch, const float* inv2, int64_t valid, unsigned int* rho2max, int batch = 1,
+                    int64_t w_stride = 0, int64_t o_stride = 0);
 bool bloch_dfquad_ok(const Ctx& c);
 void launch_bloch_dfquad(Ctx& c, const GridTables& t, int idf0, int64_t row_lo, int64_t nrows, int64_t pitch,
                          int metric, __half* d_a, float* d_inv2);

@@ -66,7 +66,11 @@ template <int NW>
 __global__ void __launch_bounds__(256) k_project(const __half* __restrict__ A, int64_t kpad, int kt,
                                                  const __half* __restrict__ W, __half* __restrict__ out,
                                                  int opitch, const float* __restrict__ inv2, int64_t valid,
-                                                 unsigned int* __restrict__ rho2max) {
+                                                 unsigned int* __restrict__ rho2max, int64_t w_stride,
+                                                 int64_t o_stride) {
+    // blockIdx.y: batch of bases over the same rows (the query projections of all df)
+    W += blockIdx.y * w_stride;
+    out += blockIdx.y * o_stride;
     extern __shared__ __align__(16) __half wsm[];  // NW x (kt + kWPad)
     const int wp = kt + kWPad;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -131,14 +135,15 @@ __global__ void __launch_bounds__(256) k_project(const __half* __restrict__ A, i
 
 template <int NW>
 void project_variant(Ctx& c, const __half* A, int64_t rows, int64_t kpad, const __half* W, __half* out, int opitch,
-                     const float* inv2, int64_t valid, unsigned int* rho2max) {
+                     const float* inv2, int64_t valid, unsigned int* rho2max, int batch, int64_t w_stride,
+                     int64_t o_stride) {
     // the largest K tile (a divisor of kpad, multiple of 32) whose basis tile fits ~128 KB
     int kt = static_cast<int>(kpad);
     while (static_cast<int64_t>(sizeof(__half)) * NW * (kt + kWPad) > 132 * 1024 && kt % 64 == 0) kt /= 2;
     const int smem = static_cast<int>(sizeof(__half) * NW * (kt + kWPad));
     MRFG_CUDA(cudaFuncSetAttribute(k_project<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_project<NW><<<static_cast<unsigned>(rows / kProjRows), 256, smem, c.stream>>>(A, kpad, kt, W, out, opitch, inv2,
-                                                                                   valid, rho2max);
+    k_project<NW><<<dim3(static_cast<unsigned>(rows / kProjRows), batch), 256, smem, c.stream>>>(
+        A, kpad, kt, W, out, opitch, inv2, valid, rho2max, w_stride, o_stride);
     MRFG_CUDA(cudaGetLastError());
 }
 
@@ -150,14 +155,15 @@ int subspace_cols(int r) { return 2 * subspace_rank(r); }
 int subspace_pitch(int r) { return (subspace_cols(r) + 63) / 64 * 64; }
 
 void launch_project(Ctx& c, const __half* A, int64_t rows, int64_t kpad, const __half* W, int nw, __half* out,
-                    int opitch, const float* inv2, int64_t valid, unsigned int* rho2max) {
+                    int opitch, const float* inv2, int64_t valid, unsigned int* rho2max, int batch,
+                    int64_t w_stride, int64_t o_stride) {
     MRFG_REQUIRE(rows % kProjRows == 0 && kpad % 64 == 0, MRFG_E_INVALID, "project: bad operand shape");
     switch (nw) {
-        case 16: project_variant<16>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max); break;
-        case 32: project_variant<32>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max); break;
-        case 64: project_variant<64>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max); break;
-        case 96: project_variant<96>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max); break;
-        case 128: project_variant<128>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max); break;
+        case 16: project_variant<16>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max, batch, w_stride, o_stride); break;
+        case 32: project_variant<32>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max, batch, w_stride, o_stride); break;
+        case 64: project_variant<64>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max, batch, w_stride, o_stride); break;
+        case 96: project_variant<96>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max, batch, w_stride, o_stride); break;
+        case 128: project_variant<128>(c, A, rows, kpad, W, out, opitch, inv2, valid, rho2max, batch, w_stride, o_stride); break;
         default: throw Error{MRFG_E_INVALID, "project: unsupported basis width"};
     }
 }
