@@ -38,7 +38,6 @@ constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int NTHREADS = 256;
-constexpr int NTHREADS2 = 384;  // the CTA-pair kernel: 4 role warps + 8 epilogue warps
 
 struct alignas(1024) Smem {
     uint8_t a[STAGES][A_BYTES];
@@ -504,7 +503,7 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
         : "memory");
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     k_match_sm100_2cta(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                        Dev p) {
     extern __shared__ uint8_t smem_raw[];
@@ -524,7 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s.tfull[i], 1);
-            mbar_init(&s.tempty[i], 16);  // 8 epilogue warps x 2 CTAs
+            mbar_init(&s.tempty[i], 8);  // 4 epilogue warps x 2 CTAs
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
@@ -597,10 +596,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1)
             }
         }
     } else if (warp >= 4) {
-        // eight epilogue warps: warps 4-7 and 8-11 share the TMEM lane quarters
-        // (a warp reads lanes 32 (warp % 4) ..) and split a tile's 256 columns --
-        // with short K (subspace operands) the epilogue, not the MMA, bounds K2
-        const int ew = (warp - 4) & 3, half = (warp - 4) >> 2;
+        const int ew = warp - 4;
         const int row = ew * 32 + lane;
         const uint32_t tempty_leader[2] = {map_to_rank(smem_u32(&s.tempty[0]), 0),
                                            map_to_rank(smem_u32(&s.tempty[1]), 0)};
@@ -609,14 +605,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1)
         for (int64_t t = cid; t < n_tiles; t += ncl) {
             int64_t at, vt;
             tile_coords(t, n_at, n_vt, p.ga, at, vt);
-            if (half == 0) {
+            {
                 const int64_t v = vt * 128 + row;
                 float b = v < p.nvox ? __ldcg(p.best + v) : 1e30f;
                 s.thr[acc][row] = v < p.nvox ? threshold_of(b, p.delta, p.metric) : __int_as_float(0x7f800000);
                 s.bst[acc][row] = b;
                 s.hv[acc][row] = audit_hash_voxel(static_cast<uint64_t>(p.vox_base + v));
             }
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            asm volatile("bar.sync 1, 128;" ::: "memory");
             mbar_wait(&s.tfull[acc], acc_phase);
             tc_fence_after();
             const int64_t atom = at * 256 + static_cast<int64_t>(rank) * 128 + row;
@@ -627,7 +623,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1)
             const uint32_t tbase = tmem + (static_cast<uint32_t>(ew * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-            for (int q = 2 * half; q < 2 * half + 2; ++q) {
+            for (int q = 0; q < 4; ++q) {
                 uint32_t r[64];
                 TMEM_LD_X64(tbase + q * 64, r);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -797,7 +793,7 @@ void launch_match(Ctx& c, const MatchParams& p) {
         const int64_t tiles = (p.atoms / 256) * d.n_vt;
         const int64_t pairs = std::min<int64_t>(tiles, c.num_sms / 2);
         d.ga = group_of(p, pairs);
-        k_match_sm100_2cta<<<static_cast<int>(2 * pairs), NTHREADS2, SMEM2_BYTES, c.stream>>>(ma, mb, d);
+        k_match_sm100_2cta<<<static_cast<int>(2 * pairs), NTHREADS, SMEM2_BYTES, c.stream>>>(ma, mb, d);
         MRFG_CUDA(cudaGetLastError());
         return;
     }
