@@ -107,11 +107,20 @@ def scan_grid_distributed(ctx, grid, d_queries, nq: int, group=None, opts=None, 
     d_out = torch.empty(nq * 16, dtype=torch.uint8, device=dev)
     stats = None
     o = opts
+    if dev.type == "cuda":  # the queries may still be in flight on torch's stream
+        torch.cuda.current_stream(dev).synchronize()
     if world > 1 and global_seed and metric == "cc":
         seed = torch.full((nq,), -3.0, dtype=torch.float32, device=dev)
         if fe > fb:
             ctx.scan_seed_device(grid, d_queries.data_ptr(), nq, seed.data_ptr(), metric=metric,
                                  flat_range=(fb, fe), opts=opts)
+        # the context may run on its own stream: its seed copy must have landed
+        # before torch's stream reads `seed`, and the floors torch builds below
+        # must exist before the context's stream reads them (a cold start
+        # stretches these windows: without the two syncs the scan could see
+        # uninitialised floors and return "no atom above the floor")
+        if dev.type == "cuda":
+            torch.cuda.synchronize(dev)
         _all_reduce_max(seed, group)
         floor = torch.zeros((nq, 2), dtype=torch.float64, device=dev)
         floor[:, 1] = seed.double()
@@ -119,6 +128,8 @@ def scan_grid_distributed(ctx, grid, d_queries, nq: int, group=None, opts=None, 
         floor_rec[:, 0] = 0  # flat 0: "a floor is present"
         o = ScanOpts() if opts is None else ScanOpts.from_buffer_copy(opts)
         o.floor_matches = C.c_void_p(floor_rec.data_ptr())
+        if dev.type == "cuda":
+            torch.cuda.current_stream(dev).synchronize()
     if fe > fb:
         stats = ctx.scan_grid_device(grid, d_queries.data_ptr(), nq, d_out.data_ptr(), metric=metric,
                                      flat_range=(fb, fe), opts=o)
