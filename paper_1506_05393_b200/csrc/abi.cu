@@ -282,8 +282,16 @@ static bool scan_dev_once(Ctx& c, const mrfg_grid* grid, const float* d_dict, in
         sub_r = std::atoi(e);
     else if (sub_ok && fe - fb >= 4000000 && (fe - fb) / ndf >= 4096)
         sub_r = 48;  // held-out residual 5e-4 on config 2 (rank 32: 3e-3, a margin of 8.6e-3 and an overflow pass)
+    const bool sub_auto = std::getenv("MRFG_SUBSPACE") == nullptr;
     if (sub_r > 0) sub_r = subspace_rank(sub_r);
     if (!sub_ok) sub_r = 0;
+    // a lattice whose slabs do not compress (held-out residual above 2e-3 at the
+    // default rank: the margin and the candidate lists would grow) keeps the
+    // full-length screening
+    if (sub_r && sub_auto) {
+        ensure_subspace(c, *tp, sub_r);
+        if (tp->sub_rho_held > 2e-3) sub_r = 0;
+    }
     const int sub_nw = sub_r ? subspace_cols(sub_r) : 0, sub_kc = sub_r ? subspace_pitch(sub_r) : 0;
     const __half* sub_w = sub_r ? ensure_subspace(c, *tp, sub_r) : nullptr;  // cached per grid
     // the truncation adds at most |q_perp| |a_perp| / |a| <= rho to the screening
